@@ -1,0 +1,123 @@
+"""Seeded synthetic input generators shared by the tests, the oracle's callers and bench.py.
+
+This module holds ONLY random draws and their plumbing (seed streams, symbol alphabets,
+circular-Gaussian noise, power picks, random taps).  It contains none of the LDBP method's
+arithmetic (no FIR, no Kerr rotation, no split-step, no gradient), so both the CPU oracle
+(`oracle/`) and the CUDA path can consume its output without sharing method code.
+
+Seed tree (SURVEY.md §8(d) "Seeds"): each configuration's root is
+``SeedSequence([201014258, cfg_index])``; every draw is keyed by
+``(global block index, purpose)`` so that the union of the blocks a rank generates is
+identical for any number of ranks G.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SEED_ROOT = 201014258
+
+# purpose ids for the keyed streams (stable numbering; never reorder)
+PURPOSES = {
+    "symbols": 1,
+    "ase": 2,
+    "taps": 3,
+    "power": 4,
+    "augment": 5,
+    "signal": 6,
+    "target": 7,
+    "gamma": 8,
+    "grad": 9,
+}
+
+
+def rng(cfg_index: int, block: int, purpose: str, sub: int = 0) -> np.random.Generator:
+    """Independent PCG64 stream keyed by (config, global block index, purpose, sub-key)."""
+    ss = np.random.SeedSequence([SEED_ROOT, int(cfg_index), int(block), PURPOSES[purpose], int(sub)])
+    return np.random.Generator(np.random.PCG64(ss))
+
+
+def cn(g: np.random.Generator, shape) -> np.ndarray:
+    """Circularly-symmetric complex Gaussian CN(0, 1) draws (E|z|^2 = 1), complex128."""
+    re = g.standard_normal(shape)
+    im = g.standard_normal(shape)
+    return (re + 1j * im) * np.sqrt(0.5)
+
+
+QAM16_LEVELS = np.array([-3.0, -1.0, 1.0, 3.0]) / np.sqrt(10.0)
+
+
+def qam16(g: np.random.Generator, count: int) -> np.ndarray:
+    """Uniform iid 16-QAM symbols, per-dimension levels {+-1, +-3}/sqrt(10) (unit mean power)."""
+    i = g.integers(0, 4, size=count)
+    q = g.integers(0, 4, size=count)
+    return QAM16_LEVELS[i] + 1j * QAM16_LEVELS[q]
+
+
+def dbm_to_w(p_dbm):
+    return 10.0 ** ((np.asarray(p_dbm, dtype=np.float64) - 30.0) / 10.0)
+
+
+def pick_powers_dbm(cfg_index: int, blocks, power_set_dbm) -> np.ndarray:
+    """Per-block launch power drawn uniformly from the discrete set P (paper P:839-843)."""
+    ps = np.asarray(power_set_dbm, dtype=np.float64)
+    return np.array([ps[rng(cfg_index, b, "power").integers(0, len(ps))] for b in blocks])
+
+
+def gaussian_blocks(cfg_index: int, blocks, n: int, power_w, purpose: str = "signal") -> np.ndarray:
+    """complex128 [len(blocks)][n] circular-Gaussian blocks with mean power power_w[b] (W).
+
+    After 2000 km of chromatic dispersion the received samples are close to circular complex
+    Gaussian with the launch power (SURVEY.md §8(d) "Value distribution"); this is the bench's
+    stand-in for SSFM output at sizes the CPU channel simulator cannot produce in time.
+    """
+    blocks = list(blocks)
+    pw = np.broadcast_to(np.asarray(power_w, dtype=np.float64), (len(blocks),))
+    out = np.empty((len(blocks), n), dtype=np.complex128)
+    for i, b in enumerate(blocks):
+        out[i] = cn(rng(cfg_index, b, purpose), n) * np.sqrt(pw[i])
+    return out
+
+
+def random_sym_taps(cfg_index: int, steps: int, taps: int, scale: float = 0.1) -> np.ndarray:
+    """Seeded symmetric taps h = delta_0 + scale*CN(0,1) on the half taps.
+
+    Returned as complex128 [steps][taps], tap j in [-Kh, Kh] stored at index j+Kh.
+    """
+    kh = (taps - 1) // 2
+    g = rng(cfg_index, 0, "taps")
+    half = cn(g, (steps, kh + 1)) * scale
+    half[:, 0] += 1.0
+    full = np.empty((steps, taps), dtype=np.complex128)
+    for j in range(kh + 1):
+        full[:, kh + j] = half[:, j]
+        full[:, kh - j] = half[:, j]
+    return full
+
+
+def random_general_taps(cfg_index: int, steps: int, taps: int, scale: float = 0.1, sub: int = 0) -> np.ndarray:
+    """Seeded non-symmetric taps delta_0 + scale*CN(0,1) on all T taps, complex128 [steps][taps]."""
+    kh = (taps - 1) // 2
+    g = rng(cfg_index, 0, "taps", sub=1000 + sub)
+    full = cn(g, (steps, taps)) * scale
+    full[:, kh] += 1.0
+    return full
+
+
+def random_gamma(cfg_index: int, steps: int, lo: float = -30.0, hi: float = -5.0, sub: int = 0) -> np.ndarray:
+    """Seeded per-step signed nonlinearity scalars gamma' (1/W), uniform in [lo, hi]."""
+    g = rng(cfg_index, 0, "gamma", sub=sub)
+    return g.uniform(lo, hi, size=steps)
+
+
+def augment_params(cfg_index: int, blocks, n: int):
+    """Per-block (circular shift k_b, phase phi_b) for the equivariant pool augmentation (§8(d))."""
+    ks, phis = [], []
+    for b in blocks:
+        g = rng(cfg_index, b, "augment")
+        ks.append(int(g.integers(0, n)))
+        phis.append(float(g.uniform(-np.pi, np.pi)))
+    return np.array(ks, dtype=np.int64), np.array(phis)
+
+
+def to_complex64(a: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.complex64)
