@@ -1,0 +1,158 @@
+/*
+ * ldbp.h — C ABI of libldbp, the B200 (sm_100a) hot path of learned digital backpropagation.
+ *
+ * Method: C. Häger, H. D. Pfister, "Physics-Based Deep Learning for Fiber-Optic
+ * Communication Systems", arXiv:2010.14258.  Citations "P:n" are lines of that paper's
+ * source; "S:n" lines of SPEC.md; "§8(x)" sections of SURVEY.md.
+ *
+ * The model (Eq. (7)) maps each independent circular block x in C^n through
+ * M steps,   a = h^(i) (*) u   (circular, centred FIR, reading G1 of DESIGN.md:
+ *            a_t = sum_{j=-Kh}^{Kh} h_j u_{(t-j) mod n}, frequency response
+ *            sum_k h_k e^{-jk omega} as in P:895-896),
+ *            u <- a * exp(j gamma'_i |a|^2)  (Kerr step, P:384-388 with the per-step scalar of
+ *            Remark 2; gamma' is signed and carries gamma*L_eff*xi).
+ *
+ * CONVENTIONS (every entry point)
+ *  - All data pointers are DEVICE pointers owned by the caller.  The library never allocates
+ *    in a call, keeps no mutable global state, is thread-safe, and enqueues its work
+ *    asynchronously on `cuda_stream` (a cudaStream_t; NULL = legacy default stream).  No call
+ *    synchronises the host, so every call is CUDA-graph capturable.  Results are valid once
+ *    the stream has completed the enqueued work.
+ *  - Complex arrays are complex64: interleaved (re, im) float32 pairs, row-major, 8-byte
+ *    aligned.  Blocks: [B][n].  Taps: [M][T], tap j in [-Kh, Kh] stored at index j + Kh.
+ *    gamma: float32 [M] (phase = gamma[i] * |a|^2, radians, |a|^2 in the units of x^2).
+ *  - Gradient convention for a complex z and real loss L: dL/dRe z + i dL/dIm z.
+ *    Real-valued gradient outputs are float64; complex ones are stored as [..][2] float64.
+ *  - Every call returns an ldbp_status.  Validation failures return before anything is
+ *    enqueued; a CUDA launch failure returns LDBP_ECUDA.  ldbp_last_error() then returns a
+ *    thread-local human-readable detail string.
+ *  - Results are deterministic: fixed reduction order, no floating-point atomics.
+ */
+#ifndef LDBP_H_
+#define LDBP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LDBP_ABI_VERSION 1
+
+/* Problem dimensions. */
+typedef struct ldbp_dims {
+  int64_t batch;   /* B >= 0 independent circular blocks (B = 0: every call is a no-op)   */
+  int64_t n;       /* samples per block, n >= 1                                             */
+  int32_t steps;   /* M >= 1 model steps (layers)                                */
+  int32_t taps;    /* T = 2*Kh + 1, odd, 1 <= T <= LDBP_MAX_TAPS and T <= n                 */
+  uint32_t flags;  /* bitwise OR of ldbp_flags                                              */
+  int32_t reserved;/* must be 0                                                             */
+} ldbp_dims;
+
+#define LDBP_MAX_TAPS 15
+
+enum ldbp_flags {
+  /* Symmetric filters h_{-j} = h_j.  The kernels read only taps[Kh..T-1] of each
+     step (the caller promises symmetry), use the folded FIR of fig:filter, and
+     return tied-parameter gradients: dtaps[j] = dtaps[-j] = g_j + g_{-j}. */
+  LDBP_SYMMETRIC = 1u,
+  /* Use IEEE-accurate sincosf for the Kerr rotation instead of the MUFU approximation. */
+  LDBP_PRECISE = 2u
+};
+
+typedef enum ldbp_status {
+  LDBP_OK = 0,
+  LDBP_EINVAL = -1,      /* null/aliased pointer, reserved != 0, unknown flag, bad hyper-parameter */
+  LDBP_ESHAPE = -2,      /* T even, T > LDBP_MAX_TAPS, T > n, M < 1, n < 1, B < 0          */
+  LDBP_EALIGN = -3,      /* a complex pointer is not 8-byte aligned, a double one not 8-byte */
+  LDBP_EWORKSPACE = -4,  /* ws_bytes < ldbp_workspace_bytes(...) or ws == NULL when needed  */
+  LDBP_ECUDA = -5        /* a CUDA runtime error (detail in ldbp_last_error())               */
+} ldbp_status;
+
+typedef enum ldbp_op {
+  LDBP_OP_FORWARD = 0,
+  LDBP_OP_BACKWARD = 1,
+  LDBP_OP_LOSS_GRAD = 2,
+  LDBP_OP_TRAIN_STEP = 3
+} ldbp_op;
+
+int ldbp_abi_version(void);
+const char* ldbp_status_string(int status);
+/* Thread-local detail of the last failing call on this thread ("" if none). */
+const char* ldbp_last_error(void);
+
+/* Device workspace (bytes) the given op needs for these dims; 0 means ws may be NULL.
+   Returns a status; *bytes is written on LDBP_OK. */
+int ldbp_workspace_bytes(const ldbp_dims* d, int op, size_t* bytes);
+
+/* Number of CUDA kernel launches the op enqueues for these dims (for accounting). */
+int ldbp_launch_count(const ldbp_dims* d, int op, int* launches);
+
+/*
+ * ldbp_forward — y = f_theta(x), Eq. (7) for every block.
+ *   x      [B][n] complex64 in;  y [B][n] complex64 out (must not alias x or ws)
+ *   taps   [M][T] complex64;     gamma [M] float32
+ *   ws     workspace of ldbp_workspace_bytes(d, LDBP_OP_FORWARD) bytes (may be 0 -> NULL ok)
+ */
+int ldbp_forward(const ldbp_dims* d, const void* x, void* y, const void* taps, const float* gamma,
+                 void* ws, size_t ws_bytes, void* cuda_stream);
+
+/*
+ * ldbp_backward — reverse-mode sweep of Eq. (7) for an incoming gradient gy = dL/dy
+ * (per step: c = Im(gv conj v), ga = gv e^{-j phi} + 2 gamma' c a,
+ * dgamma' = sum c|a|^2, dh_j = sum ga_t conj(u_{t-j}), gu_s = sum_j conj(h_j) ga_{s+j}).
+ *   x      [B][n] complex64 (the forward input; activations are recomputed, not stored)
+ *   gy     [B][n] complex64
+ *   dtaps  [M][T][2] float64 out: sum over all blocks (tied-parameter form with LDBP_SYMMETRIC)
+ *   dgamma [M] float64 out
+ *   gx     [B][n] complex64 out, or NULL to skip dL/dx
+ */
+int ldbp_backward(const ldbp_dims* d, const void* x, const void* gy, const void* taps,
+                  const float* gamma, double* dtaps, double* dgamma, void* gx_or_null,
+                  void* ws, size_t ws_bytes, void* cuda_stream);
+
+/*
+ * ldbp_loss_grad — waveform-MSE training gradient (reading G7; Eq. (2) P:280-285 with the
+ * 1/N applied later): with e = f_theta(x) - target,
+ *   buf[0]                    = sum_{blocks,t} |e|^2                       (UNscaled)
+ *   buf[1 .. M]               = d buf[0] / d gamma'_i
+ *   buf[1+M .. 1+M+2MT)       = d buf[0] / d taps as [M][T][2]
+ * Taps are multiplied by tap_mask (uint8 [M][T], 1 keep / 0 prune) when non-NULL;
+ * masked taps get gradient 0.  buf is this device's UNREDUCED contribution (data parallel:
+ * all-reduce SUM it across ranks, then call ldbp_adam_update with n_global = sum B*n).
+ */
+int ldbp_loss_grad(const ldbp_dims* d, const void* x, const void* target, const void* taps,
+                   const float* gamma, const uint8_t* tap_mask_or_null, double* buf,
+                   void* ws, size_t ws_bytes, void* cuda_stream);
+
+/*
+ * ldbp_adam_update — bias-corrected Adam (mu per Table I) on the real
+ * parameter vector master = [taps as [M][T][2] | gamma[M]] (float64, length 2MT+M), with
+ * gradient g = reorder(buf_reduced)/n_global.  m, v: float64 moments (same layout), t >= 1 the
+ * 1-based step.  Masked taps are forced to 0 with m = v = 0; gamma entries with
+ * gamma_learnable[i] == 0 are left unchanged.  Writes the float32 working copies taps_out
+ * ([M][T] complex64) and gamma_out ([M]).  Requires lr > 0, 0 <= b1,b2 < 1, eps > 0, n_global > 0.
+ */
+int ldbp_adam_update(const ldbp_dims* d, const double* buf_reduced, double n_global,
+                     double* master, double* m, double* v, int64_t t,
+                     double lr, double b1, double b2, double eps,
+                     const uint8_t* tap_mask_or_null, const uint8_t* gamma_learnable_or_null,
+                     void* taps_out, float* gamma_out, void* cuda_stream);
+
+/*
+ * ldbp_train_step — single-process training step: ldbp_loss_grad on the working copies
+ * (taps_work, gamma_work) then ldbp_adam_update with n_global = B*n.  buf receives the
+ * gradient buffer of this step (buf[0] = sum |e|^2 before the update).
+ */
+int ldbp_train_step(const ldbp_dims* d, const void* x, const void* target,
+                    void* taps_work, float* gamma_work, double* master, double* m, double* v,
+                    int64_t t, double lr, double b1, double b2, double eps,
+                    const uint8_t* tap_mask_or_null, const uint8_t* gamma_learnable_or_null,
+                    double* buf, void* ws, size_t ws_bytes, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LDBP_H_ */

@@ -1,0 +1,89 @@
+"""ctypes loader for libldbp.so (the C ABI declared in include/ldbp.h).
+
+Argument marshalling only.  If the shared library is missing this module raises at import
+time: there is no CPU fallback anywhere in the product path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("LDBP_LIB", os.path.join(_HERE, "libldbp.so"))
+
+LDBP_SYMMETRIC = 1
+LDBP_PRECISE = 2
+OP_FORWARD, OP_BACKWARD, OP_LOSS_GRAD, OP_TRAIN_STEP = 0, 1, 2, 3
+
+# Every symbol include/ldbp.h declares (checked by tests/test_abi.py).
+EXPORTED = (
+    "ldbp_abi_version",
+    "ldbp_status_string",
+    "ldbp_last_error",
+    "ldbp_workspace_bytes",
+    "ldbp_launch_count",
+    "ldbp_forward",
+    "ldbp_backward",
+    "ldbp_loss_grad",
+    "ldbp_adam_update",
+    "ldbp_train_step",
+)
+
+
+class LdbpDims(ctypes.Structure):
+    _fields_ = [
+        ("batch", ctypes.c_int64),
+        ("n", ctypes.c_int64),
+        ("steps", ctypes.c_int32),
+        ("taps", ctypes.c_int32),
+        ("flags", ctypes.c_uint32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+class LdbpError(RuntimeError):
+    def __init__(self, status: int, func: str, detail: str):
+        super().__init__(f"{func} failed with status {status}: {detail}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"libldbp.so not found at {LIB_PATH}; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    D = ctypes.POINTER(LdbpDims)
+    dbl = ctypes.c_double
+    sig = {
+        "ldbp_abi_version": (ctypes.c_int, []),
+        "ldbp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+        "ldbp_last_error": (ctypes.c_char_p, []),
+        "ldbp_workspace_bytes": (ctypes.c_int, [D, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
+        "ldbp_launch_count": (ctypes.c_int, [D, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+        "ldbp_forward": (ctypes.c_int, [D, P, P, P, P, P, ctypes.c_size_t, P]),
+        "ldbp_backward": (ctypes.c_int, [D, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
+        "ldbp_loss_grad": (ctypes.c_int, [D, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
+        "ldbp_adam_update": (ctypes.c_int, [D, P, dbl, P, P, P, ctypes.c_int64, dbl, dbl, dbl, dbl, P, P, P, P, P]),
+        "ldbp_train_step": (ctypes.c_int, [D, P, P, P, P, P, P, P, ctypes.c_int64, dbl, dbl, dbl, dbl, P, P, P, P,
+                                           ctypes.c_size_t, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int, func: str) -> None:
+    if status != 0:
+        detail = lib.ldbp_last_error().decode(errors="replace")
+        raise LdbpError(status, func, f"{lib.ldbp_status_string(status).decode()} ({detail})")
+
+
+def dims(batch: int, n: int, steps: int, taps: int, flags: int = 0) -> LdbpDims:
+    return LdbpDims(int(batch), int(n), int(steps), int(taps), int(flags), 0)

@@ -1,0 +1,217 @@
+"""Thin Python binding of libldbp (same names as the C ABI, include/ldbp.h).
+
+PyTorch is plumbing only: tensors provide device memory, the current CUDA stream and (in
+``dp.py``) the process group.  Every step of the hot path runs inside libldbp's kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from ._lib import LDBP_PRECISE, LDBP_SYMMETRIC, OP_BACKWARD, OP_FORWARD, OP_LOSS_GRAD, OP_TRAIN_STEP, check, lib
+
+_VP = ctypes.c_void_p
+
+
+def _p(t):
+    return None if t is None else _VP(t.data_ptr())
+
+
+def _stream_handle(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return _VP(s.cuda_stream)
+
+
+def _flags(symmetric: bool, precise: bool) -> int:
+    return (LDBP_SYMMETRIC if symmetric else 0) | (LDBP_PRECISE if precise else 0)
+
+
+def _need(t, name, dtype, shape=None):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (libldbp has no CPU path)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+def make_dims(B, n, M, T, symmetric=True, precise=False):
+    return _lib.dims(B, n, M, T, _flags(symmetric, precise))
+
+
+def workspace_bytes(d, op: int) -> int:
+    out = ctypes.c_size_t(0)
+    check(lib.ldbp_workspace_bytes(ctypes.byref(d), op, ctypes.byref(out)), "ldbp_workspace_bytes")
+    return int(out.value)
+
+
+def launch_count(d, op: int) -> int:
+    out = ctypes.c_int(0)
+    check(lib.ldbp_launch_count(ctypes.byref(d), op, ctypes.byref(out)), "ldbp_launch_count")
+    return int(out.value)
+
+
+class Workspace:
+    """Grow-only device scratch buffer (allocated by torch's caching allocator, outside any call)."""
+
+    def __init__(self, device=None):
+        self.device = device
+        self.buf = None
+
+    def get(self, nbytes: int, device):
+        if nbytes == 0:
+            return None
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_default_ws = {}
+
+
+def _ws(device, nbytes, ws):
+    if ws is None:
+        ws = _default_ws.setdefault(str(device), Workspace())
+    b = ws.get(nbytes, device)
+    return b, nbytes
+
+
+def _check_model(x, taps, gamma):
+    _need(x, "x", torch.complex64)
+    if x.dim() != 2:
+        raise ValueError("x must be [B][n]")
+    _need(taps, "taps", torch.complex64)
+    if taps.dim() != 2:
+        raise ValueError("taps must be [M][T]")
+    M, T = taps.shape
+    _need(gamma, "gamma", torch.float32, (M,))
+    return x.shape[0], x.shape[1], M, T
+
+
+def ldbp_forward(x, taps, gamma, *, symmetric=True, precise=False, out=None, ws=None, stream=None):
+    """y = f_theta(x) (Eq. 7) for complex64 x [B][n], taps [M][T], gamma [M]."""
+    B, n, M, T = _check_model(x, taps, gamma)
+    d = make_dims(B, n, M, T, symmetric, precise)
+    y = torch.empty_like(x) if out is None else out
+    _need(y, "out", torch.complex64, x.shape)
+    nb = workspace_bytes(d, OP_FORWARD)
+    w, nb = _ws(x.device, nb, ws)
+    check(lib.ldbp_forward(ctypes.byref(d), _p(x), _p(y), _p(taps), _p(gamma), _p(w), nb, _stream_handle(stream)),
+          "ldbp_forward")
+    return y
+
+
+def ldbp_backward(x, gy, taps, gamma, *, symmetric=True, precise=False, need_gx=True, ws=None, stream=None):
+    """Reverse mode for incoming gy = dL/dy.  Returns (dtaps complex128 [M][T], dgamma f64 [M], gx or None)."""
+    B, n, M, T = _check_model(x, taps, gamma)
+    _need(gy, "gy", torch.complex64, x.shape)
+    d = make_dims(B, n, M, T, symmetric, precise)
+    dt = torch.empty((M, T, 2), dtype=torch.float64, device=x.device)
+    dg = torch.empty((M,), dtype=torch.float64, device=x.device)
+    gx = torch.empty_like(x) if need_gx else None
+    nb = workspace_bytes(d, OP_BACKWARD)
+    w, nb = _ws(x.device, nb, ws)
+    check(lib.ldbp_backward(ctypes.byref(d), _p(x), _p(gy), _p(taps), _p(gamma), _p(dt), _p(dg), _p(gx), _p(w), nb,
+                            _stream_handle(stream)), "ldbp_backward")
+    return torch.view_as_complex(dt), dg, gx
+
+
+def ldbp_loss_grad(x, target, taps, gamma, *, mask=None, symmetric=True, precise=False, buf=None, ws=None,
+                   stream=None):
+    """[sum|e|^2 | dgamma[M] | dtaps[M][T][2]] (float64, unscaled, this device's blocks only)."""
+    B, n, M, T = _check_model(x, taps, gamma)
+    _need(target, "target", torch.complex64, x.shape)
+    if mask is not None:
+        _need(mask, "mask", torch.uint8, (M, T))
+    d = make_dims(B, n, M, T, symmetric, precise)
+    out = torch.empty(1 + M + 2 * M * T, dtype=torch.float64, device=x.device) if buf is None else buf
+    nb = workspace_bytes(d, OP_LOSS_GRAD)
+    w, nb = _ws(x.device, nb, ws)
+    check(lib.ldbp_loss_grad(ctypes.byref(d), _p(x), _p(target), _p(taps), _p(gamma), _p(mask), _p(out), _p(w), nb,
+                             _stream_handle(stream)), "ldbp_loss_grad")
+    return out
+
+
+@dataclass
+class AdamConfig:
+    lr: float = 1e-3  # Table I
+    b1: float = 0.9   # reading G13 (paper silent)
+    b2: float = 0.999
+    eps: float = 1e-8
+
+
+@dataclass
+class TrainState:
+    """Parameters + Adam state on the device: fp64 master, fp32 working copies (row a10)."""
+
+    taps: torch.Tensor          # complex64 [M][T] working copy
+    gamma: torch.Tensor         # float32 [M] working copy
+    master: torch.Tensor        # float64 [2MT + M]
+    m: torch.Tensor
+    v: torch.Tensor
+    t: int = 0
+    mask: torch.Tensor | None = None            # uint8 [M][T]
+    gamma_learnable: torch.Tensor | None = None  # uint8 [M]
+    symmetric: bool = True
+    precise: bool = False
+    adam: AdamConfig = field(default_factory=AdamConfig)
+
+    @staticmethod
+    def create(taps, gamma, *, device="cuda", mask=None, gamma_learnable=None, symmetric=True, precise=False,
+               adam=None):
+        taps = torch.as_tensor(taps).to(torch.complex128)
+        gamma = torch.as_tensor(gamma).to(torch.float64)
+        M, T = taps.shape
+        master = torch.cat([torch.view_as_real(taps).reshape(-1), gamma]).to(device)
+        z = torch.zeros_like(master)
+        st = TrainState(taps=taps.to(torch.complex64).to(device).contiguous(),
+                        gamma=gamma.to(torch.float32).to(device).contiguous(), master=master.contiguous(),
+                        m=z.clone(), v=z.clone(), symmetric=symmetric, precise=precise, adam=adam or AdamConfig())
+        if mask is not None:
+            st.mask = torch.as_tensor(mask, dtype=torch.uint8).to(device).contiguous()
+        if gamma_learnable is not None:
+            st.gamma_learnable = torch.as_tensor(gamma_learnable, dtype=torch.uint8).to(device).contiguous()
+        return st
+
+    @property
+    def M(self):
+        return self.taps.shape[0]
+
+    @property
+    def T(self):
+        return self.taps.shape[1]
+
+
+def ldbp_adam_update(state: TrainState, buf_reduced, n_global: float, *, stream=None):
+    """One Adam step on the device from an (all-reduced) gradient buffer."""
+    state.t += 1
+    d = make_dims(1, state.T, state.M, state.T, state.symmetric, state.precise)
+    a = state.adam
+    check(lib.ldbp_adam_update(ctypes.byref(d), _p(buf_reduced), float(n_global), _p(state.master), _p(state.m),
+                               _p(state.v), int(state.t), a.lr, a.b1, a.b2, a.eps, _p(state.mask),
+                               _p(state.gamma_learnable), _p(state.taps), _p(state.gamma), _stream_handle(stream)),
+          "ldbp_adam_update")
+
+
+def ldbp_train_step(state: TrainState, x, target, *, buf=None, ws=None, stream=None):
+    """Single-process step: loss_grad on the working copies then Adam with n_global = B*n."""
+    B, n, M, T = _check_model(x, state.taps, state.gamma)
+    _need(target, "target", torch.complex64, x.shape)
+    d = make_dims(B, n, M, T, state.symmetric, state.precise)
+    out = torch.empty(1 + M + 2 * M * T, dtype=torch.float64, device=x.device) if buf is None else buf
+    nb = workspace_bytes(d, OP_TRAIN_STEP)
+    w, nb = _ws(x.device, nb, ws)
+    state.t += 1
+    a = state.adam
+    check(lib.ldbp_train_step(ctypes.byref(d), _p(x), _p(target), _p(state.taps), _p(state.gamma), _p(state.master),
+                              _p(state.m), _p(state.v), int(state.t), a.lr, a.b1, a.b2, a.eps, _p(state.mask),
+                              _p(state.gamma_learnable), _p(out), _p(w), nb, _stream_handle(stream)),
+          "ldbp_train_step")
+    return out

@@ -1,0 +1,595 @@
+// ldbp_api.cu — C ABI of libldbp (include/ldbp.h): validation, launch planning, dispatch.
+//
+// Planning: every kernel runs on a 1-D tiling of the "extended index space"
+// (see ldbp_kernels.cuh).  The planner picks, per launch, the threads per CTA, the halo H =
+// (#steps in the launch) * Kh (x2 for backward segments), and the owned width W such that the
+// grid is a whole number of waves of resident CTAs on this device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "ldbp.h"
+#define LDBP_AUX_KERNELS
+#include "ldbp_kernels.cuh"
+
+using FwdFn = void (*)(const ldbp::FwdArgs);
+using BwdFn = void (*)(const ldbp::BwdArgs);
+
+namespace {
+
+thread_local char g_err[1024] = "";
+
+int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(LDBP_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return LDBP_OK;
+}
+
+constexpr int kFwdR = LDBP_FWD_R;
+constexpr int kBwdR = LDBP_BWD_R;
+constexpr int kFwdMaxThreads = 512;
+constexpr int kBwdMaxThreads = 256;
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int ntaps_used(int kh, bool sym) { return sym ? kh + 1 : 2 * kh + 1; }
+
+// ----------------------------------------------------------------------------------------
+// Kernel dispatch tables
+// ----------------------------------------------------------------------------------------
+
+// Kernel instantiations live in ldbp_inst.cu, compiled once per Kh (parallel build).
+#define LDBP_DECL_GETTERS(K)                        \
+  FwdFn ldbp_get_fwd_##K(bool sym, bool fast);      \
+  BwdFn ldbp_get_bwd_##K(bool sym, bool fast);
+}  // namespace
+LDBP_DECL_GETTERS(0)
+LDBP_DECL_GETTERS(1)
+LDBP_DECL_GETTERS(2)
+LDBP_DECL_GETTERS(3)
+LDBP_DECL_GETTERS(4)
+LDBP_DECL_GETTERS(5)
+LDBP_DECL_GETTERS(6)
+LDBP_DECL_GETTERS(7)
+namespace {
+
+FwdFn get_fwd(int kh, bool sym, bool fast) {
+  switch (kh) {
+    case 0: return ldbp_get_fwd_0(sym, fast);
+    case 1: return ldbp_get_fwd_1(sym, fast);
+    case 2: return ldbp_get_fwd_2(sym, fast);
+    case 3: return ldbp_get_fwd_3(sym, fast);
+    case 4: return ldbp_get_fwd_4(sym, fast);
+    case 5: return ldbp_get_fwd_5(sym, fast);
+    case 6: return ldbp_get_fwd_6(sym, fast);
+    case 7: return ldbp_get_fwd_7(sym, fast);
+  }
+  return nullptr;
+}
+BwdFn get_bwd(int kh, bool sym, bool fast) {
+  switch (kh) {
+    case 0: return ldbp_get_bwd_0(sym, fast);
+    case 1: return ldbp_get_bwd_1(sym, fast);
+    case 2: return ldbp_get_bwd_2(sym, fast);
+    case 3: return ldbp_get_bwd_3(sym, fast);
+    case 4: return ldbp_get_bwd_4(sym, fast);
+    case 5: return ldbp_get_bwd_5(sym, fast);
+    case 6: return ldbp_get_bwd_6(sym, fast);
+    case 7: return ldbp_get_bwd_7(sym, fast);
+  }
+  return nullptr;
+}
+
+int device_sms() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetLastError();
+  return sms > 0 ? sms : 148;
+}
+
+// ----------------------------------------------------------------------------------------
+// Planning
+// ----------------------------------------------------------------------------------------
+struct Tile {
+  int nthreads = 0;
+  int grid = 0;
+  size_t smem = 0;
+  ldbp::Geo g{};
+};
+
+size_t fwd_smem(int kh, bool sym, int steps) {
+  return sizeof(float2) * 4 * ldbp::kMaxWarps * std::max(kh, 1) +
+         sizeof(float2) * steps * ntaps_used(kh, sym) + sizeof(float) * steps + 16;
+}
+
+size_t bwd_smem(int kh, bool sym, int steps, int nthreads) {
+  const int nw = nthreads / 32;
+  const int V = 1 + 2 * ntaps_used(kh, sym);
+  size_t s = sizeof(float2) * 8 * ldbp::kMaxWarps * std::max(kh, 1);  // two edge arrays
+  s += sizeof(float2) * steps * ntaps_used(kh, sym) + sizeof(float) * steps;
+  s += sizeof(float) * ((steps * nw * V + 3) & ~3);
+  s += 16;  // alignment slack of the tape start
+  s += sizeof(float2) * size_t(steps) * kBwdR * nthreads;
+  return s;
+}
+
+// Choose the owned width and grid for a tiling with halo H, R samples per thread and at most
+// max_threads threads.  `occ_per_sm` = resident CTAs/SM at max_threads (from the occupancy API).
+Tile plan_tiles(int64_t B, int64_t n, int H, int R, int max_threads, int occ_per_sm, int sms) {
+  Tile t;
+  const int64_t ext = n + 2 * (int64_t)H;
+  const int64_t E = B * ext;
+  const int64_t cap = (int64_t)max_threads * R;
+  int64_t W0 = cap - 2 * (int64_t)H;
+  if (W0 < R) W0 = R;  // caller guarantees H <= cap/4 normally
+  const int64_t slots = (int64_t)std::max(occ_per_sm, 1) * sms;
+  int64_t tiles = cdiv(E, W0);
+  int64_t grid;
+  if (tiles >= slots) {
+    grid = cdiv(tiles, slots) * slots;  // whole waves
+  } else {
+    // small problem: spread over up to `slots` CTAs while keeping W >= max(4H, 32R)
+    const int64_t wmin = std::max<int64_t>(4 * (int64_t)H, 32 * (int64_t)R);
+    grid = std::max<int64_t>(tiles, std::min<int64_t>(slots, cdiv(E, wmin)));
+  }
+  const int64_t W = cdiv(E, grid);
+  grid = cdiv(E, W);
+  int nthr = (int)cdiv(cdiv(W + 2 * (int64_t)H, R), 32) * 32;
+  nthr = std::min(std::max(nthr, 32), max_threads);
+  t.nthreads = nthr;
+  t.grid = (int)grid;
+  t.g.B = B;
+  t.g.n = n;
+  t.g.ext = ext;
+  t.g.E = E;
+  t.g.W = W;
+  t.g.H = H;
+  t.g.big_halo = H > n ? 1 : 0;
+  return t;
+}
+
+struct FwdPlan {
+  int segs = 1;       // number of launches
+  int steps_per = 1;  // steps per launch (last may be shorter)
+};
+
+FwdPlan plan_fwd_segments(int M, int kh) {
+  FwdPlan p;
+  const int cap = env_int("LDBP_FWD_THREADS", kFwdMaxThreads) * kFwdR;
+  int cmax = kh > 0 ? std::max(1, cap / (16 * kh)) : M;
+  cmax = std::min(cmax, env_int("LDBP_FWD_MAX_STEPS", 1 << 30));
+  p.segs = (int)cdiv(M, cmax);
+  p.steps_per = (int)cdiv(M, p.segs);
+  return p;
+}
+
+struct BwdPlan {
+  int C = 1;     // steps per backward segment (last may be shorter)
+  int K = 1;     // number of segments
+  int nthreads = kBwdMaxThreads;
+  Tile tile;     // uniform geometry for all segments (H = 2*C*kh)
+  int V = 1;
+};
+
+int bwd_occupancy(BwdFn fn, int nthreads, size_t smem) {
+  int occ = 0;
+  cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, nthreads, smem) != cudaSuccess) occ = 1;
+  cudaGetLastError();
+  return std::max(occ, 1);
+}
+
+int fwd_occupancy(FwdFn fn, int nthreads, size_t smem) {
+  int occ = 0;
+  cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, nthreads, smem) != cudaSuccess) occ = 1;
+  cudaGetLastError();
+  return std::max(occ, 1);
+}
+
+BwdPlan plan_bwd(const ldbp_dims* d, bool query_device) {
+  BwdPlan p;
+  const int kh = (d->taps - 1) / 2;
+  const bool sym = d->flags & LDBP_SYMMETRIC;
+  const int M = d->steps;
+  p.nthreads = env_int("LDBP_BWD_THREADS", kBwdMaxThreads);
+  p.V = 1 + 2 * ntaps_used(kh, sym);
+  const size_t budget = (size_t)env_int("LDBP_BWD_SMEM_KB", 110) * 1024;
+  int C = 1;
+  for (int c = 1; c <= M; ++c) {
+    if (bwd_smem(kh, sym, c, p.nthreads) <= budget) C = c; else break;
+  }
+  C = std::min(C, env_int("LDBP_BWD_MAX_STEPS", 1 << 30));
+  C = std::max(C, 1);
+  p.K = (int)cdiv(M, C);
+  p.C = (int)cdiv(M, p.K);  // equalised segment lengths
+  const int H = 2 * p.C * kh;
+  int occ = 1, sms = 148;
+  if (query_device) {
+    sms = device_sms();
+    BwdFn fn = get_bwd(kh, sym, !(d->flags & LDBP_PRECISE));
+    occ = bwd_occupancy(fn, p.nthreads, bwd_smem(kh, sym, p.C, p.nthreads));
+  }
+  p.tile = plan_tiles(d->batch, d->n, H, kBwdR, p.nthreads, occ, sms);
+  return p;
+}
+
+Tile plan_fwd_tile(const ldbp_dims* d, int steps, bool query_device) {
+  const int kh = (d->taps - 1) / 2;
+  const bool sym = d->flags & LDBP_SYMMETRIC;
+  const int maxthr = env_int("LDBP_FWD_THREADS", kFwdMaxThreads);
+  int occ = 1, sms = 148;
+  const size_t smem = fwd_smem(kh, sym, steps);
+  if (query_device) {
+    sms = device_sms();
+    occ = fwd_occupancy(get_fwd(kh, sym, !(d->flags & LDBP_PRECISE)), maxthr, smem);
+  }
+  Tile t = plan_tiles(d->batch, d->n, steps * kh, kFwdR, maxthr, occ, sms);
+  t.smem = smem;
+  return t;
+}
+
+// ----------------------------------------------------------------------------------------
+// Validation
+// ----------------------------------------------------------------------------------------
+int validate_dims(const ldbp_dims* d) {
+  if (!d) return fail(LDBP_EINVAL, "dims is NULL");
+  if (d->reserved != 0) return fail(LDBP_EINVAL, "dims.reserved must be 0");
+  if (d->flags & ~(uint32_t)(LDBP_SYMMETRIC | LDBP_PRECISE)) return fail(LDBP_EINVAL, "unknown flag bits 0x%x", d->flags);
+  if (d->batch < 0) return fail(LDBP_ESHAPE, "batch %lld < 0", (long long)d->batch);
+  if (d->n < 1) return fail(LDBP_ESHAPE, "n %lld < 1", (long long)d->n);
+  if (d->steps < 1) return fail(LDBP_ESHAPE, "steps %d < 1", d->steps);
+  if (d->taps < 1 || (d->taps % 2) == 0) return fail(LDBP_ESHAPE, "taps %d must be odd and >= 1", d->taps);
+  if (d->taps > LDBP_MAX_TAPS) return fail(LDBP_ESHAPE, "taps %d > LDBP_MAX_TAPS (%d)", d->taps, LDBP_MAX_TAPS);
+  if (d->taps > d->n) return fail(LDBP_ESHAPE, "filter longer than block: taps %d > n %lld", d->taps, (long long)d->n);
+  return LDBP_OK;
+}
+
+int check_ptr(const void* p, const char* name, size_t align) {
+  if (!p) return fail(LDBP_EINVAL, "%s is NULL", name);
+  if (((uintptr_t)p) % align) return fail(LDBP_EALIGN, "%s not %zu-byte aligned", name, align);
+  return LDBP_OK;
+}
+
+#define LDBP_TRY(expr)          \
+  do {                          \
+    int _s = (expr);            \
+    if (_s != LDBP_OK) return _s; \
+  } while (0)
+
+// ----------------------------------------------------------------------------------------
+// Workspace layouts
+// ----------------------------------------------------------------------------------------
+struct FwdWs {
+  size_t pingpong = 0;  // bytes of one [B][n] buffer (only when segs >= 2)
+  size_t total = 0;
+};
+
+FwdWs fwd_ws(const ldbp_dims* d) {
+  FwdWs w;
+  const FwdPlan p = plan_fwd_segments(d->steps, (d->taps - 1) / 2);
+  if (p.segs >= 2) w.pingpong = align256(sizeof(float2) * d->batch * d->n);
+  w.total = w.pingpong;
+  return w;
+}
+
+struct BwdWs {
+  size_t ck_off = 0, ck_each = 0;   // (K-1) checkpoints
+  size_t g_off = 0, g_each = 0;     // 2 adjoint ping-pong buffers (when K >= 2)
+  size_t part_off = 0, part_bytes = 0;
+  size_t loss_off = 0, loss_bytes = 0;
+  size_t total = 0;
+};
+
+BwdWs bwd_ws(const ldbp_dims* d, const BwdPlan& p) {
+  BwdWs w;
+  const size_t blk = align256(sizeof(float2) * d->batch * d->n);
+  w.ck_off = 0;
+  w.ck_each = blk;
+  size_t off = blk * (p.K - 1);
+  w.g_off = off;
+  w.g_each = blk;
+  off += (p.K >= 2) ? 2 * blk : 0;
+  w.part_off = off;
+  w.part_bytes = align256(sizeof(double) * (size_t)p.tile.grid * d->steps * p.V);
+  off += w.part_bytes;
+  w.loss_off = off;
+  w.loss_bytes = align256(sizeof(double) * (size_t)p.tile.grid);
+  off += w.loss_bytes;
+  w.total = off;
+  return w;
+}
+
+// ----------------------------------------------------------------------------------------
+// Launch helpers
+// ----------------------------------------------------------------------------------------
+int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2* taps, const float* gamma,
+               const uint8_t* mask, int s0, int s1, cudaStream_t st) {
+  const int kh = (d->taps - 1) / 2;
+  const bool sym = d->flags & LDBP_SYMMETRIC;
+  const bool fast = !(d->flags & LDBP_PRECISE);
+  Tile t = plan_fwd_tile(d, s1 - s0, true);
+  FwdFn fn = get_fwd(kh, sym, fast);
+  ldbp::FwdArgs a;
+  a.src = src;
+  a.dst = dst;
+  a.taps = taps;
+  a.gamma = gamma;
+  a.mask = mask;
+  a.T = d->taps;
+  a.s0 = s0;
+  a.s1 = s1;
+  a.g = t.g;
+  cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
+  fn<<<t.grid, t.nthreads, t.smem, st>>>(a);
+  return cuda_check("fwd_tile_kernel launch");
+}
+
+// Full multi-launch forward from src to dst over steps [0, M) using pp as ping-pong buffer.
+int run_forward_chain(const ldbp_dims* d, const float2* x, float2* y, const float2* taps, const float* gamma,
+                      const uint8_t* mask, float2* pp, cudaStream_t st) {
+  const FwdPlan p = plan_fwd_segments(d->steps, (d->taps - 1) / 2);
+  const float2* src = x;
+  for (int k = 0; k < p.segs; ++k) {
+    const int s0 = k * p.steps_per, s1 = std::min(d->steps, s0 + p.steps_per);
+    // the last launch writes y; earlier ones alternate so that happens
+    const int remaining = p.segs - 1 - k;
+    float2* dst = (remaining % 2 == 0) ? y : pp;
+    LDBP_TRY(launch_fwd(d, src, dst, taps, gamma, mask, s0, s1, st));
+    src = dst;
+  }
+  return LDBP_OK;
+}
+
+// Backward over all segments. `gy` != nullptr: incoming gradient; else seed from target.
+int run_backward_chain(const ldbp_dims* d, const float2* x, const float2* gy, const float2* target,
+                       const float2* taps, const float* gamma, const uint8_t* mask, float2* gx,
+                       unsigned char* ws, const BwdPlan& p, const BwdWs& w, cudaStream_t st,
+                       double* buf, double* dtaps, double* dgamma) {
+  const int kh = (d->taps - 1) / 2;
+  const bool sym = d->flags & LDBP_SYMMETRIC;
+  const bool fast = !(d->flags & LDBP_PRECISE);
+  auto ck = [&](int k) -> float2* { return reinterpret_cast<float2*>(ws + w.ck_off + (size_t)(k - 1) * w.ck_each); };
+  auto gb = [&](int k) -> float2* { return reinterpret_cast<float2*>(ws + w.g_off + (size_t)(k & 1) * w.g_each); };
+  // forward checkpoint pass: ck[k] = u^(k*C), k = 1..K-1
+  for (int k = 0; k + 1 < p.K; ++k) {
+    const int s0 = k * p.C, s1 = (k + 1) * p.C;
+    LDBP_TRY(launch_fwd(d, k == 0 ? x : ck(k), ck(k + 1), taps, gamma, mask, s0, s1, st));
+  }
+  BwdFn fn = get_bwd(kh, sym, fast);
+  double* partials = reinterpret_cast<double*>(ws + w.part_off);
+  double* lossp = reinterpret_cast<double*>(ws + w.loss_off);
+  for (int k = p.K - 1; k >= 0; --k) {
+    const int s0 = k * p.C, s1 = std::min(d->steps, (k + 1) * p.C);
+    ldbp::BwdArgs a;
+    a.ck = k == 0 ? x : ck(k);
+    a.gin = (k == p.K - 1) ? gy : gb(k + 1);
+    a.target = target;
+    a.gout = (k == 0) ? gx : gb(k);
+    a.taps = taps;
+    a.gamma = gamma;
+    a.mask = mask;
+    a.partials = partials;
+    a.loss_partials = lossp;
+    a.seed_scale = 2.0f;
+    a.T = d->taps;
+    a.M = d->steps;
+    a.s0 = s0;
+    a.s1 = s1;
+    a.g = p.tile.g;
+    const size_t smem = bwd_smem(kh, sym, s1 - s0, p.tile.nthreads);
+    cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fn<<<p.tile.grid, p.tile.nthreads, smem, st>>>(a);
+    LDBP_TRY(cuda_check("bwd_segment_kernel launch"));
+  }
+  ldbp::ReduceArgs r;
+  r.partials = partials;
+  r.loss_partials = gy ? nullptr : lossp;
+  r.nblk = p.tile.grid;
+  r.M = d->steps;
+  r.T = d->taps;
+  r.V = p.V;
+  r.kh = kh;
+  r.sym = sym ? 1 : 0;
+  r.mask = mask;
+  r.buf = buf;
+  r.dtaps = dtaps;
+  r.dgamma = dgamma;
+  const int total = d->steps * p.V + 1;
+  ldbp::reduce_partials_kernel<<<(total + 255) / 256, 256, 0, st>>>(r);
+  return cuda_check("reduce_partials_kernel launch");
+}
+
+int zero_outputs(double* p, size_t count, cudaStream_t st) {
+  if (count && cudaMemsetAsync(p, 0, count * sizeof(double), st) != cudaSuccess)
+    return fail(LDBP_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(cudaGetLastError()));
+  return LDBP_OK;
+}
+
+}  // namespace
+
+// ==========================================================================================
+// Exported C ABI
+// ==========================================================================================
+extern "C" {
+
+int ldbp_abi_version(void) { return LDBP_ABI_VERSION; }
+
+const char* ldbp_status_string(int s) {
+  switch (s) {
+    case LDBP_OK: return "LDBP_OK";
+    case LDBP_EINVAL: return "LDBP_EINVAL: invalid argument";
+    case LDBP_ESHAPE: return "LDBP_ESHAPE: unsupported or inconsistent shape";
+    case LDBP_EALIGN: return "LDBP_EALIGN: misaligned pointer";
+    case LDBP_EWORKSPACE: return "LDBP_EWORKSPACE: workspace too small";
+    case LDBP_ECUDA: return "LDBP_ECUDA: CUDA runtime error";
+  }
+  return "LDBP: unknown status";
+}
+
+const char* ldbp_last_error(void) { return g_err; }
+
+int ldbp_workspace_bytes(const ldbp_dims* d, int op, size_t* bytes) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  if (!bytes) return fail(LDBP_EINVAL, "bytes is NULL");
+  if (d->batch == 0) { *bytes = 0; return LDBP_OK; }
+  switch (op) {
+    case LDBP_OP_FORWARD: *bytes = fwd_ws(d).total; return LDBP_OK;
+    case LDBP_OP_BACKWARD:
+    case LDBP_OP_LOSS_GRAD:
+    case LDBP_OP_TRAIN_STEP: {
+      BwdPlan p = plan_bwd(d, true);
+      *bytes = bwd_ws(d, p).total;
+      return LDBP_OK;
+    }
+  }
+  return fail(LDBP_EINVAL, "unknown op %d", op);
+}
+
+int ldbp_launch_count(const ldbp_dims* d, int op, int* launches) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  if (!launches) return fail(LDBP_EINVAL, "launches is NULL");
+  if (d->batch == 0) { *launches = (op == LDBP_OP_FORWARD) ? 0 : 1; return LDBP_OK; }
+  if (op == LDBP_OP_FORWARD) { *launches = plan_fwd_segments(d->steps, (d->taps - 1) / 2).segs; return LDBP_OK; }
+  BwdPlan p = plan_bwd(d, false);
+  int n = (p.K - 1) + p.K + 1;
+  if (op == LDBP_OP_TRAIN_STEP) n += 1;
+  *launches = n;
+  return LDBP_OK;
+}
+
+int ldbp_forward(const ldbp_dims* d, const void* x, void* y, const void* taps, const float* gamma,
+                 void* ws, size_t ws_bytes, void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  if (d->batch == 0) return LDBP_OK;
+  LDBP_TRY(check_ptr(x, "x", 8));
+  LDBP_TRY(check_ptr(y, "y", 8));
+  LDBP_TRY(check_ptr(taps, "taps", 8));
+  LDBP_TRY(check_ptr(gamma, "gamma", 4));
+  if (x == y) return fail(LDBP_EINVAL, "y must not alias x");
+  const FwdWs w = fwd_ws(d);
+  if (w.total > 0) {
+    if (!ws || ws_bytes < w.total) return fail(LDBP_EWORKSPACE, "forward needs %zu workspace bytes, got %zu", w.total, ws_bytes);
+    LDBP_TRY(check_ptr(ws, "ws", 8));
+  }
+  return run_forward_chain(d, (const float2*)x, (float2*)y, (const float2*)taps, gamma, nullptr, (float2*)ws,
+                           (cudaStream_t)cuda_stream);
+}
+
+int ldbp_backward(const ldbp_dims* d, const void* x, const void* gy, const void* taps, const float* gamma,
+                  double* dtaps, double* dgamma, void* gx_or_null, void* ws, size_t ws_bytes, void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  LDBP_TRY(check_ptr(dtaps, "dtaps", 8));
+  LDBP_TRY(check_ptr(dgamma, "dgamma", 8));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (d->batch == 0) {
+    LDBP_TRY(zero_outputs(dtaps, (size_t)2 * d->steps * d->taps, st));
+    return zero_outputs(dgamma, d->steps, st);
+  }
+  LDBP_TRY(check_ptr(x, "x", 8));
+  LDBP_TRY(check_ptr(gy, "gy", 8));
+  LDBP_TRY(check_ptr(taps, "taps", 8));
+  LDBP_TRY(check_ptr(gamma, "gamma", 4));
+  if (gx_or_null) LDBP_TRY(check_ptr(gx_or_null, "gx", 8));
+  if (gx_or_null == x || gx_or_null == gy) return fail(LDBP_EINVAL, "gx must not alias x or gy");
+  BwdPlan p = plan_bwd(d, true);
+  BwdWs w = bwd_ws(d, p);
+  if (!ws || ws_bytes < w.total) return fail(LDBP_EWORKSPACE, "backward needs %zu workspace bytes, got %zu", w.total, ws_bytes);
+  LDBP_TRY(check_ptr(ws, "ws", 8));
+  if (gx_or_null == nullptr && p.K == 1) { /* nothing to write besides partials */ }
+  return run_backward_chain(d, (const float2*)x, (const float2*)gy, nullptr, (const float2*)taps, gamma, nullptr,
+                            (float2*)gx_or_null, (unsigned char*)ws, p, w, st, nullptr, dtaps, dgamma);
+}
+
+int ldbp_loss_grad(const ldbp_dims* d, const void* x, const void* target, const void* taps, const float* gamma,
+                   const uint8_t* mask, double* buf, void* ws, size_t ws_bytes, void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  LDBP_TRY(check_ptr(buf, "buf", 8));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (d->batch == 0) return zero_outputs(buf, (size_t)1 + d->steps + 2 * (size_t)d->steps * d->taps, st);
+  LDBP_TRY(check_ptr(x, "x", 8));
+  LDBP_TRY(check_ptr(target, "target", 8));
+  LDBP_TRY(check_ptr(taps, "taps", 8));
+  LDBP_TRY(check_ptr(gamma, "gamma", 4));
+  BwdPlan p = plan_bwd(d, true);
+  BwdWs w = bwd_ws(d, p);
+  if (!ws || ws_bytes < w.total) return fail(LDBP_EWORKSPACE, "loss_grad needs %zu workspace bytes, got %zu", w.total, ws_bytes);
+  LDBP_TRY(check_ptr(ws, "ws", 8));
+  return run_backward_chain(d, (const float2*)x, nullptr, (const float2*)target, (const float2*)taps, gamma, mask,
+                            nullptr, (unsigned char*)ws, p, w, st, buf, nullptr, nullptr);
+}
+
+int ldbp_adam_update(const ldbp_dims* d, const double* buf, double n_global, double* master, double* m, double* v,
+                     int64_t t, double lr, double b1, double b2, double eps, const uint8_t* mask,
+                     const uint8_t* glearn, void* taps_out, float* gamma_out, void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  LDBP_TRY(check_ptr(buf, "buf", 8));
+  LDBP_TRY(check_ptr(master, "master", 8));
+  LDBP_TRY(check_ptr(m, "m", 8));
+  LDBP_TRY(check_ptr(v, "v", 8));
+  LDBP_TRY(check_ptr(taps_out, "taps_out", 8));
+  LDBP_TRY(check_ptr(gamma_out, "gamma_out", 4));
+  if (!(n_global > 0)) return fail(LDBP_EINVAL, "n_global must be > 0");
+  if (t < 1) return fail(LDBP_EINVAL, "t must be >= 1");
+  if (!(lr > 0) || !(b1 >= 0 && b1 < 1) || !(b2 >= 0 && b2 < 1) || !(eps > 0))
+    return fail(LDBP_EINVAL, "bad Adam hyper-parameters");
+  ldbp::AdamArgs a;
+  a.buf = buf;
+  a.inv_n = 1.0 / n_global;
+  a.master = master;
+  a.m = m;
+  a.v = v;
+  a.lr = lr;
+  a.b1 = b1;
+  a.b2 = b2;
+  a.eps = eps;
+  a.bc1 = 1.0 - pow(b1, (double)t);
+  a.bc2 = 1.0 - pow(b2, (double)t);
+  a.mask = mask;
+  a.glearn = glearn;
+  a.taps_out = (float2*)taps_out;
+  a.gamma_out = gamma_out;
+  a.M = d->steps;
+  a.T = d->taps;
+  const int total = 2 * d->steps * d->taps + d->steps;
+  ldbp::adam_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)cuda_stream>>>(a);
+  return cuda_check("adam_kernel launch");
+}
+
+int ldbp_train_step(const ldbp_dims* d, const void* x, const void* target, void* taps_work, float* gamma_work,
+                    double* master, double* m, double* v, int64_t t, double lr, double b1, double b2, double eps,
+                    const uint8_t* mask, const uint8_t* glearn, double* buf, void* ws, size_t ws_bytes,
+                    void* cuda_stream) {
+  LDBP_TRY(ldbp_loss_grad(d, x, target, taps_work, gamma_work, mask, buf, ws, ws_bytes, cuda_stream));
+  const double n_global = (double)d->batch * (double)d->n;
+  if (d->batch == 0) return LDBP_OK;
+  return ldbp_adam_update(d, buf, n_global, master, m, v, t, lr, b1, b2, eps, mask, glearn, taps_work, gamma_work,
+                          cuda_stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,25 @@
+// ldbp_inst.cu — explicit kernel instantiations for one half-length Kh (compiled with
+// -DLDBP_KH=<Kh>); split per Kh so the build parallelises.
+#include "ldbp_kernels.cuh"
+
+#ifndef LDBP_KH
+#error "compile with -DLDBP_KH=<0..7>"
+#endif
+
+using FwdFn = void (*)(const ldbp::FwdArgs);
+using BwdFn = void (*)(const ldbp::BwdArgs);
+
+#define LDBP_CAT2(a, b) a##b
+#define LDBP_CAT(a, b) LDBP_CAT2(a, b)
+
+FwdFn LDBP_CAT(ldbp_get_fwd_, LDBP_KH)(bool sym, bool fast) {
+  constexpr int K = LDBP_KH, R = LDBP_FWD_R;
+  if (sym) return fast ? ldbp::fwd_tile_kernel<K, R, true, true> : ldbp::fwd_tile_kernel<K, R, true, false>;
+  return fast ? ldbp::fwd_tile_kernel<K, R, false, true> : ldbp::fwd_tile_kernel<K, R, false, false>;
+}
+
+BwdFn LDBP_CAT(ldbp_get_bwd_, LDBP_KH)(bool sym, bool fast) {
+  constexpr int K = LDBP_KH, R = LDBP_BWD_R;
+  if (sym) return fast ? ldbp::bwd_segment_kernel<K, R, true, true> : ldbp::bwd_segment_kernel<K, R, true, false>;
+  return fast ? ldbp::bwd_segment_kernel<K, R, false, true> : ldbp::bwd_segment_kernel<K, R, false, false>;
+}

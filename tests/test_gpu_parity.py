@@ -1,0 +1,288 @@
+"""GPU-vs-oracle parity of the CUDA path through the C ABI (SURVEY.md §8(c) "the gate").
+
+Tolerances (BASELINE.json north_star): outputs rel-L2 <= 1e-5 per block; gradients rel-L2 <=
+1e-4 per step for taps and for gamma' separately; loss <= 1e-5; effective SNR +-0.01 dB.
+The oracle runs on the same fp32-rounded inputs in complex128.
+"""
+import numpy as np
+import pytest
+import torch
+
+import ldbp_inputs as li
+from oracle import channel, ldbp as O, physics, receiver, steps
+
+pytestmark = pytest.mark.gpu
+
+OUT_TOL = 1e-5
+GRAD_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def P():
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2010_14258_b200 as P
+
+    return P
+
+
+def dev(a, dtype=np.complex64):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a).astype(dtype))).cuda()
+
+
+def r32(a):
+    """What the GPU sees, promoted for the oracle."""
+    a = np.asarray(a)
+    if np.iscomplexobj(a):
+        return a.astype(np.complex64).astype(np.complex128)
+    return a.astype(np.float32).astype(np.float64)
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+def model(cfg, M, T, sym, scale=0.1, ls=False, sub=0):
+    if ls:
+        _, g = steps.dbp_plan(M, 80.0, 1, 0.2, 1.3)
+        xi = [steps.xi_of(80.0, physics.ps2_per_km(-21.7), 21.4e9)] * M
+        taps = np.stack([steps.ls_taps(x, T) for x in xi])
+        return taps, g
+    taps = li.random_sym_taps(cfg, M, T, scale) if sym else li.random_general_taps(cfg, M, T, scale, sub=sub)
+    gamma = li.random_gamma(cfg, M, sub=sub)
+    return taps, gamma
+
+
+FWD_CASES = [
+    # (B, n, M, T, sym, power_w)
+    (4, 1024, 4, 3, True, 1e-3),     # C1 shape
+    (3, 1000, 6, 5, True, 1e-3),     # ragged n (not a multiple of the per-thread chunk)
+    (2, 777, 3, 9, False, 1e-3),     # general (non-symmetric) taps, odd n
+    (1, 5, 2, 5, True, 1e-3),        # n == T
+    (2, 16, 10, 7, True, 1e-3),      # halo H = 30 > n: multiple wraps
+    (2, 64, 1, 1, True, 1e-3),       # T = 1 (pointwise), M = 1
+    (5, 4099, 12, 15, True, 1e-3),   # Kh = 7, several tiles, ragged tail
+    (3, 3000, 7, 13, False, 2e-3),   # Kh = 6 general
+    (1, 9000, 5, 11, True, 1e-3),
+]
+
+
+@pytest.mark.parametrize("B,n,M,T,sym,pw", FWD_CASES)
+def test_forward_parity(P, B, n, M, T, sym, pw):
+    x = li.gaussian_blocks(11, range(B), n, pw)
+    taps, gamma = model(11, M, T, sym)
+    y = P.ldbp_forward(dev(x), dev(taps), dev(gamma, np.float32), symmetric=sym).cpu().numpy()
+    ref = O.forward(r32(x), r32(taps), r32(gamma))
+    for b in range(B):
+        assert rel(y[b], ref[b]) <= OUT_TOL, (b, rel(y[b], ref[b]))
+
+
+def test_forward_precise_flag(P):
+    B, n, M, T = 3, 2500, 8, 5
+    x = li.gaussian_blocks(12, range(B), n, 2e-3)
+    taps, gamma = model(12, M, T, True)
+    ref = O.forward(r32(x), r32(taps), r32(gamma))
+    yp = P.ldbp_forward(dev(x), dev(taps), dev(gamma, np.float32), precise=True).cpu().numpy()
+    yf = P.ldbp_forward(dev(x), dev(taps), dev(gamma, np.float32)).cpu().numpy()
+    assert rel(yp, ref) <= 2e-6 and rel(yf, ref) <= OUT_TOL
+
+
+def test_forward_chained_launches(P, monkeypatch):
+    """Force several launches per forward (checkpoint-style chaining through the workspace)."""
+    B, n, M, T = 3, 1500, 10, 5
+    x = li.gaussian_blocks(13, range(B), n, 1e-3)
+    taps, gamma = model(13, M, T, True)
+    ref = O.forward(r32(x), r32(taps), r32(gamma))
+    for cmax in ("3", "4", "10"):
+        monkeypatch.setenv("LDBP_FWD_MAX_STEPS", cmax)
+        y = P.ldbp_forward(dev(x), dev(taps), dev(gamma, np.float32)).cpu().numpy()
+        assert rel(y, ref) <= OUT_TOL, cmax
+
+
+def test_delay_taps_closed_form(P):
+    """P9: h^(i) = e^{j th_i} delta_{j_i} (general path) gives
+    y_t = x_{t-S} exp(j(sum th + sum gamma' |x_{t-S}|^2)) — exercises halos and the wrap."""
+    B, n, T = 3, 4099, 7
+    shifts, th = [3, -2, 3, 1, -3], [0.3, -1.1, 2.0, 0.2, 0.9]
+    M = len(shifts)
+    taps = np.zeros((M, T), complex)
+    for i, (j, t) in enumerate(zip(shifts, th)):
+        taps[i, j + 3] = np.exp(1j * t)
+    gamma = np.array([-20.0, 15.0, -30.0, 10.0, -5.0])
+    x = li.gaussian_blocks(14, range(B), n, 2e-3)
+    y = P.ldbp_forward(dev(x), dev(taps), dev(gamma, np.float32), symmetric=False).cpu().numpy()
+    xs = np.roll(r32(x), sum(shifts), axis=-1)
+    ref = xs * np.exp(1j * (np.sum(th) + r32(gamma).sum() * np.abs(xs) ** 2))
+    assert rel(y, ref) <= 1e-6
+
+
+def test_equivariance_c2_size(P):
+    """P10 at the C2 size: f(shift_k(e^{j phi} x)) = shift_k(e^{j phi} f(x))."""
+    B, n, M, T = 256, 16384, 25, 5
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = (torch.randn(B, n, dtype=torch.complex64, device="cuda", generator=g) * np.sqrt(1e-3)).contiguous()
+    taps, gamma = model(0, M, T, True, ls=True)
+    ht, gt = dev(taps), dev(gamma, np.float32)
+    y = P.ldbp_forward(x, ht, gt)
+    k, phi = 4321, 0.7
+    rot = torch.tensor(np.exp(1j * phi), dtype=torch.complex64, device="cuda")
+    y2 = P.ldbp_forward(torch.roll(x * rot, k, dims=1).contiguous(), ht, gt)
+    ref = torch.roll(y * rot, k, dims=1)
+    err = (torch.linalg.vector_norm(y2 - ref, dim=1) / torch.linalg.vector_norm(ref, dim=1)).max().item()
+    assert err <= 1e-6
+
+
+BWD_CASES = [
+    # (B, n, M, T, sym, max_steps_env)
+    (4, 1024, 4, 3, True, None),   # C1
+    (3, 1000, 6, 5, True, "2"),    # 3 segments
+    (2, 700, 5, 7, False, "3"),    # general, 2 uneven segments
+    (2, 40, 7, 9, True, "3"),      # H > n
+    (2, 300, 3, 1, True, None),    # T = 1
+    (3, 2100, 9, 15, True, "4"),
+]
+
+
+@pytest.mark.parametrize("B,n,M,T,sym,cmax", BWD_CASES)
+def test_backward_parity(P, monkeypatch, B, n, M, T, sym, cmax):
+    if cmax:
+        monkeypatch.setenv("LDBP_BWD_MAX_STEPS", cmax)
+    x = li.gaussian_blocks(21, range(B), n, 1e-3)
+    gy = li.gaussian_blocks(21, range(B), n, 1.0, purpose="grad")
+    taps, gamma = model(21, M, T, sym)
+    dt, dg, gx = P.ldbp_backward(dev(x), dev(gy), dev(taps), dev(gamma, np.float32), symmetric=sym)
+    rdt, rdg, rgx = O.backward(r32(x), r32(gy), r32(taps), r32(gamma))
+    if sym:
+        rdt = O.sym_fold(rdt)
+    dt, dg, gx = dt.cpu().numpy(), dg.cpu().numpy(), gx.cpu().numpy()
+    for i in range(M):
+        assert rel(dt[i], rdt[i]) <= GRAD_TOL, (i, rel(dt[i], rdt[i]))
+        assert abs(dg[i] - rdg[i]) <= GRAD_TOL * abs(rdg[i]) + 1e-12 * np.abs(rdg).max(), (i, dg[i], rdg[i])
+    for b in range(B):
+        assert rel(gx[b], rgx[b]) <= OUT_TOL * 10, (b, rel(gx[b], rgx[b]))
+
+
+@pytest.mark.parametrize("sym,masked,cmax", [(True, False, None), (True, True, "2"), (False, True, None)])
+def test_loss_grad_parity(P, monkeypatch, sym, masked, cmax):
+    if cmax:
+        monkeypatch.setenv("LDBP_BWD_MAX_STEPS", cmax)
+    B, n, M, T = 4, 1536, 6, 9
+    x = li.gaussian_blocks(31, range(B), n, 1e-3)
+    tgt = li.gaussian_blocks(31, range(B), n, 1e-3, purpose="target")
+    taps, gamma = model(31, M, T, sym)
+    mask = None
+    if masked:
+        mask = np.ones((M, T), np.uint8)
+        mask[1, [0, 8]] = 0
+        mask[4, [0, 1, 7, 8]] = 0
+    buf = P.ldbp_loss_grad(dev(x), dev(tgt), dev(taps), dev(gamma, np.float32), symmetric=sym,
+                           mask=None if mask is None else torch.from_numpy(mask).cuda()).cpu().numpy()
+    ref = O.loss_grad(r32(x), r32(tgt), r32(taps), r32(gamma), mask=mask, symmetric=sym)
+    assert abs(buf[0] - ref[0]) <= OUT_TOL * ref[0]
+    assert rel(buf[1:1 + M], ref[1:1 + M]) <= GRAD_TOL
+    dt, rdt = buf[1 + M:].reshape(M, T, 2), ref[1 + M:].reshape(M, T, 2)
+    for i in range(M):
+        assert rel(dt[i], rdt[i]) <= GRAD_TOL, i
+    if masked:
+        assert np.all(dt[mask == 0] == 0)
+
+
+def test_gradient_gauge_identities_gpu(P):
+    """P6/P7 on the GPU gradients (Remark 4): exact in exact arithmetic, <= 1e-4 relative here."""
+    B, n, M, T = 8, 4096, 10, 5
+    x = li.gaussian_blocks(41, range(B), n, 2e-3)
+    tgt = li.gaussian_blocks(41, range(B), n, 2e-3, purpose="target")
+    taps, gamma = model(41, M, T, False)
+    buf = P.ldbp_loss_grad(dev(x), dev(tgt), dev(taps), dev(gamma, np.float32), symmetric=False).cpu().numpy()
+    dg = buf[1:1 + M]
+    dt = buf[1 + M:].reshape(M, T, 2)
+    dt = dt[..., 0] + 1j * dt[..., 1]
+    h = r32(taps)
+    g32 = r32(gamma)
+    ip = [np.sum(np.conj(dt[i]) * h[i]) for i in range(M)]
+    mag = max(max(abs(v) for v in ip), np.max(np.abs(2 * g32 * dg)))
+    for i in range(M - 1):
+        assert abs(ip[i + 1].real - ip[i].real + 2 * g32[i] * dg[i]) <= 1e-4 * mag
+        assert abs(ip[i].imag - ip[i + 1].imag) <= 1e-4 * mag
+
+
+def test_adam_parity_same_gradient(P):
+    """G13: GPU Adam vs oracle Adam fed the same gradient buffer (<= 1e-12 rel in fp64 master)."""
+    M, T = 5, 9
+    taps, gamma = model(51, M, T, True)
+    mask = np.ones((M, T), np.uint8)
+    mask[2, [0, 8]] = 0
+    gl = np.array([1, 1, 0, 1, 1], np.uint8)
+    st = P.TrainState.create(taps, gamma, mask=mask, gamma_learnable=gl)
+    theta = O.pack_params(taps, gamma)
+    m = np.zeros_like(theta)
+    v = np.zeros_like(theta)
+    rng = np.random.default_rng(5)
+    for t in range(1, 4):
+        buf = rng.standard_normal(1 + M + 2 * M * T) * 10.0 ** rng.uniform(-6, 2, 1 + M + 2 * M * T)
+        P.ldbp_adam_update(st, torch.from_numpy(buf).cuda(), 12345.0)
+        theta, m, v = O.adam_update(buf, 12345.0, theta, m, v, t, M, T, tap_mask=mask, gamma_learnable=gl)
+        assert rel(st.master.cpu().numpy(), theta) <= 1e-12
+        assert rel(st.m.cpu().numpy(), m) <= 1e-12 and rel(st.v.cpu().numpy(), v) <= 1e-12
+    w = st.taps.cpu().numpy()
+    th_t, th_g = O.unpack_params(theta, M, T)
+    np.testing.assert_array_equal(w, th_t.astype(np.complex64))
+    np.testing.assert_array_equal(st.gamma.cpu().numpy(), th_g.astype(np.float32))
+
+
+def test_train_step_is_loss_grad_plus_adam(P):
+    B, n, M, T = 3, 2048, 5, 5
+    x = dev(li.gaussian_blocks(61, range(B), n, 1e-3))
+    tgt = dev(li.gaussian_blocks(61, range(B), n, 1e-3, purpose="target"))
+    taps, gamma = model(61, M, T, True)
+    s1 = P.TrainState.create(taps, gamma)
+    s2 = P.TrainState.create(taps, gamma)
+    for _ in range(3):
+        b1 = P.ldbp_train_step(s1, x, tgt)
+        b2 = P.ldbp_loss_grad(x, tgt, s2.taps, s2.gamma)
+        P.ldbp_adam_update(s2, b2, B * n)
+        assert torch.equal(b1, b2)
+    assert torch.equal(s1.master, s2.master) and torch.equal(s1.taps, s2.taps)
+
+
+def test_determinism_and_shard_sum(P):
+    """Fixed-order reductions: bitwise repeatable; the data-parallel sum of per-shard buffers
+    equals the full-batch buffer (gradient is linear in the blocks; §8(e))."""
+    B, n, M, T = 8, 3000, 6, 5
+    x = li.gaussian_blocks(71, range(B), n, 1e-3)
+    tgt = li.gaussian_blocks(71, range(B), n, 1e-3, purpose="target")
+    taps, gamma = model(71, M, T, True)
+    ht, gt = dev(taps), dev(gamma, np.float32)
+    full = P.ldbp_loss_grad(dev(x), dev(tgt), ht, gt)
+    again = P.ldbp_loss_grad(dev(x), dev(tgt), ht, gt)
+    assert torch.equal(full, again)
+    parts = sum(P.ldbp_loss_grad(dev(x[s:s + 2]), dev(tgt[s:s + 2]), ht, gt).cpu().numpy() for s in range(0, B, 2))
+    assert rel(parts, full.cpu().numpy()) <= 1e-6
+
+
+def test_snr_parity_on_simulated_link(P):
+    """Effective SNR after LDBP (oracle receiver on both outputs) agrees to 0.01 dB, on seeded
+    SSFM + EDFA blocks of the C2 link (25 x 80 km, 1 StPS, LS taps) at several powers."""
+    nsym, spans, M, T = 1024, 25, 25, 5
+    link = dict(span_km=80.0, alpha_db=0.2, beta2=physics.ps2_per_km(-21.7), gamma=1.3, baud_hz=10.7e9,
+                rho_a=4, rho_d=2, nf_db=5.0, nu_hz=1.946e14)
+    deltas, gam = steps.dbp_plan(spans, 80.0, 1, 0.2, 1.3)
+    xi = steps.xi_of(80.0, physics.ps2_per_km(-21.7), 21.4e9)
+    taps = np.stack([steps.ls_taps(xi, T)] * M)
+    for pdbm in (-4.0, 0.0, 4.0, 6.0):
+        pw = float(physics.dbm_to_w(pdbm))
+        rs, ss = [], []
+        for b in range(4):
+            s = li.qam16(li.rng(2, b, "symbols", sub=int(pdbm + 10)), nsym)
+            ase = [li.cn(li.rng(2, b, "ase", sub=100 * int(pdbm + 10) + k), nsym * 4) for k in range(spans)]
+            r, _ = channel.simulate_link(s, pw, num_spans=spans, steps_per_span=8, ase_draws=ase, **link)
+            rs.append(r)
+            ss.append(s)
+        rs = np.array(rs)
+        y = P.ldbp_forward(dev(rs), dev(taps), dev(gam, np.float32)).cpu().numpy()
+        yo = O.forward(r32(rs), r32(taps), r32(gam))
+        snr_gpu = receiver.evaluate(y.astype(np.complex128), ss, [pw] * 4)
+        snr_ref = receiver.evaluate(yo, ss, [pw] * 4)
+        assert abs(snr_gpu[0] - snr_ref[0]) <= 0.01 and abs(snr_gpu[1] - snr_ref[1]) <= 0.01, (pdbm, snr_gpu, snr_ref)
+        assert snr_ref[0] > 8.0  # the equaliser is doing its job
