@@ -1,0 +1,460 @@
+#!/usr/bin/env python
+"""LDBP hot-path benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path over one batch:
+forward, waveform-MSE seed, backward, fp64 reductions, all-reduce (N > 1) and Adam — the C3
+"LDBP training step" of BASELINE.json (512 blocks x 2^14 samples, M = 50, T = 9, gamma'
+learnable) on every rank (weak scaling: per-GPU work fixed).  `value` is the whole-job
+throughput in Gsample*steps/s = (sum over ranks of B*n) * M / step time / 1e9.  The forward-only
+configurations (C2, C4) and the 2^28-sample training configuration (C5) are reported under
+"extra" on single-GPU runs.
+
+Inputs are synthetic and seeded (ldbp_inputs): band-limited circular Gaussian blocks with per-
+block launch power drawn from P = {-2,-1,0,1} dBm, LS inverse-CD taps (gain-capped) and the DBP
+gamma' schedule.  L2 is flushed (a 256 MiB write) between timed steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LDBP Gsample·steps/s fwd and fwd+bwd at 1/2/4/8 B200; % of FP32/HBM roofline"
+UNIT = "Gsample·steps/s"
+POWERS_DBM = (-2.0, -1.0, 0.0, 1.0)  # training power set of §V-A
+
+CONFIGS = {
+    # name: blocks per GPU, samples per block, spans, steps per span, taps, mode
+    "C1": dict(B=4, n=1024, spans=2, sps=2, T=3, mode="train"),
+    "C2": dict(B=256, n=16384, spans=25, sps=1, T=5, mode="fwd"),
+    "C3": dict(B=512, n=16384, spans=25, sps=2, T=9, mode="train"),
+    "C4": dict(B=4096, n=16384, spans=25, sps=4, T=15, mode="fwd"),
+    "C5": dict(B=8192, n=32768, spans=25, sps=1, T=3, mode="train"),
+}
+WORKLOAD = {
+    "C1": "Tiny LDBP fwd+bwd: 4 blocks x 1024, M=4, T=3",
+    "C2": "Long-haul LDBP inference: 256 blocks x 2^14, M=25 (1 StPS), T=5",
+    "C3": "LDBP training step: 512 blocks x 2^14, M=50 (2 StPS), T=9, gamma' learnable, MSE vs tx waveform, fwd+bwd+Adam",
+    "C4": "Unpruned-filter LDBP inference: 4096 blocks x 2^14, M=100 (4 StPS), T=15",
+    "C5": "Data-parallel LDBP training: 8192 blocks x 2^15, M=25, T=3, gamma' learnable, fwd+bwd+allreduce+Adam",
+}
+SMS = 148
+FP32_LANES_PER_SM = 128  # B200: 4 SMSPs x 32 FP32 lanes (B200_PROFILING.md / B300_MICROARCH.md)
+L2_FLUSH_BYTES = 256 << 20
+
+
+def instr_fwd(kh):
+    """Algorithmic FP32 instructions per sample-step, forward (folded FIR 6Kh+4 + Kerr 8; §8(d))."""
+    return 6 * kh + 12
+
+
+def instr_bwd(kh):
+    """Algorithmic FP32 instructions per sample-step of the reverse sweep (12Kh+18; §8(a) a6)."""
+    return 12 * kh + 18
+
+
+# ----------------------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler (B200_PROFILING.md clocks line), started before the timed region."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(gpu_index)], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self, t0, t1):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        rows = []
+        for line in open(self.path):
+            p = [c.strip() for c in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                ts = time.mktime(time.strptime(p[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+                rows.append((ts, float(p[2]), float(p[3]), p[5:9]))
+            except ValueError:
+                continue
+        inwin = [r for r in rows if t0 - 1.0 <= r[0] <= t1 + 1.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in inwin for i, v in enumerate(r[3]) if v.lower() == "active"})
+        if not inwin:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(r[1] for r in inwin), "sm_max_mhz": max(r[2] for r in inwin),
+                "reasons": reasons, "samples": len(inwin)}
+
+
+# ----------------------------------------------------------------------------------------
+# workload
+# ----------------------------------------------------------------------------------------
+def make_model(cfg):
+    import numpy as np
+
+    from paper_2010_14258_b200 import init
+
+    deltas, gamma = init.dbp_schedule(cfg["spans"], 80.0, cfg["sps"])
+    taps = init.model_taps(deltas, cfg["T"], cap=1.0)
+    return taps.astype(np.complex128), gamma
+
+
+def make_inputs(cfg, rank, seed_base=1000):
+    import ldbp_inputs as li
+
+    B, n = cfg["B"], cfg["n"]
+    blocks = range(rank * B, (rank + 1) * B)  # global block indices of this rank
+    pw = li.dbm_to_w(li.pick_powers_dbm(seed_base, blocks, POWERS_DBM))
+    x = li.bandlimited_blocks_torch(seed_base + 2 * rank, B, n, pw)
+    tgt = li.bandlimited_blocks_torch(seed_base + 2 * rank + 1, B, n, pw)
+    return x, tgt
+
+
+def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_clocks=True):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_14258_b200 as P
+    from paper_2010_14258_b200 import _lib
+    from paper_2010_14258_b200.dp import DataParallelLDBP
+
+    taps, gamma = make_model(cfg)
+    M, T = taps.shape
+    kh = (T - 1) // 2
+    B, n = cfg["B"], cfg["n"]
+    x, tgt = make_inputs(cfg, rank)
+    train = cfg["mode"] == "train"
+    st = P.TrainState.create(taps, gamma, device=dev)
+    ws = P.Workspace()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    y = torch.empty_like(x)
+    trainer = None
+    if train:
+        trainer = DataParallelLDBP(state=st, loss_grad_fn=lambda a, b: P.ldbp_loss_grad(a, b, st.taps, st.gamma, ws=ws))
+        trainer.set_local_samples(B * n)
+
+    def step(xx, tt):
+        if train:
+            return trainer.step(xx, tt)
+        return P.ldbp_forward(xx, st.taps, st.gamma, out=y, ws=ws)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        step(x, tgt)
+    torch.cuda.synchronize()
+
+    clocks = Clocks(torch.cuda.current_device()) if (want_clocks and rank == 0) else None
+    if dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.time()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(float(i))  # evict L2 between timed steps (outside the events)
+        evs[i][0].record(stream)
+        step(x, tgt)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    if dist.is_initialized():
+        dist.barrier()
+    t_wall1 = time.time()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    if dist.is_initialized():
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clk = clocks.stop(t_wall0, t_wall1) if clocks else None
+    ms_per_step = ms / steps
+    samples_global = B * n * world
+    value = samples_global * M / (ms_per_step * 1e-3) / 1e9
+
+    # per-kernel durations, live (CUDA events around each launch, same stream), separate pass
+    with P.api.trace(capacity=8192) as tr:
+        for i in range(steps):
+            flush.fill_(float(i))
+            step(x, tgt)
+        torch.cuda.synchronize()
+    per_kind = {}
+    for kind, nsteps, samples, kms in tr.records:
+        d = per_kind.setdefault(kind, {"ms": 0.0, "launches": 0, "sample_steps": 0})
+        d["ms"] += kms
+        d["launches"] += 1
+        d["sample_steps"] += samples * nsteps
+    launches_per_step = P.launch_count(P.make_dims(B, n, M, T), _lib.OP_TRAIN_STEP if train else _lib.OP_FORWARD)
+    gpu_launches = launches_per_step * steps
+
+    # e2e: pinned host inputs -> device, step, device -> host read of the result, every step
+    e2e = None
+    if want_e2e:
+        hx = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        ht = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        hx.copy_(x)
+        ht.copy_(tgt)
+        dx, dt = torch.empty_like(x), torch.empty_like(tgt)
+        res = torch.empty(1 if train else y.numel(), dtype=torch.float64 if train else torch.complex64,
+                          pin_memory=True)
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2e_steps = max(1, min(steps, 10))
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            dx.copy_(hx, non_blocking=True)
+            if train:
+                dt.copy_(ht, non_blocking=True)
+            out = step(dx, dt)
+            if train:
+                res.copy_(out[:1], non_blocking=True)
+            else:
+                res.copy_(out.view(-1), non_blocking=True)
+            stream.synchronize()  # the host reads the step's result
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / e2e_steps
+        if dist.is_initialized():
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        bi = x.numel() * 8 * (2 if train else 1)
+        bo = 8 if train else y.numel() * 8
+        e2e = {"value": samples_global * M / (e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo, "ms_per_step": e_ms}
+
+    # roofline of the dominant kernel (largest total time)
+    sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+    peak_tinst = SMS * FP32_LANES_PER_SM * sm_mhz * 1e6 / 1e12
+    peak_max = SMS * FP32_LANES_PER_SM * 1965.0 * 1e6 / 1e12
+    dom = max(per_kind.items(), key=lambda kv: kv[1]["ms"]) if per_kind else None
+    roof = None
+    kernel_shares = {}
+    tot_ms = sum(v["ms"] for v in per_kind.values()) or 1.0
+    names = {_lib.K_FORWARD: "fwd_tile_kernel", _lib.K_BACKWARD: "bwd_segment_kernel",
+             _lib.K_REDUCE: "reduce_partials_kernel", _lib.K_ADAM: "adam_kernel"}
+    for k, v in per_kind.items():
+        kernel_shares[names[k]] = {"share": v["ms"] / tot_ms, "avg_ms": v["ms"] / v["launches"],
+                                   "launches": v["launches"]}
+    if dom:
+        kind, v = dom
+        ipss = instr_fwd(kh) if kind == _lib.K_FORWARD else instr_bwd(kh)
+        avg_ms = v["ms"] / v["launches"]
+        per_launch_instr = ipss * v["sample_steps"] / v["launches"]
+        achieved = per_launch_instr / (avg_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "kernel": names[kind], "achieved": achieved, "peak": peak_tinst,
+                "unit": "Tinst/s (FP32 lane-instructions)", "frac": achieved / peak_tinst,
+                "frac_at_max_clock": achieved / peak_max, "peak_source": "derived: 148 SM x 128 FP32 lanes x "
+                f"{sm_mhz:.0f} MHz (median SM clock during the timed region)",
+                "algorithmic_instr_per_sample_step": ipss, "traffic": traffic_from_profiles(name, names[kind])}
+    # whole-step roofline: throughput vs the FP32 bound of the step's algorithmic work
+    ips = instr_fwd(kh) + (instr_bwd(kh) if train else 0)
+    bound = SMS * FP32_LANES_PER_SM * sm_mhz * 1e6 / ips / 1e9 * world
+    step_roof = {"bound_gsample_steps": bound, "frac": value / bound, "instr_per_sample_step": ips}
+    return dict(value=value, ms_per_step=ms_per_step, clk=clk, roof=roof, step_roof=step_roof, e2e=e2e,
+                gpu_launches=gpu_launches, kernel_shares=kernel_shares, samples_global=samples_global, M=M, T=T,
+                B=B, n=n, wall_s=t_wall1 - t_wall0)
+
+
+def traffic_from_profiles(cfg_name, kernel):
+    """dram bytes per launch from a committed `ncu --set full` summary, if one exists."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))
+        return d[cfg_name][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------------------
+# CPU oracle legs (cpu_baseline and --impl reference): the oracle as it stands, on host cores
+# ----------------------------------------------------------------------------------------
+def _oracle_block(args):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import numpy as np
+
+    import ldbp_inputs as li
+    from oracle import ldbp as O
+
+    cfg_name, b, taps, gamma, train = args
+    cfg = CONFIGS[cfg_name]
+    pw = li.dbm_to_w(li.pick_powers_dbm(1000, [b], POWERS_DBM))
+    x = li.bandlimited_blocks(1000, [b], cfg["n"], pw)
+    if train:
+        t = li.bandlimited_blocks(1000, [b], cfg["n"], pw, purpose="target")
+        t0 = time.perf_counter()
+        O.loss_grad(x, t, taps, gamma, symmetric=True)
+    else:
+        t0 = time.perf_counter()
+        O.forward(x, taps, gamma)
+    return time.perf_counter() - t0
+
+
+def oracle_throughput(cfg_name, target_s, cores, pool=None):
+    """Run the oracle over a bounded sample of blocks on `cores` processes; sample-steps/s."""
+    import multiprocessing as mp
+
+    import numpy as np
+
+    cfg = CONFIGS[cfg_name]
+    taps, gamma = make_model(cfg)
+    taps = taps.astype(np.complex64).astype(np.complex128)
+    gamma = gamma.astype(np.float32).astype(np.float64)
+    train = cfg["mode"] == "train"
+    t1 = _oracle_block((cfg_name, 0, taps, gamma, train))  # calibration (also warms imports)
+    nblk = int(max(1, min(cfg["B"], round(target_s * cores / max(t1, 1e-3)))))
+    own = pool is None
+    pool = pool or mp.get_context("fork").Pool(cores)
+    t0 = time.perf_counter()
+    pool.map(_oracle_block, [(cfg_name, b, taps, gamma, train) for b in range(nblk)])
+    wall = time.perf_counter() - t0
+    if own:
+        pool.close()
+        pool.join()
+    M = len(gamma)
+    return nblk * cfg["n"] * M / wall / 1e9, nblk, wall
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU oracle timed on this box's host cores (rank 0 only)."""
+    import multiprocessing as mp
+
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    pool = mp.get_context("fork").Pool(cores)
+    per_step_s = 4.0
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, nblk, wall = oracle_throughput(args.config, per_step_s, cores, pool)
+        if i >= args.warmup:
+            vals.append((v, nblk, wall))
+    pool.close()
+    pool.join()
+    value = statistics.median(v for v, _, _ in vals)
+    nblk = vals[-1][1]
+    ms = statistics.median(w for _, _, w in vals) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD[args.config], "config": args.config, "B": cfg["B"], "n": cfg["n"],
+                   "sample_blocks_per_step": nblk},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{nblk} of {cfg['B']} blocks per step (numpy fp64 oracle, process pool)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (libldbp has no CPU path)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    import __graft_entry__
+
+    if rank == 0:
+        __graft_entry__.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2010_14258_b200  # noqa: F401
+
+    main_cfg = CONFIGS[args.config]
+    r = run_config(args.config, main_cfg, args.steps, args.warmup, world, rank, dev)
+    extra = {}
+    if world == 1 and not args.no_extra:
+        for nm in ("C2", "C4", "C5", "C1"):
+            if nm == args.config:
+                continue
+            c = CONFIGS[nm]
+            k = 20 if nm in ("C2", "C1") else 10
+            rr = run_config(nm, c, k, 3, world, rank, dev, want_e2e=False, want_clocks=False)
+            extra[nm] = {"workload": WORKLOAD[nm], "mode": c["mode"], "value": rr["value"], "unit": UNIT,
+                         "ms_per_step": rr["ms_per_step"], "roofline": rr["roof"], "step_roofline": rr["step_roof"],
+                         "kernel_shares": rr["kernel_shares"]}
+            torch.cuda.empty_cache()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        v, nblk, wall = oracle_throughput(args.config, 15.0, cores)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{nblk} of {main_cfg['B']} {args.config} blocks, full fwd+bwd (numpy fp64), {wall:.1f} s "
+                         f"on a {cores}-process pool"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD[args.config], "config": args.config, "blocks_per_gpu": r["B"],
+                       "global_blocks": r["B"] * world, "n": r["n"], "steps_M": r["M"], "taps_T": r["T"],
+                       "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) between timed steps",
+                       "inputs": "band-limited circular Gaussian, P in {-2,-1,0,1} dBm, LS inverse-CD taps (cap 1)"},
+            "clocks": r["clk"], "roofline": r["roof"], "step_roofline": r["step_roof"], "cpu_baseline": cpu,
+            "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "kernel_shares": r["kernel_shares"],
+            "extra": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

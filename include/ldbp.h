@@ -151,6 +151,34 @@ int ldbp_train_step(const ldbp_dims* d, const void* x, const void* target,
                     const uint8_t* tap_mask_or_null, const uint8_t* gamma_learnable_or_null,
                     double* buf, void* ws, size_t ws_bytes, void* cuda_stream);
 
+/*
+ * Launch tracing (profiling aid; off by default; per calling thread).
+ * ldbp_trace_begin(capacity) makes every kernel launch of later calls on this thread be
+ * bracketed by two CUDA events recorded on the call's stream (events are created here, not
+ * in the hot calls' non-traced path).  ldbp_trace_end() waits for those events, writes up to
+ * `capacity` records in launch order and stops tracing.  `kind` is an ldbp_kernel_kind;
+ * `steps` the model steps the launch covers; `samples` the real (owned) samples B*n it
+ * produces; `ms` the event-timed duration.  Recording more launches than the capacity given
+ * to ldbp_trace_begin drops the excess (count reports all launches seen).
+ */
+typedef enum ldbp_kernel_kind {
+  LDBP_K_FORWARD = 1,   /* fused forward tile kernel (rows a1-a4)                 */
+  LDBP_K_BACKWARD = 2,  /* backward segment kernel (rows a5-a8, recompute + adjoint) */
+  LDBP_K_REDUCE = 3,    /* fp64 partial reduction (row a8)                         */
+  LDBP_K_ADAM = 4       /* Adam + mask (row a10)                                   */
+} ldbp_kernel_kind;
+
+typedef struct ldbp_trace_record {
+  int32_t kind;
+  int32_t steps;
+  int64_t samples;
+  float ms;
+  int32_t reserved;
+} ldbp_trace_record;
+
+int ldbp_trace_begin(int capacity);
+int ldbp_trace_end(ldbp_trace_record* out, int capacity, int* count);
+
 #ifdef __cplusplus
 }
 #endif

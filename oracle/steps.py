@@ -44,7 +44,7 @@ def xi_of(delta_km: float, beta2_s2_per_km: float, fs_hz: float) -> float:
 
 
 def ls_taps(xi: float, taps: int, n_grid: int = 512, band: float | None = None,
-            oob_weight: float = 1e-2) -> np.ndarray:
+            oob_weight: float = 1e-2, cap: float | None = None) -> np.ndarray:
     """Least-squares FIR fit of the inverse-CD response d(omega) = e^{j xi omega^2}.
 
     min_h || B h - d ||^2 with B_{i,k} = e^{-j k omega_i} (the paper's DTFT),
@@ -53,7 +53,11 @@ def ls_taps(xi: float, taps: int, n_grid: int = 512, band: float | None = None,
     f_s, e.g. 0.275 for 10% RRC at 2 sps) the out-of-band rows are down-weighted by
     ``oob_weight`` — a simplified stand-in for the constrained design of Sheikh2016, which
     the paper does not reproduce (parity unpinned for the weighted variant; full-band is
-    pinned against the closed-form truncated IDFT).  Returns complex128 [T], index j+Kh.
+    pinned against the closed-form truncated IDFT).  With ``cap`` the filter is then scaled
+    so that max_w |F(h)(w)| <= cap on a dense grid (reading G12b: a stand-in for the paper's
+    out-of-band gain constraint, with SPEC's default cap 1.0; it makes every step
+    non-expansive so short filters cannot inflate the signal power over many steps).
+    Returns complex128 [T], index j+Kh.
     """
     kh = (taps - 1) // 2
     i = np.arange(-n_grid // 2, n_grid // 2)
@@ -66,6 +70,11 @@ def ls_taps(xi: float, taps: int, n_grid: int = 512, band: float | None = None,
         B = B * wt[:, None]
         d = d * wt
     h, *_ = np.linalg.lstsq(B, d, rcond=None)
+    if cap is not None:
+        wd = np.linspace(-np.pi, np.pi, 8193)
+        gain = np.abs(np.exp(-1j * np.outer(wd, k)) @ h).max()
+        if gain > cap:
+            h = h * (cap / gain)
     return h
 
 

@@ -27,7 +27,11 @@ EXPORTED = (
     "ldbp_loss_grad",
     "ldbp_adam_update",
     "ldbp_train_step",
+    "ldbp_trace_begin",
+    "ldbp_trace_end",
 )
+
+K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM = 1, 2, 3, 4
 
 
 class LdbpDims(ctypes.Structure):
@@ -37,6 +41,16 @@ class LdbpDims(ctypes.Structure):
         ("steps", ctypes.c_int32),
         ("taps", ctypes.c_int32),
         ("flags", ctypes.c_uint32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+class TraceRecord(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("steps", ctypes.c_int32),
+        ("samples", ctypes.c_int64),
+        ("ms", ctypes.c_float),
         ("reserved", ctypes.c_int32),
     ]
 
@@ -68,6 +82,8 @@ def _load():
         "ldbp_adam_update": (ctypes.c_int, [D, P, dbl, P, P, P, ctypes.c_int64, dbl, dbl, dbl, dbl, P, P, P, P, P]),
         "ldbp_train_step": (ctypes.c_int, [D, P, P, P, P, P, P, P, ctypes.c_int64, dbl, dbl, dbl, dbl, P, P, P, P,
                                            ctypes.c_size_t, P]),
+        "ldbp_trace_begin": (ctypes.c_int, [ctypes.c_int]),
+        "ldbp_trace_end": (ctypes.c_int, [ctypes.POINTER(TraceRecord), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -215,3 +215,29 @@ def ldbp_train_step(state: TrainState, x, target, *, buf=None, ws=None, stream=N
                               _p(state.gamma_learnable), _p(out), _p(w), nb, _stream_handle(stream)),
           "ldbp_train_step")
     return out
+
+
+class trace:
+    """Context manager: per-launch CUDA-event timing of libldbp kernels on this thread.
+
+    >>> with trace() as t:
+    ...     ldbp_forward(x, taps, gamma)
+    >>> t.records  # [(kind, steps, samples, ms), ...]
+    """
+
+    def __init__(self, capacity: int = 4096):
+        self.capacity = capacity
+        self.records = []
+        self.count = 0
+
+    def __enter__(self):
+        check(lib.ldbp_trace_begin(self.capacity), "ldbp_trace_begin")
+        return self
+
+    def __exit__(self, *exc):
+        arr = (_lib.TraceRecord * self.capacity)()
+        cnt = ctypes.c_int(0)
+        check(lib.ldbp_trace_end(arr, self.capacity, ctypes.byref(cnt)), "ldbp_trace_end")
+        self.count = cnt.value
+        self.records = [(r.kind, r.steps, r.samples, r.ms) for r in arr[: min(cnt.value, self.capacity)]]
+        return False

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "ldbp.h"
 #define LDBP_AUX_KERNELS
@@ -42,6 +43,42 @@ constexpr int kFwdR = LDBP_FWD_R;
 constexpr int kBwdR = LDBP_BWD_R;
 constexpr int kFwdMaxThreads = 512;
 constexpr int kBwdMaxThreads = 256;
+
+// ---- launch tracing (thread-local; see ldbp_trace_begin in ldbp.h) ----
+struct TraceRec {
+  int kind, steps;
+  int64_t samples;
+  cudaEvent_t a, b;
+};
+thread_local bool g_trace_on = false;
+thread_local int g_trace_cap = 0;
+thread_local int g_trace_seen = 0;
+thread_local std::vector<TraceRec> g_trace;
+
+struct TraceScope {
+  TraceRec rec{};
+  bool active = false;
+  cudaStream_t st;
+  TraceScope(int kind, int steps, int64_t samples, cudaStream_t s) : st(s) {
+    if (!g_trace_on) return;
+    ++g_trace_seen;
+    if ((int)g_trace.size() >= g_trace_cap) return;
+    rec.kind = kind;
+    rec.steps = steps;
+    rec.samples = samples;
+    if (cudaEventCreate(&rec.a) != cudaSuccess || cudaEventCreate(&rec.b) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    cudaEventRecord(rec.a, st);
+    active = true;
+  }
+  ~TraceScope() {
+    if (!active) return;
+    cudaEventRecord(rec.b, st);
+    g_trace.push_back(rec);
+  }
+};
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -125,10 +162,10 @@ size_t bwd_smem(int kh, bool sym, int steps, int nthreads) {
   const int nw = nthreads / 32;
   const int V = 1 + 2 * ntaps_used(kh, sym);
   size_t s = sizeof(float2) * 8 * ldbp::kMaxWarps * std::max(kh, 1);  // two edge arrays
-  s += sizeof(float2) * steps * ntaps_used(kh, sym) + sizeof(float) * steps;
-  s += sizeof(float) * ((steps * nw * V + 3) & ~3);
-  s += 16;  // alignment slack of the tape start
-  s += sizeof(float2) * size_t(steps) * kBwdR * nthreads;
+  s += sizeof(float2) * ((steps * ntaps_used(kh, sym) + 1) & ~1);       // taps (16-B rounded)
+  s += sizeof(float) * ((steps + 3) & ~3);                              // gamma
+  s += sizeof(float) * ((steps * nw * V + 3) & ~3);                     // per-warp partials
+  s += sizeof(float2) * size_t(steps) * kBwdR * nthreads;               // tape
   return s;
 }
 
@@ -292,11 +329,16 @@ FwdWs fwd_ws(const ldbp_dims* d) {
   return w;
 }
 
+constexpr int kReduceChunk = 512;  // CTAs per first-level reduction block
+
+inline int reduce_chunks(int nblk) { return nblk > 2 * kReduceChunk ? (int)cdiv(nblk, kReduceChunk) : 0; }
+
 struct BwdWs {
   size_t ck_off = 0, ck_each = 0;   // (K-1) checkpoints
   size_t g_off = 0, g_each = 0;     // 2 adjoint ping-pong buffers (when K >= 2)
   size_t part_off = 0, part_bytes = 0;
   size_t loss_off = 0, loss_bytes = 0;
+  size_t part2_off = 0, loss2_off = 0;  // first-level reduction outputs (many CTAs)
   size_t total = 0;
 };
 
@@ -315,6 +357,11 @@ BwdWs bwd_ws(const ldbp_dims* d, const BwdPlan& p) {
   w.loss_off = off;
   w.loss_bytes = align256(sizeof(double) * (size_t)p.tile.grid);
   off += w.loss_bytes;
+  const int nch = reduce_chunks(p.tile.grid);
+  w.part2_off = off;
+  off += align256(sizeof(double) * (size_t)nch * d->steps * p.V);
+  w.loss2_off = off;
+  off += align256(sizeof(double) * (size_t)nch);
   w.total = off;
   return w;
 }
@@ -340,7 +387,10 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   a.s1 = s1;
   a.g = t.g;
   cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
-  fn<<<t.grid, t.nthreads, t.smem, st>>>(a);
+  {
+    TraceScope ts(LDBP_K_FORWARD, s1 - s0, d->batch * d->n, st);
+    fn<<<t.grid, t.nthreads, t.smem, st>>>(a);
+  }
   return cuda_check("fwd_tile_kernel launch");
 }
 
@@ -398,13 +448,35 @@ int run_backward_chain(const ldbp_dims* d, const float2* x, const float2* gy, co
     a.g = p.tile.g;
     const size_t smem = bwd_smem(kh, sym, s1 - s0, p.tile.nthreads);
     cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    fn<<<p.tile.grid, p.tile.nthreads, smem, st>>>(a);
+    {
+      TraceScope ts(LDBP_K_BACKWARD, s1 - s0, d->batch * d->n, st);
+      fn<<<p.tile.grid, p.tile.nthreads, smem, st>>>(a);
+    }
     LDBP_TRY(cuda_check("bwd_segment_kernel launch"));
   }
   ldbp::ReduceArgs r;
   r.partials = partials;
   r.loss_partials = gy ? nullptr : lossp;
   r.nblk = p.tile.grid;
+  const int nch = reduce_chunks(p.tile.grid);
+  if (nch > 0) {
+    ldbp::Reduce1Args r1;
+    r1.partials = partials;
+    r1.loss_partials = r.loss_partials;
+    r1.nblk = p.tile.grid;
+    r1.total = d->steps * p.V;
+    r1.chunk = kReduceChunk;
+    r1.out = reinterpret_cast<double*>(ws + w.part2_off);
+    r1.loss_out = reinterpret_cast<double*>(ws + w.loss2_off);
+    {
+      TraceScope ts(LDBP_K_REDUCE, d->steps, 0, st);
+      ldbp::reduce_partials_pass1<<<dim3((r1.total + 31) / 32 + 1, nch), 256, 0, st>>>(r1);
+    }
+    LDBP_TRY(cuda_check("reduce_partials_pass1 launch"));
+    r.partials = r1.out;
+    r.loss_partials = r.loss_partials ? r1.loss_out : nullptr;
+    r.nblk = nch;
+  }
   r.M = d->steps;
   r.T = d->taps;
   r.V = p.V;
@@ -414,8 +486,11 @@ int run_backward_chain(const ldbp_dims* d, const float2* x, const float2* gy, co
   r.buf = buf;
   r.dtaps = dtaps;
   r.dgamma = dgamma;
-  const int total = d->steps * p.V + 1;
-  ldbp::reduce_partials_kernel<<<(total + 255) / 256, 256, 0, st>>>(r);
+  const int nblocks = (d->steps * p.V + 31) / 32 + 1;
+  {
+    TraceScope ts(LDBP_K_REDUCE, d->steps, 0, st);
+    ldbp::reduce_partials_kernel<<<nblocks, 256, 0, st>>>(r);
+  }
   return cuda_check("reduce_partials_kernel launch");
 }
 
@@ -472,8 +547,8 @@ int ldbp_launch_count(const ldbp_dims* d, int op, int* launches) {
   if (!launches) return fail(LDBP_EINVAL, "launches is NULL");
   if (d->batch == 0) { *launches = (op == LDBP_OP_FORWARD) ? 0 : 1; return LDBP_OK; }
   if (op == LDBP_OP_FORWARD) { *launches = plan_fwd_segments(d->steps, (d->taps - 1) / 2).segs; return LDBP_OK; }
-  BwdPlan p = plan_bwd(d, false);
-  int n = (p.K - 1) + p.K + 1;
+  BwdPlan p = plan_bwd(d, true);
+  int n = (p.K - 1) + p.K + 1 + (reduce_chunks(p.tile.grid) > 0 ? 1 : 0);
   if (op == LDBP_OP_TRAIN_STEP) n += 1;
   *launches = n;
   return LDBP_OK;
@@ -577,7 +652,10 @@ int ldbp_adam_update(const ldbp_dims* d, const double* buf, double n_global, dou
   a.M = d->steps;
   a.T = d->taps;
   const int total = 2 * d->steps * d->taps + d->steps;
-  ldbp::adam_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)cuda_stream>>>(a);
+  {
+    TraceScope ts(LDBP_K_ADAM, d->steps, 0, (cudaStream_t)cuda_stream);
+    ldbp::adam_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)cuda_stream>>>(a);
+  }
   return cuda_check("adam_kernel launch");
 }
 
@@ -590,6 +668,47 @@ int ldbp_train_step(const ldbp_dims* d, const void* x, const void* target, void*
   if (d->batch == 0) return LDBP_OK;
   return ldbp_adam_update(d, buf, n_global, master, m, v, t, lr, b1, b2, eps, mask, glearn, taps_work, gamma_work,
                           cuda_stream);
+}
+
+int ldbp_trace_begin(int capacity) {
+  g_err[0] = 0;
+  if (capacity < 0) return fail(LDBP_EINVAL, "capacity < 0");
+  for (auto& r : g_trace) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_trace.clear();
+  g_trace.reserve(capacity);
+  g_trace_cap = capacity;
+  g_trace_seen = 0;
+  g_trace_on = true;
+  return LDBP_OK;
+}
+
+int ldbp_trace_end(ldbp_trace_record* out, int capacity, int* count) {
+  g_err[0] = 0;
+  g_trace_on = false;
+  int status = LDBP_OK;
+  int n = 0;
+  for (auto& r : g_trace) {
+    float ms = -1.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) {
+      status = fail(LDBP_ECUDA, "trace event: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    if (out && n < capacity) {
+      out[n].kind = r.kind;
+      out[n].steps = r.steps;
+      out[n].samples = r.samples;
+      out[n].ms = ms;
+      out[n].reserved = 0;
+    }
+    ++n;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_trace.clear();
+  if (count) *count = g_trace_seen;
+  return status;
 }
 
 }  // extern "C"

@@ -63,37 +63,71 @@ __device__ __forceinline__ int64_t thread_e0(const Geo& g, int R) {
   return (int64_t)blockIdx.x * g.W - g.H + (int64_t)threadIdx.x * R;
 }
 
+// Per-thread view of its R consecutive extended samples [e0, e0+R): block b0 and extended
+// position q0 of the first one.  When ext >= R (the normal case) the R samples touch at most
+// blocks b0 and b0+1, so every per-sample index below is 32-bit arithmetic on q0 + k.
+struct Span {
+  int64_t b0;   // block of sample 0 (-1 when e0 < 0)
+  int q0;       // extended position of sample 0, in [0, ext)
+};
+
+__device__ __forceinline__ Span make_span(int64_t e0, const Geo& g) {
+  Span sp;
+  sp.b0 = e0 >= 0 ? e0 / g.ext : -1;
+  sp.q0 = (int)(e0 - sp.b0 * g.ext);
+  return sp;
+}
+
+// Sample k of the span -> (block, sample position in [0,n)); returns false if outside [0, B).
+// `small` = (ext < R): the span may cross several blocks (tiny n): fall back to division.
+template <int R>
+__device__ __forceinline__ bool span_at(const Span& sp, int k, const Geo& g, int64_t e0, int64_t* b, int64_t* pos,
+                                        int* q_out) {
+  int64_t bb;
+  int q;
+  if (g.ext >= R) {
+    q = sp.q0 + k;
+    bb = sp.b0;
+    if (q >= g.ext) { q -= (int)g.ext; ++bb; }
+  } else {
+    const int64_t e = e0 + k;
+    bb = e >= 0 ? e / g.ext : -1;
+    q = (int)(e - bb * g.ext);
+  }
+  *b = bb;
+  *q_out = q;
+  *pos = wrap_pos((int64_t)q - g.H, g);
+  return bb >= 0 && bb < g.B && e0 + k >= 0;
+}
+
 // Load R consecutive extended samples starting at e0 (zeros outside [0, E)).
 template <int R>
 __device__ __forceinline__ void load_window(const float2* __restrict__ src, int64_t e0, const Geo& g,
                                             float2 (&u)[R]) {
-  int64_t b = e0 >= 0 ? e0 / g.ext : -1;
-  int64_t q = e0 - b * g.ext;  // in [0, ext) (also for e0 < 0 with b = -1 when e0 >= -ext)
+  const Span sp = make_span(e0, g);
 #pragma unroll
   for (int k = 0; k < R; ++k) {
-    const bool ok = (b >= 0) && (b < g.B) && (e0 + k >= 0);
-    float2 v = make_float2(0.f, 0.f);
-    if (ok) v = __ldg(src + b * g.n + wrap_pos(q - g.H, g));
-    u[k] = v;
-    if (++q == g.ext) { q = 0; ++b; }
+    int64_t b, pos;
+    int q;
+    const bool ok = span_at<R>(sp, k, g, e0, &b, &pos, &q);
+    u[k] = ok ? __ldg(src + b * g.n + pos) : make_float2(0.f, 0.f);
   }
 }
 
 // Bitmask of which of this thread's R samples are owned real samples of this CTA.
 template <int R>
-__device__ __forceinline__ uint32_t owned_mask(int64_t e0, const Geo& g, int64_t* b_out, int64_t* q_out) {
+__device__ __forceinline__ uint32_t owned_mask(int64_t e0, const Geo& g) {
   const int64_t lo = (int64_t)blockIdx.x * g.W;
   const int64_t hi = min(lo + g.W, g.E);
-  int64_t b = e0 >= 0 ? e0 / g.ext : -1;
-  int64_t q = e0 - b * g.ext;
-  *b_out = b;
-  *q_out = q;
+  const Span sp = make_span(e0, g);
   uint32_t m = 0;
 #pragma unroll
   for (int k = 0; k < R; ++k) {
+    int64_t b, pos;
+    int q;
+    span_at<R>(sp, k, g, e0, &b, &pos, &q);
     const int64_t e = e0 + k;
     if (e >= lo && e < hi && q >= g.H && q < g.H + g.n) m |= (1u << k);
-    if (++q == g.ext) { q = 0; ++b; }
   }
   return m;
 }
@@ -101,12 +135,14 @@ __device__ __forceinline__ uint32_t owned_mask(int64_t e0, const Geo& g, int64_t
 template <int R>
 __device__ __forceinline__ void store_owned(float2* __restrict__ dst, int64_t e0, const Geo& g,
                                             const float2 (&u)[R]) {
-  int64_t b, q;
-  const uint32_t m = owned_mask<R>(e0, g, &b, &q);
+  const uint32_t m = owned_mask<R>(e0, g);
+  const Span sp = make_span(e0, g);
 #pragma unroll
   for (int k = 0; k < R; ++k) {
-    if (m & (1u << k)) dst[b * g.n + (q - g.H)] = u[k];
-    if (++q == g.ext) { q = 0; ++b; }
+    int64_t b, pos;
+    int q;
+    span_at<R>(sp, k, g, e0, &b, &pos, &q);
+    if (m & (1u << k)) dst[b * g.n + pos] = u[k];
   }
 }
 
@@ -146,6 +182,77 @@ __device__ __forceinline__ void exchange(const float2 (&u)[R], float2 (&hl)[KH >
   } else {
     (void)u; (void)hl; (void)hr; (void)sh; (void)buf; (void)lane; (void)warp; (void)nwarps;
   }
+}
+
+// Two arrays exchanged around one barrier (backward reverse sweep).
+template <int KH, int R>
+__device__ __forceinline__ void exchange2(const float2 (&u)[R], float2 (&hl)[KH > 0 ? KH : 1],
+                                          float2 (&hr)[KH > 0 ? KH : 1], float2* sh, int buf,
+                                          const float2 (&v)[R], float2 (&gl)[KH > 0 ? KH : 1],
+                                          float2 (&gr)[KH > 0 ? KH : 1], float2* sh2, int buf2,
+                                          int lane, int warp, int nwarps) {
+  if constexpr (KH > 0) {
+#pragma unroll
+    for (int j = 0; j < KH; ++j) {
+      hl[j].x = __shfl_up_sync(kFull, u[R - KH + j].x, 1);
+      hl[j].y = __shfl_up_sync(kFull, u[R - KH + j].y, 1);
+      hr[j].x = __shfl_down_sync(kFull, u[j].x, 1);
+      hr[j].y = __shfl_down_sync(kFull, u[j].y, 1);
+      gl[j].x = __shfl_up_sync(kFull, v[R - KH + j].x, 1);
+      gl[j].y = __shfl_up_sync(kFull, v[R - KH + j].y, 1);
+      gr[j].x = __shfl_down_sync(kFull, v[j].x, 1);
+      gr[j].y = __shfl_down_sync(kFull, v[j].y, 1);
+    }
+    float2* head = sh + ((buf * 2 + 0) * kMaxWarps) * KH;
+    float2* tail = sh + ((buf * 2 + 1) * kMaxWarps) * KH;
+    float2* head2 = sh2 + ((buf2 * 2 + 0) * kMaxWarps) * KH;
+    float2* tail2 = sh2 + ((buf2 * 2 + 1) * kMaxWarps) * KH;
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < KH; ++j) { head[warp * KH + j] = u[j]; head2[warp * KH + j] = v[j]; }
+    }
+    if (lane == 31) {
+#pragma unroll
+      for (int j = 0; j < KH; ++j) { tail[warp * KH + j] = u[R - KH + j]; tail2[warp * KH + j] = v[R - KH + j]; }
+    }
+    __syncthreads();
+    if (lane == 0 && warp > 0) {
+#pragma unroll
+      for (int j = 0; j < KH; ++j) { hl[j] = tail[(warp - 1) * KH + j]; gl[j] = tail2[(warp - 1) * KH + j]; }
+    }
+    if (lane == 31 && warp < nwarps - 1) {
+#pragma unroll
+      for (int j = 0; j < KH; ++j) { hr[j] = head[(warp + 1) * KH + j]; gr[j] = head2[(warp + 1) * KH + j]; }
+    }
+  } else {
+    (void)u; (void)hl; (void)hr; (void)sh; (void)buf; (void)v; (void)gl; (void)gr; (void)sh2; (void)buf2;
+    (void)lane; (void)warp; (void)nwarps;
+  }
+}
+
+// Warp reduce-scatter of N values (N a power of two, 2 <= N <= 32) by a transposing butterfly:
+// at each level a lane keeps half of its vector and adds the partner's copy of that half, so
+// only N-1 shuffles are needed (vs 5N for N separate reductions).  Afterwards lane l holds the
+// full warp sum of value index (l >> (5 - log2 N)) ... for N = 16: index l >> 1, replicated in
+// the lane pair (l, l^1) after the final xor-1 add.  Returns that lane's sum.
+template <int N>
+__device__ __forceinline__ float warp_reduce_scatter(float (&v)[N], int lane) {
+  static_assert(N >= 2 && N <= 32 && (N & (N - 1)) == 0, "N must be a power of two in [2, 32]");
+#pragma unroll
+  for (int L = N, o = 16; L > 1; L >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < L / 2; ++i) {
+      const float send = up ? v[i] : v[i + L / 2];
+      const float keep = up ? v[i + L / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(kFull, send, o);
+    }
+  }
+  // remaining lanes that share an index: levels o < 32/N
+  float r = v[0];
+#pragma unroll
+  for (int o = 16 / N; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
+  return r;
 }
 
 // Window accessor: index i in [-KH, R+KH).
@@ -243,7 +350,7 @@ struct FwdArgs {
 // Forward tile kernel: steps [s0, s1) of Eq. (7) for one tile, all on chip (rows a0-a4).
 // ---------------------------------------------------------------------------------------
 template <int KH, int R, bool SYM, bool FAST>
-__global__ void __launch_bounds__(512) fwd_tile_kernel(const FwdArgs a) {
+__global__ void __launch_bounds__(512, 2) fwd_tile_kernel(const FwdArgs a) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* sh_edge = reinterpret_cast<float2*>(smem_raw);                 // 2*2*32*KH
@@ -310,11 +417,12 @@ __global__ void __launch_bounds__(256) bwd_segment_kernel(const BwdArgs a) {
   const int nthr = blockDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = nthr >> 5;
 
+  // carve-up (every region 16-byte aligned; mirrored by bwd_smem() on the host)
   float2* sh_edge = reinterpret_cast<float2*>(smem_raw);  // two arrays: 2 * (2*2*32*KH)
   float2* sh_edge2 = sh_edge + 4 * kMaxWarps * (KH > 0 ? KH : 1);
   float2* sh_taps = sh_edge2 + 4 * kMaxWarps * (KH > 0 ? KH : 1);
-  float* sh_gamma = reinterpret_cast<float*>(sh_taps + C * NTU);
-  float* sh_red = sh_gamma + C;                               // [C][nwarps][V]
+  float* sh_gamma = reinterpret_cast<float*>(sh_taps + ((C * NTU + 1) & ~1));
+  float* sh_red = sh_gamma + ((C + 3) & ~3);                  // [C][nwarps][V]
   float2* tape = reinterpret_cast<float2*>(sh_red + ((C * nwarps * V + 3) & ~3));  // [C][R][nthr]
 
   stage_params<KH, SYM>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, sh_gamma);
@@ -322,8 +430,7 @@ __global__ void __launch_bounds__(256) bwd_segment_kernel(const BwdArgs a) {
   float2 u[R];
   const int64_t e0 = thread_e0(a.g, R);
   load_window<R>(a.ck, e0, a.g, u);
-  int64_t b0, q0;
-  const uint32_t own = owned_mask<R>(e0, a.g, &b0, &q0);
+  const uint32_t own = owned_mask<R>(e0, a.g);
   __syncthreads();
 
   float2 hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1];
@@ -394,8 +501,7 @@ __global__ void __launch_bounds__(256) bwd_segment_kernel(const BwdArgs a) {
     for (int k = 0; k < R; ++k) u[k] = tape[(l * R + k) * nthr + threadIdx.x];
     // exchange halos of u and ga (one barrier each).  The u buffers continue the forward
     // loop's parity sequence (the last forward exchange used (C-1)&1), hence (l+1)&1.
-    exchange<KH, R>(u, hl, hr, sh_edge, (l + 1) & 1, lane, warp, nwarps);
-    exchange<KH, R>(ga, gl, gr, sh_edge2, l & 1, lane, warp, nwarps);
+    exchange2<KH, R>(u, hl, hr, sh_edge, (l + 1) & 1, ga, gl, gr, sh_edge2, l & 1, lane, warp, nwarps);
     // tap gradients over owned samples: dh_j += ga_t conj(u_{t-j})
     float2 dh[NTU];
 #pragma unroll
@@ -459,15 +565,20 @@ __global__ void __launch_bounds__(256) bwd_segment_kernel(const BwdArgs a) {
       }
       g[k] = acc;
     }
-    // per-warp reduction of this step's partials
-    float* red = sh_red + (l * nwarps + warp) * V;
-    dgam = warp_sum<R>(dgam);
-    if (lane == 0) red[0] = dgam;
+    // per-warp reduction of this step's partials (transposing butterfly, see above)
+    {
+      constexpr int VP = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
+      float vals[VP];
+      vals[0] = dgam;
 #pragma unroll
-    for (int j = 0; j < NTU; ++j) {
-      const float rx = warp_sum<R>(dh[j].x);
-      const float ry = warp_sum<R>(dh[j].y);
-      if (lane == 0) { red[1 + 2 * j] = rx; red[2 + 2 * j] = ry; }
+      for (int j = 0; j < NTU; ++j) { vals[1 + 2 * j] = dh[j].x; vals[2 + 2 * j] = dh[j].y; }
+#pragma unroll
+      for (int i = V; i < VP; ++i) vals[i] = 0.f;
+      const float r = warp_reduce_scatter<VP>(vals, lane);
+      constexpr int SH = VP == 2 ? 4 : VP == 4 ? 3 : VP == 8 ? 2 : VP == 16 ? 1 : 0;  // lanes per index = 32/VP
+      const int idx = lane >> SH;
+      float* red = sh_red + (l * nwarps + warp) * V;
+      if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
     }
   }
   if (a.gout) store_owned<R>(a.gout, e0, a.g, g);
@@ -496,38 +607,103 @@ struct ReduceArgs {
   double* dgamma;  // mode 1: [M]
 };
 
-__global__ void reduce_partials_kernel(const ReduceArgs a) {
-  const int total = a.M * a.V;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total + 1; i += gridDim.x * blockDim.x) {
-    if (i == total) {
-      if (a.buf) {
-        double s = 0.0;
-        if (a.loss_partials)
-          for (int c = 0; c < a.nblk; ++c) s += a.loss_partials[c];
-        a.buf[0] = s;
-      }
-      continue;
-    }
+// First level of the two-level reduction (used when there are many CTAs): grid
+// (ceil(total/32) + 1, nchunks); block (x, y) sums CTAs [y*chunk, (y+1)*chunk) for outputs
+// x*32 + lane (the extra x column does the loss partials) into out[y][...] in fixed order.
+struct Reduce1Args {
+  const double* partials;       // [nblk][total]
+  const double* loss_partials;  // [nblk] or null
+  int nblk, total, chunk;
+  double* out;                  // [nchunks][total]
+  double* loss_out;             // [nchunks]
+};
+
+__global__ void __launch_bounds__(256) reduce_partials_pass1(const Reduce1Args a) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nout_blocks = (a.total + 31) / 32;
+  const int c0 = blockIdx.y * a.chunk, c1 = min(c0 + a.chunk, a.nblk);
+  if ((int)blockIdx.x == nout_blocks) {
     double s = 0.0;
-    for (int c = 0; c < a.nblk; ++c) s += a.partials[(int64_t)c * total + i];
-    const int st = i / a.V, v = i % a.V;
-    double* dg = a.buf ? a.buf + 1 : a.dgamma;
-    double* dt = a.buf ? a.buf + 1 + a.M : a.dtaps;
-    if (v == 0) {
-      dg[st] = s;
+    if (a.loss_partials)
+      for (int c = c0 + threadIdx.x; c < c1; c += 256) s += a.loss_partials[c];
+    red[warp][lane] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w)
+        for (int l = 0; l < 32; ++l) t += red[w][l];
+      a.loss_out[blockIdx.y] = t;
+    }
+    return;
+  }
+  const int i = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (i < a.total) {
+    const double* p = a.partials + i;
+#pragma unroll 4
+    for (int c = c0 + warp; c < c1; c += 8) s += p[(int64_t)c * a.total];
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp != 0 || i >= a.total) return;
+  s = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s += red[w][lane];
+  a.out[(int64_t)blockIdx.y * a.total + i] = s;
+}
+
+// Launch with 256 threads and ceil(M*V/32) + 1 blocks.  Block k < last: lane = output
+// (coalesced 256-B rows), warp w sums CTAs c = w, w+8, ... in order, then warp 0 adds the 8
+// warp sums in order.  The last block reduces the loss partials the same way.  Fixed order
+// everywhere -> bitwise deterministic.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const ReduceArgs a) {
+  __shared__ double red[8][33];
+  const int total = a.M * a.V;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nout_blocks = (total + 31) / 32;
+  if ((int)blockIdx.x == nout_blocks) {  // loss
+    if (!a.buf) return;
+    double s = 0.0;
+    if (a.loss_partials)
+      for (int c = threadIdx.x; c < a.nblk; c += 256) s += a.loss_partials[c];
+    red[warp][lane] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w)
+        for (int l = 0; l < 32; ++l) t += red[w][l];
+      a.buf[0] = t;
+    }
+    return;
+  }
+  const int i = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (i < total) {
+    const double* p = a.partials + i;
+#pragma unroll 4
+    for (int c = warp; c < a.nblk; c += 8) s += p[(int64_t)c * total];
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp != 0 || i >= total) return;
+  s = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s += red[w][lane];
+  const int st = i / a.V, v = i % a.V;
+  double* dg = a.buf ? a.buf + 1 : a.dgamma;
+  double* dt = a.buf ? a.buf + 1 + a.M : a.dtaps;
+  if (v == 0) {
+    dg[st] = s;
+  } else {
+    const int ti = (v - 1) / 2, comp = (v - 1) % 2;
+    if (a.sym) {
+      // folded index ti = j >= 0 -> positions kh +- j
+      const int p1 = a.kh + ti, p2 = a.kh - ti;
+      dt[((int64_t)st * a.T + p1) * 2 + comp] = (a.mask && !a.mask[st * a.T + p1]) ? 0.0 : s;
+      dt[((int64_t)st * a.T + p2) * 2 + comp] = (a.mask && !a.mask[st * a.T + p2]) ? 0.0 : s;
     } else {
-      const int ti = (v - 1) / 2, comp = (v - 1) % 2;
-      if (a.sym) {
-        // folded index ti = j >= 0 -> positions kh +- j
-        const int p1 = a.kh + ti, p2 = a.kh - ti;
-        const double m1 = (a.mask && !a.mask[st * a.T + p1]) ? 0.0 : s;
-        const double m2 = (a.mask && !a.mask[st * a.T + p2]) ? 0.0 : s;
-        dt[((int64_t)st * a.T + p1) * 2 + comp] = m1;
-        dt[((int64_t)st * a.T + p2) * 2 + comp] = m2;
-      } else {
-        const double m1 = (a.mask && !a.mask[st * a.T + ti]) ? 0.0 : s;
-        dt[((int64_t)st * a.T + ti) * 2 + comp] = m1;
-      }
+      dt[((int64_t)st * a.T + ti) * 2 + comp] = (a.mask && !a.mask[st * a.T + ti]) ? 0.0 : s;
     }
   }
 }

@@ -44,15 +44,23 @@ def dbp_schedule(num_spans: int, span_km: float, steps_per_span: int, alpha_db_p
 
 
 def inverse_cd_taps(delta_km: float, taps: int, beta2_ps2_per_km: float = -21.7, fs_hz: float = 21.4e9,
-                    grid: int = 512) -> np.ndarray:
-    """Symmetric complex taps h_{-K..K} (index j+K) fitting e^{j xi w^2}, xi = -beta2 delta f_s^2 / 2."""
+                    grid: int = 512, cap: float | None = 1.0) -> np.ndarray:
+    """Symmetric complex taps h_{-K..K} (index j+K) fitting e^{j xi w^2}, xi = -beta2 delta f_s^2 / 2.
+
+    With ``cap`` (default 1.0) the fit is scaled so that its gain never exceeds ``cap`` at any
+    frequency (a non-expansive stand-in for the out-of-band gain constraint of P:905-907)."""
     xi = -(beta2_ps2_per_km * 1e-24) * delta_km * fs_hz ** 2 / 2.0
     K = (taps - 1) // 2
     w = 2.0 * np.pi * (np.arange(grid) - grid // 2) / grid
     resp = np.exp(1j * xi * w * w)
     # centred inverse DTFT: h_k = (1/N) sum_i d(w_i) e^{j k w_i}; d is even so h_k = h_{-k}
     ks = np.arange(-K, K + 1)
-    return (resp[None, :] * np.exp(1j * ks[:, None] * w[None, :])).mean(axis=1)
+    h = (resp[None, :] * np.exp(1j * ks[:, None] * w[None, :])).mean(axis=1)
+    if cap is not None:
+        dense = np.linspace(-np.pi, np.pi, 8193)
+        peak = float(np.max(np.abs(np.exp(-1j * dense[:, None] * ks[None, :]) @ h)))
+        h = h * min(1.0, cap / peak)
+    return h
 
 
 def model_taps(deltas_km, taps: int, **kw) -> np.ndarray:

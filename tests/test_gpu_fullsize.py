@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 import torch
 
+import ldbp_inputs as li
 from oracle import ldbp as O, physics, steps
 
 pytestmark = pytest.mark.gpu
@@ -24,14 +25,18 @@ def rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-def gauss(B, n, seed, pw=1e-3):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    return (torch.randn(B, n, dtype=torch.complex64, device="cuda", generator=g) * np.sqrt(pw)).contiguous()
+POWERS_DBM = (-2.0, -1.0, 0.0, 1.0)  # training set P of §V-A
+
+
+def gauss(B, n, seed):
+    """Band-limited circular Gaussian blocks at per-block powers drawn from P (ldbp_inputs recipe)."""
+    pw = li.dbm_to_w(li.pick_powers_dbm(seed, range(B), POWERS_DBM))
+    return li.bandlimited_blocks_torch(seed, B, n, pw)
 
 
 def ls_model(spans, sps, T):
     d, g = steps.dbp_plan(spans, 80.0, sps, 0.2, 1.3)
-    taps = np.stack([steps.ls_taps(steps.xi_of(dd, physics.ps2_per_km(-21.7), 21.4e9), T) for dd in d])
+    taps = np.stack([steps.ls_taps(steps.xi_of(dd, physics.ps2_per_km(-21.7), 21.4e9), T, cap=1.0) for dd in d])
     return taps, g
 
 

@@ -47,7 +47,7 @@ def model(cfg, M, T, sym, scale=0.1, ls=False, sub=0):
     if ls:
         _, g = steps.dbp_plan(M, 80.0, 1, 0.2, 1.3)
         xi = [steps.xi_of(80.0, physics.ps2_per_km(-21.7), 21.4e9)] * M
-        taps = np.stack([steps.ls_taps(x, T) for x in xi])
+        taps = np.stack([steps.ls_taps(x, T, cap=1.0) for x in xi])
         return taps, g
     taps = li.random_sym_taps(cfg, M, T, scale) if sym else li.random_general_taps(cfg, M, T, scale, sub=sub)
     gamma = li.random_gamma(cfg, M, sub=sub)
@@ -120,8 +120,7 @@ def test_delay_taps_closed_form(P):
 def test_equivariance_c2_size(P):
     """P10 at the C2 size: f(shift_k(e^{j phi} x)) = shift_k(e^{j phi} f(x))."""
     B, n, M, T = 256, 16384, 25, 5
-    g = torch.Generator(device="cuda").manual_seed(1)
-    x = (torch.randn(B, n, dtype=torch.complex64, device="cuda", generator=g) * np.sqrt(1e-3)).contiguous()
+    x = li.bandlimited_blocks_torch(1, B, n, 1e-3)
     taps, gamma = model(0, M, T, True, ls=True)
     ht, gt = dev(taps), dev(gamma, np.float32)
     y = P.ldbp_forward(x, ht, gt)
@@ -261,16 +260,27 @@ def test_determinism_and_shard_sum(P):
     assert rel(parts, full.cpu().numpy()) <= 1e-6
 
 
+def _inband_unit_taps(T, band=0.275):
+    """LS inverse-CD taps for one 80 km step fitted in band (10% RRC at 2 sps occupies |f| <= 0.275
+    f_s) and normalised to unit mean in-band gain — an init-quality stand-in so that the 1-StPS
+    receiver is a working equaliser in this test (the taps are an input; parity is unaffected)."""
+    xi = steps.xi_of(80.0, physics.ps2_per_km(-21.7), 21.4e9)
+    h = steps.ls_taps(xi, T, band=band, oob_weight=0.3)
+    w = np.linspace(-2 * np.pi * band, 2 * np.pi * band, 2001)
+    k = np.arange(T) - (T - 1) // 2
+    return h / np.sqrt(np.mean(np.abs(np.exp(-1j * np.outer(w, k)) @ h) ** 2))
+
+
 def test_snr_parity_on_simulated_link(P):
     """Effective SNR after LDBP (oracle receiver on both outputs) agrees to 0.01 dB, on seeded
-    SSFM + EDFA blocks of the C2 link (25 x 80 km, 1 StPS, LS taps) at several powers."""
-    nsym, spans, M, T = 1024, 25, 25, 5
+    SSFM + EDFA blocks of the C2 link (25 x 80 km, 1 StPS) at several launch powers, for the
+    C2 filter length (T = 5) and a working in-band equaliser (T = 15)."""
+    nsym, spans, M = 1024, 25, 25
     link = dict(span_km=80.0, alpha_db=0.2, beta2=physics.ps2_per_km(-21.7), gamma=1.3, baud_hz=10.7e9,
                 rho_a=4, rho_d=2, nf_db=5.0, nu_hz=1.946e14)
-    deltas, gam = steps.dbp_plan(spans, 80.0, 1, 0.2, 1.3)
-    xi = steps.xi_of(80.0, physics.ps2_per_km(-21.7), 21.4e9)
-    taps = np.stack([steps.ls_taps(xi, T)] * M)
-    for pdbm in (-4.0, 0.0, 4.0, 6.0):
+    _, gam = steps.dbp_plan(spans, 80.0, 1, 0.2, 1.3)
+    snr = {}
+    for pdbm in (-4.0, 2.0, 6.0):
         pw = float(physics.dbm_to_w(pdbm))
         rs, ss = [], []
         for b in range(4):
@@ -280,9 +290,18 @@ def test_snr_parity_on_simulated_link(P):
             rs.append(r)
             ss.append(s)
         rs = np.array(rs)
-        y = P.ldbp_forward(dev(rs), dev(taps), dev(gam, np.float32)).cpu().numpy()
-        yo = O.forward(r32(rs), r32(taps), r32(gam))
-        snr_gpu = receiver.evaluate(y.astype(np.complex128), ss, [pw] * 4)
-        snr_ref = receiver.evaluate(yo, ss, [pw] * 4)
-        assert abs(snr_gpu[0] - snr_ref[0]) <= 0.01 and abs(snr_gpu[1] - snr_ref[1]) <= 0.01, (pdbm, snr_gpu, snr_ref)
-        assert snr_ref[0] > 8.0  # the equaliser is doing its job
+        for T in (5, 15):
+            taps = np.stack([_inband_unit_taps(T)] * M)
+            for nl in (True, False):
+                g = gam if nl else 0 * gam
+                y = P.ldbp_forward(dev(rs), dev(taps), dev(g, np.float32)).cpu().numpy()
+                yo = O.forward(r32(rs), r32(taps), r32(g))
+                snr_gpu = receiver.evaluate(y.astype(np.complex128), ss, [pw] * 4)
+                snr_ref = receiver.evaluate(yo, ss, [pw] * 4)
+                assert abs(snr_gpu[0] - snr_ref[0]) <= 0.01, (pdbm, T, nl, snr_gpu, snr_ref)
+                assert abs(snr_gpu[1] - snr_ref[1]) <= 0.01, (pdbm, T, nl, snr_gpu, snr_ref)
+                snr[(pdbm, T, nl)] = snr_gpu[0]
+    # the T = 15 receiver equalises, and its nonlinear steps help at high power (DBP works)
+    assert snr[(-4.0, 15, True)] > 12.0
+    assert snr[(2.0, 15, True)] > snr[(2.0, 15, False)] + 3.0
+    assert snr[(6.0, 15, True)] > snr[(6.0, 15, False)] + 3.0

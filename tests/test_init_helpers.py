@@ -16,7 +16,10 @@ def test_schedule_matches_oracle():
 def test_inverse_cd_taps_match_oracle_ls():
     for T in (3, 5, 9, 15):
         for delta in (0.0, 20.0, 80.0):
-            h1 = pinit.inverse_cd_taps(delta, T)
             xi = steps.xi_of(delta, physics.ps2_per_km(-21.7), 21.4e9)
+            h1 = pinit.inverse_cd_taps(delta, T, cap=None)
             h2 = steps.ls_taps(xi, T, n_grid=512)
             np.testing.assert_allclose(h1, h2, atol=1e-12)
+            h1c = pinit.inverse_cd_taps(delta, T, cap=1.0)
+            h2c = steps.ls_taps(xi, T, n_grid=512, cap=1.0)
+            np.testing.assert_allclose(h1c, h2c, atol=1e-12)

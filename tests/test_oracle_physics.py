@@ -115,3 +115,18 @@ def test_gamma_prime_closed_forms():
         assert np.all(np.diff(d2) < 0)  # DBP order: largest step first
         assert abs(g2.sum() + 1.3 * physics.l_eff(80.0, a)) < 1e-12
         assert np.all(np.abs(g2) < 1.3 * physics.l_eff(80.0, a))
+
+
+def test_ls_taps_gain_cap():
+    """With cap=1 the fitted filter is non-expansive: |F(h)(w)| <= 1 for all w (DTFT of P:895-896,
+    evaluated independently at random frequencies); without it the short fit over-amplifies."""
+    xi = steps.xi_of(80.0, physics.ps2_per_km(-21.7), 21.4e9)
+    rng = np.random.default_rng(3)
+    w = rng.uniform(-np.pi, np.pi, 20000)
+    for T in (3, 5, 9):
+        k = np.arange(T) - (T - 1) // 2
+        h = steps.ls_taps(xi, T, cap=1.0)
+        assert np.abs(np.exp(-1j * np.outer(w, k)) @ h).max() <= 1.0 + 1e-6
+        h0 = steps.ls_taps(xi, T)
+        ratio = h0 / h
+        assert np.allclose(ratio, ratio[0]) and abs(ratio[0].imag) < 1e-12 and ratio[0].real >= 1.0
