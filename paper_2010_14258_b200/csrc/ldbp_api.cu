@@ -154,15 +154,16 @@ struct Tile {
 };
 
 size_t fwd_smem(int kh, bool sym, int steps) {
-  return sizeof(float2) * 4 * ldbp::kMaxWarps * std::max(kh, 1) +
-         sizeof(float2) * steps * ntaps_used(kh, sym) + sizeof(float) * steps + 16;
+  return sizeof(uint64_t) * 2 * ldbp::kMaxWarps + sizeof(float2) * 4 * ldbp::kMaxWarps * std::max(kh, 1) +
+         sizeof(ldbp::TapP) * steps * ntaps_used(kh, sym) + sizeof(float) * steps + 16;
 }
 
 size_t bwd_smem(int kh, bool sym, int steps, int nthreads) {
   const int nw = nthreads / 32;
   const int V = 1 + 2 * ntaps_used(kh, sym);
-  size_t s = sizeof(float2) * 8 * ldbp::kMaxWarps * std::max(kh, 1);  // two edge arrays
-  s += sizeof(float2) * ((steps * ntaps_used(kh, sym) + 1) & ~1);       // taps (16-B rounded)
+  size_t s = sizeof(uint64_t) * 2 * ldbp::kMaxWarps;                   // mbarriers
+  s += sizeof(float2) * 8 * ldbp::kMaxWarps * std::max(kh, 1);          // two edge arrays
+  s += 2 * sizeof(ldbp::TapP) * steps * ntaps_used(kh, sym);             // packed fwd + adj taps
   s += sizeof(float) * ((steps + 3) & ~3);                              // gamma
   s += sizeof(float) * ((steps * nw * V + 3) & ~3);                     // per-warp partials
   s += sizeof(float2) * size_t(steps) * kBwdR * nthreads;               // tape
@@ -211,7 +212,8 @@ struct FwdPlan {
 
 FwdPlan plan_fwd_segments(int M, int kh) {
   FwdPlan p;
-  const int cap = env_int("LDBP_FWD_THREADS", kFwdMaxThreads) * kFwdR;
+  if (M <= 0) return p;
+  const int cap = std::min(env_int("LDBP_FWD_THREADS", kFwdMaxThreads), ldbp::fwd_max_threads(kh)) * kFwdR;
   int cmax = kh > 0 ? std::max(1, cap / (16 * kh)) : M;
   cmax = std::min(cmax, env_int("LDBP_FWD_MAX_STEPS", 1 << 30));
   p.segs = (int)cdiv(M, cmax);
@@ -273,7 +275,7 @@ BwdPlan plan_bwd(const ldbp_dims* d, bool query_device) {
 Tile plan_fwd_tile(const ldbp_dims* d, int steps, bool query_device) {
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
-  const int maxthr = env_int("LDBP_FWD_THREADS", kFwdMaxThreads);
+  const int maxthr = std::min(env_int("LDBP_FWD_THREADS", kFwdMaxThreads), ldbp::fwd_max_threads(kh));
   int occ = 1, sms = 148;
   const size_t smem = fwd_smem(kh, sym, steps);
   if (query_device) {
@@ -370,7 +372,8 @@ BwdWs bwd_ws(const ldbp_dims* d, const BwdPlan& p) {
 // Launch helpers
 // ----------------------------------------------------------------------------------------
 int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2* taps, const float* gamma,
-               const uint8_t* mask, int s0, int s1, cudaStream_t st) {
+               const uint8_t* mask, int s0, int s1, cudaStream_t st, float2* ckpt = nullptr, int ckpt_every = 0,
+               int64_t ckpt_stride = 0) {
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const bool fast = !(d->flags & LDBP_PRECISE);
@@ -379,6 +382,9 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   ldbp::FwdArgs a;
   a.src = src;
   a.dst = dst;
+  a.ckpt = ckpt;
+  a.ckpt_stride = ckpt_stride;
+  a.ckpt_every = ckpt_every > 0 ? ckpt_every : 1;
   a.taps = taps;
   a.gamma = gamma;
   a.mask = mask;
@@ -420,10 +426,18 @@ int run_backward_chain(const ldbp_dims* d, const float2* x, const float2* gy, co
   const bool fast = !(d->flags & LDBP_PRECISE);
   auto ck = [&](int k) -> float2* { return reinterpret_cast<float2*>(ws + w.ck_off + (size_t)(k - 1) * w.ck_each); };
   auto gb = [&](int k) -> float2* { return reinterpret_cast<float2*>(ws + w.g_off + (size_t)(k & 1) * w.g_each); };
-  // forward checkpoint pass: ck[k] = u^(k*C), k = 1..K-1
-  for (int k = 0; k + 1 < p.K; ++k) {
-    const int s0 = k * p.C, s1 = (k + 1) * p.C;
-    LDBP_TRY(launch_fwd(d, k == 0 ? x : ck(k), ck(k + 1), taps, gamma, mask, s0, s1, st));
+  // forward checkpoint pass: ck[k] = u^(k*C), k = 1..K-1.  Each launch covers G segments
+  // (halo G*C*Kh, bounded by plan_fwd_segments) and writes the intermediate checkpoints on the
+  // fly, so the input is read once per launch instead of once per segment.
+  if (p.K > 1) {
+    const FwdPlan fp = plan_fwd_segments((p.K - 1) * p.C, kh);
+    const int G = std::max(1, fp.steps_per / p.C);
+    for (int k0 = 0; k0 + 1 < p.K; k0 += G) {
+      const int k1 = std::min(p.K - 1, k0 + G);  // this launch produces ck[k0+1 .. k1]
+      // ck(k) for k >= 1 are consecutive buffers: ck(k0+1) + (j-1)*stride
+      LDBP_TRY(launch_fwd(d, k0 == 0 ? x : ck(k0), ck(k1), taps, gamma, mask, k0 * p.C, k1 * p.C, st,
+                          k1 - k0 >= 2 ? ck(1) : nullptr, p.C, (int64_t)(w.ck_each / sizeof(float2))));
+    }
   }
   BwdFn fn = get_bwd(kh, sym, fast);
   double* partials = reinterpret_cast<double*>(ws + w.part_off);
@@ -548,7 +562,13 @@ int ldbp_launch_count(const ldbp_dims* d, int op, int* launches) {
   if (d->batch == 0) { *launches = (op == LDBP_OP_FORWARD) ? 0 : 1; return LDBP_OK; }
   if (op == LDBP_OP_FORWARD) { *launches = plan_fwd_segments(d->steps, (d->taps - 1) / 2).segs; return LDBP_OK; }
   BwdPlan p = plan_bwd(d, true);
-  int n = (p.K - 1) + p.K + 1 + (reduce_chunks(p.tile.grid) > 0 ? 1 : 0);
+  int nf = 0;
+  if (p.K > 1) {
+    const FwdPlan fp = plan_fwd_segments((p.K - 1) * p.C, (d->taps - 1) / 2);
+    const int G = std::max(1, fp.steps_per / p.C);
+    nf = (int)cdiv(p.K - 1, G);
+  }
+  int n = nf + p.K + 1 + (reduce_chunks(p.tile.grid) > 0 ? 1 : 0);
   if (op == LDBP_OP_TRAIN_STEP) n += 1;
   *launches = n;
   return LDBP_OK;

@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "ldbp_f32x2.cuh"
+
 #ifndef LDBP_FWD_R
 #define LDBP_FWD_R 16  // samples per thread, forward kernels
 #endif
@@ -27,12 +29,16 @@
 #define LDBP_BWD_R 8   // samples per thread, backward kernels
 #endif
 
+#ifndef LDBP_NB_SYNC
+#define LDBP_NB_SYNC 0  // 1: neighbour-only mbarrier sync per step (measured 2x slower on B200; kept
+                        // as an option), 0: one __syncthreads per step
+#endif
+
 namespace ldbp {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxWarps = 32;
 
-__device__ __forceinline__ float2 operator+(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 
 // Kerr rotation helpers: (c, s) = (cos phi, sin phi).
 template <bool FAST>
@@ -100,17 +106,32 @@ __device__ __forceinline__ bool span_at(const Span& sp, int k, const Geo& g, int
   return bb >= 0 && bb < g.B && e0 + k >= 0;
 }
 
+// Fast path: the thread's R samples are R consecutive real samples of one block (no wrap, no
+// block junction) -> plain contiguous addressing.  True for all but a few threads per block.
+template <int R>
+__device__ __forceinline__ bool span_fast(const Span& sp, const Geo& g, int64_t e0) {
+  return e0 >= 0 && sp.b0 < g.B && sp.q0 >= g.H && (int64_t)sp.q0 + R <= g.H + g.n;
+}
+
+// Values are complex64 kept as one 64-bit register pair (f2x, see ldbp_f32x2.cuh).
 // Load R consecutive extended samples starting at e0 (zeros outside [0, E)).
 template <int R>
 __device__ __forceinline__ void load_window(const float2* __restrict__ src, int64_t e0, const Geo& g,
-                                            float2 (&u)[R]) {
+                                            f2x (&u)[R]) {
+  const f2x* s2 = reinterpret_cast<const f2x*>(src);
   const Span sp = make_span(e0, g);
+  if (span_fast<R>(sp, g, e0)) {
+    const f2x* p = s2 + sp.b0 * g.n + (sp.q0 - g.H);
+#pragma unroll
+    for (int k = 0; k < R; ++k) u[k] = __ldg(p + k);
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < R; ++k) {
     int64_t b, pos;
     int q;
     const bool ok = span_at<R>(sp, k, g, e0, &b, &pos, &q);
-    u[k] = ok ? __ldg(src + b * g.n + pos) : make_float2(0.f, 0.f);
+    u[k] = ok ? __ldg(s2 + b * g.n + pos) : 0ull;
   }
 }
 
@@ -120,6 +141,8 @@ __device__ __forceinline__ uint32_t owned_mask(int64_t e0, const Geo& g) {
   const int64_t lo = (int64_t)blockIdx.x * g.W;
   const int64_t hi = min(lo + g.W, g.E);
   const Span sp = make_span(e0, g);
+  if (span_fast<R>(sp, g, e0) && e0 >= lo && e0 + R <= hi) return R >= 32 ? 0xffffffffu : ((1u << R) - 1u);
+  if (e0 + R <= lo || e0 >= hi) return 0u;
   uint32_t m = 0;
 #pragma unroll
   for (int k = 0; k < R; ++k) {
@@ -132,36 +155,62 @@ __device__ __forceinline__ uint32_t owned_mask(int64_t e0, const Geo& g) {
   return m;
 }
 
+// Per-thread store descriptor, computed once: fast threads store R contiguous samples.
+struct StoreMap {
+  int64_t off;    // element offset of sample 0 (fast path), -1 if the slow path is needed
+  uint32_t mask;  // owned samples
+};
+
 template <int R>
-__device__ __forceinline__ void store_owned(float2* __restrict__ dst, int64_t e0, const Geo& g,
-                                            const float2 (&u)[R]) {
-  const uint32_t m = owned_mask<R>(e0, g);
+__device__ __forceinline__ StoreMap store_map(int64_t e0, const Geo& g) {
+  StoreMap sm;
+  sm.mask = owned_mask<R>(e0, g);
   const Span sp = make_span(e0, g);
+  sm.off = (sm.mask == (R >= 32 ? 0xffffffffu : ((1u << R) - 1u)) && span_fast<R>(sp, g, e0))
+               ? sp.b0 * g.n + (sp.q0 - g.H)
+               : -1;
+  return sm;
+}
+
+template <int R>
+__device__ __forceinline__ void store_mapped(float2* __restrict__ dst, const StoreMap& sm, int64_t e0, const Geo& g,
+                                             f2x (&u)[R]) {
+  f2x* d2 = reinterpret_cast<f2x*>(dst);
+  if (sm.off >= 0) {
 #pragma unroll
-  for (int k = 0; k < R; ++k) {
-    int64_t b, pos;
-    int q;
-    span_at<R>(sp, k, g, e0, &b, &pos, &q);
-    if (m & (1u << k)) dst[b * g.n + pos] = u[k];
+    for (int k = 0; k < R; ++k) d2[sm.off + k] = u[k];
+  } else if (sm.mask) {
+    // owned samples have q in [H, H+n): position q - H, no wrap; only block crossings remain
+    const Span sp = make_span(e0, g);
+    int64_t b = sp.b0;
+    int q = sp.q0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (sm.mask & (1u << k)) d2[b * g.n + (q - g.H)] = u[k];
+      if (++q == g.ext) { q = 0; ++b; }
+    }
   }
+}
+
+template <int R>
+__device__ __forceinline__ void store_owned(float2* __restrict__ dst, int64_t e0, const Geo& g, f2x (&u)[R]) {
+  const StoreMap sm = store_map<R>(e0, g);
+  store_mapped<R>(dst, sm, e0, g, u);
 }
 
 // Halo exchange of one register array: hl = Kh samples left of u[0], hr = Kh samples right
 // of u[R-1].  Shuffles inside the warp; warp edges through sh[2 buffers][2 sides][32 warps][KH].
 template <int KH, int R>
-__device__ __forceinline__ void exchange(const float2 (&u)[R], float2 (&hl)[KH > 0 ? KH : 1],
-                                         float2 (&hr)[KH > 0 ? KH : 1], float2* sh, int buf,
-                                         int lane, int warp, int nwarps) {
+__device__ __forceinline__ void exchange(const f2x (&u)[R], f2x (&hl)[KH > 0 ? KH : 1], f2x (&hr)[KH > 0 ? KH : 1],
+                                         f2x* sh, int buf, int lane, int warp, int nwarps) {
   if constexpr (KH > 0) {
 #pragma unroll
     for (int j = 0; j < KH; ++j) {
-      hl[j].x = __shfl_up_sync(kFull, u[R - KH + j].x, 1);
-      hl[j].y = __shfl_up_sync(kFull, u[R - KH + j].y, 1);
-      hr[j].x = __shfl_down_sync(kFull, u[j].x, 1);
-      hr[j].y = __shfl_down_sync(kFull, u[j].y, 1);
+      hl[j] = __shfl_up_sync(kFull, u[R - KH + j], 1);
+      hr[j] = __shfl_down_sync(kFull, u[j], 1);
     }
-    float2* head = sh + ((buf * 2 + 0) * kMaxWarps) * KH;
-    float2* tail = sh + ((buf * 2 + 1) * kMaxWarps) * KH;
+    f2x* head = sh + ((buf * 2 + 0) * kMaxWarps) * KH;
+    f2x* tail = sh + ((buf * 2 + 1) * kMaxWarps) * KH;
     if (lane == 0) {
 #pragma unroll
       for (int j = 0; j < KH; ++j) head[warp * KH + j] = u[j];
@@ -184,29 +233,119 @@ __device__ __forceinline__ void exchange(const float2 (&u)[R], float2 (&hl)[KH >
   }
 }
 
+// ---- neighbour-only synchronisation (mbarrier) -----------------------------------------
+// Instead of a CTA-wide __syncthreads per step, warp w publishes its edge samples, arrives on
+// its own mbarrier bar[it&1][w] (count 1) and waits only for warps w-1 / w+1 of the same
+// iteration.  Double buffering is safe: a warp can overwrite buffer b at iteration it+2 only
+// after its neighbours published iteration it+1, which they do after reading iteration it.
+// For the same reason no barrier can run two phases ahead of a waiter, so the parity test
+// (it >> 1) & 1 is exact.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  // try_wait suspends the thread in hardware for a bounded time; a bounded retry count turns a
+  // (never expected) lost arrival into a trap instead of a hung GPU.
+  unsigned ok = 0, n = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok && ++n < (1u << 24));
+  if (!ok) __trap();
+}
+// bars: [2][kMaxWarps] mbarriers; call once per CTA (followed by a __syncthreads()).
+__device__ __forceinline__ void nb_init(uint64_t* bars) {
+  for (int i = threadIdx.x; i < 2 * kMaxWarps; i += blockDim.x) mbar_init(bars + i, 1);
+}
+
+// Exchange of up to two arrays (N = 1 or 2) with neighbour-only synchronisation.
+template <int KH, int R, int N>
+__device__ __forceinline__ void exchange_nb(const f2x (&u)[R], f2x (&hl)[KH > 0 ? KH : 1], f2x (&hr)[KH > 0 ? KH : 1],
+                                            f2x* sh, const f2x (&v)[R], f2x (&gl)[KH > 0 ? KH : 1],
+                                            f2x (&gr)[KH > 0 ? KH : 1], f2x* sh2, uint64_t* bars, int it, int lane,
+                                            int warp, int nwarps) {
+  if constexpr (KH > 0) {
+    const int b = it & 1;
+    const unsigned parity = (it >> 1) & 1;
+#pragma unroll
+    for (int j = 0; j < KH; ++j) {
+      hl[j] = __shfl_up_sync(kFull, u[R - KH + j], 1);
+      hr[j] = __shfl_down_sync(kFull, u[j], 1);
+      if constexpr (N == 2) {
+        gl[j] = __shfl_up_sync(kFull, v[R - KH + j], 1);
+        gr[j] = __shfl_down_sync(kFull, v[j], 1);
+      }
+    }
+    f2x* head = sh + ((b * 2 + 0) * kMaxWarps) * KH;
+    f2x* tail = sh + ((b * 2 + 1) * kMaxWarps) * KH;
+    f2x* head2 = sh2 + ((b * 2 + 0) * kMaxWarps) * KH;
+    f2x* tail2 = sh2 + ((b * 2 + 1) * kMaxWarps) * KH;
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < KH; ++j) {
+        head[warp * KH + j] = u[j];
+        if constexpr (N == 2) head2[warp * KH + j] = v[j];
+      }
+    }
+    if (lane == 31) {
+#pragma unroll
+      for (int j = 0; j < KH; ++j) {
+        tail[warp * KH + j] = u[R - KH + j];
+        if constexpr (N == 2) tail2[warp * KH + j] = v[R - KH + j];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bars + b * kMaxWarps + warp);
+    if (lane == 0 && warp > 0) {
+      mbar_wait(bars + b * kMaxWarps + warp - 1, parity);
+#pragma unroll
+      for (int j = 0; j < KH; ++j) {
+        hl[j] = tail[(warp - 1) * KH + j];
+        if constexpr (N == 2) gl[j] = tail2[(warp - 1) * KH + j];
+      }
+    }
+    if (lane == 31 && warp < nwarps - 1) {
+      mbar_wait(bars + b * kMaxWarps + warp + 1, parity);
+#pragma unroll
+      for (int j = 0; j < KH; ++j) {
+        hr[j] = head[(warp + 1) * KH + j];
+        if constexpr (N == 2) gr[j] = head2[(warp + 1) * KH + j];
+      }
+    }
+    __syncwarp();
+  } else {
+    (void)u; (void)hl; (void)hr; (void)sh; (void)v; (void)gl; (void)gr; (void)sh2; (void)bars; (void)it;
+    (void)lane; (void)warp; (void)nwarps;
+  }
+}
+
 // Two arrays exchanged around one barrier (backward reverse sweep).
 template <int KH, int R>
-__device__ __forceinline__ void exchange2(const float2 (&u)[R], float2 (&hl)[KH > 0 ? KH : 1],
-                                          float2 (&hr)[KH > 0 ? KH : 1], float2* sh, int buf,
-                                          const float2 (&v)[R], float2 (&gl)[KH > 0 ? KH : 1],
-                                          float2 (&gr)[KH > 0 ? KH : 1], float2* sh2, int buf2,
-                                          int lane, int warp, int nwarps) {
+__device__ __forceinline__ void exchange2(const f2x (&u)[R], f2x (&hl)[KH > 0 ? KH : 1], f2x (&hr)[KH > 0 ? KH : 1],
+                                          f2x* sh, int buf, const f2x (&v)[R], f2x (&gl)[KH > 0 ? KH : 1],
+                                          f2x (&gr)[KH > 0 ? KH : 1], f2x* sh2, int buf2, int lane, int warp,
+                                          int nwarps) {
   if constexpr (KH > 0) {
 #pragma unroll
     for (int j = 0; j < KH; ++j) {
-      hl[j].x = __shfl_up_sync(kFull, u[R - KH + j].x, 1);
-      hl[j].y = __shfl_up_sync(kFull, u[R - KH + j].y, 1);
-      hr[j].x = __shfl_down_sync(kFull, u[j].x, 1);
-      hr[j].y = __shfl_down_sync(kFull, u[j].y, 1);
-      gl[j].x = __shfl_up_sync(kFull, v[R - KH + j].x, 1);
-      gl[j].y = __shfl_up_sync(kFull, v[R - KH + j].y, 1);
-      gr[j].x = __shfl_down_sync(kFull, v[j].x, 1);
-      gr[j].y = __shfl_down_sync(kFull, v[j].y, 1);
+      hl[j] = __shfl_up_sync(kFull, u[R - KH + j], 1);
+      hr[j] = __shfl_down_sync(kFull, u[j], 1);
+      gl[j] = __shfl_up_sync(kFull, v[R - KH + j], 1);
+      gr[j] = __shfl_down_sync(kFull, v[j], 1);
     }
-    float2* head = sh + ((buf * 2 + 0) * kMaxWarps) * KH;
-    float2* tail = sh + ((buf * 2 + 1) * kMaxWarps) * KH;
-    float2* head2 = sh2 + ((buf2 * 2 + 0) * kMaxWarps) * KH;
-    float2* tail2 = sh2 + ((buf2 * 2 + 1) * kMaxWarps) * KH;
+    f2x* head = sh + ((buf * 2 + 0) * kMaxWarps) * KH;
+    f2x* tail = sh + ((buf * 2 + 1) * kMaxWarps) * KH;
+    f2x* head2 = sh2 + ((buf2 * 2 + 0) * kMaxWarps) * KH;
+    f2x* tail2 = sh2 + ((buf2 * 2 + 1) * kMaxWarps) * KH;
     if (lane == 0) {
 #pragma unroll
       for (int j = 0; j < KH; ++j) { head[warp * KH + j] = u[j]; head2[warp * KH + j] = v[j]; }
@@ -232,9 +371,8 @@ __device__ __forceinline__ void exchange2(const float2 (&u)[R], float2 (&hl)[KH 
 
 // Warp reduce-scatter of N values (N a power of two, 2 <= N <= 32) by a transposing butterfly:
 // at each level a lane keeps half of its vector and adds the partner's copy of that half, so
-// only N-1 shuffles are needed (vs 5N for N separate reductions).  Afterwards lane l holds the
-// full warp sum of value index (l >> (5 - log2 N)) ... for N = 16: index l >> 1, replicated in
-// the lane pair (l, l^1) after the final xor-1 add.  Returns that lane's sum.
+// N-1 shuffles replace the 5N of N independent reductions.  Afterwards lane l holds the warp
+// total of value index l >> (5 - log2 N) (replicated over the 32/N lanes sharing it).
 template <int N>
 __device__ __forceinline__ float warp_reduce_scatter(float (&v)[N], int lane) {
   static_assert(N >= 2 && N <= 32 && (N & (N - 1)) == 0, "N must be a power of two in [2, 32]");
@@ -248,7 +386,6 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&v)[N], int lane) {
       v[i] = keep + __shfl_xor_sync(kFull, send, o);
     }
   }
-  // remaining lanes that share an index: levels o < 32/N
   float r = v[0];
 #pragma unroll
   for (int o = 16 / N; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
@@ -258,72 +395,78 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&v)[N], int lane) {
 // Window accessor: index i in [-KH, R+KH).
 #define LDBP_WIN(arr, hl, hr, i) ((i) < 0 ? hl[KH + (i)] : ((i) >= R ? hr[(i) - R] : arr[(i)]))
 
-// One FIR evaluation for output k (compile-time), a_k = sum_j h_j w_{k-j}.
-// SYM: taps hs[0..KH] hold h_0..h_KH (folded, fig:filter P:494-509).
-// GEN: taps hs[0..2KH] hold h_{-KH}..h_{KH}.
+// Packed taps (ldbp_f32x2.cuh): forward h*s = lo(s)*(hx,hy) + hi(s)*(-hy,hx);
+// adjoint conj(h)*s = lo(s)*(hx,-hy) + hi(s)*(hy,hx).  Staged once per CTA in shared memory.
+struct TapP {
+  f2x a, b;
+};
+
+__device__ __forceinline__ TapP tap_fwd(float2 h) { return {pk(h.x, h.y), pk(-h.y, h.x)}; }
+__device__ __forceinline__ TapP tap_adj(float2 h) { return {pk(h.x, -h.y), pk(h.y, h.x)}; }
+// acc + t*s  (t a packed tap of either kind): 2 FFMA2, broadcasts of lo(s)/hi(s) are free.
+__device__ __forceinline__ f2x tmac(f2x acc, const TapP& t, f2x s) {
+  return fma2(bcast(lof(s)), t.a, fma2(bcast(hif(s)), t.b, acc));
+}
+// Two independent accumulation chains (acc_a gets the lo(s) terms, acc_b the hi(s) terms):
+// halves the dependent FFMA2 chain per output; the caller adds the two at the end.
+__device__ __forceinline__ void tmac2(f2x& acc_a, f2x& acc_b, const TapP& t, f2x s) {
+  acc_a = fma2(bcast(lof(s)), t.a, acc_a);
+  acc_b = fma2(bcast(hif(s)), t.b, acc_b);
+}
+__device__ __forceinline__ f2x tmul(const TapP& t, f2x s) { return fma2(bcast(lof(s)), t.a, mul2(bcast(hif(s)), t.b)); }
+
+// One FIR output k (compile-time), a_k = sum_j h_j w_{k-j} (packed FP32x2 complex MACs).
+// SYM: taps hs[0..KH] = h_0..h_KH (folded, fig:filter P:494-509: pre-add u_{k-j}+u_{k+j}).
+// GEN: taps hs[0..2KH] = h_{-KH}..h_{KH}.
 template <int KH, int R, bool SYM, int K>
-__device__ __forceinline__ float2 fir_at(const float2 (&u)[R], const float2 (&hl)[KH > 0 ? KH : 1],
-                                         const float2 (&hr)[KH > 0 ? KH : 1],
-                                         const float2 (&hs)[SYM ? KH + 1 : 2 * KH + 1]) {
-  float2 acc;
+__device__ __forceinline__ f2x fir_at(const f2x (&u)[R], const f2x (&hl)[KH > 0 ? KH : 1],
+                                      const f2x (&hr)[KH > 0 ? KH : 1], const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1]) {
+  f2x acc_a, acc_b;
   if constexpr (SYM) {
-    const float2 c = u[K];
-    acc.x = hs[0].x * c.x;
-    acc.y = hs[0].x * c.y;
-    acc.x = fmaf(-hs[0].y, c.y, acc.x);
-    acc.y = fmaf(hs[0].y, c.x, acc.y);
+    acc_a = mul2(bcast(lof(u[K])), hs[0].a);
+    acc_b = mul2(bcast(hif(u[K])), hs[0].b);
 #pragma unroll
-    for (int j = 1; j <= KH; ++j) {
-      const float2 l = LDBP_WIN(u, hl, hr, K - j);
-      const float2 r = LDBP_WIN(u, hl, hr, K + j);
-      const float2 s = make_float2(l.x + r.x, l.y + r.y);
-      acc.x = fmaf(hs[j].x, s.x, acc.x);
-      acc.y = fmaf(hs[j].x, s.y, acc.y);
-      acc.x = fmaf(-hs[j].y, s.y, acc.x);
-      acc.y = fmaf(hs[j].y, s.x, acc.y);
-    }
+    for (int j = 1; j <= KH; ++j)
+      tmac2(acc_a, acc_b, hs[j], add2(LDBP_WIN(u, hl, hr, K - j), LDBP_WIN(u, hl, hr, K + j)));
   } else {
-    acc = make_float2(0.f, 0.f);
+    const f2x w0 = LDBP_WIN(u, hl, hr, K + KH);
+    acc_a = mul2(bcast(lof(w0)), hs[0].a);
+    acc_b = mul2(bcast(hif(w0)), hs[0].b);
 #pragma unroll
-    for (int jj = 0; jj < 2 * KH + 1; ++jj) {
-      const int j = jj - KH;
-      const float2 w = LDBP_WIN(u, hl, hr, K - j);
-      acc.x = fmaf(hs[jj].x, w.x, acc.x);
-      acc.y = fmaf(hs[jj].x, w.y, acc.y);
-      acc.x = fmaf(-hs[jj].y, w.y, acc.x);
-      acc.y = fmaf(hs[jj].y, w.x, acc.y);
-    }
+    for (int jj = 1; jj < 2 * KH + 1; ++jj) tmac2(acc_a, acc_b, hs[jj], LDBP_WIN(u, hl, hr, K - (jj - KH)));
   }
-  return acc;
+  return add2(acc_a, acc_b);
 }
 
 template <int KH, int R, bool SYM, int K = 0>
-__device__ __forceinline__ void fir_all(const float2 (&u)[R], const float2 (&hl)[KH > 0 ? KH : 1],
-                                        const float2 (&hr)[KH > 0 ? KH : 1],
-                                        const float2 (&hs)[SYM ? KH + 1 : 2 * KH + 1], float2 (&a)[R]) {
+__device__ __forceinline__ void fir_all(const f2x (&u)[R], const f2x (&hl)[KH > 0 ? KH : 1],
+                                        const f2x (&hr)[KH > 0 ? KH : 1], const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1],
+                                        f2x (&a)[R]) {
   if constexpr (K < R) {
     a[K] = fir_at<KH, R, SYM, K>(u, hl, hr, hs);
     fir_all<KH, R, SYM, K + 1>(u, hl, hr, hs, a);
   }
 }
 
-// Kerr: v = a e^{j g |a|^2}.
+// Kerr: v = a e^{j g |a|^2} = ax*(c, s) + ay*(-s, c).
 template <bool FAST>
-__device__ __forceinline__ float2 kerr(float2 a, float g) {
-  const float p = fmaf(a.x, a.x, a.y * a.y);
+__device__ __forceinline__ f2x kerr(f2x a, float g) {
+  const float ax = lof(a), ay = hif(a);
+  const float p = fmaf(ax, ax, ay * ay);
   float s, c;
   sincos_phase<FAST>(g * p, &s, &c);
-  return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+  return fma2(bcast(ax), pk(c, s), mul2(bcast(ay), pk(-s, c)));
 }
 
 template <bool SYM, int KH>
 __device__ __forceinline__ constexpr int ntaps_used() { return SYM ? KH + 1 : 2 * KH + 1; }
 
-// Stage taps/gamma of steps [s0, s1) into shared memory (masked; SYM keeps only h_0..h_Kh).
-template <int KH, bool SYM>
+// Stage the packed taps and gamma of steps [s0, s1) into shared memory (masked taps -> 0;
+// SYM keeps only h_0..h_Kh).  ADJ additionally stages the adjoint (conjugate) packing.
+template <int KH, bool SYM, bool ADJ>
 __device__ __forceinline__ void stage_params(const float2* __restrict__ taps, const float* __restrict__ gamma,
                                              const uint8_t* __restrict__ mask, int T, int s0, int s1,
-                                             float2* sh_taps, float* sh_gamma) {
+                                             TapP* sh_taps, TapP* sh_taps_adj, float* sh_gamma) {
   constexpr int NT = ntaps_used<SYM, KH>();
   const int cnt = (s1 - s0) * NT;
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
@@ -331,7 +474,8 @@ __device__ __forceinline__ void stage_params(const float2* __restrict__ taps, co
     const int t = (i % NT) + (SYM ? KH : 0);  // index into the stored [T] row
     float2 h = taps[(int64_t)s * T + t];
     if (mask && !mask[(int64_t)s * T + t]) h = make_float2(0.f, 0.f);
-    sh_taps[i] = h;
+    sh_taps[i] = tap_fwd(h);
+    if constexpr (ADJ) sh_taps_adj[i] = tap_adj(h);
   }
   for (int i = threadIdx.x; i < s1 - s0; i += blockDim.x) sh_gamma[i] = gamma[s0 + i];
 }
@@ -339,6 +483,9 @@ __device__ __forceinline__ void stage_params(const float2* __restrict__ taps, co
 struct FwdArgs {
   const float2* src;
   float2* dst;
+  float2* ckpt;          // optional: after global step s with (s % ckpt_every) == 0, s in (s0, s1),
+  int64_t ckpt_stride;   //   owned samples go to ckpt + (s / ckpt_every - 1) * ckpt_stride
+  int ckpt_every;
   const float2* taps;
   const float* gamma;
   const uint8_t* mask;
@@ -349,35 +496,51 @@ struct FwdArgs {
 // ---------------------------------------------------------------------------------------
 // Forward tile kernel: steps [s0, s1) of Eq. (7) for one tile, all on chip (rows a0-a4).
 // ---------------------------------------------------------------------------------------
+// Register budget per Kh: packed taps cost 4 registers each (TapP), so wider filters get
+// fewer threads per CTA (the planner reads fwd_max_threads()).
+__host__ __device__ constexpr int fwd_max_threads(int kh) { return kh <= 2 ? 512 : 256; }
+__host__ __device__ constexpr int fwd_min_blocks(int kh) { return kh <= 2 ? 2 : kh <= 4 ? 3 : 2; }
+
 template <int KH, int R, bool SYM, bool FAST>
-__global__ void __launch_bounds__(512, 2) fwd_tile_kernel(const FwdArgs a) {
+__global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_tile_kernel(const FwdArgs a) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* sh_edge = reinterpret_cast<float2*>(smem_raw);                 // 2*2*32*KH
-  float2* sh_taps = sh_edge + 4 * kMaxWarps * (KH > 0 ? KH : 1);          // (s1-s0)*NTU
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                            // [2][32] mbarriers
+  f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);                       // 2*2*32*KH
+  TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge + 4 * kMaxWarps * (KH > 0 ? KH : 1));  // (s1-s0)*NTU
   float* sh_gamma = reinterpret_cast<float*>(sh_taps + (a.s1 - a.s0) * NTU);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  stage_params<KH, SYM>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, sh_gamma);
+  stage_params<KH, SYM, false>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, nullptr, sh_gamma);
+  if (LDBP_NB_SYNC) nb_init(bars);
 
-  float2 u[R];
+  f2x u[R];
   const int64_t e0 = thread_e0(a.g, R);
   load_window<R>(a.src, e0, a.g, u);
+  const StoreMap smap = store_map<R>(e0, a.g);
   __syncthreads();
 
-  float2 hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1];
+  f2x hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1];
   for (int s = 0; s < a.s1 - a.s0; ++s) {
-    float2 hs[NTU];
+    TapP hs[NTU];
 #pragma unroll
     for (int j = 0; j < NTU; ++j) hs[j] = sh_taps[s * NTU + j];
     const float gm = sh_gamma[s];
-    exchange<KH, R>(u, hl, hr, sh_edge, s & 1, lane, warp, nwarps);
-    float2 acc[R];
+    if (LDBP_NB_SYNC)
+      exchange_nb<KH, R, 1>(u, hl, hr, sh_edge, u, hl, hr, sh_edge, bars, s, lane, warp, nwarps);
+    else
+      exchange<KH, R>(u, hl, hr, sh_edge, s & 1, lane, warp, nwarps);
+    f2x acc[R];
     fir_all<KH, R, SYM>(u, hl, hr, hs, acc);
 #pragma unroll
     for (int k = 0; k < R; ++k) u[k] = kerr<FAST>(acc[k], gm);
+    if (a.ckpt) {
+      const int gs = a.s0 + s + 1;  // global step count reached
+      if (gs < a.s1 && gs % a.ckpt_every == 0)
+        store_mapped<R>(a.ckpt + (int64_t)(gs / a.ckpt_every - 1) * a.ckpt_stride, smap, e0, a.g, u);
+    }
   }
-  store_owned<R>(a.dst, e0, a.g, u);
+  store_mapped<R>(a.dst, smap, e0, a.g, u);
 }
 
 struct BwdArgs {
@@ -395,7 +558,6 @@ struct BwdArgs {
   Geo g;
 };
 
-template <int R>
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
@@ -409,7 +571,10 @@ __device__ __forceinline__ float warp_sum(float v) {
 // Tape layout: tape[(l*R + k)*NT + tid] = u^(s0+l)[thread tid, sample k] (conflict free).
 // ---------------------------------------------------------------------------------------
 template <int KH, int R, bool SYM, bool FAST>
-__global__ void __launch_bounds__(256) bwd_segment_kernel(const BwdArgs a) {
+#ifndef LDBP_BWD_MINB
+#define LDBP_BWD_MINB 2
+#endif
+__global__ void __launch_bounds__(256, LDBP_BWD_MINB) bwd_segment_kernel(const BwdArgs a) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   constexpr int V = 1 + 2 * NTU;  // [dgamma | dtap re/im ...]
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -418,50 +583,58 @@ __global__ void __launch_bounds__(256) bwd_segment_kernel(const BwdArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = nthr >> 5;
 
   // carve-up (every region 16-byte aligned; mirrored by bwd_smem() on the host)
-  float2* sh_edge = reinterpret_cast<float2*>(smem_raw);  // two arrays: 2 * (2*2*32*KH)
-  float2* sh_edge2 = sh_edge + 4 * kMaxWarps * (KH > 0 ? KH : 1);
-  float2* sh_taps = sh_edge2 + 4 * kMaxWarps * (KH > 0 ? KH : 1);
-  float* sh_gamma = reinterpret_cast<float*>(sh_taps + ((C * NTU + 1) & ~1));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [2][32] mbarriers
+  f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);  // two arrays: 2 * (2*2*32*KH)
+  f2x* sh_edge2 = sh_edge + 4 * kMaxWarps * (KH > 0 ? KH : 1);
+  TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge2 + 4 * kMaxWarps * (KH > 0 ? KH : 1));
+  TapP* sh_taps_adj = sh_taps + C * NTU;
+  float* sh_gamma = reinterpret_cast<float*>(sh_taps_adj + C * NTU);
   float* sh_red = sh_gamma + ((C + 3) & ~3);                  // [C][nwarps][V]
-  float2* tape = reinterpret_cast<float2*>(sh_red + ((C * nwarps * V + 3) & ~3));  // [C][R][nthr]
+  f2x* tape = reinterpret_cast<f2x*>(sh_red + ((C * nwarps * V + 3) & ~3));  // [C][R][nthr]
 
-  stage_params<KH, SYM>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, sh_gamma);
+  stage_params<KH, SYM, true>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, sh_taps_adj, sh_gamma);
+  if (LDBP_NB_SYNC) nb_init(bars);
 
-  float2 u[R];
+  f2x u[R];
   const int64_t e0 = thread_e0(a.g, R);
   load_window<R>(a.ck, e0, a.g, u);
   const uint32_t own = owned_mask<R>(e0, a.g);
   __syncthreads();
 
-  float2 hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1];
+  f2x hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1];
   // ---- forward recompute, tape = inputs of each step ----
   for (int l = 0; l < C; ++l) {
 #pragma unroll
     for (int k = 0; k < R; ++k) tape[(l * R + k) * nthr + threadIdx.x] = u[k];
-    float2 hs[NTU];
+    TapP hs[NTU];
 #pragma unroll
     for (int j = 0; j < NTU; ++j) hs[j] = sh_taps[l * NTU + j];
     const float gm = sh_gamma[l];
-    exchange<KH, R>(u, hl, hr, sh_edge, l & 1, lane, warp, nwarps);
-    float2 acc[R];
+    if (LDBP_NB_SYNC)
+      exchange_nb<KH, R, 1>(u, hl, hr, sh_edge, u, hl, hr, sh_edge, bars, l, lane, warp, nwarps);
+    else
+      exchange<KH, R>(u, hl, hr, sh_edge, l & 1, lane, warp, nwarps);
+    f2x acc[R];
     fir_all<KH, R, SYM>(u, hl, hr, hs, acc);
 #pragma unroll
     for (int k = 0; k < R; ++k) u[k] = kerr<FAST>(acc[k], gm);
   }
 
   // ---- seed / incoming adjoint ----
-  float2 g[R];
+  f2x g[R];
   if (a.gin == nullptr) {
-    float2 t[R];
+    f2x t[R];
     load_window<R>(a.target, e0, a.g, t);
     float lsum = 0.f;
+    const f2x m1 = bcast(-1.f);
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const float ex = u[k].x - t[k].x, ey = u[k].y - t[k].y;
-      g[k] = make_float2(a.seed_scale * ex, a.seed_scale * ey);
+      const f2x e = fma2(m1, t[k], u[k]);  // y - target
+      g[k] = mul2(bcast(a.seed_scale), e);
+      const float ex = lof(e), ey = hif(e);
       if (own & (1u << k)) lsum = fmaf(ex, ex, fmaf(ey, ey, lsum));
     }
-    lsum = warp_sum<R>(lsum);
+    lsum = warp_sum(lsum);
     if (lane == 0) sh_red[warp] = lsum;  // reused below only after a barrier
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -475,95 +648,77 @@ __global__ void __launch_bounds__(256) bwd_segment_kernel(const BwdArgs a) {
   }
 
   // ---- reverse sweep ----
-  float2 gl[KH > 0 ? KH : 1], gr[KH > 0 ? KH : 1];
+  f2x gl[KH > 0 ? KH : 1], gr[KH > 0 ? KH : 1];
   for (int l = C - 1; l >= 0; --l) {
-    float2 hs[NTU];
+    TapP hs[NTU];
 #pragma unroll
-    for (int j = 0; j < NTU; ++j) hs[j] = sh_taps[l * NTU + j];
+    for (int j = 0; j < NTU; ++j) hs[j] = sh_taps_adj[l * NTU + j];
     const float gm = sh_gamma[l];
-    // NL adjoint of step l: v = u (output of step l), g = dL/dv.
+    const float gm2 = 2.f * gm;
+    // NL adjoint of step l: v = u (output of step l), g = dL/dv:
+    //   c = Im(g conj v), t = g + 2 gamma' c v, ga = t e^{-j phi} = tx*(c,-s) + ty*(s,c).
     float dgam = 0.f;
-    float2 ga[R];
+    f2x ga[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const float2 v = u[k];
-      const float p = fmaf(v.x, v.x, v.y * v.y);
+      const f2x v = u[k];
+      const float vx = lof(v), vy = hif(v);
+      const float p = fmaf(vx, vx, vy * vy);
       float sn, cs;
       sincos_phase<FAST>(gm * p, &sn, &cs);
-      const float cim = fmaf(g[k].y, v.x, -g[k].x * v.y);  // Im(g conj v)
-      const float kk = 2.f * gm * cim;
-      const float tx = fmaf(kk, v.x, g[k].x), ty = fmaf(kk, v.y, g[k].y);
-      ga[k] = make_float2(fmaf(tx, cs, ty * sn), fmaf(ty, cs, -tx * sn));  // t e^{-j phi}
+      const float cim = fmaf(hif(g[k]), vx, -lof(g[k]) * vy);  // Im(g conj v)
+      const f2x t = fma2(bcast(gm2 * cim), v, g[k]);
+      ga[k] = fma2(bcast(lof(t)), pk(cs, -sn), mul2(bcast(hif(t)), pk(sn, cs)));
       if (own & (1u << k)) dgam = fmaf(cim, p, dgam);
     }
     // u^(s0+l): FIR input of step l.
 #pragma unroll
     for (int k = 0; k < R; ++k) u[k] = tape[(l * R + k) * nthr + threadIdx.x];
-    // exchange halos of u and ga (one barrier each).  The u buffers continue the forward
+    // exchange halos of u and ga around one barrier.  The u buffers continue the forward
     // loop's parity sequence (the last forward exchange used (C-1)&1), hence (l+1)&1.
-    exchange2<KH, R>(u, hl, hr, sh_edge, (l + 1) & 1, ga, gl, gr, sh_edge2, l & 1, lane, warp, nwarps);
-    // tap gradients over owned samples: dh_j += ga_t conj(u_{t-j})
-    float2 dh[NTU];
+    if (LDBP_NB_SYNC)
+      exchange_nb<KH, R, 2>(u, hl, hr, sh_edge, ga, gl, gr, sh_edge2, bars, 2 * C - 1 - l, lane, warp, nwarps);
+    else
+      exchange2<KH, R>(u, hl, hr, sh_edge, (l + 1) & 1, ga, gl, gr, sh_edge2, l & 1, lane, warp, nwarps);
+    // tap gradients over owned samples: dh_j += ga_t conj(w),  w = u_{t-j} (+ u_{t+j} if SYM)
+    //   ga conj(w) = lo(w)*ga + hi(w)*(gy, -gx)
+    f2x dh[NTU], dhb[NTU];
 #pragma unroll
-    for (int j = 0; j < NTU; ++j) dh[j] = make_float2(0.f, 0.f);
+    for (int j = 0; j < NTU; ++j) dh[j] = dhb[j] = 0ull;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const float2 gk = (own & (1u << k)) ? ga[k] : make_float2(0.f, 0.f);
+      const f2x gk = (own & (1u << k)) ? ga[k] : 0ull;
+      const TapP gt = {gk, pk(hif(gk), -lof(gk))};
       if constexpr (SYM) {
-        const float2 w = u[k];
-        dh[0].x = fmaf(gk.x, w.x, fmaf(gk.y, w.y, dh[0].x));
-        dh[0].y = fmaf(gk.y, w.x, fmaf(-gk.x, w.y, dh[0].y));
+        tmac2(dh[0], dhb[0], gt, u[k]);
 #pragma unroll
-        for (int j = 1; j <= KH; ++j) {
-          const float2 l2 = LDBP_WIN(u, hl, hr, k - j);
-          const float2 r2 = LDBP_WIN(u, hl, hr, k + j);
-          const float2 s = make_float2(l2.x + r2.x, l2.y + r2.y);
-          dh[j].x = fmaf(gk.x, s.x, fmaf(gk.y, s.y, dh[j].x));
-          dh[j].y = fmaf(gk.y, s.x, fmaf(-gk.x, s.y, dh[j].y));
-        }
+        for (int j = 1; j <= KH; ++j)
+          tmac2(dh[j], dhb[j], gt, add2(LDBP_WIN(u, hl, hr, k - j), LDBP_WIN(u, hl, hr, k + j)));
       } else {
 #pragma unroll
-        for (int jj = 0; jj < 2 * KH + 1; ++jj) {
-          const int j = jj - KH;
-          const float2 w = LDBP_WIN(u, hl, hr, k - j);
-          dh[jj].x = fmaf(gk.x, w.x, fmaf(gk.y, w.y, dh[jj].x));
-          dh[jj].y = fmaf(gk.y, w.x, fmaf(-gk.x, w.y, dh[jj].y));
-        }
+        for (int jj = 0; jj < 2 * KH + 1; ++jj) tmac2(dh[jj], dhb[jj], gt, LDBP_WIN(u, hl, hr, k - (jj - KH)));
       }
     }
+#pragma unroll
+    for (int j = 0; j < NTU; ++j) dh[j] = add2(dh[j], dhb[j]);
     // FIR adjoint: g_s = sum_j conj(h_j) ga_{s+j}
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      float2 acc;
+      f2x acc_a, acc_b;
       if constexpr (SYM) {
-        const float2 c = ga[k];
-        acc.x = hs[0].x * c.x;
-        acc.y = hs[0].x * c.y;
-        acc.x = fmaf(hs[0].y, c.y, acc.x);
-        acc.y = fmaf(-hs[0].y, c.x, acc.y);
+        acc_a = mul2(bcast(lof(ga[k])), hs[0].a);
+        acc_b = mul2(bcast(hif(ga[k])), hs[0].b);
 #pragma unroll
-        for (int j = 1; j <= KH; ++j) {
-          const float2 l2 = LDBP_WIN(ga, gl, gr, k - j);
-          const float2 r2 = LDBP_WIN(ga, gl, gr, k + j);
-          const float2 s = make_float2(l2.x + r2.x, l2.y + r2.y);
-          acc.x = fmaf(hs[j].x, s.x, acc.x);
-          acc.y = fmaf(hs[j].x, s.y, acc.y);
-          acc.x = fmaf(hs[j].y, s.y, acc.x);
-          acc.y = fmaf(-hs[j].y, s.x, acc.y);
-        }
+        for (int j = 1; j <= KH; ++j)
+          tmac2(acc_a, acc_b, hs[j], add2(LDBP_WIN(ga, gl, gr, k - j), LDBP_WIN(ga, gl, gr, k + j)));
       } else {
-        acc = make_float2(0.f, 0.f);
+        const f2x w0 = LDBP_WIN(ga, gl, gr, k - KH);
+        acc_a = mul2(bcast(lof(w0)), hs[0].a);
+        acc_b = mul2(bcast(hif(w0)), hs[0].b);
 #pragma unroll
-        for (int jj = 0; jj < 2 * KH + 1; ++jj) {
-          const int j = jj - KH;
-          const float2 w = LDBP_WIN(ga, gl, gr, k + j);
-          acc.x = fmaf(hs[jj].x, w.x, acc.x);
-          acc.y = fmaf(hs[jj].x, w.y, acc.y);
-          acc.x = fmaf(hs[jj].y, w.y, acc.x);
-          acc.y = fmaf(-hs[jj].y, w.x, acc.y);
-        }
+        for (int jj = 1; jj < 2 * KH + 1; ++jj) tmac2(acc_a, acc_b, hs[jj], LDBP_WIN(ga, gl, gr, k + (jj - KH)));
       }
-      g[k] = acc;
+      g[k] = add2(acc_a, acc_b);
     }
     // per-warp reduction of this step's partials (transposing butterfly, see above)
     {
@@ -571,7 +726,7 @@ __global__ void __launch_bounds__(256) bwd_segment_kernel(const BwdArgs a) {
       float vals[VP];
       vals[0] = dgam;
 #pragma unroll
-      for (int j = 0; j < NTU; ++j) { vals[1 + 2 * j] = dh[j].x; vals[2 + 2 * j] = dh[j].y; }
+      for (int j = 0; j < NTU; ++j) { vals[1 + 2 * j] = lof(dh[j]); vals[2 + 2 * j] = hif(dh[j]); }
 #pragma unroll
       for (int i = V; i < VP; ++i) vals[i] = 0.f;
       const float r = warp_reduce_scatter<VP>(vals, lane);
