@@ -1,0 +1,6 @@
+# One GPU call: full bench line, reference arm, launch list (ncu) for profiles/.
+set -x
+timeout 600 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo bench_exit=$?
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_exit=$?
+timeout 300 python bench.py --steps 2 --warmup 3 --no-extra --no-cpu > gpurun_out/b_small.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 2 --warmup 3 --no-extra --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo ncu_exit=$?
