@@ -155,18 +155,20 @@ struct Tile {
 
 size_t fwd_smem(int kh, bool sym, int steps) {
   return sizeof(uint64_t) * 2 * ldbp::kMaxWarps + sizeof(float2) * 4 * ldbp::kMaxWarps * std::max(kh, 1) +
-         sizeof(ldbp::TapP) * steps * ntaps_used(kh, sym) + sizeof(float) * steps + 16;
+         sizeof(ldbp::TapP) * steps * ntaps_used(kh, sym) + sizeof(ldbp::StepNorm) * steps + sizeof(float) * steps +
+         32;
 }
 
 size_t bwd_smem(int kh, bool sym, int steps, int nthreads) {
   const int nw = nthreads / 32;
   const int V = 1 + 2 * ntaps_used(kh, sym);
-  size_t s = sizeof(uint64_t) * 2 * ldbp::kMaxWarps;                   // mbarriers
-  s += sizeof(float2) * 8 * ldbp::kMaxWarps * std::max(kh, 1);          // two edge arrays
+  size_t s = sizeof(uint64_t) * 2 * ldbp::kBwdWarps;                   // mbarriers
+  s += sizeof(float2) * 8 * ldbp::kBwdWarps * std::max(kh, 1);          // two edge arrays
   s += 2 * sizeof(ldbp::TapP) * steps * ntaps_used(kh, sym);             // packed fwd + adj taps
-  s += sizeof(float) * ((steps + 3) & ~3);                              // gamma
+  s += sizeof(ldbp::StepNorm) * steps;                                  // normalisation
+  s += sizeof(float) * ((steps + 3) & ~3) + 16;                         // gamma + flag
   s += sizeof(float) * ((steps * nw * V + 3) & ~3);                     // per-warp partials
-  s += sizeof(float2) * size_t(steps) * kBwdR * nthreads;               // tape
+  s += sizeof(float2) * size_t(steps + 1) * kBwdR * nthreads;           // tape + prefetch buffer
   return s;
 }
 

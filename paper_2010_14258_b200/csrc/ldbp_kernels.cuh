@@ -29,6 +29,9 @@
 #define LDBP_BWD_R 8   // samples per thread, backward kernels
 #endif
 
+#ifndef LDBP_NORM
+#define LDBP_NORM 1  // h0-normalised FIR when well conditioned (saves one complex multiply per FIR)
+#endif
 #ifndef LDBP_NB_SYNC
 #define LDBP_NB_SYNC 0  // 1: neighbour-only mbarrier sync per step (measured 2x slower on B200; kept
                         // as an option), 0: one __syncthreads per step
@@ -192,6 +195,27 @@ __device__ __forceinline__ void store_mapped(float2* __restrict__ dst, const Sto
   }
 }
 
+// Same, storing P * u[k] (complex scale applied per sample on the way out, no extra registers).
+template <int R>
+__device__ __forceinline__ void store_mapped_scaled(float2* __restrict__ dst, const StoreMap& sm, int64_t e0,
+                                                    const Geo& g, const f2x (&u)[R], float2 P) {
+  f2x* d2 = reinterpret_cast<f2x*>(dst);
+  const f2x pa = pk(P.x, P.y), pb = pk(-P.y, P.x);
+  if (sm.off >= 0) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) d2[sm.off + k] = fma2(bcast(lof(u[k])), pa, mul2(bcast(hif(u[k])), pb));
+  } else if (sm.mask) {
+    const Span sp = make_span(e0, g);
+    int64_t b = sp.b0;
+    int q = sp.q0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (sm.mask & (1u << k)) d2[b * g.n + (q - g.H)] = fma2(bcast(lof(u[k])), pa, mul2(bcast(hif(u[k])), pb));
+      if (++q == g.ext) { q = 0; ++b; }
+    }
+  }
+}
+
 template <int R>
 __device__ __forceinline__ void store_owned(float2* __restrict__ dst, int64_t e0, const Geo& g, f2x (&u)[R]) {
   const StoreMap sm = store_map<R>(e0, g);
@@ -200,7 +224,7 @@ __device__ __forceinline__ void store_owned(float2* __restrict__ dst, int64_t e0
 
 // Halo exchange of one register array: hl = Kh samples left of u[0], hr = Kh samples right
 // of u[R-1].  Shuffles inside the warp; warp edges through sh[2 buffers][2 sides][32 warps][KH].
-template <int KH, int R>
+template <int KH, int R, int MW = kMaxWarps>
 __device__ __forceinline__ void exchange(const f2x (&u)[R], f2x (&hl)[KH > 0 ? KH : 1], f2x (&hr)[KH > 0 ? KH : 1],
                                          f2x* sh, int buf, int lane, int warp, int nwarps) {
   if constexpr (KH > 0) {
@@ -209,8 +233,8 @@ __device__ __forceinline__ void exchange(const f2x (&u)[R], f2x (&hl)[KH > 0 ? K
       hl[j] = __shfl_up_sync(kFull, u[R - KH + j], 1);
       hr[j] = __shfl_down_sync(kFull, u[j], 1);
     }
-    f2x* head = sh + ((buf * 2 + 0) * kMaxWarps) * KH;
-    f2x* tail = sh + ((buf * 2 + 1) * kMaxWarps) * KH;
+    f2x* head = sh + ((buf * 2 + 0) * MW) * KH;
+    f2x* tail = sh + ((buf * 2 + 1) * MW) * KH;
     if (lane == 0) {
 #pragma unroll
       for (int j = 0; j < KH; ++j) head[warp * KH + j] = u[j];
@@ -268,7 +292,7 @@ __device__ __forceinline__ void nb_init(uint64_t* bars) {
 }
 
 // Exchange of up to two arrays (N = 1 or 2) with neighbour-only synchronisation.
-template <int KH, int R, int N>
+template <int KH, int R, int N, int MW = kMaxWarps>
 __device__ __forceinline__ void exchange_nb(const f2x (&u)[R], f2x (&hl)[KH > 0 ? KH : 1], f2x (&hr)[KH > 0 ? KH : 1],
                                             f2x* sh, const f2x (&v)[R], f2x (&gl)[KH > 0 ? KH : 1],
                                             f2x (&gr)[KH > 0 ? KH : 1], f2x* sh2, uint64_t* bars, int it, int lane,
@@ -285,10 +309,10 @@ __device__ __forceinline__ void exchange_nb(const f2x (&u)[R], f2x (&hl)[KH > 0 
         gr[j] = __shfl_down_sync(kFull, v[j], 1);
       }
     }
-    f2x* head = sh + ((b * 2 + 0) * kMaxWarps) * KH;
-    f2x* tail = sh + ((b * 2 + 1) * kMaxWarps) * KH;
-    f2x* head2 = sh2 + ((b * 2 + 0) * kMaxWarps) * KH;
-    f2x* tail2 = sh2 + ((b * 2 + 1) * kMaxWarps) * KH;
+    f2x* head = sh + ((b * 2 + 0) * MW) * KH;
+    f2x* tail = sh + ((b * 2 + 1) * MW) * KH;
+    f2x* head2 = sh2 + ((b * 2 + 0) * MW) * KH;
+    f2x* tail2 = sh2 + ((b * 2 + 1) * MW) * KH;
     if (lane == 0) {
 #pragma unroll
       for (int j = 0; j < KH; ++j) {
@@ -304,9 +328,9 @@ __device__ __forceinline__ void exchange_nb(const f2x (&u)[R], f2x (&hl)[KH > 0 
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(bars + b * kMaxWarps + warp);
+    if (lane == 0) mbar_arrive(bars + b * MW + warp);
     if (lane == 0 && warp > 0) {
-      mbar_wait(bars + b * kMaxWarps + warp - 1, parity);
+      mbar_wait(bars + b * MW + warp - 1, parity);
 #pragma unroll
       for (int j = 0; j < KH; ++j) {
         hl[j] = tail[(warp - 1) * KH + j];
@@ -314,7 +338,7 @@ __device__ __forceinline__ void exchange_nb(const f2x (&u)[R], f2x (&hl)[KH > 0 
       }
     }
     if (lane == 31 && warp < nwarps - 1) {
-      mbar_wait(bars + b * kMaxWarps + warp + 1, parity);
+      mbar_wait(bars + b * MW + warp + 1, parity);
 #pragma unroll
       for (int j = 0; j < KH; ++j) {
         hr[j] = head[(warp + 1) * KH + j];
@@ -329,7 +353,7 @@ __device__ __forceinline__ void exchange_nb(const f2x (&u)[R], f2x (&hl)[KH > 0 
 }
 
 // Two arrays exchanged around one barrier (backward reverse sweep).
-template <int KH, int R>
+template <int KH, int R, int MW = kMaxWarps>
 __device__ __forceinline__ void exchange2(const f2x (&u)[R], f2x (&hl)[KH > 0 ? KH : 1], f2x (&hr)[KH > 0 ? KH : 1],
                                           f2x* sh, int buf, const f2x (&v)[R], f2x (&gl)[KH > 0 ? KH : 1],
                                           f2x (&gr)[KH > 0 ? KH : 1], f2x* sh2, int buf2, int lane, int warp,
@@ -342,10 +366,10 @@ __device__ __forceinline__ void exchange2(const f2x (&u)[R], f2x (&hl)[KH > 0 ? 
       gl[j] = __shfl_up_sync(kFull, v[R - KH + j], 1);
       gr[j] = __shfl_down_sync(kFull, v[j], 1);
     }
-    f2x* head = sh + ((buf * 2 + 0) * kMaxWarps) * KH;
-    f2x* tail = sh + ((buf * 2 + 1) * kMaxWarps) * KH;
-    f2x* head2 = sh2 + ((buf2 * 2 + 0) * kMaxWarps) * KH;
-    f2x* tail2 = sh2 + ((buf2 * 2 + 1) * kMaxWarps) * KH;
+    f2x* head = sh + ((buf * 2 + 0) * MW) * KH;
+    f2x* tail = sh + ((buf * 2 + 1) * MW) * KH;
+    f2x* head2 = sh2 + ((buf2 * 2 + 0) * MW) * KH;
+    f2x* tail2 = sh2 + ((buf2 * 2 + 1) * MW) * KH;
     if (lane == 0) {
 #pragma unroll
       for (int j = 0; j < KH; ++j) { head[warp * KH + j] = u[j]; head2[warp * KH + j] = v[j]; }
@@ -418,11 +442,21 @@ __device__ __forceinline__ f2x tmul(const TapP& t, f2x s) { return fma2(bcast(lo
 // One FIR output k (compile-time), a_k = sum_j h_j w_{k-j} (packed FP32x2 complex MACs).
 // SYM: taps hs[0..KH] = h_0..h_KH (folded, fig:filter P:494-509: pre-add u_{k-j}+u_{k+j}).
 // GEN: taps hs[0..2KH] = h_{-KH}..h_{KH}.
-template <int KH, int R, bool SYM, int K>
+template <int KH, int R, bool SYM, int K, bool NORM = false>
 __device__ __forceinline__ f2x fir_at(const f2x (&u)[R], const f2x (&hl)[KH > 0 ? KH : 1],
                                       const f2x (&hr)[KH > 0 ? KH : 1], const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1]) {
   f2x acc_a, acc_b;
-  if constexpr (SYM) {
+  if constexpr (SYM && NORM) {
+    // h0-normalised folded FIR: h_0 = 1, a_k = u_k + sum_j h_j (u_{k-j} + u_{k+j})
+    if constexpr (KH == 0) return u[K];
+    acc_a = u[K];
+    const f2x s1 = add2(LDBP_WIN(u, hl, hr, K - 1), LDBP_WIN(u, hl, hr, K + 1));
+    acc_a = fma2(bcast(lof(s1)), hs[1].a, acc_a);
+    acc_b = mul2(bcast(hif(s1)), hs[1].b);
+#pragma unroll
+    for (int j = 2; j <= KH; ++j)
+      tmac2(acc_a, acc_b, hs[j], add2(LDBP_WIN(u, hl, hr, K - j), LDBP_WIN(u, hl, hr, K + j)));
+  } else if constexpr (SYM) {
     acc_a = mul2(bcast(lof(u[K])), hs[0].a);
     acc_b = mul2(bcast(hif(u[K])), hs[0].b);
 #pragma unroll
@@ -458,27 +492,117 @@ __device__ __forceinline__ f2x kerr(f2x a, float g) {
   return fma2(bcast(ax), pk(c, s), mul2(bcast(ay), pk(-s, c)));
 }
 
+#ifndef LDBP_PIPE_D
+#define LDBP_PIPE_D 2  // software-pipelining distance between FIR(k) and Kerr(k - D) in one step
+#endif
+// One full step (FIR + Kerr) for the R samples with the Kerr of sample k-D issued right after
+// the FIR of sample k, so each warp's instruction stream mixes FMA-pipe and MUFU work instead
+// of a pure-FMA phase followed by a MUFU-bound phase (all warps of a CTA are phase-aligned by
+// the per-step barrier, so phase separation would idle one pipe at a time).
+template <int KH, int R, bool SYM, bool FAST, bool NORM, int K = 0>
+__device__ __forceinline__ void step_pipelined(const f2x (&u)[R], const f2x (&hl)[KH > 0 ? KH : 1],
+                                               const f2x (&hr)[KH > 0 ? KH : 1],
+                                               const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1], float gm, f2x (&acc)[R],
+                                               f2x (&out)[R]) {
+  constexpr int D = LDBP_PIPE_D;
+  if constexpr (K < R + D) {
+    if constexpr (K < R) acc[K] = fir_at<KH, R, SYM, K, NORM>(u, hl, hr, hs);
+    if constexpr (K >= D) out[K - D] = kerr<FAST>(acc[K - D], gm);
+    step_pipelined<KH, R, SYM, FAST, NORM, K + 1>(u, hl, hr, hs, gm, acc, out);
+  }
+}
+
 template <bool SYM, int KH>
 __device__ __forceinline__ constexpr int ntaps_used() { return SYM ? KH + 1 : 2 * KH + 1; }
 
+// Per-step normalisation data (h0-normalised model).
+struct StepNorm {
+  float2 P;  // P_rel(i) = prod_{k=s0..i} c_k, c_k = h0^(k): u^(i+1) = P_rel(i) * u_hat^(i+1)
+  float2 c;  // c_i = h0^(i)
+};
+
 // Stage the packed taps and gamma of steps [s0, s1) into shared memory (masked taps -> 0;
 // SYM keeps only h_0..h_Kh).  ADJ additionally stages the adjoint (conjugate) packing.
+// SYM: thread 0 first decides whether the h0-normalised model is well conditioned for this
+// launch (|h0|^2 >= 1e-6 sum|h|^2 at every step and 1e-12 <= |P_rel| <= 1e12); if so the staged
+// taps are h/h0, gamma is gamma*|P_rel|^2 and *sh_flag = 1.
 template <int KH, bool SYM, bool ADJ>
 __device__ __forceinline__ void stage_params(const float2* __restrict__ taps, const float* __restrict__ gamma,
                                              const uint8_t* __restrict__ mask, int T, int s0, int s1,
-                                             TapP* sh_taps, TapP* sh_taps_adj, float* sh_gamma) {
+                                             TapP* sh_taps, TapP* sh_taps_adj, float* sh_gamma, StepNorm* sh_norm,
+                                             int* sh_flag) {
   constexpr int NT = ntaps_used<SYM, KH>();
+  auto tap = [&](int s, int t) -> float2 {
+    float2 h = taps[(int64_t)s * T + t];
+    if (mask && !mask[(int64_t)s * T + t]) h = make_float2(0.f, 0.f);
+    return h;
+  };
+  const int S = s1 - s0;
+  if (threadIdx.x == 0) *sh_flag = (SYM && LDBP_NORM) ? 1 : 0;
+  __syncthreads();
+  // phase A (parallel over steps): c_i = h0 and its conditioning
+  if (SYM && LDBP_NORM)
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+      const float2 h0 = tap(s0 + i, KH);
+      float e = 0.f;
+      for (int t = 0; t < T; ++t) {
+        const float2 h = tap(s0 + i, t);
+        e = fmaf(h.x, h.x, fmaf(h.y, h.y, e));
+      }
+      const float m0 = h0.x * h0.x + h0.y * h0.y;
+      if (!(m0 > 0.f) || m0 < 1e-6f * e) *sh_flag = 0;
+      sh_norm[i].c = h0;
+    }
+  __syncthreads();
+  // phase B (one thread, from shared memory): prefix products P_rel(i) in fp64
+  if (threadIdx.x == 0 && *sh_flag) {
+    double pr = 1.0, pi = 0.0;
+    int ok = 1;
+    for (int i = 0; i < S; ++i) {
+      const float2 c = sh_norm[i].c;
+      const double nr = pr * c.x - pi * c.y, ni = pr * c.y + pi * c.x;
+      pr = nr;
+      pi = ni;
+      const double mp = pr * pr + pi * pi;
+      if (!(mp >= 1e-24 && mp <= 1e24)) ok = 0;
+      sh_norm[i].P = make_float2((float)pr, (float)pi);
+    }
+    *sh_flag = ok;
+  }
+  __syncthreads();
+  // phase C (parallel): gamma_hat = gamma |P_rel|^2, or the plain model
+  {
+    const bool nrm = *sh_flag != 0;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+      if (nrm) {
+        const float2 P = sh_norm[i].P;
+        sh_gamma[i] = (float)((double)gamma[s0 + i] * ((double)P.x * P.x + (double)P.y * P.y));
+      } else {
+        sh_norm[i].P = make_float2(1.f, 0.f);
+        sh_norm[i].c = make_float2(1.f, 0.f);
+        sh_gamma[i] = gamma[s0 + i];
+      }
+    }
+  }
+  const bool norm = *sh_flag != 0;
   const int cnt = (s1 - s0) * NT;
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
     const int s = s0 + i / NT;
     const int t = (i % NT) + (SYM ? KH : 0);  // index into the stored [T] row
-    float2 h = taps[(int64_t)s * T + t];
-    if (mask && !mask[(int64_t)s * T + t]) h = make_float2(0.f, 0.f);
+    float2 h = tap(s, t);
+    if (norm) {  // h / c = h conj(c) / |c|^2
+      const float2 c = sh_norm[s - s0].c;
+      const float inv = 1.f / (c.x * c.x + c.y * c.y);
+      h = make_float2((h.x * c.x + h.y * c.y) * inv, (h.y * c.x - h.x * c.y) * inv);
+      if (t == KH) h = make_float2(1.f, 0.f);
+    }
     sh_taps[i] = tap_fwd(h);
     if constexpr (ADJ) sh_taps_adj[i] = tap_adj(h);
   }
-  for (int i = threadIdx.x; i < s1 - s0; i += blockDim.x) sh_gamma[i] = gamma[s0 + i];
 }
+
+// P * v for a staged complex scale P.
+__device__ __forceinline__ f2x cscale(float2 P, f2x v) { return tmul(tap_fwd(P), v); }
 
 struct FwdArgs {
   const float2* src;
@@ -498,28 +622,19 @@ struct FwdArgs {
 // ---------------------------------------------------------------------------------------
 // Register budget per Kh: packed taps cost 4 registers each (TapP), so wider filters get
 // fewer threads per CTA (the planner reads fwd_max_threads()).
-__host__ __device__ constexpr int fwd_max_threads(int kh) { return kh <= 2 ? 512 : 256; }
-__host__ __device__ constexpr int fwd_min_blocks(int kh) { return kh <= 2 ? 2 : kh <= 4 ? 3 : 2; }
+#ifndef LDBP_FWD_WIDE_THREADS
+#define LDBP_FWD_WIDE_THREADS 256
+#endif
+__host__ __device__ constexpr int fwd_max_threads(int kh) { return kh <= 2 ? 512 : kh <= 5 ? 256 : LDBP_FWD_WIDE_THREADS; }
+__host__ __device__ constexpr int fwd_min_blocks(int kh) {
+  return kh <= 2 ? 2 : kh <= 4 ? 3 : (LDBP_FWD_WIDE_THREADS >= 512 && kh >= 6) ? 1 : 2;
+}
 
-template <int KH, int R, bool SYM, bool FAST>
-__global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_tile_kernel(const FwdArgs a) {
+template <int KH, int R, bool SYM, bool FAST, bool NORM>
+__device__ __forceinline__ void fwd_steps(const FwdArgs& a, f2x (&u)[R], const TapP* sh_taps, const float* sh_gamma,
+                                          const StepNorm* sh_norm, f2x* sh_edge, uint64_t* bars, const StoreMap& smap,
+                                          int64_t e0, int lane, int warp, int nwarps) {
   constexpr int NTU = ntaps_used<SYM, KH>();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                            // [2][32] mbarriers
-  f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);                       // 2*2*32*KH
-  TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge + 4 * kMaxWarps * (KH > 0 ? KH : 1));  // (s1-s0)*NTU
-  float* sh_gamma = reinterpret_cast<float*>(sh_taps + (a.s1 - a.s0) * NTU);
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  stage_params<KH, SYM, false>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, nullptr, sh_gamma);
-  if (LDBP_NB_SYNC) nb_init(bars);
-
-  f2x u[R];
-  const int64_t e0 = thread_e0(a.g, R);
-  load_window<R>(a.src, e0, a.g, u);
-  const StoreMap smap = store_map<R>(e0, a.g);
-  __syncthreads();
-
   f2x hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1];
   for (int s = 0; s < a.s1 - a.s0; ++s) {
     TapP hs[NTU];
@@ -530,17 +645,51 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
       exchange_nb<KH, R, 1>(u, hl, hr, sh_edge, u, hl, hr, sh_edge, bars, s, lane, warp, nwarps);
     else
       exchange<KH, R>(u, hl, hr, sh_edge, s & 1, lane, warp, nwarps);
-    f2x acc[R];
-    fir_all<KH, R, SYM>(u, hl, hr, hs, acc);
+    f2x acc[R], nu[R];
+    step_pipelined<KH, R, SYM, FAST, NORM>(u, hl, hr, hs, gm, acc, nu);
 #pragma unroll
-    for (int k = 0; k < R; ++k) u[k] = kerr<FAST>(acc[k], gm);
-    if (a.ckpt) {
-      const int gs = a.s0 + s + 1;  // global step count reached
-      if (gs < a.s1 && gs % a.ckpt_every == 0)
+    for (int k = 0; k < R; ++k) u[k] = nu[k];
+    const int gs = a.s0 + s + 1;  // global step count reached
+    if (a.ckpt && gs < a.s1 && gs % a.ckpt_every == 0) {
+      if constexpr (NORM) {
+        store_mapped_scaled<R>(a.ckpt + (int64_t)(gs / a.ckpt_every - 1) * a.ckpt_stride, smap, e0, a.g, u,
+                               sh_norm[s].P);
+      } else {
         store_mapped<R>(a.ckpt + (int64_t)(gs / a.ckpt_every - 1) * a.ckpt_stride, smap, e0, a.g, u);
+      }
     }
   }
-  store_mapped<R>(a.dst, smap, e0, a.g, u);
+  if constexpr (NORM)
+    store_mapped_scaled<R>(a.dst, smap, e0, a.g, u, sh_norm[a.s1 - a.s0 - 1].P);
+  else
+    store_mapped<R>(a.dst, smap, e0, a.g, u);
+}
+
+template <int KH, int R, bool SYM, bool FAST>
+__global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_tile_kernel(const FwdArgs a) {
+  constexpr int NTU = ntaps_used<SYM, KH>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int S = a.s1 - a.s0;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                            // [2][32] mbarriers
+  f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);                       // 2*2*32*KH
+  TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge + 4 * kMaxWarps * (KH > 0 ? KH : 1));  // S*NTU
+  StepNorm* sh_norm = reinterpret_cast<StepNorm*>(sh_taps + S * NTU);                // S
+  float* sh_gamma = reinterpret_cast<float*>(sh_norm + S);                           // S
+  int* sh_flag = reinterpret_cast<int*>(sh_gamma + S);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (LDBP_NB_SYNC) nb_init(bars);
+  f2x u[R];
+  const int64_t e0 = thread_e0(a.g, R);
+  load_window<R>(a.src, e0, a.g, u);
+  const StoreMap smap = store_map<R>(e0, a.g);
+  stage_params<KH, SYM, false>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, nullptr, sh_gamma, sh_norm,
+                               sh_flag);
+  __syncthreads();
+  if (SYM && *sh_flag)
+    fwd_steps<KH, R, SYM, FAST, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane, warp, nwarps);
+  else
+    fwd_steps<KH, R, SYM, FAST, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane, warp, nwarps);
 }
 
 struct BwdArgs {
@@ -570,81 +719,102 @@ __device__ __forceinline__ float warp_sum(float v) {
 // partial sums of dgamma' and dtaps per step (fp32 within the CTA, fp64 out).
 // Tape layout: tape[(l*R + k)*NT + tid] = u^(s0+l)[thread tid, sample k] (conflict free).
 // ---------------------------------------------------------------------------------------
-template <int KH, int R, bool SYM, bool FAST>
-#ifndef LDBP_BWD_MINB
-#define LDBP_BWD_MINB 2
-#endif
-__global__ void __launch_bounds__(256, LDBP_BWD_MINB) bwd_segment_kernel(const BwdArgs a) {
+constexpr int kBwdWarps = 8;  // backward CTAs have at most 256 threads
+
+// cp.async (LDGSTS) 8-byte global -> shared copy, and the wait for all of this thread's copies.
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+struct BwdSmem {
+  uint64_t* bars;
+  f2x* sh_edge;
+  f2x* sh_edge2;
+  TapP* sh_taps;
+  TapP* sh_taps_adj;
+  StepNorm* sh_norm;
+  float* sh_gamma;
+  int* sh_flag;
+  float* sh_red;
+  f2x* tape;
+  f2x* pre;  // [R][nthr] prefetched target / incoming adjoint (fast-path threads)
+};
+
+template <int KH, int R, bool SYM, bool FAST, bool NORM>
+__device__ __forceinline__ void bwd_body(const BwdArgs& a, const BwdSmem& sm, f2x (&u)[R], uint32_t own, int64_t e0,
+                                         bool prefetched, int lane, int warp, int nwarps) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   constexpr int V = 1 + 2 * NTU;  // [dgamma | dtap re/im ...]
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int C = a.s1 - a.s0;
   const int nthr = blockDim.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = nthr >> 5;
-
-  // carve-up (every region 16-byte aligned; mirrored by bwd_smem() on the host)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [2][32] mbarriers
-  f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);  // two arrays: 2 * (2*2*32*KH)
-  f2x* sh_edge2 = sh_edge + 4 * kMaxWarps * (KH > 0 ? KH : 1);
-  TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge2 + 4 * kMaxWarps * (KH > 0 ? KH : 1));
-  TapP* sh_taps_adj = sh_taps + C * NTU;
-  float* sh_gamma = reinterpret_cast<float*>(sh_taps_adj + C * NTU);
-  float* sh_red = sh_gamma + ((C + 3) & ~3);                  // [C][nwarps][V]
-  f2x* tape = reinterpret_cast<f2x*>(sh_red + ((C * nwarps * V + 3) & ~3));  // [C][R][nthr]
-
-  stage_params<KH, SYM, true>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, sh_taps_adj, sh_gamma);
-  if (LDBP_NB_SYNC) nb_init(bars);
-
-  f2x u[R];
-  const int64_t e0 = thread_e0(a.g, R);
-  load_window<R>(a.ck, e0, a.g, u);
-  const uint32_t own = owned_mask<R>(e0, a.g);
-  __syncthreads();
+  f2x* tape = sm.tape;
 
   f2x hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1];
-  // ---- forward recompute, tape = inputs of each step ----
+  // ---- forward recompute, tape = inputs of each step (normalised state u_hat when NORM) ----
   for (int l = 0; l < C; ++l) {
 #pragma unroll
     for (int k = 0; k < R; ++k) tape[(l * R + k) * nthr + threadIdx.x] = u[k];
     TapP hs[NTU];
 #pragma unroll
-    for (int j = 0; j < NTU; ++j) hs[j] = sh_taps[l * NTU + j];
-    const float gm = sh_gamma[l];
+    for (int j = 0; j < NTU; ++j) hs[j] = sm.sh_taps[l * NTU + j];
+    const float gm = sm.sh_gamma[l];
     if (LDBP_NB_SYNC)
-      exchange_nb<KH, R, 1>(u, hl, hr, sh_edge, u, hl, hr, sh_edge, bars, l, lane, warp, nwarps);
+      exchange_nb<KH, R, 1, kBwdWarps>(u, hl, hr, sm.sh_edge, u, hl, hr, sm.sh_edge, sm.bars, l, lane, warp, nwarps);
     else
-      exchange<KH, R>(u, hl, hr, sh_edge, l & 1, lane, warp, nwarps);
-    f2x acc[R];
-    fir_all<KH, R, SYM>(u, hl, hr, hs, acc);
+      exchange<KH, R, kBwdWarps>(u, hl, hr, sm.sh_edge, l & 1, lane, warp, nwarps);
+    f2x acc[R], nu[R];
+    step_pipelined<KH, R, SYM, FAST, NORM>(u, hl, hr, hs, gm, acc, nu);
 #pragma unroll
-    for (int k = 0; k < R; ++k) u[k] = kerr<FAST>(acc[k], gm);
+    for (int k = 0; k < R; ++k) u[k] = nu[k];
   }
 
-  // ---- seed / incoming adjoint ----
+  // ---- seed / incoming adjoint (for the normalised state: g_hat = conj(P_end) g) ----
+  const float2 Pend = sm.sh_norm[C - 1].P;
+  const TapP conjP = tap_adj(Pend);  // conj(P) * v
   f2x g[R];
+  // target / incoming adjoint: prefetched into shared memory at kernel start (fast-path threads)
+  const bool pf = prefetched;
+  cp_async_wait_all();
   if (a.gin == nullptr) {
     f2x t[R];
-    load_window<R>(a.target, e0, a.g, t);
+    if (pf) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) t[k] = sm.pre[k * nthr + threadIdx.x];
+    } else {
+      load_window<R>(a.target, e0, a.g, t);
+    }
     float lsum = 0.f;
     const f2x m1 = bcast(-1.f);
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const f2x e = fma2(m1, t[k], u[k]);  // y - target
-      g[k] = mul2(bcast(a.seed_scale), e);
+      const f2x y = NORM ? cscale(Pend, u[k]) : u[k];
+      const f2x e = fma2(m1, t[k], y);  // y - target
+      const f2x ge = mul2(bcast(a.seed_scale), e);
+      g[k] = NORM ? tmul(conjP, ge) : ge;
       const float ex = lof(e), ey = hif(e);
       if (own & (1u << k)) lsum = fmaf(ex, ex, fmaf(ey, ey, lsum));
     }
     lsum = warp_sum(lsum);
-    if (lane == 0) sh_red[warp] = lsum;  // reused below only after a barrier
+    if (lane == 0) sm.sh_red[warp] = lsum;  // reused below only after a barrier
     __syncthreads();
     if (threadIdx.x == 0) {
       double tot = 0.0;
-      for (int w = 0; w < nwarps; ++w) tot += (double)sh_red[w];
+      for (int w = 0; w < nwarps; ++w) tot += (double)sm.sh_red[w];
       a.loss_partials[blockIdx.x] = tot;
     }
     __syncthreads();
   } else {
-    load_window<R>(a.gin, e0, a.g, g);
+    if (pf) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) g[k] = sm.pre[k * nthr + threadIdx.x];
+    } else {
+      load_window<R>(a.gin, e0, a.g, g);
+    }
+    if constexpr (NORM) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) g[k] = tmul(conjP, g[k]);
+    }
   }
 
   // ---- reverse sweep ----
@@ -652,8 +822,8 @@ __global__ void __launch_bounds__(256, LDBP_BWD_MINB) bwd_segment_kernel(const B
   for (int l = C - 1; l >= 0; --l) {
     TapP hs[NTU];
 #pragma unroll
-    for (int j = 0; j < NTU; ++j) hs[j] = sh_taps_adj[l * NTU + j];
-    const float gm = sh_gamma[l];
+    for (int j = 0; j < NTU; ++j) hs[j] = sm.sh_taps_adj[l * NTU + j];
+    const float gm = sm.sh_gamma[l];
     const float gm2 = 2.f * gm;
     // NL adjoint of step l: v = u (output of step l), g = dL/dv:
     //   c = Im(g conj v), t = g + 2 gamma' c v, ga = t e^{-j phi} = tx*(c,-s) + ty*(s,c).
@@ -677,9 +847,10 @@ __global__ void __launch_bounds__(256, LDBP_BWD_MINB) bwd_segment_kernel(const B
     // exchange halos of u and ga around one barrier.  The u buffers continue the forward
     // loop's parity sequence (the last forward exchange used (C-1)&1), hence (l+1)&1.
     if (LDBP_NB_SYNC)
-      exchange_nb<KH, R, 2>(u, hl, hr, sh_edge, ga, gl, gr, sh_edge2, bars, 2 * C - 1 - l, lane, warp, nwarps);
+      exchange_nb<KH, R, 2, kBwdWarps>(u, hl, hr, sm.sh_edge, ga, gl, gr, sm.sh_edge2, sm.bars, 2 * C - 1 - l, lane, warp,
+                            nwarps);
     else
-      exchange2<KH, R>(u, hl, hr, sh_edge, (l + 1) & 1, ga, gl, gr, sh_edge2, l & 1, lane, warp, nwarps);
+      exchange2<KH, R, kBwdWarps>(u, hl, hr, sm.sh_edge, (l + 1) & 1, ga, gl, gr, sm.sh_edge2, l & 1, lane, warp, nwarps);
     // tap gradients over owned samples: dh_j += ga_t conj(w),  w = u_{t-j} (+ u_{t+j} if SYM)
     //   ga conj(w) = lo(w)*ga + hi(w)*(gy, -gx)
     f2x dh[NTU], dhb[NTU];
@@ -701,11 +872,17 @@ __global__ void __launch_bounds__(256, LDBP_BWD_MINB) bwd_segment_kernel(const B
     }
 #pragma unroll
     for (int j = 0; j < NTU; ++j) dh[j] = add2(dh[j], dhb[j]);
-    // FIR adjoint: g_s = sum_j conj(h_j) ga_{s+j}
+    // FIR adjoint: g_s = sum_j conj(h_j) ga_{s+j}   (NORM: h_0 = 1)
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       f2x acc_a, acc_b;
-      if constexpr (SYM) {
+      if constexpr (SYM && NORM) {
+        acc_a = ga[k];
+        acc_b = 0ull;
+#pragma unroll
+        for (int j = 1; j <= KH; ++j)
+          tmac2(acc_a, acc_b, hs[j], add2(LDBP_WIN(ga, gl, gr, k - j), LDBP_WIN(ga, gl, gr, k + j)));
+      } else if constexpr (SYM) {
         acc_a = mul2(bcast(lof(ga[k])), hs[0].a);
         acc_b = mul2(bcast(hif(ga[k])), hs[0].b);
 #pragma unroll
@@ -718,7 +895,7 @@ __global__ void __launch_bounds__(256, LDBP_BWD_MINB) bwd_segment_kernel(const B
 #pragma unroll
         for (int jj = 1; jj < 2 * KH + 1; ++jj) tmac2(acc_a, acc_b, hs[jj], LDBP_WIN(ga, gl, gr, k + (jj - KH)));
       }
-      g[k] = add2(acc_a, acc_b);
+      g[k] = (SYM && NORM && KH == 0) ? acc_a : add2(acc_a, acc_b);
     }
     // per-warp reduction of this step's partials (transposing butterfly, see above)
     {
@@ -732,18 +909,97 @@ __global__ void __launch_bounds__(256, LDBP_BWD_MINB) bwd_segment_kernel(const B
       const float r = warp_reduce_scatter<VP>(vals, lane);
       constexpr int SH = VP == 2 ? 4 : VP == 4 ? 3 : VP == 8 ? 2 : VP == 16 ? 1 : 0;  // lanes per index = 32/VP
       const int idx = lane >> SH;
-      float* red = sh_red + (l * nwarps + warp) * V;
+      float* red = sm.sh_red + (l * nwarps + warp) * V;
       if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
     }
   }
-  if (a.gout) store_owned<R>(a.gout, e0, a.g, g);
+  if (a.gout) store_owned<R>(a.gout, e0, a.g, g);  // gout needs no scaling: P_rel before step s0 is 1
+}
+
+template <int KH, int R, bool SYM, bool FAST>
+#ifndef LDBP_BWD_MINB
+#define LDBP_BWD_MINB 2
+#endif
+__global__ void __launch_bounds__(256, LDBP_BWD_MINB) bwd_segment_kernel(const BwdArgs a) {
+  constexpr int NTU = ntaps_used<SYM, KH>();
+  constexpr int V = 1 + 2 * NTU;  // [dgamma | dtap re/im ...]
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int C = a.s1 - a.s0;
+  const int nthr = blockDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = nthr >> 5;
+
+  // carve-up (every region 16-byte aligned; mirrored by bwd_smem() on the host)
+  BwdSmem sm;
+  sm.bars = reinterpret_cast<uint64_t*>(smem_raw);  // [2][8] mbarriers
+  sm.sh_edge = reinterpret_cast<f2x*>(sm.bars + 2 * kBwdWarps);  // two arrays: 2 * (2*2*8*KH)
+  sm.sh_edge2 = sm.sh_edge + 4 * kBwdWarps * (KH > 0 ? KH : 1);
+  sm.sh_taps = reinterpret_cast<TapP*>(sm.sh_edge2 + 4 * kBwdWarps * (KH > 0 ? KH : 1));
+  sm.sh_taps_adj = sm.sh_taps + C * NTU;
+  sm.sh_norm = reinterpret_cast<StepNorm*>(sm.sh_taps_adj + C * NTU);
+  sm.sh_gamma = reinterpret_cast<float*>(sm.sh_norm + C);
+  sm.sh_flag = reinterpret_cast<int*>(sm.sh_gamma + ((C + 3) & ~3));
+  sm.sh_red = reinterpret_cast<float*>(sm.sh_flag + 4);                        // [C][nwarps][V]
+  sm.tape = reinterpret_cast<f2x*>(sm.sh_red + ((C * nwarps * V + 3) & ~3));  // [C][R][nthr]
+  sm.pre = sm.tape + (size_t)C * R * nthr;                                     // [R][nthr]
+
+  if (LDBP_NB_SYNC) {
+    for (int i = threadIdx.x; i < 2 * kBwdWarps; i += blockDim.x) mbar_init(sm.bars + i, 1);
+  }
+  const int64_t e0 = thread_e0(a.g, R);
+  // Issue the (late-needed) target / incoming-adjoint loads first, asynchronously into smem, so
+  // their latency overlaps the checkpoint load, the staging and the whole forward recompute.
+  bool prefetched = false;
+  {
+    const Span sp = make_span(e0, a.g);
+    if (span_fast<R>(sp, a.g, e0)) {
+      const float2* src = a.gin ? a.gin : a.target;
+      const float2* p = src + sp.b0 * a.g.n + (sp.q0 - a.g.H);
+#pragma unroll
+      for (int k = 0; k < R; ++k) cp_async8(sm.pre + k * nthr + threadIdx.x, p + k);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      prefetched = true;
+    }
+  }
+  f2x u[R];
+  load_window<R>(a.ck, e0, a.g, u);
+  const uint32_t own = owned_mask<R>(e0, a.g);
+  stage_params<KH, SYM, true>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sm.sh_taps, sm.sh_taps_adj, sm.sh_gamma,
+                              sm.sh_norm, sm.sh_flag);
   __syncthreads();
-  // CTA reduction in fp64, fixed order over warps.
-  for (int i = threadIdx.x; i < C * V; i += nthr) {
-    const int l = i / V, v = i % V;
-    double acc = 0.0;
-    for (int w = 0; w < nwarps; ++w) acc += (double)sh_red[(l * nwarps + w) * V + v];
-    a.partials[((int64_t)blockIdx.x * a.M + (a.s0 + l)) * V + v] = acc;
+  const bool norm = SYM && *sm.sh_flag;
+  if (norm)
+    bwd_body<KH, R, SYM, FAST, true>(a, sm, u, own, e0, prefetched, lane, warp, nwarps);
+  else
+    bwd_body<KH, R, SYM, FAST, false>(a, sm, u, own, e0, prefetched, lane, warp, nwarps);
+  __syncthreads();
+  // CTA reduction in fp64, fixed order over warps; normalised-model gradients are mapped back
+  // to the original parameters: dgamma_i = |P_rel(i)|^2 dgamma_hat_i, dh^(i) = conj(1/c_i) dh_hat^(i).
+  const int npairs = 1 + NTU;  // slot 0: dgamma, slots 1..: complex taps
+  for (int i = threadIdx.x; i < C * npairs; i += nthr) {
+    const int l = i / npairs, q = i % npairs;
+    double* out = a.partials + ((int64_t)blockIdx.x * a.M + (a.s0 + l)) * V;
+    const StepNorm nm = sm.sh_norm[l];
+    if (q == 0) {
+      double acc = 0.0;
+      for (int w = 0; w < nwarps; ++w) acc += (double)sm.sh_red[(l * nwarps + w) * V];
+      if (norm) acc *= (double)nm.P.x * nm.P.x + (double)nm.P.y * nm.P.y;
+      out[0] = acc;
+    } else {
+      const int v = 1 + 2 * (q - 1);
+      double re = 0.0, im = 0.0;
+      for (int w = 0; w < nwarps; ++w) {
+        re += (double)sm.sh_red[(l * nwarps + w) * V + v];
+        im += (double)sm.sh_red[(l * nwarps + w) * V + v + 1];
+      }
+      if (norm) {  // conj(1/c) = c / |c|^2
+        const double cx = nm.c.x, cy = nm.c.y, m = cx * cx + cy * cy;
+        const double r2 = (re * cx - im * cy) / m, i2 = (re * cy + im * cx) / m;
+        re = r2;
+        im = i2;
+      }
+      out[v] = re;
+      out[v + 1] = im;
+    }
   }
 }
 

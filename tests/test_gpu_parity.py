@@ -305,3 +305,67 @@ def test_snr_parity_on_simulated_link(P):
     assert snr[(-4.0, 15, True)] > 12.0
     assert snr[(2.0, 15, True)] > snr[(2.0, 15, False)] + 3.0
     assert snr[(6.0, 15, True)] > snr[(6.0, 15, False)] + 3.0
+
+
+def test_backward_unnormalised_path(P):
+    """Taps whose centre tap is ~0 make the h0-normalised kernels fall back to the plain folded
+    FIR (launch-wide, decided on the device); gradients must still match the oracle."""
+    B, n, M, T = 2, 900, 4, 5
+    x = li.gaussian_blocks(81, range(B), n, 1e-3)
+    gy = li.gaussian_blocks(81, range(B), n, 1.0, purpose="grad")
+    taps, gamma = model(81, M, T, True)
+    taps[2, 2] = 1e-6  # h0 of step 2 ~ 0 -> not normalisable
+    y = P.ldbp_forward(dev(x), dev(taps), dev(gamma, np.float32)).cpu().numpy()
+    assert rel(y, O.forward(r32(x), r32(taps), r32(gamma))) <= OUT_TOL
+    dt, dg, gx = P.ldbp_backward(dev(x), dev(gy), dev(taps), dev(gamma, np.float32))
+    rdt, rdg, rgx = O.backward(r32(x), r32(gy), r32(taps), r32(gamma))
+    rdt = O.sym_fold(rdt)
+    dt, dg = dt.cpu().numpy(), dg.cpu().numpy()
+    for i in range(M):
+        assert rel(dt[i], rdt[i]) <= GRAD_TOL, i
+    assert rel(dg, rdg) <= GRAD_TOL
+    assert rel(gx.cpu().numpy(), rgx) <= 1e-4
+
+
+def test_precise_backward(P):
+    B, n, M, T = 2, 1200, 5, 7
+    x = li.gaussian_blocks(82, range(B), n, 1e-3)
+    tgt = li.gaussian_blocks(82, range(B), n, 1e-3, purpose="target")
+    taps, gamma = model(82, M, T, True)
+    buf = P.ldbp_loss_grad(dev(x), dev(tgt), dev(taps), dev(gamma, np.float32), precise=True).cpu().numpy()
+    ref = O.loss_grad(r32(x), r32(tgt), r32(taps), r32(gamma), symmetric=True)
+    assert abs(buf[0] - ref[0]) <= 1e-6 * ref[0]
+    assert rel(buf[1:], ref[1:]) <= 2e-5
+
+
+def test_train_step_cuda_graph_capture(P):
+    """The ABI promises no host sync inside calls: a whole training step (loss_grad + Adam) is
+    captured in a CUDA graph and replayed; results equal eager execution."""
+    B, n, M, T = 4, 2048, 6, 9
+    x = dev(li.gaussian_blocks(83, range(B), n, 1e-3))
+    tgt = dev(li.gaussian_blocks(83, range(B), n, 1e-3, purpose="target"))
+    taps, gamma = model(83, M, T, True)
+    eager = P.TrainState.create(taps, gamma)
+    graphed = P.TrainState.create(taps, gamma)
+    ws = P.Workspace()
+    buf = torch.empty(1 + M + 2 * M * T, dtype=torch.float64, device="cuda")
+    # warm up on a side stream (allocates the workspace), then capture one step
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        P.ldbp_loss_grad(x, tgt, graphed.taps, graphed.gamma, buf=buf, ws=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        P.ldbp_loss_grad(x, tgt, graphed.taps, graphed.gamma, buf=buf, ws=ws)
+        P.ldbp_adam_update(graphed, buf, B * n)
+    graphed.t = 0  # capture advanced the host-side counter; the captured launch uses t = 1
+    for it in range(3):
+        b_e = P.ldbp_loss_grad(x, tgt, eager.taps, eager.gamma)
+        P.ldbp_adam_update(eager, b_e, B * n)
+        g.replay()
+        torch.cuda.synchronize()
+        if it == 0:
+            assert torch.equal(b_e, buf)
+            assert torch.equal(eager.master, graphed.master)
