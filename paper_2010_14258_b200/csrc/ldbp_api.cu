@@ -153,8 +153,9 @@ struct Tile {
   ldbp::Geo g{};
 };
 
-size_t fwd_smem(int kh, bool sym, int steps) {
-  return sizeof(uint64_t) * 2 * ldbp::kMaxWarps + sizeof(float2) * 4 * ldbp::kMaxWarps * std::max(kh, 1) +
+size_t fwd_smem(int kh, bool sym, int steps, int nthreads = 1024) {
+  const int edge_rows = LDBP_FWD_XSMEM ? nthreads : ldbp::kMaxWarps;
+  return sizeof(uint64_t) * 2 * ldbp::kMaxWarps + sizeof(float2) * 4 * edge_rows * std::max(kh, 1) +
          sizeof(ldbp::TapP) * steps * ntaps_used(kh, sym) + sizeof(ldbp::StepNorm) * steps + sizeof(float) * steps +
          32;
 }
@@ -168,7 +169,7 @@ size_t bwd_smem(int kh, bool sym, int steps, int nthreads) {
   s += sizeof(ldbp::StepNorm) * steps;                                  // normalisation
   s += sizeof(float) * ((steps + 3) & ~3) + 16;                         // gamma + flag
   s += sizeof(float) * ((steps * nw * V + 3) & ~3);                     // per-warp partials
-  s += sizeof(float2) * size_t(steps + 1) * kBwdR * nthreads;           // tape + prefetch buffer
+  s += sizeof(float2) * size_t(steps + LDBP_BWD_PREFETCH) * kBwdR * nthreads;  // tape (+ prefetch buffer)
   return s;
 }
 
@@ -279,13 +280,13 @@ Tile plan_fwd_tile(const ldbp_dims* d, int steps, bool query_device) {
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const int maxthr = std::min(env_int("LDBP_FWD_THREADS", kFwdMaxThreads), ldbp::fwd_max_threads(kh));
   int occ = 1, sms = 148;
-  const size_t smem = fwd_smem(kh, sym, steps);
+  const size_t smem = fwd_smem(kh, sym, steps, maxthr);
   if (query_device) {
     sms = device_sms();
     occ = fwd_occupancy(get_fwd(kh, sym, !(d->flags & LDBP_PRECISE)), maxthr, smem);
   }
   Tile t = plan_tiles(d->batch, d->n, steps * kh, kFwdR, maxthr, occ, sms);
-  t.smem = smem;
+  t.smem = fwd_smem(kh, sym, steps, t.nthreads);
   return t;
 }
 

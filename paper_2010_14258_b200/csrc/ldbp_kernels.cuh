@@ -32,6 +32,12 @@
 #ifndef LDBP_NORM
 #define LDBP_NORM 1  // h0-normalised FIR when well conditioned (saves one complex multiply per FIR)
 #endif
+#ifndef LDBP_BWD_PREFETCH
+#define LDBP_BWD_PREFETCH 0  // 1: cp.async-prefetch target/adjoint into smem (costs one tape slot)
+#endif
+#ifndef LDBP_FWD_XSMEM
+#define LDBP_FWD_XSMEM 1  // forward halo exchange through shared memory only (no shuffles)
+#endif
 #ifndef LDBP_NB_SYNC
 #define LDBP_NB_SYNC 0  // 1: neighbour-only mbarrier sync per step (measured 2x slower on B200; kept
                         // as an option), 0: one __syncthreads per step
@@ -352,6 +358,34 @@ __device__ __forceinline__ void exchange_nb(const f2x (&u)[R], f2x (&hl)[KH > 0 
   }
 }
 
+// Shared-memory exchange without shuffles (forward kernel): every thread publishes its Kh head
+// and tail samples in [Kh][nthr] arrays (consecutive lanes -> consecutive 8-byte words, no bank
+// conflicts), one barrier, then reads thread tid-1's tail and tid+1's head.  Warp boundaries
+// need no special case; 4*Kh LDS/STS replace 4*Kh 64-bit shuffles plus the divergent
+// warp-edge code.  Double-buffered by step parity (one barrier per step).
+template <int KH, int R>
+__device__ __forceinline__ void exchange_smem(const f2x (&u)[R], f2x (&hl)[KH > 0 ? KH : 1],
+                                              f2x (&hr)[KH > 0 ? KH : 1], f2x* sh, int buf, int nthr, int left,
+                                              int right) {
+  if constexpr (KH > 0) {
+    f2x* head = sh + (buf * 2 + 0) * KH * nthr;
+    f2x* tail = sh + (buf * 2 + 1) * KH * nthr;
+#pragma unroll
+    for (int j = 0; j < KH; ++j) {
+      head[j * nthr + threadIdx.x] = u[j];
+      tail[j * nthr + threadIdx.x] = u[R - KH + j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < KH; ++j) {
+      hl[j] = tail[j * nthr + left];
+      hr[j] = head[j * nthr + right];
+    }
+  } else {
+    (void)u; (void)hl; (void)hr; (void)sh; (void)buf; (void)nthr; (void)left; (void)right;
+  }
+}
+
 // Two arrays exchanged around one barrier (backward reverse sweep).
 template <int KH, int R, int MW = kMaxWarps>
 __device__ __forceinline__ void exchange2(const f2x (&u)[R], f2x (&hl)[KH > 0 ? KH : 1], f2x (&hr)[KH > 0 ? KH : 1],
@@ -532,29 +566,39 @@ __device__ __forceinline__ void stage_params(const float2* __restrict__ taps, co
                                              TapP* sh_taps, TapP* sh_taps_adj, float* sh_gamma, StepNorm* sh_norm,
                                              int* sh_flag) {
   constexpr int NT = ntaps_used<SYM, KH>();
-  auto tap = [&](int s, int t) -> float2 {
+  const int S = s1 - s0;
+  // Phase 0: one coalesced, fully parallel read of the raw (masked) taps this launch needs and
+  // of gamma; the packed-tap array doubles as the raw staging area (NT float2 <= NT TapP).
+  // The per-step scalars are derived from shared memory only, so no global-memory latency is
+  // serialised behind the barriers below.
+  float2* raw = reinterpret_cast<float2*>(sh_taps_adj ? sh_taps_adj : sh_taps) + (ADJ ? 0 : S * NT);
+  const int cnt = S * NT;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const int s = s0 + i / NT;
+    const int t = (i % NT) + (SYM ? KH : 0);  // index into the stored [T] row
     float2 h = taps[(int64_t)s * T + t];
     if (mask && !mask[(int64_t)s * T + t]) h = make_float2(0.f, 0.f);
-    return h;
-  };
-  const int S = s1 - s0;
+    raw[i] = h;
+  }
+  for (int i = threadIdx.x; i < S; i += blockDim.x) sh_gamma[i] = gamma[s0 + i];
   if (threadIdx.x == 0) *sh_flag = (SYM && LDBP_NORM) ? 1 : 0;
   __syncthreads();
-  // phase A (parallel over steps): c_i = h0 and its conditioning
+  // Phase A (parallel over steps): c_i = h0 and its conditioning (SYM stores h_0..h_Kh; the
+  // energy of the full symmetric filter is |h0|^2 + 2 sum_{j>0} |h_j|^2).
   if (SYM && LDBP_NORM)
     for (int i = threadIdx.x; i < S; i += blockDim.x) {
-      const float2 h0 = tap(s0 + i, KH);
+      const float2 h0 = raw[i * NT];
       float e = 0.f;
-      for (int t = 0; t < T; ++t) {
-        const float2 h = tap(s0 + i, t);
-        e = fmaf(h.x, h.x, fmaf(h.y, h.y, e));
+      for (int t = 0; t < NT; ++t) {
+        const float2 h = raw[i * NT + t];
+        e = fmaf(t ? 2.f : 1.f, h.x * h.x + h.y * h.y, e);
       }
       const float m0 = h0.x * h0.x + h0.y * h0.y;
       if (!(m0 > 0.f) || m0 < 1e-6f * e) *sh_flag = 0;
       sh_norm[i].c = h0;
     }
   __syncthreads();
-  // phase B (one thread, from shared memory): prefix products P_rel(i) in fp64
+  // Phase B (one thread, shared memory only): prefix products P_rel(i) in fp64
   if (threadIdx.x == 0 && *sh_flag) {
     double pr = 1.0, pi = 0.0;
     int ok = 1;
@@ -570,34 +614,46 @@ __device__ __forceinline__ void stage_params(const float2* __restrict__ taps, co
     *sh_flag = ok;
   }
   __syncthreads();
-  // phase C (parallel): gamma_hat = gamma |P_rel|^2, or the plain model
-  {
-    const bool nrm = *sh_flag != 0;
-    for (int i = threadIdx.x; i < S; i += blockDim.x) {
-      if (nrm) {
-        const float2 P = sh_norm[i].P;
-        sh_gamma[i] = (float)((double)gamma[s0 + i] * ((double)P.x * P.x + (double)P.y * P.y));
-      } else {
-        sh_norm[i].P = make_float2(1.f, 0.f);
-        sh_norm[i].c = make_float2(1.f, 0.f);
-        sh_gamma[i] = gamma[s0 + i];
-      }
+  // Phase C (parallel): gamma_hat = gamma |P_rel|^2 and the packed taps (h / h0 when normalised).
+  const bool norm = *sh_flag != 0;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+    if (norm) {
+      const float2 P = sh_norm[i].P;
+      sh_gamma[i] = (float)((double)sh_gamma[i] * ((double)P.x * P.x + (double)P.y * P.y));
+    } else {
+      sh_norm[i].P = make_float2(1.f, 0.f);
+      sh_norm[i].c = make_float2(1.f, 0.f);
     }
   }
-  const bool norm = *sh_flag != 0;
-  const int cnt = (s1 - s0) * NT;
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const int s = s0 + i / NT;
-    const int t = (i % NT) + (SYM ? KH : 0);  // index into the stored [T] row
-    float2 h = tap(s, t);
+  // raw -> packed.  With ADJ the raw copy lives in sh_taps_adj: read everything first, then write
+  // (raw[i] and the TapP slots it overlaps belong to thread-strided indices; a barrier separates).
+  float2 hv[4];
+  int nloc = 0;
+  for (int i = threadIdx.x; i < cnt && nloc < 4; i += blockDim.x) hv[nloc++] = raw[i];
+  const bool spill = cnt > 4 * (int)blockDim.x;
+  __syncthreads();
+  auto pack = [&](int i, float2 h) {
+    const int t = (i % NT) + (SYM ? KH : 0);
     if (norm) {  // h / c = h conj(c) / |c|^2
-      const float2 c = sh_norm[s - s0].c;
+      const float2 c = sh_norm[i / NT].c;
       const float inv = 1.f / (c.x * c.x + c.y * c.y);
       h = make_float2((h.x * c.x + h.y * c.y) * inv, (h.y * c.x - h.x * c.y) * inv);
       if (t == KH) h = make_float2(1.f, 0.f);
     }
     sh_taps[i] = tap_fwd(h);
     if constexpr (ADJ) sh_taps_adj[i] = tap_adj(h);
+  };
+  if (!spill) {
+    nloc = 0;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) pack(i, hv[nloc++]);
+  } else {  // very long launches: re-read the masked taps from global (rare: S*NT > 4*blockDim)
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const int s = s0 + i / NT;
+      const int t = (i % NT) + (SYM ? KH : 0);
+      float2 h = taps[(int64_t)s * T + t];
+      if (mask && !mask[(int64_t)s * T + t]) h = make_float2(0.f, 0.f);
+      pack(i, h);
+    }
   }
 }
 
@@ -636,12 +692,16 @@ __device__ __forceinline__ void fwd_steps(const FwdArgs& a, f2x (&u)[R], const T
                                           int64_t e0, int lane, int warp, int nwarps) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   f2x hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1];
+  const int left = threadIdx.x > 0 ? threadIdx.x - 1 : 0;
+  const int right = threadIdx.x + 1 < blockDim.x ? threadIdx.x + 1 : threadIdx.x;
   for (int s = 0; s < a.s1 - a.s0; ++s) {
     TapP hs[NTU];
 #pragma unroll
     for (int j = 0; j < NTU; ++j) hs[j] = sh_taps[s * NTU + j];
     const float gm = sh_gamma[s];
-    if (LDBP_NB_SYNC)
+    if (LDBP_FWD_XSMEM)
+      exchange_smem<KH, R>(u, hl, hr, sh_edge, s & 1, blockDim.x, left, right);
+    else if (LDBP_NB_SYNC)
       exchange_nb<KH, R, 1>(u, hl, hr, sh_edge, u, hl, hr, sh_edge, bars, s, lane, warp, nwarps);
     else
       exchange<KH, R>(u, hl, hr, sh_edge, s & 1, lane, warp, nwarps);
@@ -671,8 +731,9 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int S = a.s1 - a.s0;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                            // [2][32] mbarriers
-  f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);                       // 2*2*32*KH
-  TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge + 4 * kMaxWarps * (KH > 0 ? KH : 1));  // S*NTU
+  f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);  // 2*2*KH*(XSMEM ? nthreads : 32)
+  TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge + 4 * (LDBP_FWD_XSMEM ? (int)blockDim.x : kMaxWarps) *
+                                                        (KH > 0 ? KH : 1));  // S*NTU
   StepNorm* sh_norm = reinterpret_cast<StepNorm*>(sh_taps + S * NTU);                // S
   float* sh_gamma = reinterpret_cast<float*>(sh_norm + S);                           // S
   int* sh_flag = reinterpret_cast<int*>(sh_gamma + S);
@@ -949,7 +1010,7 @@ __global__ void __launch_bounds__(256, LDBP_BWD_MINB) bwd_segment_kernel(const B
   // Issue the (late-needed) target / incoming-adjoint loads first, asynchronously into smem, so
   // their latency overlaps the checkpoint load, the staging and the whole forward recompute.
   bool prefetched = false;
-  {
+  if (LDBP_BWD_PREFETCH) {
     const Span sp = make_span(e0, a.g);
     if (span_fast<R>(sp, a.g, e0)) {
       const float2* src = a.gin ? a.gin : a.target;
