@@ -196,6 +196,15 @@ Tile plan_tiles(int64_t B, int64_t n, int H, int R, int max_threads, int occ_per
   grid = cdiv(E, W);
   int nthr = (int)cdiv(cdiv(W + 2 * (int64_t)H, R), 32) * 32;
   nthr = std::min(std::max(nthr, 32), max_threads);
+  // phase staggering (see tile_lo in ldbp_kernels.cuh): with >= 2 resident CTAs per SM and
+  // more than one wave, the first `sms` tiles are half width; the grid grows to cover E.
+  int NS = 0;
+  int64_t Wh = W;
+  if (env_int("LDBP_STAGGER", 0) && occ_per_sm >= 2 && grid > slots && W >= 2 * R) {
+    NS = sms;
+    Wh = W / 2;
+    grid = NS + cdiv(std::max<int64_t>(E - (int64_t)NS * Wh, 0), W);
+  }
   t.nthreads = nthr;
   t.grid = (int)grid;
   t.g.B = B;
@@ -205,6 +214,8 @@ Tile plan_tiles(int64_t B, int64_t n, int H, int R, int max_threads, int occ_per
   t.g.W = W;
   t.g.H = H;
   t.g.big_halo = H > n ? 1 : 0;
+  t.g.NS = NS;
+  t.g.Wh = Wh;
   return t;
 }
 
@@ -467,7 +478,18 @@ int run_backward_chain(const ldbp_dims* d, const float2* x, const float2* gy, co
     cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     {
       TraceScope ts(LDBP_K_BACKWARD, s1 - s0, d->batch * d->n, st);
-      fn<<<p.tile.grid, p.tile.nthreads, smem, st>>>(a);
+      // programmatic dependent launch: this segment's prologue overlaps the previous kernel's tail
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(p.tile.grid);
+      cfg.blockDim = dim3(p.tile.nthreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = env_int("LDBP_PDL", 1) && !g_trace_on ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, fn, a);
     }
     LDBP_TRY(cuda_check("bwd_segment_kernel launch"));
   }

@@ -63,7 +63,18 @@ struct Geo {
   int64_t B, n, ext, E, W;  // blocks, block length, n + 2H, B*ext, owned width per CTA
   int H;                    // halo per side (samples)
   int big_halo;             // H > n: positions may wrap more than once
+  int NS;                   // the first NS tiles are half-width (Wh) — see tile_lo()
+  int64_t Wh;
 };
+
+// Owned range [tile_lo, tile_hi) of CTA b.  The first NS CTAs (one per SM in the first wave)
+// get half-width tiles: the CTA that later follows on the same SM slot then runs half a tile
+// out of phase with its neighbour slot, so one CTA's load/stage/epilogue latency overlaps the
+// other's compute instead of both stalling together (identical CTAs would otherwise stay
+// phase-locked for the whole launch).
+__device__ __forceinline__ int64_t tile_lo(const Geo& g, int64_t b) {
+  return b < g.NS ? b * g.Wh : (int64_t)g.NS * g.Wh + (b - g.NS) * g.W;
+}
 
 __device__ __forceinline__ int64_t wrap_pos(int64_t p, const Geo& g) {
   if (g.big_halo) {
@@ -75,7 +86,7 @@ __device__ __forceinline__ int64_t wrap_pos(int64_t p, const Geo& g) {
 
 // Extended index of this thread's first sample.
 __device__ __forceinline__ int64_t thread_e0(const Geo& g, int R) {
-  return (int64_t)blockIdx.x * g.W - g.H + (int64_t)threadIdx.x * R;
+  return tile_lo(g, blockIdx.x) - g.H + (int64_t)threadIdx.x * R;
 }
 
 // Per-thread view of its R consecutive extended samples [e0, e0+R): block b0 and extended
@@ -147,8 +158,8 @@ __device__ __forceinline__ void load_window(const float2* __restrict__ src, int6
 // Bitmask of which of this thread's R samples are owned real samples of this CTA.
 template <int R>
 __device__ __forceinline__ uint32_t owned_mask(int64_t e0, const Geo& g) {
-  const int64_t lo = (int64_t)blockIdx.x * g.W;
-  const int64_t hi = min(lo + g.W, g.E);
+  const int64_t lo = tile_lo(g, blockIdx.x);
+  const int64_t hi = min(lo + ((int64_t)blockIdx.x < g.NS ? g.Wh : g.W), g.E);
   const Span sp = make_span(e0, g);
   if (span_fast<R>(sp, g, e0) && e0 >= lo && e0 + R <= hi) return R >= 32 ? 0xffffffffu : ((1u << R) - 1u);
   if (e0 + R <= lo || e0 >= hi) return 0u;
@@ -681,7 +692,9 @@ struct FwdArgs {
 #ifndef LDBP_FWD_WIDE_THREADS
 #define LDBP_FWD_WIDE_THREADS 256
 #endif
-__host__ __device__ constexpr int fwd_max_threads(int kh) { return kh <= 2 ? 512 : kh <= 5 ? 256 : LDBP_FWD_WIDE_THREADS; }
+__host__ __device__ constexpr int fwd_max_threads(int kh) {
+  return LDBP_FWD_R > 16 ? 256 : (kh <= 2 ? 512 : kh <= 5 ? 256 : LDBP_FWD_WIDE_THREADS);
+}
 __host__ __device__ constexpr int fwd_min_blocks(int kh) {
   return kh <= 2 ? 2 : kh <= 4 ? 3 : (LDBP_FWD_WIDE_THREADS >= 512 && kh >= 6) ? 1 : 2;
 }
@@ -974,6 +987,7 @@ __device__ __forceinline__ void bwd_body(const BwdArgs& a, const BwdSmem& sm, f2
       if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
     }
   }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.gout) store_owned<R>(a.gout, e0, a.g, g);  // gout needs no scaling: P_rel before step s0 is 1
 }
 
@@ -1021,11 +1035,15 @@ __global__ void __launch_bounds__(256, LDBP_BWD_MINB) bwd_segment_kernel(const B
       prefetched = true;
     }
   }
-  f2x u[R];
-  load_window<R>(a.ck, e0, a.g, u);
+  // Programmatic dependent launch: taps/gamma/mask/target are never written by the preceding
+  // kernel (the previous backward segment or the checkpoint forward), so they are staged before
+  // waiting; the checkpoint and the incoming adjoint are read after griddepcontrol.wait.
   const uint32_t own = owned_mask<R>(e0, a.g);
   stage_params<KH, SYM, true>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sm.sh_taps, sm.sh_taps_adj, sm.sh_gamma,
                               sm.sh_norm, sm.sh_flag);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  f2x u[R];
+  load_window<R>(a.ck, e0, a.g, u);
   __syncthreads();
   const bool norm = SYM && *sm.sh_flag;
   if (norm)
