@@ -123,3 +123,56 @@ def test_ase_noise_variance():
     assert abs(np.mean(np.abs(out) ** 2) / (psd * 42.8e9) - 1) < 0.02
     u = np.ones(4, complex)
     np.testing.assert_allclose(np.abs(channel.edfa(u, a, 80.0, psd, 42.8e9, None)) ** 2, np.exp(a * 80.0))
+
+
+def test_rx_fir_matched_filter_pins():
+    """The truncated-FIR matched filter (reading G19) agrees with the exact frequency-domain RRC
+    matched filter to the truncation error, keeps the Nyquist property (RRC^2 at symbol instants
+    = delta) and its adjoint is the transpose (<M y, g> = <y, M^T g>)."""
+    s = li.qam16(li.rng(0, 3, "symbols"), 512)
+    for sps in (2, 4):
+        h = receiver.rrc_fir_taps(sps, 0.1, 32)
+        assert len(h) == 2 * 32 * sps + 1
+        np.testing.assert_allclose(h, h[::-1], atol=1e-15)
+        x = channel.modulate(s, sps, 1.0)
+        st = receiver.mf_fir_downsample(x, h, sps)
+        assert np.max(np.abs(st - s)) < 2e-3  # 10% roll-off tails beyond 32 symbols
+        # exact FIR (full circular response) reproduces the frequency-domain MF to 1e-12
+        n = len(x)
+        hfull = np.fft.ifft(channel.rrc_response(n, sps, 0.1)).real
+        # lags -n/2..n/2; +-n/2 alias to the same circular lag, so each carries half its weight
+        hfull = np.concatenate([hfull[-(n // 2):], hfull[: n // 2 + 1]])
+        hfull[0] *= 0.5
+        hfull[-1] *= 0.5
+        np.testing.assert_allclose(receiver.mf_fir_downsample(x, hfull, sps), s, atol=1e-10)
+    rng = np.random.default_rng(8)
+    y = rng.standard_normal((2, 96)) + 1j * rng.standard_normal((2, 96))
+    g = rng.standard_normal((2, 48)) + 1j * rng.standard_normal((2, 48))
+    h = receiver.rrc_fir_taps(2, 0.1, 8)
+    lhs = np.sum(np.conj(g) * receiver.mf_fir_downsample(y, h, 2))
+    rhs = np.sum(np.conj(receiver.mf_fir_adjoint(g, h, 2, 96)) * y)
+    assert abs(lhs - rhs) < 1e-12 * abs(lhs)
+
+
+def test_rx_loss_gradient_finite_differences():
+    """Symbol-MSE loss after MF + genie phase (Eq. (12)-(13)): the chain-rule gradient w.r.t. the
+    LDBP output matches central differences; dL/dphi vanishes at the genie phase (it minimises
+    the error over phi), so the phase path contributes nothing."""
+    rng = np.random.default_rng(9)
+    n, sps = 64, 2
+    h = receiver.rrc_fir_taps(sps, 0.1, 4)
+    y = (rng.standard_normal((2, n)) + 1j * rng.standard_normal((2, n))) * 0.1
+    s = li.qam16(li.rng(0, 4, "symbols"), n).reshape(2, n // 2)
+    P = np.array([1e-2, 2e-2])
+    errs, gy, dphi = receiver.rx_loss_grad(y, s, P, h, sps)
+    assert np.all(np.abs(dphi) < 1e-12 * np.abs(errs).max())
+    eps = 1e-6
+    scale = np.abs(gy).max()
+    for b, t in [(0, 0), (0, 7), (1, 63), (1, 30)]:
+        for u in (1.0, 1j):
+            yp, ym = y.copy(), y.copy()
+            yp[b, t] += eps * u
+            ym[b, t] -= eps * u
+            fd = (receiver.rx_loss(yp, s, P, h, sps)[0].sum() - receiver.rx_loss(ym, s, P, h, sps)[0].sum()) / (2 * eps)
+            an = gy[b, t].real if u == 1.0 else gy[b, t].imag
+            assert abs(fd - an) <= 1e-6 * scale
