@@ -263,7 +263,7 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
     kernel_shares = {}
     tot_ms = sum(v["ms"] for v in per_kind.values()) or 1.0
     names = {_lib.K_FORWARD: "fwd_tile_kernel", _lib.K_BACKWARD: "bwd_segment_kernel",
-             _lib.K_REDUCE: "reduce_partials_kernel", _lib.K_ADAM: "adam_kernel"}
+             _lib.K_REDUCE: "reduce_partials_kernel", _lib.K_ADAM: "adam_kernel", _lib.K_REVERSE: "rev_tile_kernel"}
     for k, v in per_kind.items():
         kernel_shares[names[k]] = {"share": v["ms"] / tot_ms, "avg_ms": v["ms"] / v["launches"],
                                    "launches": v["launches"]}

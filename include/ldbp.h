@@ -83,7 +83,13 @@ const char* ldbp_status_string(int status);
 const char* ldbp_last_error(void);
 
 /* Device workspace (bytes) the given op needs for these dims; 0 means ws may be NULL.
-   Returns a status; *bytes is written on LDBP_OK. */
+   Returns a status; *bytes is written on LDBP_OK.
+   Backward / loss_grad / train_step choose between two schedules for row a7 (activations):
+   checkpoint + recompute segments with ~M/6 checkpoints (default, env LDBP_BWD_MODE=0), or
+   "store-all" (LDBP_BWD_MODE=1; -1 = auto while M*B*n*8 bytes <= LDBP_ACT_BUDGET_GB, default
+   96): the forward stores every step's activation in the workspace (M*B*n*8 bytes +
+   O(grid*M*T)) and one fused reverse kernel needs no recompute.  The choice depends only on dims and
+   the environment, so this query and the call agree. */
 int ldbp_workspace_bytes(const ldbp_dims* d, int op, size_t* bytes);
 
 /* Number of CUDA kernel launches the op enqueues for these dims (for accounting). */
@@ -102,7 +108,7 @@ int ldbp_forward(const ldbp_dims* d, const void* x, void* y, const void* taps, c
  * ldbp_backward — reverse-mode sweep of Eq. (7) for an incoming gradient gy = dL/dy
  * (per step: c = Im(gv conj v), ga = gv e^{-j phi} + 2 gamma' c a,
  * dgamma' = sum c|a|^2, dh_j = sum ga_t conj(u_{t-j}), gu_s = sum_j conj(h_j) ga_{s+j}).
- *   x      [B][n] complex64 (the forward input; activations are recomputed, not stored)
+ *   x      [B][n] complex64 (the forward input; the call re-runs the forward into ws)
  *   gy     [B][n] complex64
  *   dtaps  [M][T][2] float64 out: sum over all blocks (tied-parameter form with LDBP_SYMMETRIC)
  *   dgamma [M] float64 out
@@ -165,7 +171,8 @@ typedef enum ldbp_kernel_kind {
   LDBP_K_FORWARD = 1,   /* fused forward tile kernel (rows a1-a4)                 */
   LDBP_K_BACKWARD = 2,  /* backward segment kernel (rows a5-a8, recompute + adjoint) */
   LDBP_K_REDUCE = 3,    /* fp64 partial reduction (row a8)                         */
-  LDBP_K_ADAM = 4       /* Adam + mask (row a10)                                   */
+  LDBP_K_ADAM = 4,      /* Adam + mask (row a10)                                   */
+  LDBP_K_REVERSE = 5    /* store-all reverse tile kernel (rows a5, a6, a8)         */
 } ldbp_kernel_kind;
 
 typedef struct ldbp_trace_record {

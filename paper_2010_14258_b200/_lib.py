@@ -31,7 +31,7 @@ EXPORTED = (
     "ldbp_trace_end",
 )
 
-K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM = 1, 2, 3, 4
+K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM, K_REVERSE = 1, 2, 3, 4, 5
 
 
 class LdbpDims(ctypes.Structure):

@@ -20,6 +20,7 @@
 
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
+using RevFn = void (*)(const ldbp::RevArgs);
 
 namespace {
 
@@ -41,6 +42,7 @@ int cuda_check(const char* what) {
 
 constexpr int kFwdR = LDBP_FWD_R;
 constexpr int kBwdR = LDBP_BWD_R;
+constexpr int kRevR = LDBP_REV_R;
 constexpr int kFwdMaxThreads = 512;
 constexpr int kBwdMaxThreads = 256;
 
@@ -97,7 +99,8 @@ int ntaps_used(int kh, bool sym) { return sym ? kh + 1 : 2 * kh + 1; }
 // Kernel instantiations live in ldbp_inst.cu, compiled once per Kh (parallel build).
 #define LDBP_DECL_GETTERS(K)                        \
   FwdFn ldbp_get_fwd_##K(bool sym, bool fast);      \
-  BwdFn ldbp_get_bwd_##K(bool sym, bool fast);
+  BwdFn ldbp_get_bwd_##K(bool sym, bool fast);      \
+  RevFn ldbp_get_rev_##K(bool sym, bool fast);
 }  // namespace
 LDBP_DECL_GETTERS(0)
 LDBP_DECL_GETTERS(1)
@@ -136,6 +139,20 @@ BwdFn get_bwd(int kh, bool sym, bool fast) {
   return nullptr;
 }
 
+RevFn get_rev(int kh, bool sym, bool fast) {
+  switch (kh) {
+    case 0: return ldbp_get_rev_0(sym, fast);
+    case 1: return ldbp_get_rev_1(sym, fast);
+    case 2: return ldbp_get_rev_2(sym, fast);
+    case 3: return ldbp_get_rev_3(sym, fast);
+    case 4: return ldbp_get_rev_4(sym, fast);
+    case 5: return ldbp_get_rev_5(sym, fast);
+    case 6: return ldbp_get_rev_6(sym, fast);
+    case 7: return ldbp_get_rev_7(sym, fast);
+  }
+  return nullptr;
+}
+
 int device_sms() {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -153,11 +170,24 @@ struct Tile {
   ldbp::Geo g{};
 };
 
-size_t fwd_smem(int kh, bool sym, int steps, int nthreads = 1024) {
+size_t fwd_smem(int kh, bool sym, int steps, int nthreads = 1024, int nnorm = 0) {
   const int edge_rows = LDBP_FWD_XSMEM ? nthreads : ldbp::kMaxWarps;
   return sizeof(uint64_t) * 2 * ldbp::kMaxWarps + sizeof(float2) * 4 * edge_rows * std::max(kh, 1) +
-         sizeof(ldbp::TapP) * steps * ntaps_used(kh, sym) + sizeof(ldbp::StepNorm) * steps + sizeof(float) * steps +
-         32;
+         sizeof(ldbp::TapP) * steps * ntaps_used(kh, sym) + sizeof(ldbp::StepNorm) * std::max(steps, nnorm) +
+         sizeof(float) * steps + 32;
+}
+
+// Store-all reverse kernel shared memory (mirrors the carve-up in rev_tile_kernel).
+size_t rev_smem(int kh, bool sym, int steps, int M, int nthreads) {
+  const int nw = nthreads / 32;
+  const int V = 1 + 2 * ntaps_used(kh, sym);
+  size_t s = sizeof(float2) * 2 * (size_t)kRevR * nthreads;         // u window copies
+  s += sizeof(float2) * 4 * (size_t)std::max(kh, 1) * nthreads;       // ga edges
+  s += sizeof(ldbp::TapP) * (size_t)steps * ntaps_used(kh, sym);      // adjoint taps
+  s += sizeof(ldbp::StepNorm) * (size_t)M;                            // global normalisation
+  s += sizeof(float) * (size_t)((2 * nw * V + 3) & ~3);               // per-warp partials
+  s += sizeof(float) * (size_t)((steps + 3) & ~3) + 16;               // gamma_hat + flag
+  return s;
 }
 
 size_t bwd_smem(int kh, bool sym, int steps, int nthreads) {
@@ -301,6 +331,68 @@ Tile plan_fwd_tile(const ldbp_dims* d, int steps, bool query_device) {
   return t;
 }
 
+// Store-all training path: forward launches store every activation, then
+// Kr reverse launches of Cr steps each (halo Cr*Kh), adjoint passed through HBM between them.
+struct RevPlan {
+  int Cr = 1, Kr = 1;  // steps per reverse launch, number of reverse launches
+  int V = 1;
+  Tile tile;           // uniform geometry for all reverse launches (H = Cr*kh)
+};
+
+int rev_occupancy(RevFn fn, int nthreads, size_t smem) {
+  int occ = 0;
+  cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, nthreads, smem) != cudaSuccess) occ = 1;
+  cudaGetLastError();
+  return std::max(occ, 1);
+}
+
+RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
+  RevPlan p;
+  const int kh = (d->taps - 1) / 2;
+  const bool sym = d->flags & LDBP_SYMMETRIC;
+  const int M = d->steps;
+  const int nthr = std::min(env_int("LDBP_REV_THREADS", LDBP_REV_MAXT), LDBP_REV_MAXT);
+  p.V = 1 + 2 * ntaps_used(kh, sym);
+  // cost model in step units: a launch of S steps costs S * window / (window - 2*S*kh) plus a
+  // fixed ~2 steps (prologue: staging, first load, seed); pick the number of launches minimising it
+  const double window = (double)nthr * kRevR;
+  const double fixed = 2.0;
+  int best_k = 1;
+  double best = 1e300;
+  const int kmax = std::min(M, env_int("LDBP_REV_MAX_LAUNCHES", 64));
+  for (int k = 1; k <= kmax; ++k) {
+    const int S = (int)cdiv(M, k);
+    const double useful = window - 2.0 * S * kh;
+    if (useful < window / 4) continue;
+    const double cost = k * (S * window / useful + fixed);
+    if (cost < best) { best = cost; best_k = k; }
+  }
+  if (best >= 1e300) best_k = std::max(1, (int)cdiv((int64_t)M * kh * 8, (int64_t)window));
+  const int cmax = env_int("LDBP_REV_MAX_STEPS", 1 << 30);
+  best_k = std::max(best_k, (int)cdiv(M, std::max(cmax, 1)));
+  p.Kr = best_k;
+  p.Cr = (int)cdiv(M, p.Kr);
+  p.Kr = (int)cdiv(M, p.Cr);
+  int occ = 1, sms = 148;
+  if (query_device) {
+    sms = device_sms();
+    occ = rev_occupancy(get_rev(kh, sym, !(d->flags & LDBP_PRECISE)), nthr, rev_smem(kh, sym, p.Cr, M, nthr));
+  }
+  p.tile = plan_tiles(d->batch, d->n, p.Cr * kh, kRevR, nthr, occ, sms);
+  return p;
+}
+
+// Which training path: 1 = store-all activations + fused reverse (default when the activations
+// fit the budget), 0 = checkpoint + recompute segments (memory-lean fallback).
+bool use_store_all(const ldbp_dims* d) {
+  const int mode = env_int("LDBP_BWD_MODE", 0);
+  if (mode == 0) return false;
+  if (mode == 1) return true;
+  const double act_gb = (double)d->steps * (double)d->batch * (double)d->n * sizeof(float2) / 1073741824.0;
+  return act_gb <= (double)env_int("LDBP_ACT_BUDGET_GB", 96);
+}
+
 // ----------------------------------------------------------------------------------------
 // Validation
 // ----------------------------------------------------------------------------------------
@@ -382,16 +474,46 @@ BwdWs bwd_ws(const ldbp_dims* d, const BwdPlan& p) {
   return w;
 }
 
+struct RevWs {
+  size_t act_off = 0, act_each = 0;  // M activation buffers u_hat^(1..M)
+  size_t g_off = 0, g_each = 0;      // 2 adjoint ping-pong buffers (when Kr >= 2)
+  size_t part_off = 0, loss_off = 0, part2_off = 0, loss2_off = 0;
+  size_t total = 0;
+};
+
+RevWs rev_ws(const ldbp_dims* d, const RevPlan& p) {
+  RevWs w;
+  const size_t blk = align256(sizeof(float2) * d->batch * d->n);
+  w.act_off = 0;
+  w.act_each = blk;
+  size_t off = blk * d->steps;
+  w.g_off = off;
+  w.g_each = blk;
+  off += (p.Kr >= 2) ? 2 * blk : 0;
+  w.part_off = off;
+  off += align256(sizeof(double) * (size_t)p.tile.grid * d->steps * p.V);
+  w.loss_off = off;
+  off += align256(sizeof(double) * (size_t)p.tile.grid);
+  const int nch = reduce_chunks(p.tile.grid);
+  w.part2_off = off;
+  off += align256(sizeof(double) * (size_t)nch * d->steps * p.V);
+  w.loss2_off = off;
+  off += align256(sizeof(double) * (size_t)nch);
+  w.total = off;
+  return w;
+}
+
 // ----------------------------------------------------------------------------------------
 // Launch helpers
 // ----------------------------------------------------------------------------------------
 int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2* taps, const float* gamma,
                const uint8_t* mask, int s0, int s1, cudaStream_t st, float2* ckpt = nullptr, int ckpt_every = 0,
-               int64_t ckpt_stride = 0) {
+               int64_t ckpt_stride = 0, bool global_norm = false, bool scale_dst = false) {
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const bool fast = !(d->flags & LDBP_PRECISE);
   Tile t = plan_fwd_tile(d, s1 - s0, true);
+  if (global_norm) t.smem = fwd_smem(kh, sym, s1 - s0, t.nthreads, d->steps);
   FwdFn fn = get_fwd(kh, sym, fast);
   ldbp::FwdArgs a;
   a.src = src;
@@ -405,6 +527,10 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   a.T = d->taps;
   a.s0 = s0;
   a.s1 = s1;
+  a.n0 = global_norm ? 0 : s0;
+  a.nM = global_norm ? d->steps : s1;
+  a.global_norm = global_norm ? 1 : 0;
+  a.scale_dst = scale_dst ? 1 : 0;
   a.g = t.g;
   cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
   {
@@ -429,6 +555,10 @@ int run_forward_chain(const ldbp_dims* d, const float2* x, float2* y, const floa
   }
   return LDBP_OK;
 }
+
+int run_reduce(const ldbp_dims* d, double* partials, double* lossp, int nblk, int V, unsigned char* part2,
+               unsigned char* loss2, const uint8_t* mask, cudaStream_t st, double* buf, double* dtaps,
+               double* dgamma);
 
 // Backward over all segments. `gy` != nullptr: incoming gradient; else seed from target.
 int run_backward_chain(const ldbp_dims* d, const float2* x, const float2* gy, const float2* target,
@@ -493,20 +623,30 @@ int run_backward_chain(const ldbp_dims* d, const float2* x, const float2* gy, co
     }
     LDBP_TRY(cuda_check("bwd_segment_kernel launch"));
   }
+  return run_reduce(d, partials, gy ? nullptr : lossp, p.tile.grid, p.V, ws + w.part2_off, ws + w.loss2_off, mask,
+                    st, buf, dtaps, dgamma);
+}
+
+// Deterministic two-level fp64 reduction of per-CTA partials into buf / (dtaps, dgamma).
+int run_reduce(const ldbp_dims* d, double* partials, double* lossp, int nblk, int V, unsigned char* part2,
+               unsigned char* loss2, const uint8_t* mask, cudaStream_t st, double* buf, double* dtaps,
+               double* dgamma) {
+  const int kh = (d->taps - 1) / 2;
+  const bool sym = d->flags & LDBP_SYMMETRIC;
   ldbp::ReduceArgs r;
   r.partials = partials;
-  r.loss_partials = gy ? nullptr : lossp;
-  r.nblk = p.tile.grid;
-  const int nch = reduce_chunks(p.tile.grid);
+  r.loss_partials = lossp;
+  r.nblk = nblk;
+  const int nch = reduce_chunks(nblk);
   if (nch > 0) {
     ldbp::Reduce1Args r1;
     r1.partials = partials;
     r1.loss_partials = r.loss_partials;
-    r1.nblk = p.tile.grid;
-    r1.total = d->steps * p.V;
+    r1.nblk = nblk;
+    r1.total = d->steps * V;
     r1.chunk = kReduceChunk;
-    r1.out = reinterpret_cast<double*>(ws + w.part2_off);
-    r1.loss_out = reinterpret_cast<double*>(ws + w.loss2_off);
+    r1.out = reinterpret_cast<double*>(part2);
+    r1.loss_out = reinterpret_cast<double*>(loss2);
     {
       TraceScope ts(LDBP_K_REDUCE, d->steps, 0, st);
       ldbp::reduce_partials_pass1<<<dim3((r1.total + 31) / 32 + 1, nch), 256, 0, st>>>(r1);
@@ -518,19 +658,74 @@ int run_backward_chain(const ldbp_dims* d, const float2* x, const float2* gy, co
   }
   r.M = d->steps;
   r.T = d->taps;
-  r.V = p.V;
+  r.V = V;
   r.kh = kh;
   r.sym = sym ? 1 : 0;
   r.mask = mask;
   r.buf = buf;
   r.dtaps = dtaps;
   r.dgamma = dgamma;
-  const int nblocks = (d->steps * p.V + 31) / 32 + 1;
+  const int nblocks = (d->steps * V + 31) / 32 + 1;
   {
     TraceScope ts(LDBP_K_REDUCE, d->steps, 0, st);
     ldbp::reduce_partials_kernel<<<nblocks, 256, 0, st>>>(r);
   }
   return cuda_check("reduce_partials_kernel launch");
+}
+
+// Store-all training path: forward chain storing u_hat^(1..M) (global normalisation), then the
+// reverse launches (last steps first), then the reduction.
+int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const float2* target, const float2* taps,
+                  const float* gamma, const uint8_t* mask, float2* gx, unsigned char* ws, const RevPlan& p,
+                  const RevWs& w, cudaStream_t st, double* buf, double* dtaps, double* dgamma) {
+  const int kh = (d->taps - 1) / 2;
+  const bool sym = d->flags & LDBP_SYMMETRIC;
+  const bool fast = !(d->flags & LDBP_PRECISE);
+  const int M = d->steps;
+  auto act = [&](int i) -> float2* { return reinterpret_cast<float2*>(ws + w.act_off + (size_t)(i - 1) * w.act_each); };
+  auto gb = [&](int k) -> float2* { return reinterpret_cast<float2*>(ws + w.g_off + (size_t)(k & 1) * w.g_each); };
+  const int64_t stride = (int64_t)(w.act_each / sizeof(float2));
+  {
+    const FwdPlan fp = plan_fwd_segments(M, kh);
+    for (int k = 0; k < fp.segs; ++k) {
+      const int s0 = k * fp.steps_per, s1 = std::min(M, s0 + fp.steps_per);
+      LDBP_TRY(launch_fwd(d, s0 == 0 ? x : act(s0), act(s1), taps, gamma, mask, s0, s1, st,
+                          s1 - s0 >= 2 ? act(1) : nullptr, 1, stride, true, false));
+    }
+  }
+  RevFn fn = get_rev(kh, sym, fast);
+  double* partials = reinterpret_cast<double*>(ws + w.part_off);
+  double* lossp = reinterpret_cast<double*>(ws + w.loss_off);
+  for (int k = p.Kr - 1; k >= 0; --k) {
+    const int s0 = k * p.Cr, s1 = std::min(M, (k + 1) * p.Cr);
+    ldbp::RevArgs a;
+    a.x = x;
+    a.act = act(1);
+    a.act_stride = stride;
+    a.gin = (k == p.Kr - 1) ? gy : gb(k + 1);
+    a.target = target;
+    a.gout = (k == 0) ? gx : gb(k);
+    a.taps = taps;
+    a.gamma = gamma;
+    a.mask = mask;
+    a.partials = partials;
+    a.loss_partials = lossp;
+    a.seed_scale = 2.0f;
+    a.T = d->taps;
+    a.M = M;
+    a.s0 = s0;
+    a.s1 = s1;
+    a.g = p.tile.g;
+    const size_t smem = rev_smem(kh, sym, s1 - s0, M, p.tile.nthreads);
+    cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+      TraceScope ts(LDBP_K_REVERSE, s1 - s0, d->batch * d->n, st);
+      fn<<<p.tile.grid, p.tile.nthreads, smem, st>>>(a);
+    }
+    LDBP_TRY(cuda_check("rev_tile_kernel launch"));
+  }
+  return run_reduce(d, partials, gy ? nullptr : lossp, p.tile.grid, p.V, ws + w.part2_off, ws + w.loss2_off, mask,
+                    st, buf, dtaps, dgamma);
 }
 
 int zero_outputs(double* p, size_t count, cudaStream_t st) {
@@ -572,6 +767,10 @@ int ldbp_workspace_bytes(const ldbp_dims* d, int op, size_t* bytes) {
     case LDBP_OP_BACKWARD:
     case LDBP_OP_LOSS_GRAD:
     case LDBP_OP_TRAIN_STEP: {
+      if (use_store_all(d)) {
+        *bytes = rev_ws(d, plan_rev(d, true)).total;
+        return LDBP_OK;
+      }
       BwdPlan p = plan_bwd(d, true);
       *bytes = bwd_ws(d, p).total;
       return LDBP_OK;
@@ -586,6 +785,13 @@ int ldbp_launch_count(const ldbp_dims* d, int op, int* launches) {
   if (!launches) return fail(LDBP_EINVAL, "launches is NULL");
   if (d->batch == 0) { *launches = (op == LDBP_OP_FORWARD) ? 0 : 1; return LDBP_OK; }
   if (op == LDBP_OP_FORWARD) { *launches = plan_fwd_segments(d->steps, (d->taps - 1) / 2).segs; return LDBP_OK; }
+  if (use_store_all(d)) {
+    const RevPlan rp = plan_rev(d, true);
+    int n = plan_fwd_segments(d->steps, (d->taps - 1) / 2).segs + rp.Kr + 1 + (reduce_chunks(rp.tile.grid) > 0 ? 1 : 0);
+    if (op == LDBP_OP_TRAIN_STEP) n += 1;
+    *launches = n;
+    return LDBP_OK;
+  }
   BwdPlan p = plan_bwd(d, true);
   int nf = 0;
   if (p.K > 1) {
@@ -635,6 +841,15 @@ int ldbp_backward(const ldbp_dims* d, const void* x, const void* gy, const void*
   LDBP_TRY(check_ptr(gamma, "gamma", 4));
   if (gx_or_null) LDBP_TRY(check_ptr(gx_or_null, "gx", 8));
   if (gx_or_null == x || gx_or_null == gy) return fail(LDBP_EINVAL, "gx must not alias x or gy");
+  if (use_store_all(d)) {
+    const RevPlan rp = plan_rev(d, true);
+    const RevWs rw = rev_ws(d, rp);
+    if (!ws || ws_bytes < rw.total)
+      return fail(LDBP_EWORKSPACE, "backward needs %zu workspace bytes, got %zu", rw.total, ws_bytes);
+    LDBP_TRY(check_ptr(ws, "ws", 16));
+    return run_rev_chain(d, (const float2*)x, (const float2*)gy, nullptr, (const float2*)taps, gamma, nullptr,
+                         (float2*)gx_or_null, (unsigned char*)ws, rp, rw, st, nullptr, dtaps, dgamma);
+  }
   BwdPlan p = plan_bwd(d, true);
   BwdWs w = bwd_ws(d, p);
   if (!ws || ws_bytes < w.total) return fail(LDBP_EWORKSPACE, "backward needs %zu workspace bytes, got %zu", w.total, ws_bytes);
@@ -655,6 +870,15 @@ int ldbp_loss_grad(const ldbp_dims* d, const void* x, const void* target, const 
   LDBP_TRY(check_ptr(target, "target", 8));
   LDBP_TRY(check_ptr(taps, "taps", 8));
   LDBP_TRY(check_ptr(gamma, "gamma", 4));
+  if (use_store_all(d)) {
+    const RevPlan rp = plan_rev(d, true);
+    const RevWs rw = rev_ws(d, rp);
+    if (!ws || ws_bytes < rw.total)
+      return fail(LDBP_EWORKSPACE, "loss_grad needs %zu workspace bytes, got %zu", rw.total, ws_bytes);
+    LDBP_TRY(check_ptr(ws, "ws", 16));
+    return run_rev_chain(d, (const float2*)x, nullptr, (const float2*)target, (const float2*)taps, gamma, mask,
+                         nullptr, (unsigned char*)ws, rp, rw, st, buf, nullptr, nullptr);
+  }
   BwdPlan p = plan_bwd(d, true);
   BwdWs w = bwd_ws(d, p);
   if (!ws || ws_bytes < w.total) return fail(LDBP_EWORKSPACE, "loss_grad needs %zu workspace bytes, got %zu", w.total, ws_bytes);

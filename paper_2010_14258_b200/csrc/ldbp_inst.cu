@@ -8,6 +8,7 @@
 
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
+using RevFn = void (*)(const ldbp::RevArgs);
 
 #define LDBP_CAT2(a, b) a##b
 #define LDBP_CAT(a, b) LDBP_CAT2(a, b)
@@ -22,4 +23,10 @@ BwdFn LDBP_CAT(ldbp_get_bwd_, LDBP_KH)(bool sym, bool fast) {
   constexpr int K = LDBP_KH, R = LDBP_BWD_R;
   if (sym) return fast ? ldbp::bwd_segment_kernel<K, R, true, true> : ldbp::bwd_segment_kernel<K, R, true, false>;
   return fast ? ldbp::bwd_segment_kernel<K, R, false, true> : ldbp::bwd_segment_kernel<K, R, false, false>;
+}
+
+RevFn LDBP_CAT(ldbp_get_rev_, LDBP_KH)(bool sym, bool fast) {
+  constexpr int K = LDBP_KH, R = LDBP_REV_R;
+  if (sym) return fast ? ldbp::rev_tile_kernel<K, R, true, true> : ldbp::rev_tile_kernel<K, R, true, false>;
+  return fast ? ldbp::rev_tile_kernel<K, R, false, true> : ldbp::rev_tile_kernel<K, R, false, false>;
 }

@@ -28,6 +28,9 @@
 #ifndef LDBP_BWD_R
 #define LDBP_BWD_R 8   // samples per thread, backward kernels
 #endif
+#ifndef LDBP_REV_R
+#define LDBP_REV_R 8   // samples per thread, store-all reverse kernel
+#endif
 
 #ifndef LDBP_NORM
 #define LDBP_NORM 1  // h0-normalised FIR when well conditioned (saves one complex multiply per FIR)
@@ -197,8 +200,14 @@ __device__ __forceinline__ void store_mapped(float2* __restrict__ dst, const Sto
                                              f2x (&u)[R]) {
   f2x* d2 = reinterpret_cast<f2x*>(dst);
   if (sm.off >= 0) {
+    if (R % 2 == 0 && ((reinterpret_cast<uintptr_t>(d2 + sm.off) & 15) == 0)) {
+      ulonglong2* d4 = reinterpret_cast<ulonglong2*>(d2 + sm.off);
 #pragma unroll
-    for (int k = 0; k < R; ++k) d2[sm.off + k] = u[k];
+      for (int k = 0; k < R / 2; ++k) d4[k] = make_ulonglong2(u[2 * k], u[2 * k + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < R; ++k) d2[sm.off + k] = u[k];
+    }
   } else if (sm.mask) {
     // owned samples have q in [H, H+n): position q - H, no wrap; only block crossings remain
     const Span sp = make_span(e0, g);
@@ -566,6 +575,92 @@ struct StepNorm {
   float2 c;  // c_i = h0^(i)
 };
 
+// Normalisation over the step range [n0, nM) ("global" mode, used by the store-all training
+// path so that every launch of a chain agrees): per step c_i = h0^(i) and the prefix products
+// P_i = prod_{k=n0..i} c_k into sh_norm[i - n0]; *sh_flag = 1 iff the h0-normalised model is
+// well conditioned over the whole range (same test as stage_params).  Reads taps from global
+// memory (tiny, L2-resident); every CTA of every launch reaches the same decision.
+template <int KH, bool SYM>
+__device__ __forceinline__ void norm_range(const float2* __restrict__ taps, const uint8_t* __restrict__ mask, int T,
+                                           int n0, int nM, StepNorm* sh_norm, int* sh_flag) {
+  constexpr int NT = ntaps_used<SYM, KH>();
+  const int S = nM - n0;
+  if (threadIdx.x == 0) *sh_flag = (SYM && LDBP_NORM) ? 1 : 0;
+  __syncthreads();
+  if (SYM && LDBP_NORM)
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+      const int s = n0 + i;
+      float e = 0.f;
+      float2 h0 = make_float2(0.f, 0.f);
+      for (int t = 0; t < NT; ++t) {
+        const int ti = t + KH;
+        float2 h = taps[(int64_t)s * T + ti];
+        if (mask && !mask[(int64_t)s * T + ti]) h = make_float2(0.f, 0.f);
+        if (t == 0) h0 = h;
+        e = fmaf(t ? 2.f : 1.f, h.x * h.x + h.y * h.y, e);
+      }
+      const float m0 = h0.x * h0.x + h0.y * h0.y;
+      if (!(m0 > 0.f) || m0 < 1e-6f * e) *sh_flag = 0;
+      sh_norm[i].c = h0;
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ok = *sh_flag;
+    double pr = 1.0, pi = 0.0;
+    for (int i = 0; i < S; ++i) {
+      if (ok) {
+        const float2 c = sh_norm[i].c;
+        const double nr = pr * c.x - pi * c.y, ni = pr * c.y + pi * c.x;
+        pr = nr;
+        pi = ni;
+        const double mp = pr * pr + pi * pi;
+        if (!(mp >= 1e-24 && mp <= 1e24)) ok = 0;
+        sh_norm[i].P = make_float2((float)pr, (float)pi);
+      }
+    }
+    if (!ok)
+      for (int i = 0; i < S; ++i) {
+        sh_norm[i].P = make_float2(1.f, 0.f);
+        sh_norm[i].c = make_float2(1.f, 0.f);
+      }
+    *sh_flag = ok;
+  }
+  __syncthreads();
+}
+
+// Stage taps (packed forward and/or adjoint form) and gamma_hat of steps [s0, s1) using the
+// normalisation computed by norm_range over [n0, nM) (sh_norm indexed by step - n0).
+template <int KH, bool SYM, bool FWD, bool ADJ>
+__device__ __forceinline__ void stage_range(const float2* __restrict__ taps, const float* __restrict__ gamma,
+                                            const uint8_t* __restrict__ mask, int T, int s0, int s1, int n0,
+                                            TapP* sh_taps, TapP* sh_taps_adj, float* sh_gamma,
+                                            const StepNorm* sh_norm, bool norm) {
+  constexpr int NT = ntaps_used<SYM, KH>();
+  const int S = s1 - s0;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+    float gm = gamma[s0 + i];
+    if (norm) {
+      const float2 P = sh_norm[s0 + i - n0].P;
+      gm = (float)((double)gm * ((double)P.x * P.x + (double)P.y * P.y));
+    }
+    sh_gamma[i] = gm;
+  }
+  for (int i = threadIdx.x; i < S * NT; i += blockDim.x) {
+    const int s = s0 + i / NT;
+    const int t = (i % NT) + (SYM ? KH : 0);
+    float2 h = taps[(int64_t)s * T + t];
+    if (mask && !mask[(int64_t)s * T + t]) h = make_float2(0.f, 0.f);
+    if (norm) {
+      const float2 c = sh_norm[s - n0].c;
+      const float inv = 1.f / (c.x * c.x + c.y * c.y);
+      h = make_float2((h.x * c.x + h.y * c.y) * inv, (h.y * c.x - h.x * c.y) * inv);
+      if (t == KH) h = make_float2(1.f, 0.f);
+    }
+    if constexpr (FWD) sh_taps[i] = tap_fwd(h);
+    if constexpr (ADJ) sh_taps_adj[i] = tap_adj(h);
+  }
+}
+
 // Stage the packed taps and gamma of steps [s0, s1) into shared memory (masked taps -> 0;
 // SYM keeps only h_0..h_Kh).  ADJ additionally stages the adjoint (conjugate) packing.
 // SYM: thread 0 first decides whether the h0-normalised model is well conditioned for this
@@ -681,6 +776,13 @@ struct FwdArgs {
   const float* gamma;
   const uint8_t* mask;
   int T, s0, s1;
+  // Normalisation range.  Local mode (n0 == s0, nM == s1): src is u^(s0) in the original scale,
+  // every store is scaled back (P relative to s0).  Global mode (n0 = 0, nM = M, the store-all
+  // training path): src is the normalised state u_hat^(s0), P is relative to step 0, and
+  // checkpoints / dst are stored raw (normalised) unless scale_dst (then dst = y, original scale).
+  int n0, nM;
+  int global_norm;
+  int scale_dst;
   Geo g;
 };
 
@@ -703,6 +805,8 @@ template <int KH, int R, bool SYM, bool FAST, bool NORM>
 __device__ __forceinline__ void fwd_steps(const FwdArgs& a, f2x (&u)[R], const TapP* sh_taps, const float* sh_gamma,
                                           const StepNorm* sh_norm, f2x* sh_edge, uint64_t* bars, const StoreMap& smap,
                                           int64_t e0, int lane, int warp, int nwarps) {
+  const bool global = a.global_norm != 0;
+  sh_norm += a.s0 - a.n0;  // sh_norm[s] = normalisation of global step s0 + s
   constexpr int NTU = ntaps_used<SYM, KH>();
   f2x hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1];
   const int left = threadIdx.x > 0 ? threadIdx.x - 1 : 0;
@@ -724,7 +828,9 @@ __device__ __forceinline__ void fwd_steps(const FwdArgs& a, f2x (&u)[R], const T
     for (int k = 0; k < R; ++k) u[k] = nu[k];
     const int gs = a.s0 + s + 1;  // global step count reached
     if (a.ckpt && gs < a.s1 && gs % a.ckpt_every == 0) {
-      if constexpr (NORM) {
+      if (global) {
+        store_mapped<R>(a.ckpt + (int64_t)(gs / a.ckpt_every - 1) * a.ckpt_stride, smap, e0, a.g, u);
+      } else if constexpr (NORM) {
         store_mapped_scaled<R>(a.ckpt + (int64_t)(gs / a.ckpt_every - 1) * a.ckpt_stride, smap, e0, a.g, u,
                                sh_norm[s].P);
       } else {
@@ -732,7 +838,7 @@ __device__ __forceinline__ void fwd_steps(const FwdArgs& a, f2x (&u)[R], const T
       }
     }
   }
-  if constexpr (NORM)
+  if (NORM && (!global || a.scale_dst))
     store_mapped_scaled<R>(a.dst, smap, e0, a.g, u, sh_norm[a.s1 - a.s0 - 1].P);
   else
     store_mapped<R>(a.dst, smap, e0, a.g, u);
@@ -747,8 +853,8 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
   f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);  // 2*2*KH*(XSMEM ? nthreads : 32)
   TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge + 4 * (LDBP_FWD_XSMEM ? (int)blockDim.x : kMaxWarps) *
                                                         (KH > 0 ? KH : 1));  // S*NTU
-  StepNorm* sh_norm = reinterpret_cast<StepNorm*>(sh_taps + S * NTU);                // S
-  float* sh_gamma = reinterpret_cast<float*>(sh_norm + S);                           // S
+  StepNorm* sh_norm = reinterpret_cast<StepNorm*>(sh_taps + S * NTU);                // max(S, nM-n0)
+  float* sh_gamma = reinterpret_cast<float*>(sh_norm + max(S, a.nM - a.n0));         // S
   int* sh_flag = reinterpret_cast<int*>(sh_gamma + S);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -757,8 +863,14 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
   const int64_t e0 = thread_e0(a.g, R);
   load_window<R>(a.src, e0, a.g, u);
   const StoreMap smap = store_map<R>(e0, a.g);
-  stage_params<KH, SYM, false>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, nullptr, sh_gamma, sh_norm,
-                               sh_flag);
+  if (a.global_norm) {
+    norm_range<KH, SYM>(a.taps, a.mask, a.T, a.n0, a.nM, sh_norm, sh_flag);
+    stage_range<KH, SYM, true, false>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, a.n0, sh_taps, nullptr, sh_gamma,
+                                      sh_norm, *sh_flag != 0);
+  } else {
+    stage_params<KH, SYM, false>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, nullptr, sh_gamma, sh_norm,
+                                 sh_flag);
+  }
   __syncthreads();
   if (SYM && *sh_flag)
     fwd_steps<KH, R, SYM, FAST, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane, warp, nwarps);
@@ -1256,3 +1368,5 @@ __global__ void adam_kernel(const AdamArgs a) {
 #endif  // LDBP_AUX_KERNELS
 
 }  // namespace ldbp
+
+#include "ldbp_reverse.cuh"

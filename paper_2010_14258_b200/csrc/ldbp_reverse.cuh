@@ -1,0 +1,359 @@
+// ldbp_reverse.cuh — store-all reverse kernel of the training step (SURVEY.md §8(a) rows a5, a6,
+// a8; row a7 by stored activations instead of recompute).
+//
+// The forward pass of the training step (fwd_tile_kernel in global-normalisation mode, one
+// store per step) leaves every activation u_hat^(i), i = 1..M, in HBM (8 B/sample-step; C3:
+// 3.4 GB, C5: 54 GB of the 180 GB).  The reverse sweep then needs no forward recompute: one
+// launch covers steps [s0, s1) of one tile, exactly like the forward tile kernel, with the
+// adjoint g held in registers from step to step and a halo H = (s1 - s0)*Kh that shrinks by Kh
+// per reverse step (the adjoint's dependency cone).
+//
+// Per reverse step l (Appendix A of SURVEY.md, chain rule on Eq. (7)):
+//   v = u^(l+1) (registers, loaded the step before), g = dL/dv
+//   NL adjoint:  c = Im(g conj v), ga = (g + 2 gamma' c v) e^{-j phi}, dgamma' += c |v|^2
+//   tap grads:   dh_j += ga_t conj(u_{t-j} (+ u_{t+j} SYM))   over owned samples only
+//   FIR adjoint: g_s = sum_j conj(h_j) ga_{s+j}
+// u^(l) arrives by cp.async (LDGSTS) into a double-buffered shared-memory copy of the window,
+// issued one step ahead, so the HBM latency overlaps the previous step's arithmetic; each
+// thread takes its own R samples and the Kh-sample halos of its neighbours from that copy.  The
+// ga halos go through a small double-buffered edge array; one __syncthreads per step.
+// Per-step partial sums: transposing warp butterfly (fp32) -> smem -> fp64 across warps in
+// fixed order -> partials[cta][step][v] (deterministic), reduced by reduce_partials_kernel.
+#pragma once
+
+namespace ldbp {
+
+struct RevArgs {
+  const float2* x;         // u^(0) [B][n] (original scale == normalised scale at step 0)
+  const float2* act;       // u_hat^(i) at act + (i-1)*act_stride, i = 1..M (normalised state)
+  int64_t act_stride;      // elements
+  const float2* gin;       // s1 == M: dL/dy in the original scale, or nullptr -> seed from target;
+                           // s1 <  M: normalised adjoint w.r.t. u_hat^(s1) (previous launch's gout)
+  const float2* target;    // [B][n] (seed mode)
+  float2* gout;            // adjoint w.r.t. u_hat^(s0) (original scale when s0 == 0), or nullptr
+  const float2* taps;
+  const float* gamma;
+  const uint8_t* mask;
+  double* partials;        // [gridDim.x][M][V]
+  double* loss_partials;   // [gridDim.x] (seed mode)
+  float seed_scale;        // seed g = seed_scale * (y - target)
+  int T, M, s0, s1;
+  Geo g;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* gmem_src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src),
+               "r"(src_bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ const float2* rev_src(const RevArgs& a, int i) {
+  return i == 0 ? a.x : a.act + (int64_t)(i - 1) * a.act_stride;
+}
+
+// Shared-memory window copy: sample k of thread t at f2x index ((k >> 1) * nthr + t) * 2 + (k & 1)
+// (16-byte pairs, lane-consecutive -> conflict-free LDS.128 / LDGSTS.128).
+__device__ __forceinline__ int ubuf_idx(int k, int t, int nthr) { return ((k >> 1) * nthr + t) * 2 + (k & 1); }
+
+// Issue the asynchronous copy of this thread's R window samples of `src` (zeros outside [0, E)).
+template <int R>
+__device__ __forceinline__ void async_window(const float2* __restrict__ src, int64_t e0, const Geo& g, f2x* buf,
+                                             int nthr, int64_t fast_off) {
+  const int t = threadIdx.x;
+  if (fast_off >= 0) {
+    const f2x* p = reinterpret_cast<const f2x*>(src) + fast_off;
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+      for (int m = 0; m < R / 2; ++m) cp_async16(buf + ubuf_idx(2 * m, t, nthr), p + 2 * m);
+    } else {
+#pragma unroll
+      for (int k = 0; k < R; ++k) cp_async8(buf + ubuf_idx(k, t, nthr), p + k);
+    }
+  } else {
+    const Span sp = make_span(e0, g);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      int64_t b, pos;
+      int q;
+      const bool ok = span_at<R>(sp, k, g, e0, &b, &pos, &q);
+      cp_async8_zfill(buf + ubuf_idx(k, t, nthr), ok ? (const void*)(src + b * g.n + pos) : (const void*)src,
+                      ok ? 8 : 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+struct RevSmem {
+  TapP* taps_adj;   // [S][NTU]
+  StepNorm* norm;   // [M] (global normalisation, step-indexed)
+  float* gamma;     // [S] gamma_hat
+  int* flag;
+  float* red;       // [2][nwarps][V] per-warp partials of one step (double-buffered)
+  f2x* edge;        // [2 buf][2 side][KH][nthr] ga halos
+  f2x* ubuf;        // [2 buf][R][nthr] window copies of u^(l)
+};
+
+// CTA-level fp64 reduction of step l's per-warp partials (buffer b), mapped back to the original
+// parameters (dgamma_i = |P_i|^2 dgamma_hat_i, dh^(i) = conj(1/c_i) dh_hat^(i)), written to
+// partials[cta][l][.].  Complex pair q (0: dgamma, q >= 1: tap q-1) is handled by lane 0 of warp
+// q % nwarps, so the work is spread over the warps.
+template <int NTU>
+__device__ __forceinline__ void rev_flush(const RevArgs& a, const RevSmem& sm, int b, int l, bool norm, int lane,
+                                          int warp, int nwarps) {
+  constexpr int V = 1 + 2 * NTU;
+  if (lane != 0) return;
+  for (int q = warp; q <= NTU; q += nwarps) {
+    const float* red = sm.red + (size_t)b * nwarps * V;
+    double* out = a.partials + ((int64_t)blockIdx.x * a.M + l) * V;
+    const StepNorm nm = sm.norm[l];
+    if (q == 0) {
+      double acc = 0.0;
+      for (int w = 0; w < nwarps; ++w) acc += (double)red[w * V];
+      if (norm) acc *= (double)nm.P.x * nm.P.x + (double)nm.P.y * nm.P.y;
+      out[0] = acc;
+    } else {
+      const int v = 1 + 2 * (q - 1);
+      double re = 0.0, im = 0.0;
+      for (int w = 0; w < nwarps; ++w) {
+        re += (double)red[w * V + v];
+        im += (double)red[w * V + v + 1];
+      }
+      if (norm) {
+        const double cx = nm.c.x, cy = nm.c.y, m = cx * cx + cy * cy;
+        const double r2 = (re * cx - im * cy) / m, i2 = (re * cy + im * cx) / m;
+        re = r2;
+        im = i2;
+      }
+      out[v] = re;
+      out[v + 1] = im;
+    }
+  }
+}
+
+template <int KH, int R, bool SYM, bool FAST, bool NORM>
+__device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, int64_t e0, int64_t fast_off,
+                                         uint32_t own, int lane, int warp, int nwarps) {
+  constexpr int NTU = ntaps_used<SYM, KH>();
+  constexpr int V = 1 + 2 * NTU;
+  static_assert(R % 2 == 0 && R >= KH, "window pairs and neighbour halos need even R >= Kh");
+  const int nthr = blockDim.x, tid = threadIdx.x;
+  const int left = tid > 0 ? tid - 1 : 0;
+  const int right = tid + 1 < nthr ? tid + 1 : tid;
+  const int s0 = a.s0, s1 = a.s1;
+
+  // prefetch u^(s1-1) while v = u^(s1) and the seed are loaded synchronously
+  async_window<R>(rev_src(a, s1 - 1), e0, a.g, sm.ubuf + (size_t)((s1 - 1) & 1) * R * nthr, nthr, fast_off);
+  f2x v[R], g[R];
+  load_window<R>(rev_src(a, s1), e0, a.g, v);
+  const float2 Pend = sm.norm[a.M - 1].P;
+  const TapP conjP = tap_adj(Pend);  // conj(P) * x
+  if (a.gin == nullptr) {
+    f2x t[R];
+    load_window<R>(a.target, e0, a.g, t);
+    float lsum = 0.f;
+    const f2x m1 = bcast(-1.f);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const f2x y = NORM ? cscale(Pend, v[k]) : v[k];
+      const f2x e = fma2(m1, t[k], y);  // y - target
+      const f2x ge = mul2(bcast(a.seed_scale), e);
+      g[k] = NORM ? tmul(conjP, ge) : ge;
+      const float ex = lof(e), ey = hif(e);
+      if (own & (1u << k)) lsum = fmaf(ex, ex, fmaf(ey, ey, lsum));
+    }
+    lsum = warp_sum(lsum);
+    if (lane == 0) sm.red[warp] = lsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < nwarps; ++w) tot += (double)sm.red[w];
+      a.loss_partials[blockIdx.x] = tot;
+    }
+    // sm.red is next written after the first step's barrier-protected flush ordering below:
+    // the first per-warp write happens after this barrier pair.
+    __syncthreads();
+  } else {
+    load_window<R>(a.gin, e0, a.g, g);
+    if (NORM && s1 == a.M) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) g[k] = tmul(conjP, g[k]);
+    }
+  }
+
+  // NL adjoint of one sample (g -> ga in place), Appendix A: with v = u^(l+1), g = dL/dv,
+  //   c = Im(g conj v), ga = (g + 2 gamma' c v) e^{-j phi}, dgamma' += c |v|^2 (owned only).
+  auto nl_adjoint = [&](f2x& gk, f2x vk, float gm, float gm2, bool owned, float& dgam) {
+    const float vx = lof(vk), vy = hif(vk);
+    const float p = fmaf(vx, vx, vy * vy);
+    float sn, cs;
+    sincos_phase<FAST>(gm * p, &sn, &cs);
+    const float cim = fmaf(hif(gk), vx, -lof(gk) * vy);  // Im(g conj v)
+    const f2x t = fma2(bcast(gm2 * cim), vk, gk);
+    gk = fma2(bcast(lof(t)), pk(cs, -sn), mul2(bcast(hif(t)), pk(sn, cs)));
+    if (owned) dgam = fmaf(cim, p, dgam);
+  };
+  // step s1-1's NL adjoint up front; every later one is fused into the previous step's FIR-
+  // adjoint loop (software pipelining: MUFU work interleaved with the FMA-pipe work)
+  float dgam = 0.f;
+  {
+    const float gm = sm.gamma[s1 - 1 - s0];
+#pragma unroll
+    for (int k = 0; k < R; ++k) nl_adjoint(g[k], v[k], gm, 2.f * gm, (own >> k) & 1u, dgam);
+  }
+
+  for (int l = s1 - 1; l >= s0; --l) {
+    const int li = l - s0;
+    // ---- publish ga edges, wait for u^(l), one barrier ----
+    f2x* ebuf = sm.edge + (size_t)(l & 1) * 2 * (KH > 0 ? KH : 1) * nthr;
+    if constexpr (KH > 0) {
+#pragma unroll
+      for (int j = 0; j < KH; ++j) {
+        ebuf[j * nthr + tid] = g[j];                       // head
+        ebuf[(KH + j) * nthr + tid] = g[R - KH + j];       // tail
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // flush the previous step's per-warp partials (written before this barrier)
+    if (l + 1 < s1) rev_flush<NTU>(a, sm, (l + 1) & 1, l + 1, NORM, lane, warp, nwarps);
+    // prefetch u^(l-1) into the other buffer (its last reader, step l+1, is behind the barrier)
+    if (l > s0)
+      async_window<R>(rev_src(a, l - 1), e0, a.g, sm.ubuf + (size_t)((l - 1) & 1) * R * nthr, nthr, fast_off);
+    const f2x* ub = sm.ubuf + (size_t)(l & 1) * R * nthr;
+    f2x u[R], hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1], gl[KH > 0 ? KH : 1], gr[KH > 0 ? KH : 1];
+#pragma unroll
+    for (int m = 0; m < R / 2; ++m) {
+      const ulonglong2 pr = *reinterpret_cast<const ulonglong2*>(ub + ubuf_idx(2 * m, tid, nthr));
+      u[2 * m] = pr.x;
+      u[2 * m + 1] = pr.y;
+    }
+    if constexpr (KH > 0) {
+#pragma unroll
+      for (int j = 0; j < KH; ++j) {
+        hl[j] = ub[ubuf_idx(R - KH + j, left, nthr)];
+        hr[j] = ub[ubuf_idx(j, right, nthr)];
+        gl[j] = ebuf[(KH + j) * nthr + left];
+        gr[j] = ebuf[j * nthr + right];
+      }
+    }
+    // ---- tap gradients over owned samples: dh_j += ga_t conj(w), w = u_{t-j} (+ u_{t+j}) ----
+    f2x dh[NTU], dhb[NTU];
+#pragma unroll
+    for (int j = 0; j < NTU; ++j) dh[j] = dhb[j] = 0ull;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const f2x gk = (own & (1u << k)) ? g[k] : 0ull;
+      const TapP gt = {gk, pk(hif(gk), -lof(gk))};
+      if constexpr (SYM) {
+        tmac2(dh[0], dhb[0], gt, u[k]);
+#pragma unroll
+        for (int j = 1; j <= KH; ++j)
+          tmac2(dh[j], dhb[j], gt, add2(LDBP_WIN(u, hl, hr, k - j), LDBP_WIN(u, hl, hr, k + j)));
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 2 * KH + 1; ++jj) tmac2(dh[jj], dhb[jj], gt, LDBP_WIN(u, hl, hr, k - (jj - KH)));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NTU; ++j) dh[j] = add2(dh[j], dhb[j]);
+    // ---- FIR adjoint g_s = sum_j conj(h_j) ga_{s+j} (NORM: h_0 = 1), fused with the NL adjoint
+    //      of step l-1 on the fresh g_s (v = u^(l)) ----
+    const bool more = l > s0;
+    const float gmn = more ? sm.gamma[li - 1] : 0.f;
+    const float gmn2 = 2.f * gmn;
+    float dgam_next = 0.f;
+    {
+      TapP hs[NTU];
+#pragma unroll
+      for (int j = 0; j < NTU; ++j) hs[j] = sm.taps_adj[li * NTU + j];
+      f2x ng[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        f2x acc_a, acc_b;
+        if constexpr (SYM && NORM) {
+          acc_a = g[k];
+          acc_b = 0ull;
+#pragma unroll
+          for (int j = 1; j <= KH; ++j)
+            tmac2(acc_a, acc_b, hs[j], add2(LDBP_WIN(g, gl, gr, k - j), LDBP_WIN(g, gl, gr, k + j)));
+        } else if constexpr (SYM) {
+          acc_a = mul2(bcast(lof(g[k])), hs[0].a);
+          acc_b = mul2(bcast(hif(g[k])), hs[0].b);
+#pragma unroll
+          for (int j = 1; j <= KH; ++j)
+            tmac2(acc_a, acc_b, hs[j], add2(LDBP_WIN(g, gl, gr, k - j), LDBP_WIN(g, gl, gr, k + j)));
+        } else {
+          const f2x w0 = LDBP_WIN(g, gl, gr, k - KH);
+          acc_a = mul2(bcast(lof(w0)), hs[0].a);
+          acc_b = mul2(bcast(hif(w0)), hs[0].b);
+#pragma unroll
+          for (int jj = 1; jj < 2 * KH + 1; ++jj) tmac2(acc_a, acc_b, hs[jj], LDBP_WIN(g, gl, gr, k + (jj - KH)));
+        }
+        ng[k] = (SYM && NORM && KH == 0) ? acc_a : add2(acc_a, acc_b);
+        if (more) nl_adjoint(ng[k], u[k], gmn, gmn2, (own >> k) & 1u, dgam_next);
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) g[k] = ng[k];
+    }
+    // ---- per-warp reduction of this step's partials -> red[l & 1][warp][.] ----
+    {
+      constexpr int VP = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
+      float vals[VP];
+      vals[0] = dgam;
+#pragma unroll
+      for (int j = 0; j < NTU; ++j) { vals[1 + 2 * j] = lof(dh[j]); vals[2 + 2 * j] = hif(dh[j]); }
+#pragma unroll
+      for (int i = V; i < VP; ++i) vals[i] = 0.f;
+      const float r = warp_reduce_scatter<VP>(vals, lane);
+      constexpr int SH = VP == 2 ? 4 : VP == 4 ? 3 : VP == 8 ? 2 : VP == 16 ? 1 : 0;
+      const int idx = lane >> SH;
+      float* red = sm.red + ((size_t)(l & 1) * nwarps + warp) * V;
+      if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
+    }
+    dgam = dgam_next;
+  }
+  __syncthreads();
+  rev_flush<NTU>(a, sm, s0 & 1, s0, NORM, lane, warp, nwarps);
+  if (a.gout) store_owned<R>(a.gout, e0, a.g, g);
+}
+
+#ifndef LDBP_REV_MAXT
+#define LDBP_REV_MAXT 512  // threads per CTA (max); 128 registers -> 16 warps per SM either way
+#endif
+template <int KH, int R, bool SYM, bool FAST>
+__global__ void __launch_bounds__(LDBP_REV_MAXT, 65536 / (LDBP_REV_MAXT * 128)) rev_tile_kernel(const RevArgs a) {
+  constexpr int NTU = ntaps_used<SYM, KH>();
+  constexpr int V = 1 + 2 * NTU;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int S = a.s1 - a.s0;
+  const int nthr = blockDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = nthr >> 5;
+  // carve-up (16-byte aligned regions; mirrored by rev_smem() on the host)
+  RevSmem sm;
+  sm.ubuf = reinterpret_cast<f2x*>(smem_raw);                                  // 2*R*nthr
+  sm.edge = sm.ubuf + (size_t)2 * R * nthr;                                    // 4*KH*nthr
+  sm.taps_adj = reinterpret_cast<TapP*>(sm.edge + (size_t)4 * (KH > 0 ? KH : 1) * nthr);  // S*NTU
+  sm.norm = reinterpret_cast<StepNorm*>(sm.taps_adj + S * NTU);                // M
+  sm.red = reinterpret_cast<float*>(sm.norm + a.M);                            // 2*nwarps*V (>= nwarps)
+  sm.gamma = sm.red + ((2 * nwarps * V + 3) & ~3);                             // S
+  sm.flag = reinterpret_cast<int*>(sm.gamma + ((S + 3) & ~3));
+
+  const int64_t e0 = thread_e0(a.g, R);
+  const Span sp = make_span(e0, a.g);
+  const int64_t fast_off = span_fast<R>(sp, a.g, e0) ? sp.b0 * a.g.n + (sp.q0 - a.g.H) : -1;
+  const uint32_t own = owned_mask<R>(e0, a.g);
+  norm_range<KH, SYM>(a.taps, a.mask, a.T, 0, a.M, sm.norm, sm.flag);
+  const bool norm = SYM && *sm.flag;
+  stage_range<KH, SYM, false, true>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, 0, nullptr, sm.taps_adj, sm.gamma,
+                                    sm.norm, norm);
+  __syncthreads();
+  if (norm)
+    rev_body<KH, R, SYM, FAST, true>(a, sm, e0, fast_off, own, lane, warp, nwarps);
+  else
+    rev_body<KH, R, SYM, FAST, false>(a, sm, e0, fast_off, own, lane, warp, nwarps);
+}
+
+}  // namespace ldbp

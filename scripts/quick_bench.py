@@ -49,7 +49,7 @@ for name in names:
     peak = 148 * 128 * 1.965e9
     print(f"{name}: {ms_step:.3f} ms/step  {ss / ms_step / 1e6:.1f} Gss/s  step-frac@1965 {ss * ips / (ms_step * 1e-3) / peak:.3f}")
     for kind, (ms, nl, sst) in sorted(per.items()):
-        ipss = bench.instr_fwd(kh) if kind == _lib.K_FORWARD else bench.instr_bwd(kh) if kind == _lib.K_BACKWARD else 0
+        ipss = bench.instr_fwd(kh) if kind == _lib.K_FORWARD else bench.instr_bwd(kh) if kind in (_lib.K_BACKWARD, _lib.K_REVERSE) else 0
         frac = (ipss * sst / (ms * 1e-3) / peak) if ipss else 0
         print(f"   kind {kind}: {ms / reps:.3f} ms/step over {nl // reps} launches, frac {frac:.3f}")
     del x, tgt, ws

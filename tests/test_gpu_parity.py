@@ -143,10 +143,21 @@ BWD_CASES = [
 ]
 
 
-@pytest.mark.parametrize("B,n,M,T,sym,cmax", BWD_CASES)
-def test_backward_parity(P, monkeypatch, B, n, M, T, sym, cmax):
+# the two row-a7 schedules: 0 = checkpoint + recompute segments, 1 = store-all + fused reverse
+MODES = ["0", "1"]
+
+
+def set_mode(monkeypatch, mode, cmax):
+    monkeypatch.setenv("LDBP_BWD_MODE", mode)
     if cmax:
         monkeypatch.setenv("LDBP_BWD_MAX_STEPS", cmax)
+        monkeypatch.setenv("LDBP_REV_MAX_STEPS", cmax)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("B,n,M,T,sym,cmax", BWD_CASES)
+def test_backward_parity(P, monkeypatch, B, n, M, T, sym, cmax, mode):
+    set_mode(monkeypatch, mode, cmax)
     x = li.gaussian_blocks(21, range(B), n, 1e-3)
     gy = li.gaussian_blocks(21, range(B), n, 1.0, purpose="grad")
     taps, gamma = model(21, M, T, sym)
@@ -162,10 +173,10 @@ def test_backward_parity(P, monkeypatch, B, n, M, T, sym, cmax):
         assert rel(gx[b], rgx[b]) <= OUT_TOL * 10, (b, rel(gx[b], rgx[b]))
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("sym,masked,cmax", [(True, False, None), (True, True, "2"), (False, True, None)])
-def test_loss_grad_parity(P, monkeypatch, sym, masked, cmax):
-    if cmax:
-        monkeypatch.setenv("LDBP_BWD_MAX_STEPS", cmax)
+def test_loss_grad_parity(P, monkeypatch, sym, masked, cmax, mode):
+    set_mode(monkeypatch, mode, cmax)
     B, n, M, T = 4, 1536, 6, 9
     x = li.gaussian_blocks(31, range(B), n, 1e-3)
     tgt = li.gaussian_blocks(31, range(B), n, 1e-3, purpose="target")
@@ -187,8 +198,10 @@ def test_loss_grad_parity(P, monkeypatch, sym, masked, cmax):
         assert np.all(dt[mask == 0] == 0)
 
 
-def test_gradient_gauge_identities_gpu(P):
+@pytest.mark.parametrize("mode", MODES)
+def test_gradient_gauge_identities_gpu(P, monkeypatch, mode):
     """P6/P7 on the GPU gradients (Remark 4): exact in exact arithmetic, <= 1e-4 relative here."""
+    monkeypatch.setenv("LDBP_BWD_MODE", mode)
     B, n, M, T = 8, 4096, 10, 5
     x = li.gaussian_blocks(41, range(B), n, 2e-3)
     tgt = li.gaussian_blocks(41, range(B), n, 2e-3, purpose="target")
@@ -245,9 +258,11 @@ def test_train_step_is_loss_grad_plus_adam(P):
     assert torch.equal(s1.master, s2.master) and torch.equal(s1.taps, s2.taps)
 
 
-def test_determinism_and_shard_sum(P):
+@pytest.mark.parametrize("mode", MODES)
+def test_determinism_and_shard_sum(P, monkeypatch, mode):
     """Fixed-order reductions: bitwise repeatable; the data-parallel sum of per-shard buffers
     equals the full-batch buffer (gradient is linear in the blocks; §8(e))."""
+    monkeypatch.setenv("LDBP_BWD_MODE", mode)
     B, n, M, T = 8, 3000, 6, 5
     x = li.gaussian_blocks(71, range(B), n, 1e-3)
     tgt = li.gaussian_blocks(71, range(B), n, 1e-3, purpose="target")
@@ -307,9 +322,11 @@ def test_snr_parity_on_simulated_link(P):
     assert snr[(6.0, 15, True)] > snr[(6.0, 15, False)] + 3.0
 
 
-def test_backward_unnormalised_path(P):
+@pytest.mark.parametrize("mode", MODES)
+def test_backward_unnormalised_path(P, monkeypatch, mode):
     """Taps whose centre tap is ~0 make the h0-normalised kernels fall back to the plain folded
     FIR (launch-wide, decided on the device); gradients must still match the oracle."""
+    monkeypatch.setenv("LDBP_BWD_MODE", mode)
     B, n, M, T = 2, 900, 4, 5
     x = li.gaussian_blocks(81, range(B), n, 1e-3)
     gy = li.gaussian_blocks(81, range(B), n, 1.0, purpose="grad")
@@ -327,7 +344,9 @@ def test_backward_unnormalised_path(P):
     assert rel(gx.cpu().numpy(), rgx) <= 1e-4
 
 
-def test_precise_backward(P):
+@pytest.mark.parametrize("mode", MODES)
+def test_precise_backward(P, monkeypatch, mode):
+    monkeypatch.setenv("LDBP_BWD_MODE", mode)
     B, n, M, T = 2, 1200, 5, 7
     x = li.gaussian_blocks(82, range(B), n, 1e-3)
     tgt = li.gaussian_blocks(82, range(B), n, 1e-3, purpose="target")
