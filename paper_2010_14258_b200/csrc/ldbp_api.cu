@@ -171,21 +171,23 @@ struct Tile {
 };
 
 size_t fwd_smem(int kh, bool sym, int steps, int nthreads = 1024, int nnorm = 0) {
-  const int edge_rows = LDBP_FWD_XSMEM ? nthreads : ldbp::kMaxWarps;
+  (void)nthreads;
+  const int edge_rows = LDBP_FWD_XSMEM ? ldbp::fwd_max_threads(kh) : ldbp::kMaxWarps;
   return sizeof(uint64_t) * 2 * ldbp::kMaxWarps + sizeof(float2) * 4 * edge_rows * std::max(kh, 1) +
          sizeof(ldbp::TapP) * steps * ntaps_used(kh, sym) + sizeof(ldbp::StepNorm) * std::max(steps, nnorm) +
          sizeof(float) * steps + 32;
 }
 
 // Store-all reverse kernel shared memory (mirrors the carve-up in rev_tile_kernel).
-size_t rev_smem(int kh, bool sym, int steps, int M, int nthreads) {
-  const int nw = nthreads / 32;
+size_t rev_smem(int kh, bool sym, int steps, int M) {
+  const int NT = ldbp::kRevThreads, nw = NT / 32;
   const int V = 1 + 2 * ntaps_used(kh, sym);
-  size_t s = sizeof(float2) * 2 * (size_t)kRevR * nthreads;         // u window copies
-  s += sizeof(float2) * 4 * (size_t)std::max(kh, 1) * nthreads;       // ga edges
+  size_t s = sizeof(float2) * 2 * (size_t)kRevR * NT;                 // u window copies
+  s += sizeof(float2) * 4 * (size_t)std::max(kh, 1) * NT;             // ga edges
   s += sizeof(ldbp::TapP) * (size_t)steps * ntaps_used(kh, sym);      // adjoint taps
   s += sizeof(ldbp::StepNorm) * (size_t)M;                            // global normalisation
-  s += sizeof(float) * (size_t)((2 * nw * V + 3) & ~3);               // per-warp partials
+  s += sizeof(float) * (size_t)((steps * nw * V + 3) & ~3);           // per-warp partials, all steps
+  s += sizeof(float) * (size_t)((nw + 3) & ~3);                       // loss partials
   s += sizeof(float) * (size_t)((steps + 3) & ~3) + 16;               // gamma_hat + flag
   return s;
 }
@@ -205,8 +207,12 @@ size_t bwd_smem(int kh, bool sym, int steps, int nthreads) {
 
 // Choose the owned width and grid for a tiling with halo H, R samples per thread and at most
 // max_threads threads.  `occ_per_sm` = resident CTAs/SM at max_threads (from the occupancy API).
-Tile plan_tiles(int64_t B, int64_t n, int H, int R, int max_threads, int occ_per_sm, int sms) {
+// align_r: round H up and W to multiples of R, so that (for n % R == 0) every thread's R samples
+// are either all owned real samples or none (no per-sample ownership masks on the hot path).
+Tile plan_tiles(int64_t B, int64_t n, int H, int R, int max_threads, int occ_per_sm, int sms,
+                bool align_r = false) {
   Tile t;
+  if (align_r) H = (int)(cdiv(H, R) * R);
   const int64_t ext = n + 2 * (int64_t)H;
   const int64_t E = B * ext;
   const int64_t cap = (int64_t)max_threads * R;
@@ -222,7 +228,8 @@ Tile plan_tiles(int64_t B, int64_t n, int H, int R, int max_threads, int occ_per
     const int64_t wmin = std::max<int64_t>(4 * (int64_t)H, 32 * (int64_t)R);
     grid = std::max<int64_t>(tiles, std::min<int64_t>(slots, cdiv(E, wmin)));
   }
-  const int64_t W = cdiv(E, grid);
+  int64_t W = cdiv(E, grid);
+  if (align_r) W = cdiv(W, R) * R;
   grid = cdiv(E, W);
   int nthr = (int)cdiv(cdiv(W + 2 * (int64_t)H, R), 32) * 32;
   nthr = std::min(std::max(nthr, 32), max_threads);
@@ -232,7 +239,7 @@ Tile plan_tiles(int64_t B, int64_t n, int H, int R, int max_threads, int occ_per
   int64_t Wh = W;
   if (env_int("LDBP_STAGGER", 0) && occ_per_sm >= 2 && grid > slots && W >= 2 * R) {
     NS = sms;
-    Wh = W / 2;
+    Wh = align_r ? (W / 2 / R) * R : W / 2;
     grid = NS + cdiv(std::max<int64_t>(E - (int64_t)NS * Wh, 0), W);
   }
   t.nthreads = nthr;
@@ -352,34 +359,37 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const int M = d->steps;
-  const int nthr = std::min(env_int("LDBP_REV_THREADS", LDBP_REV_MAXT), LDBP_REV_MAXT);
+  const int nthr = ldbp::kRevThreads;
   p.V = 1 + 2 * ntaps_used(kh, sym);
   // cost model in step units: a launch of S steps costs S * window / (window - 2*S*kh) plus a
-  // fixed ~2 steps (prologue: staging, first load, seed); pick the number of launches minimising it
+  // fixed ~2 steps (prologue: staging, first load, seed); pick the number of launches minimising
+  // it, subject to the shared-memory budget (2 CTAs per SM)
   const double window = (double)nthr * kRevR;
   const double fixed = 2.0;
-  int best_k = 1;
+  const size_t budget = (size_t)env_int("LDBP_REV_SMEM_KB", 113) * 1024;
+  int best_k = 0;
   double best = 1e300;
-  const int kmax = std::min(M, env_int("LDBP_REV_MAX_LAUNCHES", 64));
+  const int kmax = std::min(M, env_int("LDBP_REV_MAX_LAUNCHES", 256));
+  const int cmax = std::max(1, env_int("LDBP_REV_MAX_STEPS", 1 << 30));
   for (int k = 1; k <= kmax; ++k) {
     const int S = (int)cdiv(M, k);
+    if (S > cmax || rev_smem(kh, sym, S, M) > budget) continue;
     const double useful = window - 2.0 * S * kh;
     if (useful < window / 4) continue;
     const double cost = k * (S * window / useful + fixed);
     if (cost < best) { best = cost; best_k = k; }
   }
-  if (best >= 1e300) best_k = std::max(1, (int)cdiv((int64_t)M * kh * 8, (int64_t)window));
-  const int cmax = env_int("LDBP_REV_MAX_STEPS", 1 << 30);
-  best_k = std::max(best_k, (int)cdiv(M, std::max(cmax, 1)));
+  if (best_k == 0) best_k = std::max((int)cdiv(M, cmax), (int)cdiv((int64_t)M * kh * 8, (int64_t)window));
   p.Kr = best_k;
   p.Cr = (int)cdiv(M, p.Kr);
   p.Kr = (int)cdiv(M, p.Cr);
   int occ = 1, sms = 148;
   if (query_device) {
     sms = device_sms();
-    occ = rev_occupancy(get_rev(kh, sym, !(d->flags & LDBP_PRECISE)), nthr, rev_smem(kh, sym, p.Cr, M, nthr));
+    occ = rev_occupancy(get_rev(kh, sym, !(d->flags & LDBP_PRECISE)), nthr, rev_smem(kh, sym, p.Cr, M));
   }
-  p.tile = plan_tiles(d->batch, d->n, p.Cr * kh, kRevR, nthr, occ, sms);
+  p.tile = plan_tiles(d->batch, d->n, p.Cr * kh, kRevR, nthr, occ, sms, /*align_r=*/true);
+  p.tile.nthreads = nthr;  // the kernel's layout is compiled for exactly kRevThreads threads
   return p;
 }
 
@@ -716,7 +726,7 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
     a.s0 = s0;
     a.s1 = s1;
     a.g = p.tile.g;
-    const size_t smem = rev_smem(kh, sym, s1 - s0, M, p.tile.nthreads);
+    const size_t smem = rev_smem(kh, sym, s1 - s0, M);
     cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     {
       TraceScope ts(LDBP_K_REVERSE, s1 - s0, d->batch * d->n, st);

@@ -496,9 +496,30 @@ __device__ __forceinline__ f2x tmul(const TapP& t, f2x s) { return fma2(bcast(lo
 // One FIR output k (compile-time), a_k = sum_j h_j w_{k-j} (packed FP32x2 complex MACs).
 // SYM: taps hs[0..KH] = h_0..h_KH (folded, fig:filter P:494-509: pre-add u_{k-j}+u_{k+j}).
 // GEN: taps hs[0..2KH] = h_{-KH}..h_{KH}.
+#ifndef LDBP_FIR_CHAINS
+#define LDBP_FIR_CHAINS 1  // 1: one accumulation chain per output (R outputs give the ILP); 2: split
+#endif
 template <int KH, int R, bool SYM, int K, bool NORM = false>
 __device__ __forceinline__ f2x fir_at(const f2x (&u)[R], const f2x (&hl)[KH > 0 ? KH : 1],
                                       const f2x (&hr)[KH > 0 ? KH : 1], const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1]) {
+  if constexpr (LDBP_FIR_CHAINS == 1) {
+    f2x acc;
+    if constexpr (SYM && NORM) {
+      // h0-normalised folded FIR: h_0 = 1, a_k = u_k + sum_j h_j (u_{k-j} + u_{k+j})
+      acc = u[K];
+#pragma unroll
+      for (int j = 1; j <= KH; ++j) acc = tmac(acc, hs[j], add2(LDBP_WIN(u, hl, hr, K - j), LDBP_WIN(u, hl, hr, K + j)));
+    } else if constexpr (SYM) {
+      acc = tmul(hs[0], u[K]);
+#pragma unroll
+      for (int j = 1; j <= KH; ++j) acc = tmac(acc, hs[j], add2(LDBP_WIN(u, hl, hr, K - j), LDBP_WIN(u, hl, hr, K + j)));
+    } else {
+      acc = tmul(hs[0], LDBP_WIN(u, hl, hr, K + KH));
+#pragma unroll
+      for (int jj = 1; jj < 2 * KH + 1; ++jj) acc = tmac(acc, hs[jj], LDBP_WIN(u, hl, hr, K - (jj - KH)));
+    }
+    return acc;
+  }
   f2x acc_a, acc_b;
   if constexpr (SYM && NORM) {
     // h0-normalised folded FIR: h_0 = 1, a_k = u_k + sum_j h_j (u_{k-j} + u_{k+j})
@@ -536,13 +557,19 @@ __device__ __forceinline__ void fir_all(const f2x (&u)[R], const f2x (&hl)[KH > 
   }
 }
 
-// Kerr: v = a e^{j g |a|^2} = ax*(c, s) + ay*(-s, c).
+// Kerr: v = a e^{j g |a|^2} = (ax c - ay s, ax s + ay c).  Scalar FFMAs: the packed form needs
+// (-s, c) next to (c, s), i.e. a negate + move per sample (FP32x2 has no free half-negate), so
+// the scalar form is cheaper on the FMA pipe (4 lane-ops, no moves).
+#ifndef LDBP_KERR_SCALAR
+#define LDBP_KERR_SCALAR 1
+#endif
 template <bool FAST>
 __device__ __forceinline__ f2x kerr(f2x a, float g) {
   const float ax = lof(a), ay = hif(a);
   const float p = fmaf(ax, ax, ay * ay);
   float s, c;
   sincos_phase<FAST>(g * p, &s, &c);
+  if constexpr (LDBP_KERR_SCALAR) return pk(fmaf(ax, c, -ay * s), fmaf(ax, s, ay * c));
   return fma2(bcast(ax), pk(c, s), mul2(bcast(ay), pk(-s, c)));
 }
 
@@ -844,6 +871,124 @@ __device__ __forceinline__ void fwd_steps(const FwdArgs& a, f2x (&u)[R], const T
     store_mapped<R>(a.dst, smap, e0, a.g, u);
 }
 
+// FIR + Kerr for outputs k in [K, KE), with the Kerr of output k-D issued after the FIR of output
+// k (MUFU work interleaved with FMA-pipe work); the last D Kerrs are flushed at the end.
+template <int KH, int R, bool SYM, bool FAST, bool NORM, int KB, int KE, int K = KB>
+__device__ __forceinline__ void step_range(const f2x (&u)[R], const f2x (&hl)[KH > 0 ? KH : 1],
+                                           const f2x (&hr)[KH > 0 ? KH : 1],
+                                           const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1], float gm, f2x (&acc)[R],
+                                           f2x (&out)[R]) {
+  constexpr int D = LDBP_PIPE_D;
+  if constexpr (K < KE + D) {
+    if constexpr (K < KE) acc[K] = fir_at<KH, R, SYM, K, NORM>(u, hl, hr, hs);
+    if constexpr (K - D >= KB && K - D < KE) out[K - D] = kerr<FAST>(acc[K - D], gm);
+    step_range<KH, R, SYM, FAST, NORM, KB, KE, K + 1>(u, hl, hr, hs, gm, acc, out);
+  }
+}
+
+#ifndef LDBP_FWD_UNROLL
+#define LDBP_FWD_UNROLL 1
+#endif
+constexpr int kFwdUnroll = LDBP_FWD_UNROLL;
+// mbarrier helpers for the split (arrive early / wait late) step barrier.
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) { mbar_arrive(bar); }
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+// Forward steps with a split barrier (LDBP_FWD_SPLIT): at the end of step s every warp publishes
+// its threads' Kh-sample edges into edge buffer (s+1)&1 and arrives (one elected lane, count =
+// warps) on one CTA mbarrier; step s+1 first computes the R-2Kh interior outputs, which need no
+// halo, and only then waits for phase s+1 and reads the neighbours' edges for the 2Kh boundary
+// outputs.  The barrier latency and the warp skew hide behind the interior work.  Buffer reuse:
+// buffer b is rewritten for phase p+2 by a warp that has passed phase p+1, whose arrivals all
+// come after their reads of phase p.
+template <int KH, int R, bool SYM, bool FAST, bool NORM>
+__device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], const TapP* sh_taps,
+                                                const float* sh_gamma, const StepNorm* sh_norm, f2x* sh_edge,
+                                                uint64_t* bar, const StoreMap& smap, int64_t e0, int lane) {
+  constexpr int NTU = ntaps_used<SYM, KH>();
+  constexpr int KI = KH < R - KH ? KH : R / 2;  // interior [KI, R-KI)
+  constexpr int ST = fwd_max_threads(KH);       // edge-array row stride (compile time -> immediates)
+  const bool global = a.global_norm != 0;
+  sh_norm += a.s0 - a.n0;
+  const int nthr = blockDim.x;
+  const int tid = threadIdx.x;
+  const int left = tid > 0 ? tid - 1 : 0;
+  const int right = tid + 1 < nthr ? tid + 1 : tid;
+  f2x* const my_edge = sh_edge + tid;
+  const f2x* const left_edge = sh_edge + left;
+  const f2x* const right_edge = sh_edge + right;
+  auto publish = [&](int buf) {
+    if constexpr (KH > 0) {
+      f2x* e = my_edge + buf * 2 * KH * ST;
+#pragma unroll
+      for (int j = 0; j < KH; ++j) {
+        e[j * ST] = u[j];                  // head
+        e[(KH + j) * ST] = u[R - KH + j];  // tail
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(bar);
+    }
+  };
+  publish(0);
+  f2x hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1];
+  // checkpoint schedule without a per-step modulo: next global step count to store
+  int next_ck = a.ckpt ? (a.s0 / a.ckpt_every + 1) * a.ckpt_every : 0x7fffffff;
+  float2* ck_ptr = a.ckpt ? a.ckpt + (int64_t)(next_ck / a.ckpt_every - 1) * a.ckpt_stride : nullptr;
+#pragma unroll kFwdUnroll
+  for (int s = 0; s < a.s1 - a.s0; ++s) {
+    TapP hs[NTU];
+#pragma unroll
+    for (int j = 0; j < NTU; ++j) hs[j] = sh_taps[s * NTU + j];
+    const float gm = sh_gamma[s];
+    f2x acc[R], nu[R];
+    step_range<KH, R, SYM, FAST, NORM, KI, R - KI>(u, hl, hr, hs, gm, acc, nu);
+    if constexpr (KH > 0) {
+      mbar_wait_parity(bar, s & 1);
+      const int off = (s & 1) * 2 * KH * ST;
+#pragma unroll
+      for (int j = 0; j < KH; ++j) {
+        hl[j] = left_edge[off + (KH + j) * ST];
+        hr[j] = right_edge[off + j * ST];
+      }
+    }
+    step_range<KH, R, SYM, FAST, NORM, 0, KI>(u, hl, hr, hs, gm, acc, nu);
+    step_range<KH, R, SYM, FAST, NORM, R - KI, R>(u, hl, hr, hs, gm, acc, nu);
+#pragma unroll
+    for (int k = 0; k < R; ++k) u[k] = nu[k];
+    const int gs = a.s0 + s + 1;  // global step count reached
+    if (gs < a.s1) publish((s + 1) & 1);
+    if (gs == next_ck && gs < a.s1) {
+      if (global) {
+        store_mapped<R>(ck_ptr, smap, e0, a.g, u);
+      } else if constexpr (NORM) {
+        store_mapped_scaled<R>(ck_ptr, smap, e0, a.g, u, sh_norm[s].P);
+      } else {
+        store_mapped<R>(ck_ptr, smap, e0, a.g, u);
+      }
+      next_ck += a.ckpt_every;
+      ck_ptr += a.ckpt_stride;
+    }
+  }
+  if (NORM && (!global || a.scale_dst))
+    store_mapped_scaled<R>(a.dst, smap, e0, a.g, u, sh_norm[a.s1 - a.s0 - 1].P);
+  else
+    store_mapped<R>(a.dst, smap, e0, a.g, u);
+}
+
+#ifndef LDBP_FWD_SPLIT
+#define LDBP_FWD_SPLIT 1
+#endif
+
 template <int KH, int R, bool SYM, bool FAST>
 __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_tile_kernel(const FwdArgs a) {
   constexpr int NTU = ntaps_used<SYM, KH>();
@@ -851,14 +996,17 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
   const int S = a.s1 - a.s0;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                            // [2][32] mbarriers
   f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);  // 2*2*KH*(XSMEM ? nthreads : 32)
-  TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge + 4 * (LDBP_FWD_XSMEM ? (int)blockDim.x : kMaxWarps) *
+  TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge + 4 * (LDBP_FWD_XSMEM ? fwd_max_threads(KH) : kMaxWarps) *
                                                         (KH > 0 ? KH : 1));  // S*NTU
   StepNorm* sh_norm = reinterpret_cast<StepNorm*>(sh_taps + S * NTU);                // max(S, nM-n0)
   float* sh_gamma = reinterpret_cast<float*>(sh_norm + max(S, a.nM - a.n0));         // S
   int* sh_flag = reinterpret_cast<int*>(sh_gamma + S);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  if (LDBP_NB_SYNC) nb_init(bars);
+  if (LDBP_NB_SYNC && !LDBP_FWD_SPLIT) nb_init(bars);
+  if (LDBP_FWD_SPLIT && threadIdx.x == 0) {  // split step barrier: bars[0], count = warps
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars)), "r"(nwarps) : "memory");
+  }
   f2x u[R];
   const int64_t e0 = thread_e0(a.g, R);
   load_window<R>(a.src, e0, a.g, u);
@@ -873,7 +1021,12 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
   }
   __syncthreads();
   if (SYM && *sh_flag)
-    fwd_steps<KH, R, SYM, FAST, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane, warp, nwarps);
+    if (LDBP_FWD_SPLIT)
+      fwd_steps_split<KH, R, SYM, FAST, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
+    else
+      fwd_steps<KH, R, SYM, FAST, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane, warp, nwarps);
+  else if (LDBP_FWD_SPLIT)
+    fwd_steps_split<KH, R, SYM, FAST, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
   else
     fwd_steps<KH, R, SYM, FAST, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane, warp, nwarps);
 }

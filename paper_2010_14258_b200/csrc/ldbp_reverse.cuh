@@ -54,23 +54,30 @@ __device__ __forceinline__ const float2* rev_src(const RevArgs& a, int i) {
   return i == 0 ? a.x : a.act + (int64_t)(i - 1) * a.act_stride;
 }
 
-// Shared-memory window copy: sample k of thread t at f2x index ((k >> 1) * nthr + t) * 2 + (k & 1)
+#ifndef LDBP_REV_NTHR
+#define LDBP_REV_NTHR 256  // threads per reverse CTA (compile time: every smem offset is an immediate)
+#endif
+constexpr int kRevThreads = LDBP_REV_NTHR;
+
+// Shared-memory window copy: sample k of thread t at f2x index ((k >> 1) * NT + t) * 2 + (k & 1)
 // (16-byte pairs, lane-consecutive -> conflict-free LDS.128 / LDGSTS.128).
-__device__ __forceinline__ int ubuf_idx(int k, int t, int nthr) { return ((k >> 1) * nthr + t) * 2 + (k & 1); }
+template <int NT>
+__device__ __forceinline__ constexpr int ubuf_idx(int k, int t) { return ((k >> 1) * NT + t) * 2 + (k & 1); }
 
 // Issue the asynchronous copy of this thread's R window samples of `src` (zeros outside [0, E)).
-template <int R>
+template <int R, int NT>
 __device__ __forceinline__ void async_window(const float2* __restrict__ src, int64_t e0, const Geo& g, f2x* buf,
-                                             int nthr, int64_t fast_off) {
+                                             int64_t fast_off) {
   const int t = threadIdx.x;
+  f2x* mine = buf + ubuf_idx<NT>(0, t);
   if (fast_off >= 0) {
     const f2x* p = reinterpret_cast<const f2x*>(src) + fast_off;
     if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
 #pragma unroll
-      for (int m = 0; m < R / 2; ++m) cp_async16(buf + ubuf_idx(2 * m, t, nthr), p + 2 * m);
+      for (int m = 0; m < R / 2; ++m) cp_async16(mine + m * 2 * NT, p + 2 * m);
     } else {
 #pragma unroll
-      for (int k = 0; k < R; ++k) cp_async8(buf + ubuf_idx(k, t, nthr), p + k);
+      for (int k = 0; k < R; ++k) cp_async8(mine + (k >> 1) * 2 * NT + (k & 1), p + k);
     }
   } else {
     const Span sp = make_span(e0, g);
@@ -79,7 +86,7 @@ __device__ __forceinline__ void async_window(const float2* __restrict__ src, int
       int64_t b, pos;
       int q;
       const bool ok = span_at<R>(sp, k, g, e0, &b, &pos, &q);
-      cp_async8_zfill(buf + ubuf_idx(k, t, nthr), ok ? (const void*)(src + b * g.n + pos) : (const void*)src,
+      cp_async8_zfill(mine + (k >> 1) * 2 * NT + (k & 1), ok ? (const void*)(src + b * g.n + pos) : (const void*)src,
                       ok ? 8 : 0);
     }
   }
@@ -91,61 +98,118 @@ struct RevSmem {
   StepNorm* norm;   // [M] (global normalisation, step-indexed)
   float* gamma;     // [S] gamma_hat
   int* flag;
-  float* red;       // [2][nwarps][V] per-warp partials of one step (double-buffered)
-  f2x* edge;        // [2 buf][2 side][KH][nthr] ga halos
-  f2x* ubuf;        // [2 buf][R][nthr] window copies of u^(l)
+  float* red;       // [S][NW][V] per-warp partials of every step (reduced once at the end)
+  float* lred;      // [NW] loss partials
+  f2x* edge;        // [2 buf][2 side][KH][NT] ga halos
+  f2x* ubuf;        // [2 buf][R/2][NT] 16-byte pairs: window copies of u^(l)
 };
 
-// CTA-level fp64 reduction of step l's per-warp partials (buffer b), mapped back to the original
-// parameters (dgamma_i = |P_i|^2 dgamma_hat_i, dh^(i) = conj(1/c_i) dh_hat^(i)), written to
-// partials[cta][l][.].  Complex pair q (0: dgamma, q >= 1: tap q-1) is handled by lane 0 of warp
-// q % nwarps, so the work is spread over the warps.
-template <int NTU>
-__device__ __forceinline__ void rev_flush(const RevArgs& a, const RevSmem& sm, int b, int l, bool norm, int lane,
-                                          int warp, int nwarps) {
-  constexpr int V = 1 + 2 * NTU;
-  if (lane != 0) return;
-  for (int q = warp; q <= NTU; q += nwarps) {
-    const float* red = sm.red + (size_t)b * nwarps * V;
-    double* out = a.partials + ((int64_t)blockIdx.x * a.M + l) * V;
-    const StepNorm nm = sm.norm[l];
-    if (q == 0) {
-      double acc = 0.0;
-      for (int w = 0; w < nwarps; ++w) acc += (double)red[w * V];
-      if (norm) acc *= (double)nm.P.x * nm.P.x + (double)nm.P.y * nm.P.y;
-      out[0] = acc;
+// NL adjoint of one sample (g -> ga in place), Appendix A: with v = u^(l+1), g = dL/dv,
+//   c = Im(g conj v), t = g + 2 gamma' c v, ga = t e^{-j phi} = (tx c + ty s, ty c - tx s),
+//   dgamma' += c |v|^2 (owned samples only).  Scalar rotation: no pair shuffling.
+template <bool FAST, bool MASKED>
+__device__ __forceinline__ void nl_adjoint(f2x& gk, f2x vk, float gm, float gm2, bool owned, float& dgam) {
+  const float vx = lof(vk), vy = hif(vk);
+  const float p = fmaf(vx, vx, vy * vy);
+  float sn, cs;
+  sincos_phase<FAST>(gm * p, &sn, &cs);
+  const float cim = fmaf(hif(gk), vx, -lof(gk) * vy);  // Im(g conj v)
+  const f2x t = fma2(bcast(gm2 * cim), vk, gk);
+  const float tx = lof(t), ty = hif(t);
+  gk = pk(fmaf(tx, cs, ty * sn), fmaf(ty, cs, -tx * sn));
+  if (!MASKED || owned) dgam = fmaf(cim, p, dgam);
+}
+
+// One reverse step's arithmetic after the halo exchange: tap gradients of step l (owned samples;
+// MASKED selects per sample, the common full-ownership path has no selects), then the FIR adjoint
+// g_s = sum_j conj(h_j) ga_{s+j} fused with the NL adjoint of step l-1 on each fresh g_s (NL).
+// Tap gradient form: ga conj(w) = lo(w) ga - j hi(w) ga, accumulated as A_j += lo(w) ga,
+// B_j += hi(w) ga (broadcast operands only, no per-sample pair construction); dh_j = A_j - j B_j.
+template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL>
+__device__ __forceinline__ void rev_compute(const f2x (&u)[R], const f2x (&hl)[KH > 0 ? KH : 1],
+                                            const f2x (&hr)[KH > 0 ? KH : 1], f2x (&g)[R],
+                                            const f2x (&gl)[KH > 0 ? KH : 1], const f2x (&gr)[KH > 0 ? KH : 1],
+                                            const TapP* __restrict__ hs_sm, uint32_t own, float gmn,
+                                            float (&dh)[2 * (SYM ? KH + 1 : 2 * KH + 1)], float& dgam_next) {
+  constexpr int NTU = ntaps_used<SYM, KH>();
+  f2x A[NTU], Bq[NTU];
+#pragma unroll
+  for (int j = 0; j < NTU; ++j) A[j] = Bq[j] = 0ull;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const f2x gk = (!MASKED || ((own >> k) & 1u)) ? g[k] : 0ull;
+    if constexpr (SYM) {
+      A[0] = fma2(bcast(lof(u[k])), gk, A[0]);
+      Bq[0] = fma2(bcast(hif(u[k])), gk, Bq[0]);
+#pragma unroll
+      for (int j = 1; j <= KH; ++j) {
+        const f2x w = add2(LDBP_WIN(u, hl, hr, k - j), LDBP_WIN(u, hl, hr, k + j));
+        A[j] = fma2(bcast(lof(w)), gk, A[j]);
+        Bq[j] = fma2(bcast(hif(w)), gk, Bq[j]);
+      }
     } else {
-      const int v = 1 + 2 * (q - 1);
-      double re = 0.0, im = 0.0;
-      for (int w = 0; w < nwarps; ++w) {
-        re += (double)red[w * V + v];
-        im += (double)red[w * V + v + 1];
+#pragma unroll
+      for (int jj = 0; jj < 2 * KH + 1; ++jj) {
+        const f2x w = LDBP_WIN(u, hl, hr, k - (jj - KH));
+        A[jj] = fma2(bcast(lof(w)), gk, A[jj]);
+        Bq[jj] = fma2(bcast(hif(w)), gk, Bq[jj]);
       }
-      if (norm) {
-        const double cx = nm.c.x, cy = nm.c.y, m = cx * cx + cy * cy;
-        const double r2 = (re * cx - im * cy) / m, i2 = (re * cy + im * cx) / m;
-        re = r2;
-        im = i2;
-      }
-      out[v] = re;
-      out[v + 1] = im;
     }
   }
+#pragma unroll
+  for (int j = 0; j < NTU; ++j) {
+    dh[2 * j] = lof(A[j]) + hif(Bq[j]);
+    dh[2 * j + 1] = hif(A[j]) - lof(Bq[j]);
+  }
+  TapP hs[NTU];
+#pragma unroll
+  for (int j = 0; j < NTU; ++j) hs[j] = hs_sm[j];
+  const float gmn2 = 2.f * gmn;
+  f2x ng[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    f2x acc;
+    if constexpr (SYM && NORM) {
+      acc = g[k];
+#pragma unroll
+      for (int j = 1; j <= KH; ++j) acc = tmac(acc, hs[j], add2(LDBP_WIN(g, gl, gr, k - j), LDBP_WIN(g, gl, gr, k + j)));
+    } else if constexpr (SYM) {
+      acc = tmul(hs[0], g[k]);
+#pragma unroll
+      for (int j = 1; j <= KH; ++j) acc = tmac(acc, hs[j], add2(LDBP_WIN(g, gl, gr, k - j), LDBP_WIN(g, gl, gr, k + j)));
+    } else {
+      acc = tmul(hs[0], LDBP_WIN(g, gl, gr, k - KH));
+#pragma unroll
+      for (int jj = 1; jj < 2 * KH + 1; ++jj) acc = tmac(acc, hs[jj], LDBP_WIN(g, gl, gr, k + (jj - KH)));
+    }
+    if constexpr (NL) nl_adjoint<FAST, MASKED>(acc, u[k], gmn, gmn2, (own >> k) & 1u, dgam_next);
+    ng[k] = acc;
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) g[k] = ng[k];
 }
 
 template <int KH, int R, bool SYM, bool FAST, bool NORM>
 __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, int64_t e0, int64_t fast_off,
-                                         uint32_t own, int lane, int warp, int nwarps) {
+                                         uint32_t own, int lane, int warp) {
+  constexpr int NT = kRevThreads, NW = NT / 32;
   constexpr int NTU = ntaps_used<SYM, KH>();
   constexpr int V = 1 + 2 * NTU;
+  constexpr int KE = KH > 0 ? KH : 1;
+  constexpr uint32_t FULL = R >= 32 ? 0xffffffffu : ((1u << R) - 1u);
   static_assert(R % 2 == 0 && R >= KH, "window pairs and neighbour halos need even R >= Kh");
-  const int nthr = blockDim.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   const int left = tid > 0 ? tid - 1 : 0;
-  const int right = tid + 1 < nthr ? tid + 1 : tid;
+  const int right = tid + 1 < NT ? tid + 1 : tid;
   const int s0 = a.s0, s1 = a.s1;
+  // With the R-aligned tiling (plan_rev) a thread's samples are all owned (own == FULL) or none
+  // (own == 0, halo threads): both run the same unmasked code (no divergence inside a warp) and
+  // the latter zero their partials.  Only ragged blocks (n % R != 0) have partial threads.
+  const bool full = own == FULL || own == 0;
+  const bool none = own == 0;
 
   // prefetch u^(s1-1) while v = u^(s1) and the seed are loaded synchronously
-  async_window<R>(rev_src(a, s1 - 1), e0, a.g, sm.ubuf + (size_t)((s1 - 1) & 1) * R * nthr, nthr, fast_off);
+  async_window<R, NT>(rev_src(a, s1 - 1), e0, a.g, sm.ubuf + (size_t)((s1 - 1) & 1) * R * NT, fast_off);
   f2x v[R], g[R];
   load_window<R>(rev_src(a, s1), e0, a.g, v);
   const float2 Pend = sm.norm[a.M - 1].P;
@@ -165,16 +229,13 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
       if (own & (1u << k)) lsum = fmaf(ex, ex, fmaf(ey, ey, lsum));
     }
     lsum = warp_sum(lsum);
-    if (lane == 0) sm.red[warp] = lsum;
+    if (lane == 0) sm.lred[warp] = lsum;
     __syncthreads();
     if (threadIdx.x == 0) {
       double tot = 0.0;
-      for (int w = 0; w < nwarps; ++w) tot += (double)sm.red[w];
+      for (int w = 0; w < NW; ++w) tot += (double)sm.lred[w];
       a.loss_partials[blockIdx.x] = tot;
     }
-    // sm.red is next written after the first step's barrier-protected flush ordering below:
-    // the first per-warp write happens after this barrier pair.
-    __syncthreads();
   } else {
     load_window<R>(a.gin, e0, a.g, g);
     if (NORM && s1 == a.M) {
@@ -182,163 +243,149 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
       for (int k = 0; k < R; ++k) g[k] = tmul(conjP, g[k]);
     }
   }
-
-  // NL adjoint of one sample (g -> ga in place), Appendix A: with v = u^(l+1), g = dL/dv,
-  //   c = Im(g conj v), ga = (g + 2 gamma' c v) e^{-j phi}, dgamma' += c |v|^2 (owned only).
-  auto nl_adjoint = [&](f2x& gk, f2x vk, float gm, float gm2, bool owned, float& dgam) {
-    const float vx = lof(vk), vy = hif(vk);
-    const float p = fmaf(vx, vx, vy * vy);
-    float sn, cs;
-    sincos_phase<FAST>(gm * p, &sn, &cs);
-    const float cim = fmaf(hif(gk), vx, -lof(gk) * vy);  // Im(g conj v)
-    const f2x t = fma2(bcast(gm2 * cim), vk, gk);
-    gk = fma2(bcast(lof(t)), pk(cs, -sn), mul2(bcast(hif(t)), pk(sn, cs)));
-    if (owned) dgam = fmaf(cim, p, dgam);
-  };
-  // step s1-1's NL adjoint up front; every later one is fused into the previous step's FIR-
-  // adjoint loop (software pipelining: MUFU work interleaved with the FMA-pipe work)
+  // NL adjoint of step s1-1 up front; every later one is fused into the previous step's FIR-
+  // adjoint loop (software pipelining: MUFU work interleaved with FMA-pipe work)
   float dgam = 0.f;
   {
     const float gm = sm.gamma[s1 - 1 - s0];
+    if (full) {
 #pragma unroll
-    for (int k = 0; k < R; ++k) nl_adjoint(g[k], v[k], gm, 2.f * gm, (own >> k) & 1u, dgam);
+      for (int k = 0; k < R; ++k) nl_adjoint<FAST, false>(g[k], v[k], gm, 2.f * gm, true, dgam);
+    } else {
+#pragma unroll
+      for (int k = 0; k < R; ++k) nl_adjoint<FAST, true>(g[k], v[k], gm, 2.f * gm, (own >> k) & 1u, dgam);
+    }
+    if (none) dgam = 0.f;
   }
+  f2x* const my_edge = sm.edge + tid;
+  const f2x* const left_edge = sm.edge + left;
+  const f2x* const right_edge = sm.edge + right;
 
   for (int l = s1 - 1; l >= s0; --l) {
     const int li = l - s0;
     // ---- publish ga edges, wait for u^(l), one barrier ----
-    f2x* ebuf = sm.edge + (size_t)(l & 1) * 2 * (KH > 0 ? KH : 1) * nthr;
+    const int eoff = (l & 1) * 2 * KE * NT;
     if constexpr (KH > 0) {
 #pragma unroll
       for (int j = 0; j < KH; ++j) {
-        ebuf[j * nthr + tid] = g[j];                       // head
-        ebuf[(KH + j) * nthr + tid] = g[R - KH + j];       // tail
+        my_edge[eoff + j * NT] = g[j];                   // head
+        my_edge[eoff + (KH + j) * NT] = g[R - KH + j];   // tail
       }
     }
     cp_async_wait_all();
     __syncthreads();
-    // flush the previous step's per-warp partials (written before this barrier)
-    if (l + 1 < s1) rev_flush<NTU>(a, sm, (l + 1) & 1, l + 1, NORM, lane, warp, nwarps);
     // prefetch u^(l-1) into the other buffer (its last reader, step l+1, is behind the barrier)
     if (l > s0)
-      async_window<R>(rev_src(a, l - 1), e0, a.g, sm.ubuf + (size_t)((l - 1) & 1) * R * nthr, nthr, fast_off);
-    const f2x* ub = sm.ubuf + (size_t)(l & 1) * R * nthr;
-    f2x u[R], hl[KH > 0 ? KH : 1], hr[KH > 0 ? KH : 1], gl[KH > 0 ? KH : 1], gr[KH > 0 ? KH : 1];
+      async_window<R, NT>(rev_src(a, l - 1), e0, a.g, sm.ubuf + (size_t)((l - 1) & 1) * R * NT, fast_off);
+    const f2x* ub = sm.ubuf + (size_t)(l & 1) * R * NT;
+    f2x u[R], hl[KE], hr[KE], gl[KE], gr[KE];
 #pragma unroll
     for (int m = 0; m < R / 2; ++m) {
-      const ulonglong2 pr = *reinterpret_cast<const ulonglong2*>(ub + ubuf_idx(2 * m, tid, nthr));
+      const ulonglong2 pr = *reinterpret_cast<const ulonglong2*>(ub + ubuf_idx<NT>(2 * m, tid));
       u[2 * m] = pr.x;
       u[2 * m + 1] = pr.y;
     }
     if constexpr (KH > 0) {
 #pragma unroll
       for (int j = 0; j < KH; ++j) {
-        hl[j] = ub[ubuf_idx(R - KH + j, left, nthr)];
-        hr[j] = ub[ubuf_idx(j, right, nthr)];
-        gl[j] = ebuf[(KH + j) * nthr + left];
-        gr[j] = ebuf[j * nthr + right];
+        hl[j] = ub[ubuf_idx<NT>(R - KH + j, left)];
+        hr[j] = ub[ubuf_idx<NT>(j, right)];
+        gl[j] = left_edge[eoff + (KH + j) * NT];
+        gr[j] = right_edge[eoff + j * NT];
       }
     }
-    // ---- tap gradients over owned samples: dh_j += ga_t conj(w), w = u_{t-j} (+ u_{t+j}) ----
-    f2x dh[NTU], dhb[NTU];
-#pragma unroll
-    for (int j = 0; j < NTU; ++j) dh[j] = dhb[j] = 0ull;
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const f2x gk = (own & (1u << k)) ? g[k] : 0ull;
-      const TapP gt = {gk, pk(hif(gk), -lof(gk))};
-      if constexpr (SYM) {
-        tmac2(dh[0], dhb[0], gt, u[k]);
-#pragma unroll
-        for (int j = 1; j <= KH; ++j)
-          tmac2(dh[j], dhb[j], gt, add2(LDBP_WIN(u, hl, hr, k - j), LDBP_WIN(u, hl, hr, k + j)));
-      } else {
-#pragma unroll
-        for (int jj = 0; jj < 2 * KH + 1; ++jj) tmac2(dh[jj], dhb[jj], gt, LDBP_WIN(u, hl, hr, k - (jj - KH)));
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < NTU; ++j) dh[j] = add2(dh[j], dhb[j]);
-    // ---- FIR adjoint g_s = sum_j conj(h_j) ga_{s+j} (NORM: h_0 = 1), fused with the NL adjoint
-    //      of step l-1 on the fresh g_s (v = u^(l)) ----
-    const bool more = l > s0;
-    const float gmn = more ? sm.gamma[li - 1] : 0.f;
-    const float gmn2 = 2.f * gmn;
+    float dh[2 * NTU];
     float dgam_next = 0.f;
-    {
-      TapP hs[NTU];
-#pragma unroll
-      for (int j = 0; j < NTU; ++j) hs[j] = sm.taps_adj[li * NTU + j];
-      f2x ng[R];
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        f2x acc_a, acc_b;
-        if constexpr (SYM && NORM) {
-          acc_a = g[k];
-          acc_b = 0ull;
-#pragma unroll
-          for (int j = 1; j <= KH; ++j)
-            tmac2(acc_a, acc_b, hs[j], add2(LDBP_WIN(g, gl, gr, k - j), LDBP_WIN(g, gl, gr, k + j)));
-        } else if constexpr (SYM) {
-          acc_a = mul2(bcast(lof(g[k])), hs[0].a);
-          acc_b = mul2(bcast(hif(g[k])), hs[0].b);
-#pragma unroll
-          for (int j = 1; j <= KH; ++j)
-            tmac2(acc_a, acc_b, hs[j], add2(LDBP_WIN(g, gl, gr, k - j), LDBP_WIN(g, gl, gr, k + j)));
-        } else {
-          const f2x w0 = LDBP_WIN(g, gl, gr, k - KH);
-          acc_a = mul2(bcast(lof(w0)), hs[0].a);
-          acc_b = mul2(bcast(hif(w0)), hs[0].b);
-#pragma unroll
-          for (int jj = 1; jj < 2 * KH + 1; ++jj) tmac2(acc_a, acc_b, hs[jj], LDBP_WIN(g, gl, gr, k + (jj - KH)));
-        }
-        ng[k] = (SYM && NORM && KH == 0) ? acc_a : add2(acc_a, acc_b);
-        if (more) nl_adjoint(ng[k], u[k], gmn, gmn2, (own >> k) & 1u, dgam_next);
-      }
-#pragma unroll
-      for (int k = 0; k < R; ++k) g[k] = ng[k];
+    const TapP* hs_sm = sm.taps_adj + li * NTU;
+    if (l > s0) {
+      const float gmn = sm.gamma[li - 1];
+      if (full)
+        rev_compute<KH, R, SYM, FAST, NORM, false, true>(u, hl, hr, g, gl, gr, hs_sm, own, gmn, dh, dgam_next);
+      else
+        rev_compute<KH, R, SYM, FAST, NORM, true, true>(u, hl, hr, g, gl, gr, hs_sm, own, gmn, dh, dgam_next);
+    } else {
+      if (full)
+        rev_compute<KH, R, SYM, FAST, NORM, false, false>(u, hl, hr, g, gl, gr, hs_sm, own, 0.f, dh, dgam_next);
+      else
+        rev_compute<KH, R, SYM, FAST, NORM, true, false>(u, hl, hr, g, gl, gr, hs_sm, own, 0.f, dh, dgam_next);
     }
-    // ---- per-warp reduction of this step's partials -> red[l & 1][warp][.] ----
+    if (none) {
+      dgam_next = 0.f;
+#pragma unroll
+      for (int i = 0; i < 2 * NTU; ++i) dh[i] = 0.f;
+    }
+    // ---- per-warp reduction of this step's partials -> red[li][warp][.] ----
     {
       constexpr int VP = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
       float vals[VP];
       vals[0] = dgam;
 #pragma unroll
-      for (int j = 0; j < NTU; ++j) { vals[1 + 2 * j] = lof(dh[j]); vals[2 + 2 * j] = hif(dh[j]); }
+      for (int i = 0; i < 2 * NTU; ++i) vals[1 + i] = dh[i];
 #pragma unroll
       for (int i = V; i < VP; ++i) vals[i] = 0.f;
       const float r = warp_reduce_scatter<VP>(vals, lane);
       constexpr int SH = VP == 2 ? 4 : VP == 4 ? 3 : VP == 8 ? 2 : VP == 16 ? 1 : 0;
       const int idx = lane >> SH;
-      float* red = sm.red + ((size_t)(l & 1) * nwarps + warp) * V;
+      float* red = sm.red + ((size_t)li * NW + warp) * V;
       if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
     }
     dgam = dgam_next;
   }
-  __syncthreads();
-  rev_flush<NTU>(a, sm, s0 & 1, s0, NORM, lane, warp, nwarps);
   if (a.gout) store_owned<R>(a.gout, e0, a.g, g);
+  __syncthreads();
+  // CTA reduction in fp64, fixed order over warps, mapped back to the original parameters:
+  // dgamma_i = |P_i|^2 dgamma_hat_i, dh^(i) = conj(1/c_i) dh_hat^(i)
+  constexpr int npairs = 1 + NTU;
+  const int S = s1 - s0;
+  for (int i = tid; i < S * npairs; i += NT) {
+    const int li = i / npairs, q = i % npairs;
+    const int l = s0 + li;
+    double* out = a.partials + ((int64_t)blockIdx.x * a.M + l) * V;
+    const StepNorm nm = sm.norm[l];
+    const float* red = sm.red + (size_t)li * NW * V;
+    if (q == 0) {
+      double acc = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) acc += (double)red[w * V];
+      if (NORM) acc *= (double)nm.P.x * nm.P.x + (double)nm.P.y * nm.P.y;
+      out[0] = acc;
+    } else {
+      const int v2 = 1 + 2 * (q - 1);
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        re += (double)red[w * V + v2];
+        im += (double)red[w * V + v2 + 1];
+      }
+      if (NORM) {
+        const double cx = nm.c.x, cy = nm.c.y, m = cx * cx + cy * cy;
+        const double r2 = (re * cx - im * cy) / m, i2 = (re * cy + im * cx) / m;
+        re = r2;
+        im = i2;
+      }
+      out[v2] = re;
+      out[v2 + 1] = im;
+    }
+  }
 }
 
-#ifndef LDBP_REV_MAXT
-#define LDBP_REV_MAXT 512  // threads per CTA (max); 128 registers -> 16 warps per SM either way
-#endif
 template <int KH, int R, bool SYM, bool FAST>
-__global__ void __launch_bounds__(LDBP_REV_MAXT, 65536 / (LDBP_REV_MAXT * 128)) rev_tile_kernel(const RevArgs a) {
+__global__ void __launch_bounds__(kRevThreads, 65536 / (kRevThreads * 128)) rev_tile_kernel(const RevArgs a) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   constexpr int V = 1 + 2 * NTU;
+  constexpr int NT = kRevThreads, NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int S = a.s1 - a.s0;
-  const int nthr = blockDim.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = nthr >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // carve-up (16-byte aligned regions; mirrored by rev_smem() on the host)
   RevSmem sm;
-  sm.ubuf = reinterpret_cast<f2x*>(smem_raw);                                  // 2*R*nthr
-  sm.edge = sm.ubuf + (size_t)2 * R * nthr;                                    // 4*KH*nthr
-  sm.taps_adj = reinterpret_cast<TapP*>(sm.edge + (size_t)4 * (KH > 0 ? KH : 1) * nthr);  // S*NTU
-  sm.norm = reinterpret_cast<StepNorm*>(sm.taps_adj + S * NTU);                // M
-  sm.red = reinterpret_cast<float*>(sm.norm + a.M);                            // 2*nwarps*V (>= nwarps)
-  sm.gamma = sm.red + ((2 * nwarps * V + 3) & ~3);                             // S
+  sm.ubuf = reinterpret_cast<f2x*>(smem_raw);                                        // 2*R*NT
+  sm.edge = sm.ubuf + (size_t)2 * R * NT;                                            // 4*KH*NT
+  sm.taps_adj = reinterpret_cast<TapP*>(sm.edge + (size_t)4 * (KH > 0 ? KH : 1) * NT);  // S*NTU
+  sm.norm = reinterpret_cast<StepNorm*>(sm.taps_adj + S * NTU);                      // M
+  sm.red = reinterpret_cast<float*>(sm.norm + a.M);                                  // S*NW*V
+  sm.lred = sm.red + ((S * NW * V + 3) & ~3);                                        // NW
+  sm.gamma = sm.lred + ((NW + 3) & ~3);                                              // S
   sm.flag = reinterpret_cast<int*>(sm.gamma + ((S + 3) & ~3));
 
   const int64_t e0 = thread_e0(a.g, R);
@@ -351,9 +398,9 @@ __global__ void __launch_bounds__(LDBP_REV_MAXT, 65536 / (LDBP_REV_MAXT * 128)) 
                                     sm.norm, norm);
   __syncthreads();
   if (norm)
-    rev_body<KH, R, SYM, FAST, true>(a, sm, e0, fast_off, own, lane, warp, nwarps);
+    rev_body<KH, R, SYM, FAST, true>(a, sm, e0, fast_off, own, lane, warp);
   else
-    rev_body<KH, R, SYM, FAST, false>(a, sm, e0, fast_off, own, lane, warp, nwarps);
+    rev_body<KH, R, SYM, FAST, false>(a, sm, e0, fast_off, own, lane, warp);
 }
 
 }  // namespace ldbp
