@@ -85,11 +85,11 @@ const char* ldbp_last_error(void);
 /* Device workspace (bytes) the given op needs for these dims; 0 means ws may be NULL.
    Returns a status; *bytes is written on LDBP_OK.
    Backward / loss_grad / train_step choose between two schedules for row a7 (activations):
-   checkpoint + recompute segments with ~M/6 checkpoints (default, env LDBP_BWD_MODE=0), or
-   "store-all" (LDBP_BWD_MODE=1; -1 = auto while M*B*n*8 bytes <= LDBP_ACT_BUDGET_GB, default
-   96): the forward stores every step's activation in the workspace (M*B*n*8 bytes +
-   O(grid*M*T)) and one fused reverse kernel needs no recompute.  The choice depends only on dims and
-   the environment, so this query and the call agree. */
+   "store-all" (default while B*n >= 2^20 and M*B*n*8 bytes <= LDBP_ACT_BUDGET_GB, env, default 96; forced by
+   env LDBP_BWD_MODE=1): the forward stores every step's activation in the workspace
+   (M*B*n*8 bytes + O(grid*M*T)) and one fused reverse kernel needs no recompute; otherwise (or
+   LDBP_BWD_MODE=0) checkpoint + recompute segments with ~M/6 checkpoints.  The choice depends
+   only on dims and the environment, so this query and the call agree. */
 int ldbp_workspace_bytes(const ldbp_dims* d, int op, size_t* bytes);
 
 /* Number of CUDA kernel launches the op enqueues for these dims (for accounting). */

@@ -170,10 +170,12 @@ struct Tile {
   ldbp::Geo g{};
 };
 
-size_t fwd_smem(int kh, bool sym, int steps, int nthreads = 1024, int nnorm = 0) {
+size_t fwd_smem(int kh, bool sym, int steps, int nthreads = 1024, int nnorm = 0, bool staged = false) {
   (void)nthreads;
   const int edge_rows = LDBP_FWD_XSMEM ? ldbp::fwd_max_threads(kh) : ldbp::kMaxWarps;
-  return sizeof(uint64_t) * 2 * ldbp::kMaxWarps + sizeof(float2) * 4 * edge_rows * std::max(kh, 1) +
+  const size_t edge = staged ? sizeof(float2) * (size_t)ldbp::fwd_stage_elems(kh, kFwdR)
+                             : sizeof(float2) * 4 * edge_rows * std::max(kh, 1);
+  return sizeof(uint64_t) * 2 * ldbp::kMaxWarps + edge +
          sizeof(ldbp::TapP) * steps * ntaps_used(kh, sym) + sizeof(ldbp::StepNorm) * std::max(steps, nnorm) +
          sizeof(float) * steps + 32;
 }
@@ -323,18 +325,18 @@ BwdPlan plan_bwd(const ldbp_dims* d, bool query_device) {
   return p;
 }
 
-Tile plan_fwd_tile(const ldbp_dims* d, int steps, bool query_device) {
+Tile plan_fwd_tile(const ldbp_dims* d, int steps, bool query_device, bool staged = false) {
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const int maxthr = std::min(env_int("LDBP_FWD_THREADS", kFwdMaxThreads), ldbp::fwd_max_threads(kh));
   int occ = 1, sms = 148;
-  const size_t smem = fwd_smem(kh, sym, steps, maxthr);
+  const size_t smem = fwd_smem(kh, sym, steps, maxthr, staged ? d->steps : 0, staged);
   if (query_device) {
     sms = device_sms();
     occ = fwd_occupancy(get_fwd(kh, sym, !(d->flags & LDBP_PRECISE)), maxthr, smem);
   }
-  Tile t = plan_tiles(d->batch, d->n, steps * kh, kFwdR, maxthr, occ, sms);
-  t.smem = fwd_smem(kh, sym, steps, t.nthreads);
+  Tile t = plan_tiles(d->batch, d->n, steps * kh, kFwdR, maxthr, occ, sms, /*align_r=*/staged);
+  t.smem = fwd_smem(kh, sym, steps, t.nthreads, 0, staged);
   return t;
 }
 
@@ -396,10 +398,12 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
 // Which training path: 1 = store-all activations + fused reverse (default when the activations
 // fit the budget), 0 = checkpoint + recompute segments (memory-lean fallback).
 bool use_store_all(const ldbp_dims* d) {
-  const int mode = env_int("LDBP_BWD_MODE", 0);
+  const int mode = env_int("LDBP_BWD_MODE", -1);
   if (mode == 0) return false;
   if (mode == 1) return true;
   const double act_gb = (double)d->steps * (double)d->batch * (double)d->n * sizeof(float2) / 1073741824.0;
+  // tiny problems (one wave, latency-bound, e.g. C1) keep the 3-launch segment schedule
+  if ((double)d->batch * (double)d->n < (double)env_int("LDBP_STORE_ALL_MIN_SAMPLES", 1 << 20)) return false;
   return act_gb <= (double)env_int("LDBP_ACT_BUDGET_GB", 96);
 }
 
@@ -522,8 +526,9 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const bool fast = !(d->flags & LDBP_PRECISE);
-  Tile t = plan_fwd_tile(d, s1 - s0, true);
-  if (global_norm) t.smem = fwd_smem(kh, sym, s1 - s0, t.nthreads, d->steps);
+  const bool staged = global_norm && ckpt && ckpt_every == 1 && fast && env_int("LDBP_FWD_STAGED", 1);
+  Tile t = plan_fwd_tile(d, s1 - s0, true, staged);
+  if (global_norm) t.smem = fwd_smem(kh, sym, s1 - s0, t.nthreads, d->steps, staged);
   FwdFn fn = get_fwd(kh, sym, fast);
   ldbp::FwdArgs a;
   a.src = src;
@@ -541,6 +546,7 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   a.nM = global_norm ? d->steps : s1;
   a.global_norm = global_norm ? 1 : 0;
   a.scale_dst = scale_dst ? 1 : 0;
+  a.staged = staged ? 1 : 0;
   a.g = t.g;
   cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
   {

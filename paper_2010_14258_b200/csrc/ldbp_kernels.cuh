@@ -810,6 +810,7 @@ struct FwdArgs {
   int n0, nM;
   int global_norm;
   int scale_dst;
+  int staged;  // store-all mode (ckpt_every == 1, global): coalesced stores through a smem stage
   Geo g;
 };
 
@@ -824,6 +825,8 @@ struct FwdArgs {
 __host__ __device__ constexpr int fwd_max_threads(int kh) {
   return LDBP_FWD_R > 16 ? 256 : (kh <= 2 ? 512 : kh <= 5 ? 256 : LDBP_FWD_WIDE_THREADS);
 }
+// f2x elements of the store-all stage region: 2 buffers of ST runs of RS, plus run_off[ST] (int64)
+__host__ __device__ constexpr int fwd_stage_elems(int kh, int r) { return fwd_max_threads(kh) * (2 * (r + 2) + 1); }
 __host__ __device__ constexpr int fwd_min_blocks(int kh) {
   return kh <= 2 ? 2 : kh <= 4 ? 3 : (LDBP_FWD_WIDE_THREADS >= 512 && kh >= 6) ? 1 : 2;
 }
@@ -911,10 +914,19 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity)
 // outputs.  The barrier latency and the warp skew hide behind the interior work.  Buffer reuse:
 // buffer b is rewritten for phase p+2 by a warp that has passed phase p+1, whose arrivals all
 // come after their reads of phase p.
-template <int KH, int R, bool SYM, bool FAST, bool NORM>
+// STG (store-all mode): instead of the Kh-sample edge arrays every thread publishes all R of its
+// samples into a padded run-major stage stage[buf][t*RS + k] (RS = R + 2: conflict-free 16-byte
+// stores and loads); neighbours take their halos from it and, after the barrier, the CTA copies
+// the owned runs to HBM with lane-consecutive 16-byte stores (8 lanes per 128-byte run), instead
+// of every thread storing its own R samples (lane stride R*8 bytes: one L2 sector per lane).
+template <int R>
+__device__ __forceinline__ constexpr int stage_rs() { return R + 2; }
+
+template <int KH, int R, bool SYM, bool FAST, bool NORM, bool STG>
 __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], const TapP* sh_taps,
                                                 const float* sh_gamma, const StepNorm* sh_norm, f2x* sh_edge,
                                                 uint64_t* bar, const StoreMap& smap, int64_t e0, int lane) {
+  constexpr int RS = stage_rs<R>();
   constexpr int NTU = ntaps_used<SYM, KH>();
   constexpr int KI = KH < R - KH ? KH : R / 2;  // interior [KI, R-KI)
   constexpr int ST = fwd_max_threads(KH);       // edge-array row stride (compile time -> immediates)
@@ -927,8 +939,29 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
   f2x* const my_edge = sh_edge + tid;
   const f2x* const left_edge = sh_edge + left;
   const f2x* const right_edge = sh_edge + right;
+  // STG: stage[2][ST*RS] f2x, then run_off[ST] (int64: HBM element offset of run t, -1 = not an
+  // owned real run, -2 = owned but irregular: the owner stores it itself)
+  f2x* const stage = sh_edge;
+  int64_t* const run_off = reinterpret_cast<int64_t*>(sh_edge + 2 * ST * RS);
+  int t_lo = 0, t_hi = 0;
+  if constexpr (STG) {
+    const bool fullrun = smap.off >= 0;
+    run_off[tid] = fullrun ? smap.off : (smap.mask ? -2 : -1);
+    const int64_t lo = tile_lo(a.g, blockIdx.x);
+    const int64_t wc = min(lo + ((int64_t)blockIdx.x < a.g.NS ? a.g.Wh : a.g.W), a.g.E) - lo;
+    t_lo = a.g.H / R;
+    t_hi = (int)min((int64_t)nthr, (a.g.H + wc + R - 1) / R);
+    __syncthreads();  // run_off visible before the first copy
+  }
   auto publish = [&](int buf) {
-    if constexpr (KH > 0) {
+    if constexpr (STG) {
+      f2x* st = stage + buf * ST * RS + tid * RS;
+#pragma unroll
+      for (int m = 0; m < R / 2; ++m)
+        *reinterpret_cast<ulonglong2*>(st + 2 * m) = make_ulonglong2(u[2 * m], u[2 * m + 1]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(bar);
+    } else if constexpr (KH > 0) {
       f2x* e = my_edge + buf * 2 * KH * ST;
 #pragma unroll
       for (int j = 0; j < KH; ++j) {
@@ -952,7 +985,26 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
     const float gm = sh_gamma[s];
     f2x acc[R], nu[R];
     step_range<KH, R, SYM, FAST, NORM, KI, R - KI>(u, hl, hr, hs, gm, acc, nu);
-    if constexpr (KH > 0) {
+    if constexpr (STG) {
+      mbar_wait_parity(bar, s & 1);
+      const f2x* st = stage + (s & 1) * ST * RS;
+#pragma unroll
+      for (int j = 0; j < KH; ++j) {
+        hl[j] = st[left * RS + R - KH + j];
+        hr[j] = st[right * RS + j];
+      }
+      // coalesced copy of u^(s0+s) (computed by this launch when s >= 1) to its activation slot
+      if (s >= 1) {
+        float2* dstp = a.ckpt + (int64_t)(a.s0 + s - 1) * a.ckpt_stride;
+        const int units = (t_hi - t_lo) * (R / 2);
+        for (int uu = tid; uu < units; uu += nthr) {
+          const int t = t_lo + uu / (R / 2), p2 = uu % (R / 2);
+          const int64_t off = run_off[t];
+          if (off >= 0)
+            *reinterpret_cast<ulonglong2*>(dstp + off + 2 * p2) = *reinterpret_cast<const ulonglong2*>(st + t * RS + 2 * p2);
+        }
+      }
+    } else if constexpr (KH > 0) {
       mbar_wait_parity(bar, s & 1);
       const int off = (s & 1) * 2 * KH * ST;
 #pragma unroll
@@ -967,7 +1019,10 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
     for (int k = 0; k < R; ++k) u[k] = nu[k];
     const int gs = a.s0 + s + 1;  // global step count reached
     if (gs < a.s1) publish((s + 1) & 1);
-    if (gs == next_ck && gs < a.s1) {
+    if (STG) {
+      if (gs < a.s1 && smap.off < 0 && smap.mask) store_mapped<R>(ck_ptr, smap, e0, a.g, u);  // irregular run
+      ck_ptr += a.ckpt_stride;
+    } else if (gs == next_ck && gs < a.s1) {
       if (global) {
         store_mapped<R>(ck_ptr, smap, e0, a.g, u);
       } else if constexpr (NORM) {
@@ -996,8 +1051,9 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
   const int S = a.s1 - a.s0;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                            // [2][32] mbarriers
   f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);  // 2*2*KH*(XSMEM ? nthreads : 32)
-  TapP* sh_taps = reinterpret_cast<TapP*>(sh_edge + 4 * (LDBP_FWD_XSMEM ? fwd_max_threads(KH) : kMaxWarps) *
-                                                        (KH > 0 ? KH : 1));  // S*NTU
+  TapP* sh_taps = reinterpret_cast<TapP*>(
+      sh_edge + (a.staged ? fwd_stage_elems(KH, R)
+                          : 4 * (LDBP_FWD_XSMEM ? fwd_max_threads(KH) : kMaxWarps) * (KH > 0 ? KH : 1)));  // S*NTU
   StepNorm* sh_norm = reinterpret_cast<StepNorm*>(sh_taps + S * NTU);                // max(S, nM-n0)
   float* sh_gamma = reinterpret_cast<float*>(sh_norm + max(S, a.nM - a.n0));         // S
   int* sh_flag = reinterpret_cast<int*>(sh_gamma + S);
@@ -1020,13 +1076,18 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
                                  sh_flag);
   }
   __syncthreads();
-  if (SYM && *sh_flag)
+  if (FAST && a.staged) {
+    if (SYM && *sh_flag)
+      fwd_steps_split<KH, R, SYM, FAST, true, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
+    else
+      fwd_steps_split<KH, R, SYM, FAST, false, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
+  } else if (SYM && *sh_flag)
     if (LDBP_FWD_SPLIT)
-      fwd_steps_split<KH, R, SYM, FAST, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
+      fwd_steps_split<KH, R, SYM, FAST, true, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
     else
       fwd_steps<KH, R, SYM, FAST, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane, warp, nwarps);
   else if (LDBP_FWD_SPLIT)
-    fwd_steps_split<KH, R, SYM, FAST, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
+    fwd_steps_split<KH, R, SYM, FAST, false, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
   else
     fwd_steps<KH, R, SYM, FAST, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane, warp, nwarps);
 }

@@ -70,16 +70,11 @@ __device__ __forceinline__ void async_window(const float2* __restrict__ src, int
                                              int64_t fast_off) {
   const int t = threadIdx.x;
   f2x* mine = buf + ubuf_idx<NT>(0, t);
-  if (fast_off >= 0) {
-    const f2x* p = reinterpret_cast<const f2x*>(src) + fast_off;
-    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+  const f2x* p = reinterpret_cast<const f2x*>(src) + fast_off;
+  if (fast_off >= 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
 #pragma unroll
-      for (int m = 0; m < R / 2; ++m) cp_async16(mine + m * 2 * NT, p + 2 * m);
-    } else {
-#pragma unroll
-      for (int k = 0; k < R; ++k) cp_async8(mine + (k >> 1) * 2 * NT + (k & 1), p + k);
-    }
-  } else {
+    for (int m = 0; m < R / 2; ++m) cp_async16(mine + m * 2 * NT, p + 2 * m);
+  } else {  // irregular or 8-byte aligned runs (rare): per-sample copies with zero fill
     const Span sp = make_span(e0, g);
 #pragma unroll
     for (int k = 0; k < R; ++k) {
