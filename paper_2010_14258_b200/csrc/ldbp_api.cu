@@ -184,7 +184,8 @@ size_t fwd_smem(int kh, bool sym, int steps, int nthreads = 1024, int nnorm = 0,
 size_t rev_smem(int kh, bool sym, int steps, int M) {
   const int NT = ldbp::kRevThreads, nw = NT / 32;
   const int V = 1 + 2 * ntaps_used(kh, sym);
-  size_t s = sizeof(float2) * 2 * (size_t)kRevR * NT;                 // u window copies
+  size_t s = 16;                                                      // split-barrier mbarrier
+  s += sizeof(float2) * 2 * (size_t)kRevR * NT;                       // u window copies
   s += sizeof(float2) * 4 * (size_t)std::max(kh, 1) * NT;             // ga edges
   s += sizeof(ldbp::TapP) * (size_t)steps * ntaps_used(kh, sym);      // adjoint taps
   s += sizeof(ldbp::StepNorm) * (size_t)M;                            // global normalisation

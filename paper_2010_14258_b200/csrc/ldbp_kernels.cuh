@@ -29,7 +29,7 @@
 #define LDBP_BWD_R 8   // samples per thread, backward kernels
 #endif
 #ifndef LDBP_REV_R
-#define LDBP_REV_R 8   // samples per thread, store-all reverse kernel
+#define LDBP_REV_R 16  // samples per thread, store-all reverse kernel
 #endif
 
 #ifndef LDBP_NORM

@@ -89,6 +89,7 @@ __device__ __forceinline__ void async_window(const float2* __restrict__ src, int
 }
 
 struct RevSmem {
+  uint64_t* bar;    // split step barrier (count = warps), phases = reverse steps
   TapP* taps_adj;   // [S][NTU]
   StepNorm* norm;   // [M] (global normalisation, step-indexed)
   float* gamma;     // [S] gamma_hat
@@ -115,70 +116,87 @@ __device__ __forceinline__ void nl_adjoint(f2x& gk, f2x vk, float gm, float gm2,
   if (!MASKED || owned) dgam = fmaf(cim, p, dgam);
 }
 
-// One reverse step's arithmetic after the halo exchange: tap gradients of step l (owned samples;
-// MASKED selects per sample, the common full-ownership path has no selects), then the FIR adjoint
-// g_s = sum_j conj(h_j) ga_{s+j} fused with the NL adjoint of step l-1 on each fresh g_s (NL).
-// Tap gradient form: ga conj(w) = lo(w) ga - j hi(w) ga, accumulated as A_j += lo(w) ga,
-// B_j += hi(w) ga (broadcast operands only, no per-sample pair construction); dh_j = A_j - j B_j.
-template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL>
-__device__ __forceinline__ void rev_compute(const f2x (&u)[R], const f2x (&hl)[KH > 0 ? KH : 1],
-                                            const f2x (&hr)[KH > 0 ? KH : 1], f2x (&g)[R],
-                                            const f2x (&gl)[KH > 0 ? KH : 1], const f2x (&gr)[KH > 0 ? KH : 1],
-                                            const TapP* __restrict__ hs_sm, uint32_t own, float gmn,
-                                            float (&dh)[2 * (SYM ? KH + 1 : 2 * KH + 1)], float& dgam_next) {
-  constexpr int NTU = ntaps_used<SYM, KH>();
-  f2x A[NTU], Bq[NTU];
-#pragma unroll
-  for (int j = 0; j < NTU; ++j) A[j] = Bq[j] = 0ull;
-#pragma unroll
-  for (int k = 0; k < R; ++k) {
-    const f2x gk = (!MASKED || ((own >> k) & 1u)) ? g[k] : 0ull;
+// Reverse step arithmetic for outputs s in [SB, SE) (compile-time range), shared pre-add form:
+// with ga = ga^(l) (window incl. halos gl/gr) and u_s = u^(l)_s (own samples only),
+//   P_sj = ga_{s-j} + ga_{s+j}                      (SYM; GEN uses the single term ga_{s+j})
+//   FIR adjoint   g_s  = ga_s + sum_j conj(h_j) P_sj  (NORM: h_0 = 1)
+//   tap gradient  dh_j += conj(u_s) P_sj            (= sum_t ga_t conj(u_{t-j} + u_{t+j}),
+//                                                     reindexed t -> s; each real sample is owned
+//                                                     by exactly one CTA, so the sums agree)
+// conj(u) P = ux P - j uy P is accumulated as A_j += ux P, B_j += uy P (broadcast operands only);
+// dh_j = A_j - j B_j once per step.  The NL adjoint of step l-1 follows on each fresh g_s (NL).
+template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL, int SB, int SE, int S0 = SB>
+__device__ __forceinline__ void rev_range(const f2x (&g)[R], const f2x (&gl)[KH > 0 ? KH : 1],
+                                          const f2x (&gr)[KH > 0 ? KH : 1], const f2x* __restrict__ ub_mine,
+                                          const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1],
+                                          f2x (&A)[SYM ? KH + 1 : 2 * KH + 1], f2x (&Bq)[SYM ? KH + 1 : 2 * KH + 1],
+                                          f2x (&ng)[R], uint32_t own, float gmn, float& dgam_next) {
+  if constexpr (S0 < SE) {
+    constexpr int s = S0;
+    const f2x us = ub_mine[(s >> 1) * 2 * kRevThreads + (s & 1)];
+    const bool mine = !MASKED || ((own >> s) & 1u);
+    const f2x ux = bcast(lof(us)), uy = bcast(hif(us));
+    f2x acc;
     if constexpr (SYM) {
-      A[0] = fma2(bcast(lof(u[k])), gk, A[0]);
-      Bq[0] = fma2(bcast(hif(u[k])), gk, Bq[0]);
+      const f2x g0 = g[s];
+      acc = NORM ? g0 : tmul(hs[0], g0);
+      if (mine) { A[0] = fma2(ux, g0, A[0]); Bq[0] = fma2(uy, g0, Bq[0]); }
 #pragma unroll
       for (int j = 1; j <= KH; ++j) {
-        const f2x w = add2(LDBP_WIN(u, hl, hr, k - j), LDBP_WIN(u, hl, hr, k + j));
-        A[j] = fma2(bcast(lof(w)), gk, A[j]);
-        Bq[j] = fma2(bcast(hif(w)), gk, Bq[j]);
+        const f2x P = add2(LDBP_WIN(g, gl, gr, s - j), LDBP_WIN(g, gl, gr, s + j));
+        acc = tmac(acc, hs[j], P);
+        if (mine) { A[j] = fma2(ux, P, A[j]); Bq[j] = fma2(uy, P, Bq[j]); }
       }
     } else {
+      acc = 0ull;
 #pragma unroll
       for (int jj = 0; jj < 2 * KH + 1; ++jj) {
-        const f2x w = LDBP_WIN(u, hl, hr, k - (jj - KH));
-        A[jj] = fma2(bcast(lof(w)), gk, A[jj]);
-        Bq[jj] = fma2(bcast(hif(w)), gk, Bq[jj]);
+        const f2x P = LDBP_WIN(g, gl, gr, s + (jj - KH));
+        acc = tmac(acc, hs[jj], P);
+        if (mine) { A[jj] = fma2(ux, P, A[jj]); Bq[jj] = fma2(uy, P, Bq[jj]); }
       }
     }
+    if constexpr (NL) nl_adjoint<FAST, MASKED>(acc, us, gmn, 2.f * gmn, (own >> s) & 1u, dgam_next);
+    ng[s] = acc;
+    rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, SB, SE, S0 + 1>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn,
+                                                                  dgam_next);
   }
+}
+
+// One full reverse step with the split barrier: interior outputs (no halo needed) before the
+// wait on the ga-edge mbarrier phase, boundary outputs after it.
+template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL>
+__device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub_mine, const f2x* left_edge,
+                                         const f2x* right_edge, int eoff, uint64_t* bar, unsigned parity,
+                                         const TapP* __restrict__ hs_sm, uint32_t own, float gmn,
+                                         float (&dh)[2 * (SYM ? KH + 1 : 2 * KH + 1)], float& dgam_next) {
+  constexpr int NTU = ntaps_used<SYM, KH>();
+  constexpr int NT = kRevThreads;
+  constexpr int KI = KH < R - KH ? KH : R / 2;  // interior [KI, R-KI)
+  TapP hs[NTU];
+#pragma unroll
+  for (int j = 0; j < NTU; ++j) hs[j] = hs_sm[j];
+  f2x A[NTU], Bq[NTU], ng[R];
+#pragma unroll
+  for (int j = 0; j < NTU; ++j) A[j] = Bq[j] = 0ull;
+  f2x gl[KH > 0 ? KH : 1], gr[KH > 0 ? KH : 1];
+#pragma unroll
+  for (int j = 0; j < (KH > 0 ? KH : 1); ++j) gl[j] = gr[j] = 0ull;
+  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, KI, R - KI>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn, dgam_next);
+  if constexpr (KH > 0) {
+    mbar_wait_parity(bar, parity);
+#pragma unroll
+    for (int j = 0; j < KH; ++j) {
+      gl[j] = left_edge[eoff + (KH + j) * NT];
+      gr[j] = right_edge[eoff + j * NT];
+    }
+  }
+  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, 0, KI>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn, dgam_next);
+  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, R - KI, R>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn, dgam_next);
 #pragma unroll
   for (int j = 0; j < NTU; ++j) {
     dh[2 * j] = lof(A[j]) + hif(Bq[j]);
     dh[2 * j + 1] = hif(A[j]) - lof(Bq[j]);
-  }
-  TapP hs[NTU];
-#pragma unroll
-  for (int j = 0; j < NTU; ++j) hs[j] = hs_sm[j];
-  const float gmn2 = 2.f * gmn;
-  f2x ng[R];
-#pragma unroll
-  for (int k = 0; k < R; ++k) {
-    f2x acc;
-    if constexpr (SYM && NORM) {
-      acc = g[k];
-#pragma unroll
-      for (int j = 1; j <= KH; ++j) acc = tmac(acc, hs[j], add2(LDBP_WIN(g, gl, gr, k - j), LDBP_WIN(g, gl, gr, k + j)));
-    } else if constexpr (SYM) {
-      acc = tmul(hs[0], g[k]);
-#pragma unroll
-      for (int j = 1; j <= KH; ++j) acc = tmac(acc, hs[j], add2(LDBP_WIN(g, gl, gr, k - j), LDBP_WIN(g, gl, gr, k + j)));
-    } else {
-      acc = tmul(hs[0], LDBP_WIN(g, gl, gr, k - KH));
-#pragma unroll
-      for (int jj = 1; jj < 2 * KH + 1; ++jj) acc = tmac(acc, hs[jj], LDBP_WIN(g, gl, gr, k + (jj - KH)));
-    }
-    if constexpr (NL) nl_adjoint<FAST, MASKED>(acc, u[k], gmn, gmn2, (own >> k) & 1u, dgam_next);
-    ng[k] = acc;
   }
 #pragma unroll
   for (int k = 0; k < R; ++k) g[k] = ng[k];
@@ -202,8 +220,9 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   // the latter zero their partials.  Only ragged blocks (n % R != 0) have partial threads.
   const bool full = own == FULL || own == 0;
   const bool none = own == 0;
+  uint64_t* bar = sm.bar;
 
-  // prefetch u^(s1-1) while v = u^(s1) and the seed are loaded synchronously
+  // prefetch u^(s1-1) (own slots only: no barrier is needed to consume it)
   async_window<R, NT>(rev_src(a, s1 - 1), e0, a.g, sm.ubuf + (size_t)((s1 - 1) & 1) * R * NT, fast_off);
   f2x v[R], g[R];
   load_window<R>(rev_src(a, s1), e0, a.g, v);
@@ -238,8 +257,7 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
       for (int k = 0; k < R; ++k) g[k] = tmul(conjP, g[k]);
     }
   }
-  // NL adjoint of step s1-1 up front; every later one is fused into the previous step's FIR-
-  // adjoint loop (software pipelining: MUFU work interleaved with FMA-pipe work)
+  // NL adjoint of step s1-1 up front; every later one is fused into the previous step's loop
   float dgam = 0.f;
   {
     const float gm = sm.gamma[s1 - 1 - s0];
@@ -255,55 +273,49 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   f2x* const my_edge = sm.edge + tid;
   const f2x* const left_edge = sm.edge + left;
   const f2x* const right_edge = sm.edge + right;
+  auto publish = [&](int ph) {  // ga edges of phase ph into edge buffer ph & 1, then arrive
+    if constexpr (KH > 0) {
+      const int eo = (ph & 1) * 2 * KE * NT;
+#pragma unroll
+      for (int j = 0; j < KH; ++j) {
+        my_edge[eo + j * NT] = g[j];                   // head
+        my_edge[eo + (KH + j) * NT] = g[R - KH + j];   // tail
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar);
+    }
+  };
+  publish(0);
 
   for (int l = s1 - 1; l >= s0; --l) {
     const int li = l - s0;
-    // ---- publish ga edges, wait for u^(l), one barrier ----
-    const int eoff = (l & 1) * 2 * KE * NT;
-    if constexpr (KH > 0) {
-#pragma unroll
-      for (int j = 0; j < KH; ++j) {
-        my_edge[eoff + j * NT] = g[j];                   // head
-        my_edge[eoff + (KH + j) * NT] = g[R - KH + j];   // tail
-      }
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    // prefetch u^(l-1) into the other buffer (its last reader, step l+1, is behind the barrier)
+    const int ph = s1 - 1 - l;  // barrier phase of this step
+    cp_async_wait_all();        // own u^(l) slots landed
+    // prefetch u^(l-1) into the other buffer (this thread's own slots, consumed in step l+1)
     if (l > s0)
       async_window<R, NT>(rev_src(a, l - 1), e0, a.g, sm.ubuf + (size_t)((l - 1) & 1) * R * NT, fast_off);
-    const f2x* ub = sm.ubuf + (size_t)(l & 1) * R * NT;
-    f2x u[R], hl[KE], hr[KE], gl[KE], gr[KE];
-#pragma unroll
-    for (int m = 0; m < R / 2; ++m) {
-      const ulonglong2 pr = *reinterpret_cast<const ulonglong2*>(ub + ubuf_idx<NT>(2 * m, tid));
-      u[2 * m] = pr.x;
-      u[2 * m + 1] = pr.y;
-    }
-    if constexpr (KH > 0) {
-#pragma unroll
-      for (int j = 0; j < KH; ++j) {
-        hl[j] = ub[ubuf_idx<NT>(R - KH + j, left)];
-        hr[j] = ub[ubuf_idx<NT>(j, right)];
-        gl[j] = left_edge[eoff + (KH + j) * NT];
-        gr[j] = right_edge[eoff + j * NT];
-      }
-    }
+    const f2x* ub_mine = sm.ubuf + (size_t)(l & 1) * R * NT + ubuf_idx<NT>(0, tid);
+    const int eoff = (ph & 1) * 2 * KE * NT;
     float dh[2 * NTU];
     float dgam_next = 0.f;
     const TapP* hs_sm = sm.taps_adj + li * NTU;
+    const float gmn = l > s0 ? sm.gamma[li - 1] : 0.f;
     if (l > s0) {
-      const float gmn = sm.gamma[li - 1];
       if (full)
-        rev_compute<KH, R, SYM, FAST, NORM, false, true>(u, hl, hr, g, gl, gr, hs_sm, own, gmn, dh, dgam_next);
+        rev_step<KH, R, SYM, FAST, NORM, false, true>(g, ub_mine, left_edge, right_edge, eoff, bar, ph & 1, hs_sm,
+                                                      own, gmn, dh, dgam_next);
       else
-        rev_compute<KH, R, SYM, FAST, NORM, true, true>(u, hl, hr, g, gl, gr, hs_sm, own, gmn, dh, dgam_next);
+        rev_step<KH, R, SYM, FAST, NORM, true, true>(g, ub_mine, left_edge, right_edge, eoff, bar, ph & 1, hs_sm,
+                                                     own, gmn, dh, dgam_next);
     } else {
       if (full)
-        rev_compute<KH, R, SYM, FAST, NORM, false, false>(u, hl, hr, g, gl, gr, hs_sm, own, 0.f, dh, dgam_next);
+        rev_step<KH, R, SYM, FAST, NORM, false, false>(g, ub_mine, left_edge, right_edge, eoff, bar, ph & 1, hs_sm,
+                                                       own, gmn, dh, dgam_next);
       else
-        rev_compute<KH, R, SYM, FAST, NORM, true, false>(u, hl, hr, g, gl, gr, hs_sm, own, 0.f, dh, dgam_next);
+        rev_step<KH, R, SYM, FAST, NORM, true, false>(g, ub_mine, left_edge, right_edge, eoff, bar, ph & 1, hs_sm,
+                                                      own, gmn, dh, dgam_next);
     }
+    if (l > s0) publish(ph + 1);
     if (none) {
       dgam_next = 0.f;
 #pragma unroll
@@ -374,7 +386,8 @@ __global__ void __launch_bounds__(kRevThreads, 65536 / (kRevThreads * 128)) rev_
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // carve-up (16-byte aligned regions; mirrored by rev_smem() on the host)
   RevSmem sm;
-  sm.ubuf = reinterpret_cast<f2x*>(smem_raw);                                        // 2*R*NT
+  sm.bar = reinterpret_cast<uint64_t*>(smem_raw);                                    // 2 words
+  sm.ubuf = reinterpret_cast<f2x*>(smem_raw) + 2;                                    // 2*R*NT
   sm.edge = sm.ubuf + (size_t)2 * R * NT;                                            // 4*KH*NT
   sm.taps_adj = reinterpret_cast<TapP*>(sm.edge + (size_t)4 * (KH > 0 ? KH : 1) * NT);  // S*NTU
   sm.norm = reinterpret_cast<StepNorm*>(sm.taps_adj + S * NTU);                      // M
@@ -387,6 +400,9 @@ __global__ void __launch_bounds__(kRevThreads, 65536 / (kRevThreads * 128)) rev_
   const Span sp = make_span(e0, a.g);
   const int64_t fast_off = span_fast<R>(sp, a.g, e0) ? sp.b0 * a.g.n + (sp.q0 - a.g.H) : -1;
   const uint32_t own = owned_mask<R>(e0, a.g);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(sm.bar)), "r"(NT / 32) : "memory");
+  }
   norm_range<KH, SYM>(a.taps, a.mask, a.T, 0, a.M, sm.norm, sm.flag);
   const bool norm = SYM && *sm.flag;
   stage_range<KH, SYM, false, true>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, 0, nullptr, sm.taps_adj, sm.gamma,
