@@ -99,6 +99,7 @@ int ntaps_used(int kh, bool sym) { return sym ? kh + 1 : 2 * kh + 1; }
 // Kernel instantiations live in ldbp_inst.cu, compiled once per Kh (parallel build).
 #define LDBP_DECL_GETTERS(K)                        \
   FwdFn ldbp_get_fwd_##K(bool sym, bool fast);      \
+  FwdFn ldbp_get_fwd_store_##K(bool sym);           \
   BwdFn ldbp_get_bwd_##K(bool sym, bool fast);      \
   RevFn ldbp_get_rev_##K(bool sym, bool fast);
 }  // namespace
@@ -135,6 +136,20 @@ BwdFn get_bwd(int kh, bool sym, bool fast) {
     case 5: return ldbp_get_bwd_5(sym, fast);
     case 6: return ldbp_get_bwd_6(sym, fast);
     case 7: return ldbp_get_bwd_7(sym, fast);
+  }
+  return nullptr;
+}
+
+FwdFn get_fwd_store(int kh, bool sym) {
+  switch (kh) {
+    case 0: return ldbp_get_fwd_store_0(sym);
+    case 1: return ldbp_get_fwd_store_1(sym);
+    case 2: return ldbp_get_fwd_store_2(sym);
+    case 3: return ldbp_get_fwd_store_3(sym);
+    case 4: return ldbp_get_fwd_store_4(sym);
+    case 5: return ldbp_get_fwd_store_5(sym);
+    case 6: return ldbp_get_fwd_store_6(sym);
+    case 7: return ldbp_get_fwd_store_7(sym);
   }
   return nullptr;
 }
@@ -334,7 +349,7 @@ Tile plan_fwd_tile(const ldbp_dims* d, int steps, bool query_device, bool staged
   const size_t smem = fwd_smem(kh, sym, steps, maxthr, staged ? d->steps : 0, staged);
   if (query_device) {
     sms = device_sms();
-    occ = fwd_occupancy(get_fwd(kh, sym, !(d->flags & LDBP_PRECISE)), maxthr, smem);
+    occ = fwd_occupancy(staged ? get_fwd_store(kh, sym) : get_fwd(kh, sym, !(d->flags & LDBP_PRECISE)), maxthr, smem);
   }
   Tile t = plan_tiles(d->batch, d->n, steps * kh, kFwdR, maxthr, occ, sms, /*align_r=*/staged);
   t.smem = fwd_smem(kh, sym, steps, t.nthreads, 0, staged);
@@ -530,7 +545,7 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   const bool staged = global_norm && ckpt && ckpt_every == 1 && fast && env_int("LDBP_FWD_STAGED", 1);
   Tile t = plan_fwd_tile(d, s1 - s0, true, staged);
   if (global_norm) t.smem = fwd_smem(kh, sym, s1 - s0, t.nthreads, d->steps, staged);
-  FwdFn fn = get_fwd(kh, sym, fast);
+  FwdFn fn = staged ? get_fwd_store(kh, sym) : get_fwd(kh, sym, fast);
   ldbp::FwdArgs a;
   a.src = src;
   a.dst = dst;

@@ -19,6 +19,11 @@ FwdFn LDBP_CAT(ldbp_get_fwd_, LDBP_KH)(bool sym, bool fast) {
   return fast ? ldbp::fwd_tile_kernel<K, R, false, true> : ldbp::fwd_tile_kernel<K, R, false, false>;
 }
 
+FwdFn LDBP_CAT(ldbp_get_fwd_store_, LDBP_KH)(bool sym) {
+  constexpr int K = LDBP_KH, R = LDBP_FWD_R;
+  return sym ? ldbp::fwd_store_kernel<K, R, true> : ldbp::fwd_store_kernel<K, R, false>;
+}
+
 BwdFn LDBP_CAT(ldbp_get_bwd_, LDBP_KH)(bool sym, bool fast) {
   constexpr int K = LDBP_KH, R = LDBP_BWD_R;
   if (sym) return fast ? ldbp::bwd_segment_kernel<K, R, true, true> : ldbp::bwd_segment_kernel<K, R, true, false>;

@@ -1044,15 +1044,15 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
 #define LDBP_FWD_SPLIT 1
 #endif
 
-template <int KH, int R, bool SYM, bool FAST>
-__global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_tile_kernel(const FwdArgs a) {
+template <int KH, int R, bool SYM, bool FAST, bool STG>
+__device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int S = a.s1 - a.s0;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                            // [2][32] mbarriers
   f2x* sh_edge = reinterpret_cast<f2x*>(bars + 2 * kMaxWarps);  // 2*2*KH*(XSMEM ? nthreads : 32)
   TapP* sh_taps = reinterpret_cast<TapP*>(
-      sh_edge + (a.staged ? fwd_stage_elems(KH, R)
+      sh_edge + (STG ? fwd_stage_elems(KH, R)
                           : 4 * (LDBP_FWD_XSMEM ? fwd_max_threads(KH) : kMaxWarps) * (KH > 0 ? KH : 1)));  // S*NTU
   StepNorm* sh_norm = reinterpret_cast<StepNorm*>(sh_taps + S * NTU);                // max(S, nM-n0)
   float* sh_gamma = reinterpret_cast<float*>(sh_norm + max(S, a.nM - a.n0));         // S
@@ -1076,7 +1076,7 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
                                  sh_flag);
   }
   __syncthreads();
-  if (FAST && a.staged) {
+  if constexpr (STG) {
     if (SYM && *sh_flag)
       fwd_steps_split<KH, R, SYM, FAST, true, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
     else
@@ -1090,6 +1090,20 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
     fwd_steps_split<KH, R, SYM, FAST, false, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
   else
     fwd_steps<KH, R, SYM, FAST, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane, warp, nwarps);
+}
+
+// Forward tile kernel (inference, checkpoints): register budget for fwd_min_blocks CTAs per SM.
+template <int KH, int R, bool SYM, bool FAST>
+__global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_tile_kernel(const FwdArgs a) {
+  fwd_tile_body<KH, R, SYM, FAST, false>(a);
+}
+
+// Store-all forward (training): the smem stage limits residency anyway, so the register budget
+// is raised to 1-2 CTAs per SM (no spills in the step loop).
+template <int KH, int R, bool SYM>
+__global__ void __launch_bounds__(fwd_max_threads(KH), fwd_max_threads(KH) > 256 ? 1 : 2)
+    fwd_store_kernel(const FwdArgs a) {
+  fwd_tile_body<KH, R, SYM, true, true>(a);
 }
 
 struct BwdArgs {
