@@ -197,9 +197,9 @@ size_t fwd_smem(int kh, bool sym, int steps, int nthreads = 1024, int nnorm = 0,
 
 // Store-all reverse kernel shared memory (mirrors the carve-up in rev_tile_kernel).
 size_t rev_smem(int kh, bool sym, int steps, int M) {
-  const int NT = ldbp::kRevThreads, nw = NT / 32;
+  const int NT = ldbp::rev_threads(kh), nw = NT / 32;
   const int V = 1 + 2 * ntaps_used(kh, sym);
-  size_t s = 16;                                                      // split-barrier mbarrier
+  size_t s = 16 * (size_t)nw;                                         // split-barrier mbarriers
   s += sizeof(float2) * 2 * (size_t)kRevR * NT;                       // u window copies
   s += sizeof(float2) * 4 * (size_t)std::max(kh, 1) * NT;             // ga edges
   s += sizeof(ldbp::TapP) * (size_t)steps * ntaps_used(kh, sym);      // adjoint taps
@@ -377,7 +377,7 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const int M = d->steps;
-  const int nthr = ldbp::kRevThreads;
+  const int nthr = ldbp::rev_threads(kh);
   p.V = 1 + 2 * ntaps_used(kh, sym);
   // cost model in step units: a launch of S steps costs S * window / (window - 2*S*kh) plus a
   // fixed ~2 steps (prologue: staging, first load, seed); pick the number of launches minimising
@@ -407,7 +407,7 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
     occ = rev_occupancy(get_rev(kh, sym, !(d->flags & LDBP_PRECISE)), nthr, rev_smem(kh, sym, p.Cr, M));
   }
   p.tile = plan_tiles(d->batch, d->n, p.Cr * kh, kRevR, nthr, occ, sms, /*align_r=*/true);
-  p.tile.nthreads = nthr;  // the kernel's layout is compiled for exactly kRevThreads threads
+  p.tile.nthreads = nthr;  // the kernel's layout is compiled for exactly rev_threads(kh) threads
   return p;
 }
 

@@ -895,14 +895,17 @@ __device__ __forceinline__ void step_range(const f2x (&u)[R], const f2x (&hl)[KH
 constexpr int kFwdUnroll = LDBP_FWD_UNROLL;
 // mbarrier helpers for the split (arrive early / wait late) step barrier.
 __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) { mbar_arrive(bar); }
+#ifndef LDBP_MBAR_SUSPEND_NS
+#define LDBP_MBAR_SUSPEND_NS 100000  // try_wait suspend-time hint: sleep until the phase completes
+#endif
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
   unsigned ok;
   do {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(LDBP_MBAR_SUSPEND_NS)
         : "memory");
   } while (!ok);
 }

@@ -54,10 +54,17 @@ __device__ __forceinline__ const float2* rev_src(const RevArgs& a, int i) {
   return i == 0 ? a.x : a.act + (int64_t)(i - 1) * a.act_stride;
 }
 
-#ifndef LDBP_REV_NTHR
-#define LDBP_REV_NTHR 256  // threads per reverse CTA (compile time: every smem offset is an immediate)
+#ifndef LDBP_NB_WAIT
+#define LDBP_NB_WAIT 0  // split step barrier: 1 = wait only for the neighbouring warps, 0 = CTA-wide phase
 #endif
-constexpr int kRevThreads = LDBP_REV_NTHR;
+// Threads per reverse CTA, compile time (every smem offset is an immediate).  Small CTAs (4 warps,
+// 4 CTAs/SM at 128 registers) keep the per-step barrier among few warps (measured on C3: 128
+// threads 2.05 ms, 256: 2.20, 96: 2.23); Kh <= 1 has tiny halos and prefers 64 (C5: 18.7 vs 19.3).
+#ifdef LDBP_REV_NTHR
+__host__ __device__ constexpr int rev_threads(int) { return LDBP_REV_NTHR; }
+#else
+__host__ __device__ constexpr int rev_threads(int kh) { return kh <= 1 ? 64 : 128; }
+#endif
 
 // Shared-memory window copy: sample k of thread t at f2x index ((k >> 1) * NT + t) * 2 + (k & 1)
 // (16-byte pairs, lane-consecutive -> conflict-free LDS.128 / LDGSTS.128).
@@ -133,7 +140,7 @@ __device__ __forceinline__ void rev_range(const f2x (&g)[R], const f2x (&gl)[KH 
                                           f2x (&ng)[R], uint32_t own, float gmn, float& dgam_next) {
   if constexpr (S0 < SE) {
     constexpr int s = S0;
-    const f2x us = ub_mine[(s >> 1) * 2 * kRevThreads + (s & 1)];
+    const f2x us = ub_mine[(s >> 1) * 2 * rev_threads(KH) + (s & 1)];
     const bool mine = !MASKED || ((own >> s) & 1u);
     const f2x ux = bcast(lof(us)), uy = bcast(hif(us));
     f2x acc;
@@ -171,7 +178,7 @@ __device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub
                                          const TapP* __restrict__ hs_sm, uint32_t own, float gmn,
                                          float (&dh)[2 * (SYM ? KH + 1 : 2 * KH + 1)], float& dgam_next) {
   constexpr int NTU = ntaps_used<SYM, KH>();
-  constexpr int NT = kRevThreads;
+  constexpr int NT = rev_threads(KH);
   constexpr int KI = KH < R - KH ? KH : R / 2;  // interior [KI, R-KI)
   TapP hs[NTU];
 #pragma unroll
@@ -184,7 +191,20 @@ __device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub
   for (int j = 0; j < (KH > 0 ? KH : 1); ++j) gl[j] = gr[j] = 0ull;
   rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, KI, R - KI>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn, dgam_next);
   if constexpr (KH > 0) {
-    mbar_wait_parity(bar, parity);
+    if constexpr (LDBP_NB_WAIT) {
+      // neighbour-only wait: within the warp the edges are ordered by the publisher's __syncwarp;
+      // only lane 0 (needs warp w-1's tail) and lane 31 (needs warp w+1's head) wait
+      // bar[2][NW]: phase ph uses bar[ph & 1][w]; each barrier advances every other step, so a
+      // neighbour can be at most one phase of that barrier ahead: parity (ph >> 1) & 1 is exact.
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      uint64_t* b = bar + (parity & 1) * (NT / 32);
+      const unsigned par2 = (parity >> 1) & 1;
+      if (lane == 0 && warp > 0) mbar_wait_parity(b + warp - 1, par2);
+      if (lane == 31 && warp < NT / 32 - 1) mbar_wait_parity(b + warp + 1, par2);
+      __syncwarp();
+    } else {
+      mbar_wait_parity(bar, parity);
+    }
 #pragma unroll
     for (int j = 0; j < KH; ++j) {
       gl[j] = left_edge[eoff + (KH + j) * NT];
@@ -205,7 +225,7 @@ __device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub
 template <int KH, int R, bool SYM, bool FAST, bool NORM>
 __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, int64_t e0, int64_t fast_off,
                                          uint32_t own, int lane, int warp) {
-  constexpr int NT = kRevThreads, NW = NT / 32;
+  constexpr int NT = rev_threads(KH), NW = NT / 32;
   constexpr int NTU = ntaps_used<SYM, KH>();
   constexpr int V = 1 + 2 * NTU;
   constexpr int KE = KH > 0 ? KH : 1;
@@ -282,7 +302,7 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
         my_edge[eo + (KH + j) * NT] = g[R - KH + j];   // tail
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar);
+      if (lane == 0) mbar_arrive(LDBP_NB_WAIT ? bar + (ph & 1) * NW + warp : bar);
     }
   };
   publish(0);
@@ -302,17 +322,17 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
     const float gmn = l > s0 ? sm.gamma[li - 1] : 0.f;
     if (l > s0) {
       if (full)
-        rev_step<KH, R, SYM, FAST, NORM, false, true>(g, ub_mine, left_edge, right_edge, eoff, bar, ph & 1, hs_sm,
+        rev_step<KH, R, SYM, FAST, NORM, false, true>(g, ub_mine, left_edge, right_edge, eoff, bar, LDBP_NB_WAIT ? ph : (ph & 1), hs_sm,
                                                       own, gmn, dh, dgam_next);
       else
-        rev_step<KH, R, SYM, FAST, NORM, true, true>(g, ub_mine, left_edge, right_edge, eoff, bar, ph & 1, hs_sm,
+        rev_step<KH, R, SYM, FAST, NORM, true, true>(g, ub_mine, left_edge, right_edge, eoff, bar, LDBP_NB_WAIT ? ph : (ph & 1), hs_sm,
                                                      own, gmn, dh, dgam_next);
     } else {
       if (full)
-        rev_step<KH, R, SYM, FAST, NORM, false, false>(g, ub_mine, left_edge, right_edge, eoff, bar, ph & 1, hs_sm,
+        rev_step<KH, R, SYM, FAST, NORM, false, false>(g, ub_mine, left_edge, right_edge, eoff, bar, LDBP_NB_WAIT ? ph : (ph & 1), hs_sm,
                                                        own, gmn, dh, dgam_next);
       else
-        rev_step<KH, R, SYM, FAST, NORM, true, false>(g, ub_mine, left_edge, right_edge, eoff, bar, ph & 1, hs_sm,
+        rev_step<KH, R, SYM, FAST, NORM, true, false>(g, ub_mine, left_edge, right_edge, eoff, bar, LDBP_NB_WAIT ? ph : (ph & 1), hs_sm,
                                                       own, gmn, dh, dgam_next);
     }
     if (l > s0) publish(ph + 1);
@@ -377,17 +397,17 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
 }
 
 template <int KH, int R, bool SYM, bool FAST>
-__global__ void __launch_bounds__(kRevThreads, 65536 / (kRevThreads * 128)) rev_tile_kernel(const RevArgs a) {
+__global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * 128)) rev_tile_kernel(const RevArgs a) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   constexpr int V = 1 + 2 * NTU;
-  constexpr int NT = kRevThreads, NW = NT / 32;
+  constexpr int NT = rev_threads(KH), NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int S = a.s1 - a.s0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // carve-up (16-byte aligned regions; mirrored by rev_smem() on the host)
   RevSmem sm;
-  sm.bar = reinterpret_cast<uint64_t*>(smem_raw);                                    // 2 words
-  sm.ubuf = reinterpret_cast<f2x*>(smem_raw) + 2;                                    // 2*R*NT
+  sm.bar = reinterpret_cast<uint64_t*>(smem_raw);                                    // 2*NW words
+  sm.ubuf = reinterpret_cast<f2x*>(smem_raw) + 2 * NW;                               // 2*R*NT
   sm.edge = sm.ubuf + (size_t)2 * R * NT;                                            // 4*KH*NT
   sm.taps_adj = reinterpret_cast<TapP*>(sm.edge + (size_t)4 * (KH > 0 ? KH : 1) * NT);  // S*NTU
   sm.norm = reinterpret_cast<StepNorm*>(sm.taps_adj + S * NTU);                      // M
@@ -400,8 +420,10 @@ __global__ void __launch_bounds__(kRevThreads, 65536 / (kRevThreads * 128)) rev_
   const Span sp = make_span(e0, a.g);
   const int64_t fast_off = span_fast<R>(sp, a.g, e0) ? sp.b0 * a.g.n + (sp.q0 - a.g.H) : -1;
   const uint32_t own = owned_mask<R>(e0, a.g);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(sm.bar)), "r"(NT / 32) : "memory");
+  if (LDBP_NB_WAIT ? threadIdx.x < 2 * (NT / 32) : threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(sm.bar + threadIdx.x)),
+                 "r"(LDBP_NB_WAIT ? 1 : NT / 32)
+                 : "memory");
   }
   norm_range<KH, SYM>(a.taps, a.mask, a.T, 0, a.M, sm.norm, sm.flag);
   const bool norm = SYM && *sm.flag;
