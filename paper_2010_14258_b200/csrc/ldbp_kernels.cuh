@@ -822,14 +822,26 @@ struct FwdArgs {
 #ifndef LDBP_FWD_WIDE_THREADS
 #define LDBP_FWD_WIDE_THREADS 256
 #endif
+// register target per thread for each Kh (packed taps cost 4 registers each)
+__host__ __device__ constexpr int fwd_regs(int kh) { return kh <= 2 ? 64 : kh <= 5 ? 80 : 128; }
+#ifdef LDBP_FWD_NTHR  // tuning override: fixed CTA size, residency from the register target
+__host__ __device__ constexpr int fwd_max_threads(int) { return LDBP_FWD_NTHR; }
+#else
+// measured (C2 Kh=2: 128 thr 0.494 vs 512 thr 0.470 of peak; C5 store-all Kh=1: 10.3 vs 12.2 ms;
+// C3 Kh=4 and C4 Kh=7: 256 best)
 __host__ __device__ constexpr int fwd_max_threads(int kh) {
-  return LDBP_FWD_R > 16 ? 256 : (kh <= 2 ? 512 : kh <= 5 ? 256 : LDBP_FWD_WIDE_THREADS);
+  return LDBP_FWD_R > 16 ? 256 : (kh <= 2 ? 128 : kh <= 5 ? 256 : LDBP_FWD_WIDE_THREADS);
 }
+#endif
 // f2x elements of the store-all stage region: 2 buffers of ST runs of RS, plus run_off[ST] (int64)
 __host__ __device__ constexpr int fwd_stage_elems(int kh, int r) { return fwd_max_threads(kh) * (2 * (r + 2) + 1); }
+#ifdef LDBP_FWD_NTHR
+__host__ __device__ constexpr int fwd_min_blocks(int kh) { return 65536 / (LDBP_FWD_NTHR * fwd_regs(kh)); }
+#else
 __host__ __device__ constexpr int fwd_min_blocks(int kh) {
-  return kh <= 2 ? 2 : kh <= 4 ? 3 : (LDBP_FWD_WIDE_THREADS >= 512 && kh >= 6) ? 1 : 2;
+  return kh <= 2 ? 8 : kh <= 4 ? 3 : (LDBP_FWD_WIDE_THREADS >= 512 && kh >= 6) ? 1 : 2;
 }
+#endif
 
 template <int KH, int R, bool SYM, bool FAST, bool NORM>
 __device__ __forceinline__ void fwd_steps(const FwdArgs& a, f2x (&u)[R], const TapP* sh_taps, const float* sh_gamma,
@@ -1104,7 +1116,7 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
 // Store-all forward (training): the smem stage limits residency anyway, so the register budget
 // is raised to 1-2 CTAs per SM (no spills in the step loop).
 template <int KH, int R, bool SYM>
-__global__ void __launch_bounds__(fwd_max_threads(KH), fwd_max_threads(KH) > 256 ? 1 : 2)
+__global__ void __launch_bounds__(fwd_max_threads(KH), 65536 / (fwd_max_threads(KH) * 128))
     fwd_store_kernel(const FwdArgs a) {
   fwd_tile_body<KH, R, SYM, true, true>(a);
 }
