@@ -207,6 +207,7 @@ size_t rev_smem(int kh, bool sym, int steps, int M) {
   s += sizeof(float) * (size_t)((steps * nw * V + 3) & ~3);           // per-warp partials, all steps
   s += sizeof(float) * (size_t)((nw + 3) & ~3);                       // loss partials
   s += sizeof(float) * (size_t)((steps + 3) & ~3) + 16;               // gamma_hat + flag
+  s += sizeof(int) * (size_t)steps;                                   // active taps per step
   return s;
 }
 

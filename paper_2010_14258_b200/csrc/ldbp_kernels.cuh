@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "ldbp_f32x2.cuh"
 
 #ifndef LDBP_FWD_R
@@ -499,7 +501,9 @@ __device__ __forceinline__ f2x tmul(const TapP& t, f2x s) { return fma2(bcast(lo
 #ifndef LDBP_FIR_CHAINS
 #define LDBP_FIR_CHAINS 1  // 1: one accumulation chain per output (R outputs give the ILP); 2: split
 #endif
-template <int KH, int R, bool SYM, int K, bool NORM = false>
+// KJ <= KH: number of active folded taps (per-step variable filter length, §8(f) NEXT-3: the
+// outer taps j > KJ are zero, so skipping them is exact).
+template <int KH, int R, bool SYM, int K, bool NORM = false, int KJ = KH>
 __device__ __forceinline__ f2x fir_at(const f2x (&u)[R], const f2x (&hl)[KH > 0 ? KH : 1],
                                       const f2x (&hr)[KH > 0 ? KH : 1], const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1]) {
   if constexpr (LDBP_FIR_CHAINS == 1) {
@@ -508,11 +512,11 @@ __device__ __forceinline__ f2x fir_at(const f2x (&u)[R], const f2x (&hl)[KH > 0 
       // h0-normalised folded FIR: h_0 = 1, a_k = u_k + sum_j h_j (u_{k-j} + u_{k+j})
       acc = u[K];
 #pragma unroll
-      for (int j = 1; j <= KH; ++j) acc = tmac(acc, hs[j], add2(LDBP_WIN(u, hl, hr, K - j), LDBP_WIN(u, hl, hr, K + j)));
+      for (int j = 1; j <= KJ; ++j) acc = tmac(acc, hs[j], add2(LDBP_WIN(u, hl, hr, K - j), LDBP_WIN(u, hl, hr, K + j)));
     } else if constexpr (SYM) {
       acc = tmul(hs[0], u[K]);
 #pragma unroll
-      for (int j = 1; j <= KH; ++j) acc = tmac(acc, hs[j], add2(LDBP_WIN(u, hl, hr, K - j), LDBP_WIN(u, hl, hr, K + j)));
+      for (int j = 1; j <= KJ; ++j) acc = tmac(acc, hs[j], add2(LDBP_WIN(u, hl, hr, K - j), LDBP_WIN(u, hl, hr, K + j)));
     } else {
       acc = tmul(hs[0], LDBP_WIN(u, hl, hr, K + KH));
 #pragma unroll
@@ -888,16 +892,29 @@ __device__ __forceinline__ void fwd_steps(const FwdArgs& a, f2x (&u)[R], const T
 
 // FIR + Kerr for outputs k in [K, KE), with the Kerr of output k-D issued after the FIR of output
 // k (MUFU work interleaved with FMA-pipe work); the last D Kerrs are flushed at the end.
-template <int KH, int R, bool SYM, bool FAST, bool NORM, int KB, int KE, int K = KB>
+template <int KH, int R, bool SYM, bool FAST, bool NORM, int KB, int KE, int KJ = KH, int K = KB>
 __device__ __forceinline__ void step_range(const f2x (&u)[R], const f2x (&hl)[KH > 0 ? KH : 1],
                                            const f2x (&hr)[KH > 0 ? KH : 1],
                                            const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1], float gm, f2x (&acc)[R],
                                            f2x (&out)[R]) {
   constexpr int D = LDBP_PIPE_D;
   if constexpr (K < KE + D) {
-    if constexpr (K < KE) acc[K] = fir_at<KH, R, SYM, K, NORM>(u, hl, hr, hs);
+    if constexpr (K < KE) acc[K] = fir_at<KH, R, SYM, K, NORM, KJ>(u, hl, hr, hs);
     if constexpr (K - D >= KB && K - D < KE) out[K - D] = kerr<FAST>(acc[K - D], gm);
-    step_range<KH, R, SYM, FAST, NORM, KB, KE, K + 1>(u, hl, hr, hs, gm, acc, out);
+    step_range<KH, R, SYM, FAST, NORM, KB, KE, KJ, K + 1>(u, hl, hr, hs, gm, acc, out);
+  }
+}
+
+// Per-step active half-length dispatch (NEXT-3): variants for KJ = KH, KH-1, KH-2 (smaller KJ
+// runs the KH-2 variant on zero taps: still exact); bounded code size.
+template <int KH, typename F>
+__device__ __forceinline__ void dispatch_kj(int kj, F&& f) {
+  if (KH < 1 || kj >= KH) {
+    f(std::integral_constant<int, KH>{});
+  } else if (kj == KH - 1) {
+    f(std::integral_constant<int, (KH >= 1 ? KH - 1 : 0)>{});
+  } else {
+    f(std::integral_constant<int, (KH >= 2 ? KH - 2 : 0)>{});
   }
 }
 
@@ -937,7 +954,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity)
 template <int R>
 __device__ __forceinline__ constexpr int stage_rs() { return R + 2; }
 
-template <int KH, int R, bool SYM, bool FAST, bool NORM, bool STG>
+template <int KH, int R, bool SYM, bool FAST, bool NORM, bool STG, bool VARK = false>
 __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], const TapP* sh_taps,
                                                 const float* sh_gamma, const StepNorm* sh_norm, f2x* sh_edge,
                                                 uint64_t* bar, const StoreMap& smap, int64_t e0, int lane) {
@@ -999,7 +1016,18 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
     for (int j = 0; j < NTU; ++j) hs[j] = sh_taps[s * NTU + j];
     const float gm = sh_gamma[s];
     f2x acc[R], nu[R];
-    step_range<KH, R, SYM, FAST, NORM, KI, R - KI>(u, hl, hr, hs, gm, acc, nu);
+    // active folded taps of this step (outermost non-zero tap; uniform over the CTA)
+    int kj = KH;
+    if constexpr (VARK && SYM && NORM && KH >= 1) {
+      kj = 0;
+#pragma unroll
+      for (int j = 1; j <= KH; ++j)
+        if (lof(hs[j].a) != 0.f || hif(hs[j].a) != 0.f) kj = j;
+    }
+    auto do_step = [&](auto kjc) {
+    constexpr int KJ = decltype(kjc)::value;
+    constexpr int KI2 = KJ < R - KJ ? KJ : R / 2;
+    step_range<KH, R, SYM, FAST, NORM, KI2, R - KI2, KJ>(u, hl, hr, hs, gm, acc, nu);
     if constexpr (STG) {
       mbar_wait_parity(bar, s & 1);
       const f2x* st = stage + (s & 1) * ST * RS;
@@ -1028,8 +1056,13 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
         hr[j] = right_edge[off + j * ST];
       }
     }
-    step_range<KH, R, SYM, FAST, NORM, 0, KI>(u, hl, hr, hs, gm, acc, nu);
-    step_range<KH, R, SYM, FAST, NORM, R - KI, R>(u, hl, hr, hs, gm, acc, nu);
+    step_range<KH, R, SYM, FAST, NORM, 0, KI2, KJ>(u, hl, hr, hs, gm, acc, nu);
+    step_range<KH, R, SYM, FAST, NORM, R - KI2, R, KJ>(u, hl, hr, hs, gm, acc, nu);
+    };
+    if constexpr (VARK && SYM && NORM && FAST && KH >= 1)
+      dispatch_kj<KH>(kj, do_step);
+    else
+      do_step(std::integral_constant<int, KH>{});
 #pragma unroll
     for (int k = 0; k < R; ++k) u[k] = nu[k];
     const int gs = a.s0 + s + 1;  // global step count reached
@@ -1091,15 +1124,34 @@ __device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
                                  sh_flag);
   }
   __syncthreads();
+  // NEXT-3: does any step of this launch have zero outer taps?  (then the per-step active-length
+  // loop runs; otherwise the plain loop, identical code to the unpruned kernel)
+  bool pruned = false;
+  if constexpr (SYM && FAST && KH >= 1) {
+    for (int i = 0; i < S; ++i) {
+      const TapP t = sh_taps[i * NTU + KH];
+      pruned |= (lof(t.a) == 0.f && hif(t.a) == 0.f);
+    }
+  }
   if constexpr (STG) {
-    if (SYM && *sh_flag)
-      fwd_steps_split<KH, R, SYM, FAST, true, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
-    else
+    if (SYM && *sh_flag) {
+      if (pruned)
+        fwd_steps_split<KH, R, SYM, FAST, true, true, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0,
+                                                            lane);
+      else
+        fwd_steps_split<KH, R, SYM, FAST, true, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
+    } else {
       fwd_steps_split<KH, R, SYM, FAST, false, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
+    }
   } else if (SYM && *sh_flag)
-    if (LDBP_FWD_SPLIT)
-      fwd_steps_split<KH, R, SYM, FAST, true, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);
-    else
+    if (LDBP_FWD_SPLIT) {
+      if (pruned)
+        fwd_steps_split<KH, R, SYM, FAST, true, false, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0,
+                                                             lane);
+      else
+        fwd_steps_split<KH, R, SYM, FAST, true, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0,
+                                                       lane);
+    } else
       fwd_steps<KH, R, SYM, FAST, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane, warp, nwarps);
   else if (LDBP_FWD_SPLIT)
     fwd_steps_split<KH, R, SYM, FAST, false, false>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0, lane);

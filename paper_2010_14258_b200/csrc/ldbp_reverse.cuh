@@ -54,6 +54,12 @@ __device__ __forceinline__ const float2* rev_src(const RevArgs& a, int i) {
   return i == 0 ? a.x : a.act + (int64_t)(i - 1) * a.act_stride;
 }
 
+#ifndef LDBP_REV_VARK
+#define LDBP_REV_VARK 0  // per-step active tap length in the reverse (off: the alternating code
+                         // variants cost more in instruction fetch than the skipped taps save)
+#endif
+template <int KH, bool SYM, bool NORM, bool FAST>
+__device__ __forceinline__ constexpr bool rev_vark() { return LDBP_REV_VARK && SYM && NORM && FAST && KH >= 1; }
 #ifndef LDBP_NB_WAIT
 #define LDBP_NB_WAIT 0  // split step barrier: 1 = wait only for the neighbouring warps, 0 = CTA-wide phase
 #endif
@@ -100,6 +106,7 @@ struct RevSmem {
   TapP* taps_adj;   // [S][NTU]
   StepNorm* norm;   // [M] (global normalisation, step-indexed)
   float* gamma;     // [S] gamma_hat
+  int* kj;          // [S] active folded taps per step (outermost unmasked tap; KH without a mask)
   int* flag;
   float* red;       // [S][NW][V] per-warp partials of every step (reduced once at the end)
   float* lred;      // [NW] loss partials
@@ -132,7 +139,8 @@ __device__ __forceinline__ void nl_adjoint(f2x& gk, f2x vk, float gm, float gm2,
 //                                                     by exactly one CTA, so the sums agree)
 // conj(u) P = ux P - j uy P is accumulated as A_j += ux P, B_j += uy P (broadcast operands only);
 // dh_j = A_j - j B_j once per step.  The NL adjoint of step l-1 follows on each fresh g_s (NL).
-template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL, int SB, int SE, int S0 = SB>
+template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL, int SB, int SE, int KJ = KH,
+          int S0 = SB>
 __device__ __forceinline__ void rev_range(const f2x (&g)[R], const f2x (&gl)[KH > 0 ? KH : 1],
                                           const f2x (&gr)[KH > 0 ? KH : 1], const f2x* __restrict__ ub_mine,
                                           const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1],
@@ -149,7 +157,7 @@ __device__ __forceinline__ void rev_range(const f2x (&g)[R], const f2x (&gl)[KH 
       acc = NORM ? g0 : tmul(hs[0], g0);
       if (mine) { A[0] = fma2(ux, g0, A[0]); Bq[0] = fma2(uy, g0, Bq[0]); }
 #pragma unroll
-      for (int j = 1; j <= KH; ++j) {
+      for (int j = 1; j <= KJ; ++j) {
         const f2x P = add2(LDBP_WIN(g, gl, gr, s - j), LDBP_WIN(g, gl, gr, s + j));
         acc = tmac(acc, hs[j], P);
         if (mine) { A[j] = fma2(ux, P, A[j]); Bq[j] = fma2(uy, P, Bq[j]); }
@@ -165,21 +173,21 @@ __device__ __forceinline__ void rev_range(const f2x (&g)[R], const f2x (&gl)[KH 
     }
     if constexpr (NL) nl_adjoint<FAST, MASKED>(acc, us, gmn, 2.f * gmn, (own >> s) & 1u, dgam_next);
     ng[s] = acc;
-    rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, SB, SE, S0 + 1>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn,
-                                                                  dgam_next);
+    rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, SB, SE, KJ, S0 + 1>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn,
+                                                                      dgam_next);
   }
 }
 
 // One full reverse step with the split barrier: interior outputs (no halo needed) before the
 // wait on the ga-edge mbarrier phase, boundary outputs after it.
-template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL>
+template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL, int KJ = KH>
 __device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub_mine, const f2x* left_edge,
                                          const f2x* right_edge, int eoff, uint64_t* bar, unsigned parity,
                                          const TapP* __restrict__ hs_sm, uint32_t own, float gmn,
                                          float (&dh)[2 * (SYM ? KH + 1 : 2 * KH + 1)], float& dgam_next) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   constexpr int NT = rev_threads(KH);
-  constexpr int KI = KH < R - KH ? KH : R / 2;  // interior [KI, R-KI)
+  constexpr int KI = KJ < R - KJ ? KJ : R / 2;  // interior [KI, R-KI)
   TapP hs[NTU];
 #pragma unroll
   for (int j = 0; j < NTU; ++j) hs[j] = hs_sm[j];
@@ -189,7 +197,8 @@ __device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub
   f2x gl[KH > 0 ? KH : 1], gr[KH > 0 ? KH : 1];
 #pragma unroll
   for (int j = 0; j < (KH > 0 ? KH : 1); ++j) gl[j] = gr[j] = 0ull;
-  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, KI, R - KI>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn, dgam_next);
+  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, KI, R - KI, KJ>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn,
+                                                                 dgam_next);
   if constexpr (KH > 0) {
     if constexpr (LDBP_NB_WAIT) {
       // neighbour-only wait: within the warp the edges are ordered by the publisher's __syncwarp;
@@ -211,8 +220,9 @@ __device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub
       gr[j] = right_edge[eoff + j * NT];
     }
   }
-  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, 0, KI>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn, dgam_next);
-  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, R - KI, R>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn, dgam_next);
+  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, 0, KI, KJ>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn, dgam_next);
+  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, R - KI, R, KJ>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn,
+                                                               dgam_next);
 #pragma unroll
   for (int j = 0; j < NTU; ++j) {
     dh[2 * j] = lof(A[j]) + hif(Bq[j]);
@@ -321,7 +331,17 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
     const TapP* hs_sm = sm.taps_adj + li * NTU;
     const float gmn = l > s0 ? sm.gamma[li - 1] : 0.f;
     if (l > s0) {
-      if (full)
+      if (rev_vark<KH, SYM, NORM, FAST>() && full) {
+        // active folded taps of this step: the outermost unmasked tap (masked taps are pruned:
+        // zero value and zero gradient; unmasked zero-valued taps still need their gradient)
+        if constexpr (rev_vark<KH, SYM, NORM, FAST>())
+          dispatch_kj<KH>(sm.kj[li], [&](auto kjc) {
+            constexpr int KJ = decltype(kjc)::value;
+            rev_step<KH, R, SYM, FAST, NORM, false, true, KJ>(g, ub_mine, left_edge, right_edge, eoff, bar,
+                                                              LDBP_NB_WAIT ? ph : (ph & 1), hs_sm, own, gmn, dh,
+                                                              dgam_next);
+          });
+      } else if (full)
         rev_step<KH, R, SYM, FAST, NORM, false, true>(g, ub_mine, left_edge, right_edge, eoff, bar, LDBP_NB_WAIT ? ph : (ph & 1), hs_sm,
                                                       own, gmn, dh, dgam_next);
       else
@@ -415,6 +435,7 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * 12
   sm.lred = sm.red + ((S * NW * V + 3) & ~3);                                        // NW
   sm.gamma = sm.lred + ((NW + 3) & ~3);                                              // S
   sm.flag = reinterpret_cast<int*>(sm.gamma + ((S + 3) & ~3));
+  sm.kj = sm.flag + 4;                                                               // S
 
   const int64_t e0 = thread_e0(a.g, R);
   const Span sp = make_span(e0, a.g);
@@ -429,6 +450,16 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * 12
   const bool norm = SYM && *sm.flag;
   stage_range<KH, SYM, false, true>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, 0, nullptr, sm.taps_adj, sm.gamma,
                                     sm.norm, norm);
+  for (int i = threadIdx.x; i < S; i += NT) {
+    int kj = KH;
+    if (a.mask && SYM) {
+      const uint8_t* mrow = a.mask + (int64_t)(a.s0 + i) * a.T + KH;  // centre tap
+      kj = 0;
+      for (int j = 1; j <= KH; ++j)
+        if (mrow[j] || mrow[-j]) kj = j;
+    }
+    sm.kj[i] = kj;
+  }
   __syncthreads();
   if (norm)
     rev_body<KH, R, SYM, FAST, true>(a, sm, e0, fast_off, own, lane, warp);

@@ -388,3 +388,45 @@ def test_train_step_cuda_graph_capture(P):
         if it == 0:
             assert torch.equal(b_e, buf)
             assert torch.equal(eager.master, graphed.master)
+
+
+# ---- §8(f) NEXT-3: per-step variable filter lengths (pruned outer taps are not computed) ----
+def pruned_model(seed, M, T, kh_steps):
+    """Symmetric taps whose step i keeps only |j| <= kh_steps[i] (progressive pruning
+    removes the outermost pair; Example 2's models alternate lengths)."""
+    taps, gamma = model(seed, M, T, True)
+    kh = (T - 1) // 2
+    mask = np.ones((M, T), np.uint8)
+    for i, k in enumerate(kh_steps):
+        for j in range(k + 1, kh + 1):
+            mask[i, kh + j] = mask[i, kh - j] = 0
+    return taps * mask, gamma, mask
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("B,n,M,T,kh_steps", [
+    (3, 4096, 8, 9, [4, 3, 2, 1, 0, 4, 2, 3]),   # every active length incl. below KH-2 (fallback variant)
+    (2, 3000, 6, 5, [2, 1, 2, 1, 2, 1]),         # alternating 5/3 taps (Example 2 pattern)
+    (2, 2048, 5, 15, [7, 6, 5, 3, 7]),
+])
+def test_variable_tap_lengths(P, monkeypatch, mode, B, n, M, T, kh_steps):
+    monkeypatch.setenv("LDBP_BWD_MODE", mode)
+    monkeypatch.setenv("LDBP_STORE_ALL_MIN_SAMPLES", "0")
+    taps, gamma, mask = pruned_model(91, M, T, kh_steps)
+    x = li.gaussian_blocks(91, range(B), n, 1e-3)
+    tgt = li.gaussian_blocks(91, range(B), n, 1e-3, purpose="target")
+    # forward: zero outer taps (no mask argument) -> skipped per step, result as the oracle's
+    y = P.ldbp_forward(dev(x), dev(taps), dev(gamma, np.float32)).cpu().numpy()
+    yr = O.forward(r32(x), r32(taps), r32(gamma))
+    for b in range(B):
+        assert rel(y[b], yr[b]) <= OUT_TOL, b
+    # training gradient with the pruning mask: masked taps get exactly 0, the rest match
+    buf = P.ldbp_loss_grad(dev(x), dev(tgt), dev(taps), dev(gamma, np.float32),
+                           mask=torch.from_numpy(mask).cuda()).cpu().numpy()
+    ref = O.loss_grad(r32(x), r32(tgt), r32(taps), r32(gamma), mask=mask, symmetric=True)
+    assert abs(buf[0] - ref[0]) <= OUT_TOL * ref[0]
+    assert rel(buf[1:1 + M], ref[1:1 + M]) <= GRAD_TOL
+    dt, rdt = buf[1 + M:].reshape(M, T, 2), ref[1 + M:].reshape(M, T, 2)
+    for i in range(M):
+        assert rel(dt[i], rdt[i]) <= GRAD_TOL, i
+    assert np.all(dt[mask == 0] == 0)
