@@ -158,6 +158,40 @@ int ldbp_train_step(const ldbp_dims* d, const void* x, const void* target,
                     double* buf, void* ws, size_t ws_bytes, void* cuda_stream);
 
 /*
+ * Receiver-chain symbol loss (the paper's training objective and figure
+ * of merit).  Per block b of n samples at sps samples/symbol (K = n/sps symbols):
+ *   s_tilde = M y / sqrt(P_b)      M: decimating circular FIR, real even taps h_mf[m + L],
+ *                                  m in [-L, L]  (s_tilde_k = sum_m h[m] y_{(k sps - m) mod n};
+ *                                  Eq. (12), reading G19: the periodic RRC impulse
+ *                                  response truncated to +-L samples)
+ *   phi_b = arg(s^H s_tilde)        genie phase
+ *   errs_b = sum_k |e^{-j phi_b} s_tilde_k - s_k|^2   (symbol MSE x K; Eq. (13))
+ * and gy = dL/dy of L = sum_b errs_b (full chain rule incl. the phase).
+ *   y, gy    [B][n] complex64;  symbols [B][K] complex64 (unit power);  power_w [B] float32 (W)
+ *   h_mf     [2L+1] float32, 0 <= L <= 256, 2L+1 <= n;  sps in [1, 4], n % sps == 0
+ *   errs     [B] float64 out;  gy may be NULL (loss only)
+ * Deterministic (fixed-order fp64 block reductions).  Workspace: ldbp_rx_workspace_bytes.
+ */
+int ldbp_rx_workspace_bytes(int64_t batch, int64_t n, int32_t sps, size_t* bytes);
+int ldbp_rx_loss_grad(int64_t batch, int64_t n, int32_t sps, int32_t mf_half, const void* y,
+                      const void* symbols, const float* power_w, const float* h_mf, double* errs,
+                      void* gy_or_null, void* ws, size_t ws_bytes, void* cuda_stream);
+
+/*
+ * ldbp_rx_train_grad — training gradient of the receiver-chain loss through LDBP:
+ *   buf = [sum_b errs_b | d/d gamma' [M] | d/d taps [M][T][2]]   (UNscaled, this device's blocks;
+ *   with tap_mask as in ldbp_loss_grad), y = f_theta(x) (Eq. 7).  One storing forward, the two
+ *   receiver kernels, one reverse sweep seeded with dL/dy (store-all schedule; the segment
+ *   schedule re-runs the forward for its checkpoints).  Data parallel: all-reduce buf, then
+ *   ldbp_adam_update with n_global = total symbols.  Workspace: ldbp_rx_train_workspace_bytes.
+ */
+int ldbp_rx_train_workspace_bytes(const ldbp_dims* d, int32_t sps, size_t* bytes);
+int ldbp_rx_train_grad(const ldbp_dims* d, const void* x, const void* symbols, const float* power_w,
+                       int32_t sps, int32_t mf_half, const float* h_mf, const void* taps,
+                       const float* gamma, const uint8_t* tap_mask_or_null, double* buf,
+                       void* ws, size_t ws_bytes, void* cuda_stream);
+
+/*
  * Launch tracing (profiling aid; off by default; per calling thread).
  * ldbp_trace_begin(capacity) makes every kernel launch of later calls on this thread be
  * bracketed by two CUDA events recorded on the call's stream (events are created here, not
@@ -172,7 +206,8 @@ typedef enum ldbp_kernel_kind {
   LDBP_K_BACKWARD = 2,  /* backward segment kernel (rows a5-a8, recompute + adjoint) */
   LDBP_K_REDUCE = 3,    /* fp64 partial reduction (row a8)                         */
   LDBP_K_ADAM = 4,      /* Adam + mask (row a10)                                   */
-  LDBP_K_REVERSE = 5    /* store-all reverse tile kernel (rows a5, a6, a8)         */
+  LDBP_K_REVERSE = 5,   /* store-all reverse tile kernel (rows a5, a6, a8)         */
+  LDBP_K_RX = 6         /* receiver-chain loss kernels (NEXT-1)                    */
 } ldbp_kernel_kind;
 
 typedef struct ldbp_trace_record {

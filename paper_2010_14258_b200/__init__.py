@@ -13,6 +13,8 @@ from .api import (  # noqa: F401
     ldbp_backward,
     ldbp_forward,
     ldbp_loss_grad,
+    ldbp_rx_loss_grad,
+    ldbp_rx_train_grad,
     ldbp_train_step,
     make_dims,
     workspace_bytes,

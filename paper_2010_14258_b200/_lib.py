@@ -29,9 +29,13 @@ EXPORTED = (
     "ldbp_train_step",
     "ldbp_trace_begin",
     "ldbp_trace_end",
+    "ldbp_rx_workspace_bytes",
+    "ldbp_rx_loss_grad",
+    "ldbp_rx_train_workspace_bytes",
+    "ldbp_rx_train_grad",
 )
 
-K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM, K_REVERSE = 1, 2, 3, 4, 5
+K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM, K_REVERSE, K_RX = 1, 2, 3, 4, 5, 6
 
 
 class LdbpDims(ctypes.Structure):
@@ -84,6 +88,13 @@ def _load():
                                            ctypes.c_size_t, P]),
         "ldbp_trace_begin": (ctypes.c_int, [ctypes.c_int]),
         "ldbp_trace_end": (ctypes.c_int, [ctypes.POINTER(TraceRecord), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+        "ldbp_rx_workspace_bytes": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                                   ctypes.POINTER(ctypes.c_size_t)]),
+        "ldbp_rx_loss_grad": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, P, P, P,
+                                             P, P, P, P, ctypes.c_size_t, P]),
+        "ldbp_rx_train_workspace_bytes": (ctypes.c_int, [D, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]),
+        "ldbp_rx_train_grad": (ctypes.c_int, [D, P, P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P,
+                                              ctypes.c_size_t, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

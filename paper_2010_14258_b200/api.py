@@ -217,6 +217,52 @@ def ldbp_train_step(state: TrainState, x, target, *, buf=None, ws=None, stream=N
     return out
 
 
+def _check_rx(y_like, symbols, power_w, h_mf, sps):
+    B, n = y_like.shape
+    if n % sps:
+        raise ValueError(f"n = {n} is not a multiple of sps = {sps}")
+    _need(symbols, "symbols", torch.complex64, (B, n // sps))
+    _need(power_w, "power_w", torch.float32, (B,))
+    _need(h_mf, "h_mf", torch.float32)
+    if h_mf.dim() != 1 or h_mf.numel() % 2 == 0:
+        raise ValueError("h_mf must be 1-D with an odd number of taps (2L+1)")
+    return B, n, (h_mf.numel() - 1) // 2
+
+
+def ldbp_rx_loss_grad(y, symbols, power_w, h_mf, *, sps=2, need_grad=True, ws=None, stream=None):
+    """Receiver-chain symbol loss (§8(f) NEXT-1): matched filter + downsample + genie phase.
+    Returns (errs float64 [B], gy complex64 [B][n] or None); L = sum(errs)."""
+    _need(y, "y", torch.complex64)
+    B, n, L = _check_rx(y, symbols, power_w, h_mf, sps)
+    errs = torch.empty(B, dtype=torch.float64, device=y.device)
+    gy = torch.empty_like(y) if need_grad else None
+    nb = ctypes.c_size_t(0)
+    check(lib.ldbp_rx_workspace_bytes(B, n, sps, ctypes.byref(nb)), "ldbp_rx_workspace_bytes")
+    w, nbv = _ws(y.device, int(nb.value), ws)
+    check(lib.ldbp_rx_loss_grad(B, n, sps, L, _p(y), _p(symbols), _p(power_w), _p(h_mf), _p(errs), _p(gy), _p(w),
+                                nbv, _stream_handle(stream)), "ldbp_rx_loss_grad")
+    return errs, gy
+
+
+def ldbp_rx_train_grad(x, symbols, power_w, h_mf, taps, gamma, *, sps=2, mask=None, symmetric=True, precise=False,
+                       buf=None, ws=None, stream=None):
+    """[sum errs | dgamma[M] | dtaps[M][T][2]] of the receiver-chain loss through LDBP (float64,
+    unscaled, this device's blocks only)."""
+    B, n, M, T = _check_model(x, taps, gamma)
+    _, _, L = _check_rx(x, symbols, power_w, h_mf, sps)
+    if mask is not None:
+        _need(mask, "mask", torch.uint8, (M, T))
+    d = make_dims(B, n, M, T, symmetric, precise)
+    out = torch.empty(1 + M + 2 * M * T, dtype=torch.float64, device=x.device) if buf is None else buf
+    nb = ctypes.c_size_t(0)
+    check(lib.ldbp_rx_train_workspace_bytes(ctypes.byref(d), sps, ctypes.byref(nb)), "ldbp_rx_train_workspace_bytes")
+    w, nbv = _ws(x.device, int(nb.value), ws)
+    check(lib.ldbp_rx_train_grad(ctypes.byref(d), _p(x), _p(symbols), _p(power_w), sps, L, _p(h_mf), _p(taps),
+                                 _p(gamma), _p(mask), _p(out), _p(w), nbv, _stream_handle(stream)),
+          "ldbp_rx_train_grad")
+    return out
+
+
 class trace:
     """Context manager: per-launch CUDA-event timing of libldbp kernels on this thread.
 

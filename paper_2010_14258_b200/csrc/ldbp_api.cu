@@ -17,6 +17,7 @@
 #include "ldbp.h"
 #define LDBP_AUX_KERNELS
 #include "ldbp_kernels.cuh"
+#include "ldbp_rx.cuh"
 
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
@@ -539,7 +540,7 @@ RevWs rev_ws(const ldbp_dims* d, const RevPlan& p) {
 // ----------------------------------------------------------------------------------------
 int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2* taps, const float* gamma,
                const uint8_t* mask, int s0, int s1, cudaStream_t st, float2* ckpt = nullptr, int ckpt_every = 0,
-               int64_t ckpt_stride = 0, bool global_norm = false, bool scale_dst = false) {
+               int64_t ckpt_stride = 0, bool global_norm = false, bool scale_dst = false, float2* y_out = nullptr) {
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const bool fast = !(d->flags & LDBP_PRECISE);
@@ -551,6 +552,7 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   a.src = src;
   a.dst = dst;
   a.ckpt = ckpt;
+  a.y_out = y_out;
   a.ckpt_stride = ckpt_stride;
   a.ckpt_every = ckpt_every > 0 ? ckpt_every : 1;
   a.taps = taps;
@@ -708,9 +710,12 @@ int run_reduce(const ldbp_dims* d, double* partials, double* lossp, int nblk, in
 
 // Store-all training path: forward chain storing u_hat^(1..M) (global normalisation), then the
 // reverse launches (last steps first), then the reduction.
+// forward_only: run the storing forward (and y_out) and return; skip_forward: the activations are
+// already in ws (a previous forward_only call on the same stream), run the reverse only.
 int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const float2* target, const float2* taps,
                   const float* gamma, const uint8_t* mask, float2* gx, unsigned char* ws, const RevPlan& p,
-                  const RevWs& w, cudaStream_t st, double* buf, double* dtaps, double* dgamma) {
+                  const RevWs& w, cudaStream_t st, double* buf, double* dtaps, double* dgamma,
+                  float2* y_out = nullptr, bool forward_only = false, bool skip_forward = false) {
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const bool fast = !(d->flags & LDBP_PRECISE);
@@ -718,14 +723,15 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
   auto act = [&](int i) -> float2* { return reinterpret_cast<float2*>(ws + w.act_off + (size_t)(i - 1) * w.act_each); };
   auto gb = [&](int k) -> float2* { return reinterpret_cast<float2*>(ws + w.g_off + (size_t)(k & 1) * w.g_each); };
   const int64_t stride = (int64_t)(w.act_each / sizeof(float2));
-  {
+  if (!skip_forward) {
     const FwdPlan fp = plan_fwd_segments(M, kh);
     for (int k = 0; k < fp.segs; ++k) {
       const int s0 = k * fp.steps_per, s1 = std::min(M, s0 + fp.steps_per);
       LDBP_TRY(launch_fwd(d, s0 == 0 ? x : act(s0), act(s1), taps, gamma, mask, s0, s1, st,
-                          s1 - s0 >= 2 ? act(1) : nullptr, 1, stride, true, false));
+                          s1 - s0 >= 2 ? act(1) : nullptr, 1, stride, true, false, s1 == M ? y_out : nullptr));
     }
   }
+  if (forward_only) return LDBP_OK;
   RevFn fn = get_rev(kh, sym, fast);
   double* partials = reinterpret_cast<double*>(ws + w.part_off);
   double* lossp = reinterpret_cast<double*>(ws + w.loss_off);
@@ -759,6 +765,82 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
   }
   return run_reduce(d, partials, gy ? nullptr : lossp, p.tile.grid, p.V, ws + w.part2_off, ws + w.loss2_off, mask,
                     st, buf, dtaps, dgamma);
+}
+
+// ---------------------------------------------------------------------------------------
+// Receiver-chain symbol loss (§8(f) NEXT-1), ldbp_rx.cuh
+// ---------------------------------------------------------------------------------------
+struct RxWs {
+  size_t st_off = 0, part_off = 0, epart_off = 0, total = 0;
+  int chunks = 0;
+};
+
+RxWs rx_ws(int64_t B, int64_t n, int sps) {
+  RxWs w;
+  const int64_t K = n / sps;
+  w.chunks = (int)cdiv(K, ldbp::kRxChunk);
+  w.st_off = 0;
+  size_t off = align256(sizeof(float2) * (size_t)B * K);
+  w.part_off = off;
+  off += align256(sizeof(double) * 4 * (size_t)B * w.chunks);
+  w.epart_off = off;
+  off += align256(sizeof(double) * (size_t)B * w.chunks);
+  w.total = off;
+  return w;
+}
+
+size_t rx_smem(int sps, int L) {
+  const int P = (L + sps - 1) / sps + 1;
+  const int WN = ldbp::kRxChunk + 2 * (P + ldbp::kRxTB);
+  return (size_t)ldbp::kRxTapBytes + sizeof(float2) * (size_t)sps * (WN + WN / 16 + 1);
+}
+
+int validate_rx(int64_t B, int64_t n, int sps, int L) {
+  if (B < 0) return fail(LDBP_ESHAPE, "batch %lld < 0", (long long)B);
+  if (sps < 1 || sps > ldbp::kRxMaxSps) return fail(LDBP_ESHAPE, "sps %d not in [1, %d]", sps, ldbp::kRxMaxSps);
+  if (n < sps || n % sps) return fail(LDBP_ESHAPE, "n %lld must be a positive multiple of sps %d", (long long)n, sps);
+  if (L < 0 || L > ldbp::kRxMaxL) return fail(LDBP_ESHAPE, "MF half-length %d not in [0, %d]", L, ldbp::kRxMaxL);
+  if ((int64_t)(2 * L + 1) > n) return fail(LDBP_ESHAPE, "MF longer than the block: 2L+1 = %d > n", 2 * L + 1);
+  return LDBP_OK;
+}
+
+int launch_rx(int64_t B, int64_t n, int sps, int L, const float2* y, const float2* sym, const float* pw,
+              const float* h, double* errs, float2* gy, unsigned char* ws, cudaStream_t st, double* buf = nullptr) {
+  const RxWs w = rx_ws(B, n, sps);
+  ldbp::RxArgs a;
+  a.y = y;
+  a.sym = sym;
+  a.power_w = pw;
+  a.h = h;
+  a.st = reinterpret_cast<float2*>(ws + w.st_off);
+  a.part = reinterpret_cast<double*>(ws + w.part_off);
+  a.epart = reinterpret_cast<double*>(ws + w.epart_off);
+  a.gy = gy;
+  a.errs = errs;
+  a.n = n;
+  a.K = (int)(n / sps);
+  a.sps = sps;
+  a.L = L;
+  a.chunks = w.chunks;
+  const size_t smem = rx_smem(sps, L);
+  cudaFuncSetAttribute((const void*)ldbp::rx_mf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute((const void*)ldbp::rx_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const dim3 grid(w.chunks, (unsigned)B);
+  {
+    TraceScope ts(LDBP_K_RX, 1, B * n, st);
+    ldbp::rx_mf_kernel<<<grid, ldbp::kRxThreads, smem, st>>>(a);
+  }
+  LDBP_TRY(cuda_check("rx_mf_kernel launch"));
+  {
+    TraceScope ts(LDBP_K_RX, 1, B * n, st);
+    ldbp::rx_grad_kernel<<<grid, ldbp::kRxThreads, smem, st>>>(a);
+  }
+  LDBP_TRY(cuda_check("rx_grad_kernel launch"));
+  {
+    TraceScope ts(LDBP_K_RX, 1, 0, st);
+    ldbp::rx_errs_kernel<<<1, 256, 0, st>>>(a.epart, B, w.chunks, errs, buf);
+  }
+  return cuda_check("rx_errs_kernel launch");
 }
 
 int zero_outputs(double* p, size_t count, cudaStream_t st) {
@@ -970,6 +1052,129 @@ int ldbp_train_step(const ldbp_dims* d, const void* x, const void* target, void*
   if (d->batch == 0) return LDBP_OK;
   return ldbp_adam_update(d, buf, n_global, master, m, v, t, lr, b1, b2, eps, mask, glearn, taps_work, gamma_work,
                           cuda_stream);
+}
+
+int ldbp_rx_workspace_bytes(int64_t batch, int64_t n, int32_t sps, size_t* bytes) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_rx(batch, n, sps, 0));
+  if (!bytes) return fail(LDBP_EINVAL, "bytes is NULL");
+  *bytes = batch == 0 ? 0 : rx_ws(batch, n, sps).total;
+  return LDBP_OK;
+}
+
+int ldbp_rx_loss_grad(int64_t batch, int64_t n, int32_t sps, int32_t mf_half, const void* y, const void* symbols,
+                      const float* power_w, const float* h_mf, double* errs, void* gy_or_null, void* ws,
+                      size_t ws_bytes, void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_rx(batch, n, sps, mf_half));
+  if (batch == 0) return LDBP_OK;
+  LDBP_TRY(check_ptr(y, "y", 8));
+  LDBP_TRY(check_ptr(symbols, "symbols", 8));
+  LDBP_TRY(check_ptr(power_w, "power_w", 4));
+  LDBP_TRY(check_ptr(h_mf, "h_mf", 4));
+  LDBP_TRY(check_ptr(errs, "errs", 8));
+  if (gy_or_null) {
+    LDBP_TRY(check_ptr(gy_or_null, "gy", 8));
+    if (gy_or_null == y) return fail(LDBP_EINVAL, "gy must not alias y");
+  }
+  const RxWs w = rx_ws(batch, n, sps);
+  if (!ws || ws_bytes < w.total) return fail(LDBP_EWORKSPACE, "rx needs %zu workspace bytes, got %zu", w.total, ws_bytes);
+  LDBP_TRY(check_ptr(ws, "ws", 16));
+  return launch_rx(batch, n, sps, mf_half, (const float2*)y, (const float2*)symbols, power_w, h_mf, errs,
+                   (float2*)gy_or_null, (unsigned char*)ws, (cudaStream_t)cuda_stream);
+}
+
+}  // extern "C"
+
+namespace {
+struct RxTrainWs {
+  bool store_all = false;
+  size_t train_off = 0, y_off = 0, gy_off = 0, rx_off = 0, errs_off = 0, pp_off = 0, total = 0;
+};
+
+RxTrainWs rx_train_ws(const ldbp_dims* d, int sps, bool query) {
+  RxTrainWs w;
+  w.store_all = use_store_all(d);
+  size_t off = 0;
+  if (w.store_all) {
+    off = rev_ws(d, plan_rev(d, query)).total;
+  } else {
+    off = bwd_ws(d, plan_bwd(d, query)).total;
+    w.pp_off = off;
+    off += align256(fwd_ws(d).total);
+  }
+  const size_t blk = align256(sizeof(float2) * (size_t)d->batch * d->n);
+  w.y_off = off;
+  off += blk;
+  w.gy_off = off;
+  off += blk;
+  w.rx_off = off;
+  off += rx_ws(d->batch, d->n, sps).total;
+  w.errs_off = off;
+  off += align256(sizeof(double) * (size_t)d->batch);
+  w.total = off;
+  return w;
+}
+}  // namespace
+
+extern "C" {
+
+int ldbp_rx_train_workspace_bytes(const ldbp_dims* d, int32_t sps, size_t* bytes) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  LDBP_TRY(validate_rx(d->batch, d->n, sps, 0));
+  if (!bytes) return fail(LDBP_EINVAL, "bytes is NULL");
+  *bytes = d->batch == 0 ? 0 : rx_train_ws(d, sps, true).total;
+  return LDBP_OK;
+}
+
+int ldbp_rx_train_grad(const ldbp_dims* d, const void* x, const void* symbols, const float* power_w, int32_t sps,
+                       int32_t mf_half, const float* h_mf, const void* taps, const float* gamma, const uint8_t* mask,
+                       double* buf, void* ws, size_t ws_bytes, void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  LDBP_TRY(validate_rx(d->batch, d->n, sps, mf_half));
+  LDBP_TRY(check_ptr(buf, "buf", 8));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (d->batch == 0) return zero_outputs(buf, (size_t)1 + d->steps + 2 * (size_t)d->steps * d->taps, st);
+  LDBP_TRY(check_ptr(x, "x", 8));
+  LDBP_TRY(check_ptr(symbols, "symbols", 8));
+  LDBP_TRY(check_ptr(power_w, "power_w", 4));
+  LDBP_TRY(check_ptr(h_mf, "h_mf", 4));
+  LDBP_TRY(check_ptr(taps, "taps", 8));
+  LDBP_TRY(check_ptr(gamma, "gamma", 4));
+  const RxTrainWs w = rx_train_ws(d, sps, true);
+  if (!ws || ws_bytes < w.total)
+    return fail(LDBP_EWORKSPACE, "rx_train_grad needs %zu workspace bytes, got %zu", w.total, ws_bytes);
+  LDBP_TRY(check_ptr(ws, "ws", 16));
+  unsigned char* wb = (unsigned char*)ws;
+  float2* ybuf = reinterpret_cast<float2*>(wb + w.y_off);
+  float2* gybuf = reinterpret_cast<float2*>(wb + w.gy_off);
+  double* errs = reinterpret_cast<double*>(wb + w.errs_off);
+  if (w.store_all) {
+    const RevPlan rp = plan_rev(d, true);
+    const RevWs rw = rev_ws(d, rp);
+    LDBP_TRY(run_rev_chain(d, (const float2*)x, nullptr, nullptr, (const float2*)taps, gamma, mask, nullptr, wb, rp,
+                           rw, st, nullptr, nullptr, nullptr, ybuf, /*forward_only=*/true));
+    LDBP_TRY(launch_rx(d->batch, d->n, sps, mf_half, ybuf, (const float2*)symbols, power_w, h_mf, errs, gybuf,
+                       wb + w.rx_off, st));
+    LDBP_TRY(run_rev_chain(d, (const float2*)x, gybuf, nullptr, (const float2*)taps, gamma, mask, nullptr, wb, rp, rw,
+                           st, buf, nullptr, nullptr, nullptr, false, /*skip_forward=*/true));
+  } else {
+    const BwdPlan bp = plan_bwd(d, true);
+    const BwdWs bw = bwd_ws(d, bp);
+    LDBP_TRY(run_forward_chain(d, (const float2*)x, ybuf, (const float2*)taps, gamma, mask,
+                               reinterpret_cast<float2*>(wb + w.pp_off), st));
+    LDBP_TRY(launch_rx(d->batch, d->n, sps, mf_half, ybuf, (const float2*)symbols, power_w, h_mf, errs, gybuf,
+                       wb + w.rx_off, st));
+    LDBP_TRY(run_backward_chain(d, (const float2*)x, gybuf, nullptr, (const float2*)taps, gamma, mask, nullptr, wb, bp,
+                                bw, st, buf, nullptr, nullptr));
+  }
+  // buf[0] = sum_b errs_b (the reduction above wrote 0 there: no target-seeded loss)
+  const RxWs rw2 = rx_ws(d->batch, d->n, sps);
+  ldbp::rx_errs_kernel<<<1, 256, 0, st>>>(reinterpret_cast<double*>(wb + w.rx_off + rw2.epart_off), d->batch,
+                                          rw2.chunks, errs, buf);
+  return cuda_check("rx_errs_kernel launch");
 }
 
 int ldbp_trace_begin(int capacity) {

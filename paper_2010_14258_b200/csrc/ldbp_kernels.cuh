@@ -815,6 +815,7 @@ struct FwdArgs {
   int global_norm;
   int scale_dst;
   int staged;  // store-all mode (ckpt_every == 1, global): coalesced stores through a smem stage
+  float2* y_out;  // optional second output: the final state in the original scale (y)
   Geo g;
 };
 
@@ -888,6 +889,12 @@ __device__ __forceinline__ void fwd_steps(const FwdArgs& a, f2x (&u)[R], const T
     store_mapped_scaled<R>(a.dst, smap, e0, a.g, u, sh_norm[a.s1 - a.s0 - 1].P);
   else
     store_mapped<R>(a.dst, smap, e0, a.g, u);
+  if (a.y_out) {
+    if constexpr (NORM)
+      store_mapped_scaled<R>(a.y_out, smap, e0, a.g, u, sh_norm[a.s1 - a.s0 - 1].P);
+    else
+      store_mapped<R>(a.y_out, smap, e0, a.g, u);
+  }
 }
 
 // FIR + Kerr for outputs k in [K, KE), with the Kerr of output k-D issued after the FIR of output
@@ -1086,6 +1093,12 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
     store_mapped_scaled<R>(a.dst, smap, e0, a.g, u, sh_norm[a.s1 - a.s0 - 1].P);
   else
     store_mapped<R>(a.dst, smap, e0, a.g, u);
+  if (a.y_out) {
+    if constexpr (NORM)
+      store_mapped_scaled<R>(a.y_out, smap, e0, a.g, u, sh_norm[a.s1 - a.s0 - 1].P);
+    else
+      store_mapped<R>(a.y_out, smap, e0, a.g, u);
+  }
 }
 
 #ifndef LDBP_FWD_SPLIT
