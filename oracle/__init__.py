@@ -15,6 +15,7 @@ Modules
   channel   RRC shaping, asymmetric SSFM, EDFA, brick-wall LPF/decimate  (Eqs. 4-6, 11)
   ldbp      direct-form LDBP forward, adjoint, MSE, Adam, masks, gauges  (Eq. 7)
   receiver  matched filter + downsample, genie phase, effective SNR       (Eqs. 12-14)
+  essm      learned enhanced SSM: filtered nonlinear steps + adjoint     (Eq. nl_filtered)
 
 Pins: tests/test_oracle_*.py check every function against what the paper and mathematics fix
 (worked examples in tests/golden/, closed forms, invariants, special cases, finite
