@@ -192,6 +192,25 @@ int ldbp_rx_train_grad(const ldbp_dims* d, const void* x, const void* symbols, c
                        void* ws, size_t ws_bytes, void* cuda_stream);
 
 /*
+ * Learned ESSM (paper §III-D, Eq. nl_filtered): the nonlinear
+ * step of Eq. (7) becomes  v_t = a_t exp(j gamma'_i sum_{k=-kappa}^{kappa} eta^(i)_k |a_{(t-k) mod n}|^2)
+ * with real per-step filters eta [M][2 kappa + 1] (tap k at index k + kappa), 0 <= kappa <= 32,
+ * 2 kappa + 1 <= n.  All pointers are device pointers as above; one launch per step (shared-
+ * memory tiles with circular halos: the filter's cone grows by Kh + kappa per step).
+ *   ldbp_essm_forward:   y = f_theta(x)
+ *   ldbp_essm_loss_grad: buf = [sum |y - target|^2 | dgamma' [M] | dtaps [M][T][2] | deta [M][2kappa+1]]
+ *                        (UNscaled, tied taps with LDBP_SYMMETRIC as in ldbp_loss_grad; no mask)
+ * Workspace: ldbp_essm_workspace_bytes(d, kappa, LDBP_OP_FORWARD | LDBP_OP_LOSS_GRAD).
+ */
+int ldbp_essm_workspace_bytes(const ldbp_dims* d, int32_t kappa, int op, size_t* bytes);
+int ldbp_essm_forward(const ldbp_dims* d, int32_t kappa, const void* x, void* y, const void* taps,
+                      const float* gamma, const float* eta, void* ws, size_t ws_bytes,
+                      void* cuda_stream);
+int ldbp_essm_loss_grad(const ldbp_dims* d, int32_t kappa, const void* x, const void* target,
+                        const void* taps, const float* gamma, const float* eta, double* buf,
+                        void* ws, size_t ws_bytes, void* cuda_stream);
+
+/*
  * Launch tracing (profiling aid; off by default; per calling thread).
  * ldbp_trace_begin(capacity) makes every kernel launch of later calls on this thread be
  * bracketed by two CUDA events recorded on the call's stream (events are created here, not
@@ -207,7 +226,8 @@ typedef enum ldbp_kernel_kind {
   LDBP_K_REDUCE = 3,    /* fp64 partial reduction (row a8)                         */
   LDBP_K_ADAM = 4,      /* Adam + mask (row a10)                                   */
   LDBP_K_REVERSE = 5,   /* store-all reverse tile kernel (rows a5, a6, a8)         */
-  LDBP_K_RX = 6         /* receiver-chain loss kernels (NEXT-1)                    */
+  LDBP_K_RX = 6,        /* receiver-chain loss kernels (NEXT-1)                    */
+  LDBP_K_ESSM = 7       /* ESSM step kernels (NEXT-4)                              */
 } ldbp_kernel_kind;
 
 typedef struct ldbp_trace_record {

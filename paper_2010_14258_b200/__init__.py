@@ -11,6 +11,8 @@ from .api import (  # noqa: F401
     launch_count,
     ldbp_adam_update,
     ldbp_backward,
+    ldbp_essm_forward,
+    ldbp_essm_loss_grad,
     ldbp_forward,
     ldbp_loss_grad,
     ldbp_rx_loss_grad,

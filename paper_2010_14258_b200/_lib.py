@@ -33,9 +33,12 @@ EXPORTED = (
     "ldbp_rx_loss_grad",
     "ldbp_rx_train_workspace_bytes",
     "ldbp_rx_train_grad",
+    "ldbp_essm_workspace_bytes",
+    "ldbp_essm_forward",
+    "ldbp_essm_loss_grad",
 )
 
-K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM, K_REVERSE, K_RX = 1, 2, 3, 4, 5, 6
+K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM, K_REVERSE, K_RX, K_ESSM = 1, 2, 3, 4, 5, 6, 7
 
 
 class LdbpDims(ctypes.Structure):
@@ -95,6 +98,9 @@ def _load():
         "ldbp_rx_train_workspace_bytes": (ctypes.c_int, [D, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]),
         "ldbp_rx_train_grad": (ctypes.c_int, [D, P, P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P,
                                               ctypes.c_size_t, P]),
+        "ldbp_essm_workspace_bytes": (ctypes.c_int, [D, ctypes.c_int32, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
+        "ldbp_essm_forward": (ctypes.c_int, [D, ctypes.c_int32, P, P, P, P, P, P, ctypes.c_size_t, P]),
+        "ldbp_essm_loss_grad": (ctypes.c_int, [D, ctypes.c_int32, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

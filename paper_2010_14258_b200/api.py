@@ -263,6 +263,45 @@ def ldbp_rx_train_grad(x, symbols, power_w, h_mf, taps, gamma, *, sps=2, mask=No
     return out
 
 
+def _check_eta(eta, M):
+    _need(eta, "eta", torch.float32)
+    if eta.dim() != 2 or eta.shape[0] != M or eta.shape[1] % 2 == 0:
+        raise ValueError("eta must be float32 [M][2*kappa+1]")
+    return (eta.shape[1] - 1) // 2
+
+
+def ldbp_essm_forward(x, taps, gamma, eta, *, symmetric=True, precise=False, out=None, ws=None, stream=None):
+    """Learned ESSM forward (§8(f) NEXT-4): y = f_theta(x) with filtered nonlinear steps."""
+    B, n, M, T = _check_model(x, taps, gamma)
+    kappa = _check_eta(eta, M)
+    d = make_dims(B, n, M, T, symmetric, precise)
+    y = torch.empty_like(x) if out is None else out
+    nb = ctypes.c_size_t(0)
+    check(lib.ldbp_essm_workspace_bytes(ctypes.byref(d), kappa, OP_FORWARD, ctypes.byref(nb)), "ldbp_essm_workspace_bytes")
+    w, nbv = _ws(x.device, int(nb.value), ws)
+    check(lib.ldbp_essm_forward(ctypes.byref(d), kappa, _p(x), _p(y), _p(taps), _p(gamma), _p(eta), _p(w), nbv,
+                                _stream_handle(stream)), "ldbp_essm_forward")
+    return y
+
+
+def ldbp_essm_loss_grad(x, target, taps, gamma, eta, *, symmetric=True, precise=False, buf=None, ws=None,
+                        stream=None):
+    """[sum|e|^2 | dgamma[M] | dtaps[M][T][2] | deta[M][2kappa+1]] (float64, unscaled)."""
+    B, n, M, T = _check_model(x, taps, gamma)
+    kappa = _check_eta(eta, M)
+    _need(target, "target", torch.complex64, x.shape)
+    d = make_dims(B, n, M, T, symmetric, precise)
+    out = torch.empty(1 + M + 2 * M * T + M * (2 * kappa + 1), dtype=torch.float64, device=x.device) \
+        if buf is None else buf
+    nb = ctypes.c_size_t(0)
+    check(lib.ldbp_essm_workspace_bytes(ctypes.byref(d), kappa, OP_LOSS_GRAD, ctypes.byref(nb)),
+          "ldbp_essm_workspace_bytes")
+    w, nbv = _ws(x.device, int(nb.value), ws)
+    check(lib.ldbp_essm_loss_grad(ctypes.byref(d), kappa, _p(x), _p(target), _p(taps), _p(gamma), _p(eta), _p(out),
+                                  _p(w), nbv, _stream_handle(stream)), "ldbp_essm_loss_grad")
+    return out
+
+
 class trace:
     """Context manager: per-launch CUDA-event timing of libldbp kernels on this thread.
 

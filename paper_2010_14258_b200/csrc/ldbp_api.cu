@@ -18,6 +18,7 @@
 #define LDBP_AUX_KERNELS
 #include "ldbp_kernels.cuh"
 #include "ldbp_rx.cuh"
+#include "ldbp_essm.cuh"
 
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
@@ -843,6 +844,83 @@ int launch_rx(int64_t B, int64_t n, int sps, int L, const float2* y, const float
   return cuda_check("rx_errs_kernel launch");
 }
 
+// ---------------------------------------------------------------------------------------
+// ESSM (§8(f) NEXT-4), ldbp_essm.cuh: one launch per step, smem tiles
+// ---------------------------------------------------------------------------------------
+struct EssmWs {
+  size_t act_off = 0, act_each = 0, g_off = 0, part_off = 0, total = 0;
+  int tiles = 0, V = 0;
+};
+
+EssmWs essm_ws(const ldbp_dims* d, int kappa, bool train) {
+  EssmWs w;
+  w.tiles = (int)cdiv(d->n, ldbp::kEssmW);
+  w.V = 2 + 2 * d->taps + 2 * kappa + 1;
+  const size_t blk = align256(sizeof(float2) * (size_t)d->batch * d->n);
+  w.act_each = blk;
+  size_t off = 0;
+  w.act_off = off;
+  off += blk * (train ? (size_t)d->steps : 2);  // train: u^(1..M); forward: ping-pong
+  w.g_off = off;
+  if (train) off += 2 * blk;
+  w.part_off = off;
+  if (train) off += align256(sizeof(double) * (size_t)d->steps * w.tiles * d->batch * w.V);
+  w.total = off;
+  return w;
+}
+
+size_t essm_smem(int T, int kappa, bool bwd) {
+  const int kh = (T - 1) / 2;
+  size_t s = sizeof(float2) * ldbp::kEssmMaxT + sizeof(float) * (2 * ldbp::kEssmMaxKappa + 2);
+  const int W = ldbp::kEssmW;
+  if (!bwd) {
+    const int nu = W + 2 * (kh + kappa), na = W + 2 * kappa;
+    return s + sizeof(float2) * (nu + na) + sizeof(float) * na;
+  }
+  const int nU = W + 2 * (2 * kh + 2 * kappa), nA = W + 2 * (kh + 2 * kappa), nG = W + 2 * (kh + kappa), nQ = W + 2 * kh;
+  s += sizeof(float2) * (nU + nA + nG);
+  s += sizeof(float) * (nA + 2 * nG + nQ + (nQ & 1));
+  s += sizeof(float2) * nQ + sizeof(double) * ldbp::kEssmThreads;
+  return s;
+}
+
+int validate_essm(const ldbp_dims* d, int kappa) {
+  if (kappa < 0 || kappa > ldbp::kEssmMaxKappa) return fail(LDBP_ESHAPE, "kappa %d not in [0, %d]", kappa, ldbp::kEssmMaxKappa);
+  if (2 * (int64_t)kappa + 1 > d->n) return fail(LDBP_ESHAPE, "eta longer than the block: 2kappa+1 > n");
+  return LDBP_OK;
+}
+
+int launch_essm_step(const ldbp_dims* d, int kappa, bool bwd, int step, const float2* u, const float2* gin,
+                     const float2* target, float2* out, const float2* taps, const float* gamma,
+                     const float* eta, double* partials, cudaStream_t st) {
+  ldbp::EssmArgs a;
+  a.u = u;
+  a.gin = gin;
+  a.target = target;
+  a.out = out;
+  a.taps = taps + (int64_t)step * d->taps;
+  a.eta = eta + (int64_t)step * (2 * kappa + 1);
+  a.gamma = gamma;
+  a.step = step;
+  a.partials = partials;
+  a.n = d->n;
+  a.T = d->taps;
+  a.kappa = kappa;
+  a.tiles = (int)cdiv(d->n, ldbp::kEssmW);
+  const bool fast = !(d->flags & LDBP_PRECISE);
+  const size_t smem = essm_smem(d->taps, kappa, bwd);
+  const dim3 grid(a.tiles, (unsigned)d->batch);
+  const void* fn = bwd ? (fast ? (const void*)ldbp::essm_bwd_step_kernel<true> : (const void*)ldbp::essm_bwd_step_kernel<false>)
+                       : (fast ? (const void*)ldbp::essm_fwd_step_kernel<true> : (const void*)ldbp::essm_fwd_step_kernel<false>);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    TraceScope ts(LDBP_K_ESSM, 1, d->batch * d->n, st);
+    void* args[] = {&a};
+    cudaLaunchKernel(fn, grid, dim3(ldbp::kEssmThreads), args, smem, st);
+  }
+  return cuda_check(bwd ? "essm_bwd_step_kernel launch" : "essm_fwd_step_kernel launch");
+}
+
 int zero_outputs(double* p, size_t count, cudaStream_t st) {
   if (count && cudaMemsetAsync(p, 0, count * sizeof(double), st) != cudaSuccess)
     return fail(LDBP_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(cudaGetLastError()));
@@ -1175,6 +1253,93 @@ int ldbp_rx_train_grad(const ldbp_dims* d, const void* x, const void* symbols, c
   ldbp::rx_errs_kernel<<<1, 256, 0, st>>>(reinterpret_cast<double*>(wb + w.rx_off + rw2.epart_off), d->batch,
                                           rw2.chunks, errs, buf);
   return cuda_check("rx_errs_kernel launch");
+}
+
+int ldbp_essm_workspace_bytes(const ldbp_dims* d, int32_t kappa, int op, size_t* bytes) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  LDBP_TRY(validate_essm(d, kappa));
+  if (!bytes) return fail(LDBP_EINVAL, "bytes is NULL");
+  if (op != LDBP_OP_FORWARD && op != LDBP_OP_LOSS_GRAD) return fail(LDBP_EINVAL, "ESSM ops: FORWARD or LOSS_GRAD");
+  *bytes = d->batch == 0 ? 0 : essm_ws(d, kappa, op == LDBP_OP_LOSS_GRAD).total;
+  return LDBP_OK;
+}
+
+int ldbp_essm_forward(const ldbp_dims* d, int32_t kappa, const void* x, void* y, const void* taps,
+                      const float* gamma, const float* eta, void* ws, size_t ws_bytes, void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  LDBP_TRY(validate_essm(d, kappa));
+  if (d->batch == 0) return LDBP_OK;
+  LDBP_TRY(check_ptr(x, "x", 8));
+  LDBP_TRY(check_ptr(y, "y", 8));
+  LDBP_TRY(check_ptr(taps, "taps", 8));
+  LDBP_TRY(check_ptr(gamma, "gamma", 4));
+  LDBP_TRY(check_ptr(eta, "eta", 4));
+  if (x == y) return fail(LDBP_EINVAL, "y must not alias x");
+  const EssmWs w = essm_ws(d, kappa, false);
+  if (!ws || ws_bytes < w.total) return fail(LDBP_EWORKSPACE, "essm forward needs %zu workspace bytes, got %zu", w.total, ws_bytes);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  unsigned char* wb = (unsigned char*)ws;
+  const float2* src = (const float2*)x;
+  for (int i = 0; i < d->steps; ++i) {
+    const int remaining = d->steps - 1 - i;
+    float2* dst = remaining == 0 ? (float2*)y : reinterpret_cast<float2*>(wb + w.act_off + (size_t)(i & 1) * w.act_each);
+    LDBP_TRY(launch_essm_step(d, kappa, false, i, src, nullptr, nullptr, dst, (const float2*)taps, gamma, eta,
+                              nullptr, st));
+    src = dst;
+  }
+  return LDBP_OK;
+}
+
+int ldbp_essm_loss_grad(const ldbp_dims* d, int32_t kappa, const void* x, const void* target, const void* taps,
+                        const float* gamma, const float* eta, double* buf, void* ws, size_t ws_bytes,
+                        void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  LDBP_TRY(validate_essm(d, kappa));
+  LDBP_TRY(check_ptr(buf, "buf", 8));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const size_t nbuf = 1 + d->steps + 2 * (size_t)d->steps * d->taps + (size_t)d->steps * (2 * kappa + 1);
+  if (d->batch == 0) return zero_outputs(buf, nbuf, st);
+  LDBP_TRY(check_ptr(x, "x", 8));
+  LDBP_TRY(check_ptr(target, "target", 8));
+  LDBP_TRY(check_ptr(taps, "taps", 8));
+  LDBP_TRY(check_ptr(gamma, "gamma", 4));
+  LDBP_TRY(check_ptr(eta, "eta", 4));
+  const EssmWs w = essm_ws(d, kappa, true);
+  if (!ws || ws_bytes < w.total) return fail(LDBP_EWORKSPACE, "essm loss_grad needs %zu workspace bytes, got %zu", w.total, ws_bytes);
+  unsigned char* wb = (unsigned char*)ws;
+  const int M = d->steps;
+  auto act = [&](int i) -> float2* { return reinterpret_cast<float2*>(wb + w.act_off + (size_t)(i - 1) * w.act_each); };
+  auto gb = [&](int i) -> float2* { return reinterpret_cast<float2*>(wb + w.g_off + (size_t)(i & 1) * w.act_each); };
+  double* part = reinterpret_cast<double*>(wb + w.part_off);
+  const size_t part_step = (size_t)w.tiles * d->batch * w.V;
+  // forward, storing u^(1..M-1) (u^(M) = y is recomputed by the seeded reverse step)
+  for (int i = 0; i + 1 < M; ++i)
+    LDBP_TRY(launch_essm_step(d, kappa, false, i, i == 0 ? (const float2*)x : act(i), nullptr, nullptr, act(i + 1),
+                              (const float2*)taps, gamma, eta, nullptr, st));
+  // reverse: step M-1 seeded from the target, then the incoming adjoints
+  for (int i = M - 1; i >= 0; --i) {
+    const float2* u = i == 0 ? (const float2*)x : act(i);
+    const float2* gin = i == M - 1 ? nullptr : gb(i + 1);
+    float2* gout = i == 0 ? nullptr : gb(i);
+    LDBP_TRY(launch_essm_step(d, kappa, true, i, u, gin, (const float2*)target, gout, (const float2*)taps, gamma,
+                              eta, part + (size_t)i * part_step, st));
+  }
+  ldbp::EssmReduceArgs r;
+  r.partials = part;
+  r.M = M;
+  r.nblk = w.tiles * (int)d->batch;
+  r.T = d->taps;
+  r.kappa = kappa;
+  r.sym = (d->flags & LDBP_SYMMETRIC) ? 1 : 0;
+  r.buf = buf;
+  {
+    TraceScope ts(LDBP_K_REDUCE, M, 0, st);
+    ldbp::essm_reduce_kernel<<<(M * w.V + 255) / 256, 256, 0, st>>>(r);
+  }
+  return cuda_check("essm_reduce_kernel launch");
 }
 
 int ldbp_trace_begin(int capacity) {
