@@ -870,17 +870,17 @@ EssmWs essm_ws(const ldbp_dims* d, int kappa, bool train) {
 }
 
 size_t essm_smem(int T, int kappa, bool bwd) {
+  using namespace ldbp;
   const int kh = (T - 1) / 2;
-  size_t s = sizeof(float2) * ldbp::kEssmMaxT + sizeof(float) * (2 * ldbp::kEssmMaxKappa + 2);
-  const int W = ldbp::kEssmW;
+  const int W = kEssmW, S = kESlack;
+  size_t s = sizeof(float2) * kEssmMaxT + sizeof(float) * (2 * essm_nj(kEssmMaxKappa) + 2);
   if (!bwd) {
     const int nu = W + 2 * (kh + kappa), na = W + 2 * kappa;
-    return s + sizeof(float2) * (nu + na) + sizeof(float) * na;
+    return s + sizeof(float2) * (essm_pc_size(nu + S) + essm_pc_size(na + S)) + sizeof(float) * essm_pf_size(na + S);
   }
   const int nU = W + 2 * (2 * kh + 2 * kappa), nA = W + 2 * (kh + 2 * kappa), nG = W + 2 * (kh + kappa), nQ = W + 2 * kh;
-  s += sizeof(float2) * (nU + nA + nG);
-  s += sizeof(float) * (nA + 2 * nG + nQ + (nQ & 1));
-  s += sizeof(float2) * nQ + sizeof(double) * ldbp::kEssmThreads;
+  s += sizeof(float2) * (essm_pc_size(nU + S) + essm_pc_size(nA + S) + essm_pc_size(nG + S) + essm_pc_size(nQ + S));
+  s += sizeof(float) * (essm_pf_size(nA + S) + 2 * essm_pf_size(nG + S));
   return s;
 }
 
@@ -888,6 +888,25 @@ int validate_essm(const ldbp_dims* d, int kappa) {
   if (kappa < 0 || kappa > ldbp::kEssmMaxKappa) return fail(LDBP_ESHAPE, "kappa %d not in [0, %d]", kappa, ldbp::kEssmMaxKappa);
   if (2 * (int64_t)kappa + 1 > d->n) return fail(LDBP_ESHAPE, "eta longer than the block: 2kappa+1 > n");
   return LDBP_OK;
+}
+
+template <int KH>
+const void* essm_kernel_kh(bool bwd, bool fast) {
+  if (bwd) return fast ? (const void*)ldbp::essm_bwd_step_kernel<KH, true> : (const void*)ldbp::essm_bwd_step_kernel<KH, false>;
+  return fast ? (const void*)ldbp::essm_fwd_step_kernel<KH, true> : (const void*)ldbp::essm_fwd_step_kernel<KH, false>;
+}
+
+const void* essm_kernel(int kh, bool bwd, bool fast) {
+  switch (kh) {
+    case 0: return essm_kernel_kh<0>(bwd, fast);
+    case 1: return essm_kernel_kh<1>(bwd, fast);
+    case 2: return essm_kernel_kh<2>(bwd, fast);
+    case 3: return essm_kernel_kh<3>(bwd, fast);
+    case 4: return essm_kernel_kh<4>(bwd, fast);
+    case 5: return essm_kernel_kh<5>(bwd, fast);
+    case 6: return essm_kernel_kh<6>(bwd, fast);
+    default: return essm_kernel_kh<7>(bwd, fast);
+  }
 }
 
 int launch_essm_step(const ldbp_dims* d, int kappa, bool bwd, int step, const float2* u, const float2* gin,
@@ -910,8 +929,7 @@ int launch_essm_step(const ldbp_dims* d, int kappa, bool bwd, int step, const fl
   const bool fast = !(d->flags & LDBP_PRECISE);
   const size_t smem = essm_smem(d->taps, kappa, bwd);
   const dim3 grid(a.tiles, (unsigned)d->batch);
-  const void* fn = bwd ? (fast ? (const void*)ldbp::essm_bwd_step_kernel<true> : (const void*)ldbp::essm_bwd_step_kernel<false>)
-                       : (fast ? (const void*)ldbp::essm_fwd_step_kernel<true> : (const void*)ldbp::essm_fwd_step_kernel<false>);
+  const void* fn = essm_kernel((d->taps - 1) / 2, bwd, fast);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   {
     TraceScope ts(LDBP_K_ESSM, 1, d->batch * d->n, st);

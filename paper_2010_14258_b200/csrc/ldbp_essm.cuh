@@ -50,175 +50,268 @@ __device__ __forceinline__ f2x essm_mac_conj(f2x acc, float2 h, f2x s) {
   return fma2(bcast(hif(s)), pk(h.y, h.x), fma2(bcast(lof(s)), pk(h.x, -h.y), acc));
 }
 
+// Register-blocked filters.  Every thread produces kEQ consecutive outputs; shared arrays use a
+// padded layout (f2x: one pad per 16, float: one pad per 32) so that the lanes' kEQ-element runs
+// hit distinct banks.  The real kappa-filters run over zero-padded tap tables in blocks of 8 taps
+// with compile-time register indices (the window is reloaded per block).
+constexpr int kEQ = 8;
+constexpr int kESlack = 16;  // logical slack after every array (blocked reads run past the end)
+__device__ __forceinline__ int pcx(int i) { return i + (i >> 4); }  // f2x arrays
+__device__ __forceinline__ int pfl(int i) { return i + (i >> 5); }  // float arrays
+__host__ __device__ __forceinline__ int essm_pc_size(int n) { return n + (n >> 4) + 1; }
+__host__ __device__ __forceinline__ int essm_pf_size(int n) { return n + (n >> 5) + 1; }
+__host__ __device__ __forceinline__ int essm_nj(int kap) { return ((2 * kap + 1 + 7) / 8) * 8; }
+
+// tt[j] = eta_{k}, k = kap - j (dir = +1: X index o - k = o - kap + j) or k = j - kap (dir = -1:
+// X index o + k = o - kap + j); zero for j >= 2 kap + 1.
+__device__ __forceinline__ void essm_tap_table(const float* __restrict__ eta, int kap, int dir, float* tt) {
+  const int NJ = essm_nj(kap);
+  for (int j = threadIdx.x; j < NJ; j += kEssmThreads) {
+    const int k = dir > 0 ? kap - j : j - kap;
+    tt[j] = j < 2 * kap + 1 ? eta[k + kap] : 0.f;
+  }
+}
+
+// acc[q] = sum_j tt[j] X[x0 + q - kap + j]  (X float, padded)
+__device__ __forceinline__ void essm_rfilt(const float* __restrict__ X, int x0, int kap, const float* __restrict__ tt,
+                                           float (&acc)[kEQ]) {
+  const int NJ = essm_nj(kap);
+#pragma unroll
+  for (int q = 0; q < kEQ; ++q) acc[q] = 0.f;
+  for (int j0 = 0; j0 < NJ; j0 += 8) {
+    const int b = x0 - kap + j0;
+    float w[kEQ + 7];
+#pragma unroll
+    for (int i = 0; i < kEQ + 7; ++i) w[i] = X[pfl(b + i)];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float h = tt[j0 + t];
+#pragma unroll
+      for (int q = 0; q < kEQ; ++q) acc[q] = fmaf(h, w[q + t], acc[q]);
+    }
+  }
+}
+
+// complex FIR, acc[q] = sum_j h_j In[x0 + q - j] (ADJ: sum_j conj(h_j) In[x0 + q + j]), j in [-KH, KH]
+template <int KH, bool ADJ>
+__device__ __forceinline__ void essm_cfir(const f2x* __restrict__ In, int x0, const float2* __restrict__ sh_h,
+                                          f2x (&acc)[kEQ]) {
+  f2x w[kEQ + 2 * KH];
+#pragma unroll
+  for (int i = 0; i < kEQ + 2 * KH; ++i) w[i] = In[pcx(x0 - KH + i)];
+#pragma unroll
+  for (int q = 0; q < kEQ; ++q) acc[q] = 0ull;
+#pragma unroll
+  for (int jj = 0; jj < 2 * KH + 1; ++jj) {
+    const float2 h = sh_h[jj];
+#pragma unroll
+    for (int q = 0; q < kEQ; ++q)
+      acc[q] = ADJ ? essm_mac_conj(acc[q], h, w[q + KH + (jj - KH)]) : essm_mac(acc[q], h, w[q + KH - (jj - KH)]);
+  }
+}
+
 // Forward step: U on [-(Kh+kappa), W+Kh+kappa), A/P on [-kappa, W+kappa), v on [0, W).
-template <bool FAST>
+template <int KH, bool FAST>
 __global__ void __launch_bounds__(kEssmThreads) essm_fwd_step_kernel(const EssmArgs a) {
   extern __shared__ __align__(16) unsigned char es_smem[];
-  const int kh = (a.T - 1) / 2, kap = a.kappa;
+  const int kap = a.kappa;
   const float gam = a.gamma[a.step];
   const int b = blockIdx.y, tile = blockIdx.x;
   const int64_t t0 = (int64_t)tile * kEssmW;
-  const int hu = kh + kap, nu = kEssmW + 2 * hu, na = kEssmW + 2 * kap;
-  float2* sh_h = reinterpret_cast<float2*>(es_smem);       // [kEssmMaxT]
-  float* sh_eta = reinterpret_cast<float*>(sh_h + kEssmMaxT);  // [2*kEssmMaxKappa+1]
-  f2x* U = reinterpret_cast<f2x*>(sh_eta + 2 * kEssmMaxKappa + 2);  // [nu] (8-byte aligned)
-  f2x* A = U + nu;                                           // [na]
-  float* P = reinterpret_cast<float*>(A + na);               // [na]
-  for (int i = threadIdx.x; i < a.T; i += kEssmThreads) sh_h[i] = a.taps[i];
-  for (int i = threadIdx.x; i < 2 * kap + 1; i += kEssmThreads) sh_eta[i] = a.eta[i];
+  const int hu = KH + kap, nu = kEssmW + 2 * hu, na = kEssmW + 2 * kap;
+  float2* sh_h = reinterpret_cast<float2*>(es_smem);                // [kEssmMaxT]
+  float* tt = reinterpret_cast<float*>(sh_h + kEssmMaxT);           // [essm_nj(kEssmMaxKappa)]
+  f2x* U = reinterpret_cast<f2x*>(tt + essm_nj(kEssmMaxKappa) + 2); // [pc(nu + slack)]
+  f2x* A = U + essm_pc_size(nu + kESlack);                          // [pc(na + slack)]
+  float* P = reinterpret_cast<float*>(A + essm_pc_size(na + kESlack));  // [pf(na + slack)]
+  for (int i = threadIdx.x; i < 2 * KH + 1; i += kEssmThreads) sh_h[i] = a.taps[i];
+  essm_tap_table(a.eta, kap, +1, tt);
   const f2x* ub = reinterpret_cast<const f2x*>(a.u) + (int64_t)b * a.n;
-  for (int i = threadIdx.x; i < nu; i += kEssmThreads) U[i] = ub[essm_mod(t0 - hu + i, a.n)];
+  for (int i = threadIdx.x; i < nu + kESlack; i += kEssmThreads)
+    U[pcx(i)] = i < nu ? ub[essm_mod(t0 - hu + i, a.n)] : 0ull;
+  for (int i = threadIdx.x; i < kESlack; i += kEssmThreads) P[pfl(na + i)] = 0.f;
   __syncthreads();
-  // a_t = sum_j h_j u_{t-j}, t = -kappa + i
-  for (int i = threadIdx.x; i < na; i += kEssmThreads) {
-    f2x acc = 0ull;
-    for (int jj = 0; jj < a.T; ++jj) acc = essm_mac(acc, sh_h[jj], U[i + kh - (jj - kh)]);  // U index of t-j
-    A[i] = acc;
-    const float2 av = upk(acc);
-    P[i] = fmaf(av.x, av.x, av.y * av.y);
+  // a_t = sum_j h_j u_{t-j}, A index i <-> t = t0 - kappa + i <-> U index i + KH
+  for (int o0 = threadIdx.x * kEQ; o0 < na; o0 += kEssmThreads * kEQ) {
+    f2x acc[kEQ];
+    essm_cfir<KH, false>(U, o0 + KH, sh_h, acc);
+#pragma unroll
+    for (int q = 0; q < kEQ; ++q) {
+      A[pcx(o0 + q)] = acc[q];
+      const float2 av = upk(acc[q]);
+      P[pfl(o0 + q)] = fmaf(av.x, av.x, av.y * av.y);
+    }
   }
   __syncthreads();
+  // psi_t = sum_k eta_k p_{t-k}; owned output i <-> P index i + kappa
   f2x* vb = reinterpret_cast<f2x*>(a.out) + (int64_t)b * a.n;
-  for (int i = threadIdx.x; i < kEssmW; i += kEssmThreads) {
-    if (t0 + i >= a.n) break;
-    float psi = 0.f;
-    for (int k = -kap; k <= kap; ++k) psi = fmaf(sh_eta[k + kap], P[i + kap - k], psi);  // p_{t-k}
-    float s, c;
-    sincos_phase<FAST>(gam * psi, &s, &c);
-    const float2 av = upk(A[i + kap]);
-    vb[t0 + i] = pk(fmaf(av.x, c, -av.y * s), fmaf(av.x, s, av.y * c));
+  const int own = (int)(a.n - t0 < (int64_t)kEssmW ? a.n - t0 : (int64_t)kEssmW);
+  for (int o0 = threadIdx.x * kEQ; o0 < own; o0 += kEssmThreads * kEQ) {
+    float psi[kEQ];
+    essm_rfilt(P, o0 + kap, kap, tt, psi);
+#pragma unroll
+    for (int q = 0; q < kEQ; ++q) {
+      if (o0 + q >= own) break;
+      float s, c;
+      sincos_phase<FAST>(gam * psi[q], &s, &c);
+      const float2 av = upk(A[pcx(o0 + q + kap)]);
+      vb[t0 + o0 + q] = pk(fmaf(av.x, c, -av.y * s), fmaf(av.x, s, av.y * c));
+    }
   }
 }
 
 // Backward step.  Regions relative to t0 (halo widths): U: 2Kh+2kappa, A/P: Kh+2kappa,
 // G/PSI/C (and phi): Kh+kappa, GA/Q: Kh; outputs and gradient sums on owned [0, W).
-template <bool FAST>
+template <int KH, bool FAST>
 __global__ void __launch_bounds__(kEssmThreads) essm_bwd_step_kernel(const EssmArgs a) {
   extern __shared__ __align__(16) unsigned char es_smem[];
-  const int kh = (a.T - 1) / 2, kap = a.kappa;
+  const int kap = a.kappa;
   const float gam = a.gamma[a.step];
   const int b = blockIdx.y, tile = blockIdx.x;
   const int64_t t0 = (int64_t)tile * kEssmW;
   const int own = (int)(a.n - t0 < (int64_t)kEssmW ? a.n - t0 : (int64_t)kEssmW);
-  const int hU = 2 * kh + 2 * kap, hA = kh + 2 * kap, hG = kh + kap, hQ = kh;
+  const int hU = 2 * KH + 2 * kap, hA = KH + 2 * kap, hG = KH + kap, hQ = KH;
   const int nU = kEssmW + 2 * hU, nA = kEssmW + 2 * hA, nG = kEssmW + 2 * hG, nQ = kEssmW + 2 * hQ;
-  const int NE = 2 * kap + 1;
-  const int V = 2 + 2 * a.T + NE;  // [dgamma | loss | dh re/im (T) | deta (NE)]
+  const int T = 2 * KH + 1, NE = 2 * kap + 1;
+  const int V = 2 + 2 * T + NE;  // [dgamma | loss | dh re/im (T) | deta (NE)]
   float2* sh_h = reinterpret_cast<float2*>(es_smem);
-  float* sh_eta = reinterpret_cast<float*>(sh_h + kEssmMaxT);
-  f2x* U = reinterpret_cast<f2x*>(sh_eta + 2 * kEssmMaxKappa + 2);
-  f2x* A = U + nU;
-  f2x* G = A + nA;         // g on hG, later reused for GA on hQ
-  float* P = reinterpret_cast<float*>(G + nG);
-  float* PSI = P + nA;     // psi on hG
-  float* C = PSI + nG;     // c on hG
-  float* Q = C + nG;       // q on hQ
-  f2x* GA = reinterpret_cast<f2x*>(Q + nQ + (nQ & 1));  // ga on hQ
-  double* red = reinterpret_cast<double*>(GA + nQ);     // [kEssmThreads] group sums
-  for (int i = threadIdx.x; i < a.T; i += kEssmThreads) sh_h[i] = a.taps[i];
-  for (int i = threadIdx.x; i < NE; i += kEssmThreads) sh_eta[i] = a.eta[i];
+  float* tt_f = reinterpret_cast<float*>(sh_h + kEssmMaxT);        // forward table (psi)
+  float* tt_b = tt_f + essm_nj(kEssmMaxKappa);                      // reversed table (q)
+  f2x* U = reinterpret_cast<f2x*>(tt_b + essm_nj(kEssmMaxKappa) + 2);
+  f2x* A = U + essm_pc_size(nU + kESlack);
+  f2x* G = A + essm_pc_size(nA + kESlack);
+  f2x* GA = G + essm_pc_size(nG + kESlack);
+  float* P = reinterpret_cast<float*>(GA + essm_pc_size(nQ + kESlack));
+  float* PSI = P + essm_pf_size(nA + kESlack);
+  float* C = PSI + essm_pf_size(nG + kESlack);
+  for (int i = threadIdx.x; i < T; i += kEssmThreads) sh_h[i] = a.taps[i];
+  essm_tap_table(a.eta, kap, +1, tt_f);
+  essm_tap_table(a.eta, kap, -1, tt_b);
   const f2x* ub = reinterpret_cast<const f2x*>(a.u) + (int64_t)b * a.n;
-  for (int i = threadIdx.x; i < nU; i += kEssmThreads) U[i] = ub[essm_mod(t0 - hU + i, a.n)];
-  __syncthreads();
-  // a, p on hA
-  for (int i = threadIdx.x; i < nA; i += kEssmThreads) {
-    f2x acc = 0ull;
-    const int iu = i + (hU - hA);  // U index of the same t
-    for (int jj = 0; jj < a.T; ++jj) acc = essm_mac(acc, sh_h[jj], U[iu - (jj - kh)]);
-    A[i] = acc;
-    const float2 av = upk(acc);
-    P[i] = fmaf(av.x, av.x, av.y * av.y);
+  for (int i = threadIdx.x; i < nU + kESlack; i += kEssmThreads)
+    U[pcx(i)] = i < nU ? ub[essm_mod(t0 - hU + i, a.n)] : 0ull;
+  for (int i = threadIdx.x; i < kESlack; i += kEssmThreads) {  // finite slack (zero taps x slack)
+    P[pfl(nA + i)] = 0.f;
+    C[pfl(nG + i)] = 0.f;
+    PSI[pfl(nG + i)] = 0.f;
+    GA[pcx(nQ + i)] = 0ull;
   }
   __syncthreads();
-  // psi, v, g (loaded or seeded), c on hG; the seed's loss over owned samples
+  // a, p on hA: A index i <-> U index i + (hU - hA) = i + KH
+  for (int o0 = threadIdx.x * kEQ; o0 < nA; o0 += kEssmThreads * kEQ) {
+    f2x acc[kEQ];
+    essm_cfir<KH, false>(U, o0 + KH, sh_h, acc);
+#pragma unroll
+    for (int q = 0; q < kEQ; ++q) {
+      A[pcx(o0 + q)] = acc[q];
+      const float2 av = upk(acc[q]);
+      P[pfl(o0 + q)] = fmaf(av.x, av.x, av.y * av.y);
+    }
+  }
+  __syncthreads();
+  // psi, v, g (loaded or seeded), c on hG: G index i <-> A/P index i + kappa
   const f2x* gb = a.gin ? reinterpret_cast<const f2x*>(a.gin) + (int64_t)b * a.n : nullptr;
   const f2x* tb = a.gin ? nullptr : reinterpret_cast<const f2x*>(a.target) + (int64_t)b * a.n;
   float lsum = 0.f;
-  for (int i = threadIdx.x; i < nG; i += kEssmThreads) {
-    const int ia = i + (hA - hG);
-    float psi = 0.f;
-    for (int k = -kap; k <= kap; ++k) psi = fmaf(sh_eta[k + kap], P[ia - k], psi);
-    float s, c;
-    sincos_phase<FAST>(gam * psi, &s, &c);
-    const float2 av = upk(A[ia]);
-    const float vx = fmaf(av.x, c, -av.y * s), vy = fmaf(av.x, s, av.y * c);
-    const int64_t t = essm_mod(t0 - hG + i, a.n);
-    float2 g;
-    if (gb) {
-      g = upk(gb[t]);
-    } else {
-      const float2 tv = upk(tb[t]);
-      const float ex = vx - tv.x, ey = vy - tv.y;
-      g = make_float2(2.f * ex, 2.f * ey);
-      if (i >= hG && i < hG + own) lsum = fmaf(ex, ex, fmaf(ey, ey, lsum));
+  for (int o0 = threadIdx.x * kEQ; o0 < nG; o0 += kEssmThreads * kEQ) {
+    float psi[kEQ];
+    essm_rfilt(P, o0 + kap, kap, tt_f, psi);
+#pragma unroll
+    for (int q = 0; q < kEQ; ++q) {
+      const int i = o0 + q;
+      if (i >= nG) break;
+      float s, c;
+      sincos_phase<FAST>(gam * psi[q], &s, &c);
+      const float2 av = upk(A[pcx(i + kap)]);
+      const float vx = fmaf(av.x, c, -av.y * s), vy = fmaf(av.x, s, av.y * c);
+      const int64_t t = essm_mod(t0 - hG + i, a.n);
+      float2 g;
+      if (gb) {
+        g = upk(gb[t]);
+      } else {
+        const float2 tv = upk(tb[t]);
+        const float ex = vx - tv.x, ey = vy - tv.y;
+        g = make_float2(2.f * ex, 2.f * ey);
+        if (i >= hG && i < hG + own) lsum = fmaf(ex, ex, fmaf(ey, ey, lsum));
+      }
+      G[pcx(i)] = pk(g.x, g.y);
+      PSI[pfl(i)] = psi[q];
+      C[pfl(i)] = fmaf(g.y, vx, -g.x * vy);  // Im(g conj v)
     }
-    G[i] = pk(g.x, g.y);
-    PSI[i] = psi;
-    C[i] = fmaf(g.y, vx, -g.x * vy);  // Im(g conj v)
   }
   __syncthreads();
-  // q and ga on hQ
-  for (int i = threadIdx.x; i < nQ; i += kEssmThreads) {
-    const int ig = i + (hG - hQ), ia = i + (hA - hQ);
-    float q = 0.f;
-    for (int k = -kap; k <= kap; ++k) q = fmaf(sh_eta[k + kap], C[ig + k], q);  // c_{m+k}
-    q *= gam;
-    Q[i] = q;
-    const float phi = gam * PSI[ig];
-    float s, c;
-    sincos_phase<FAST>(phi, &s, &c);
-    const float2 gv = upk(G[ig]), av = upk(A[ia]);
-    // g e^{-j phi} + 2 q a
-    GA[i] = pk(fmaf(gv.x, c, fmaf(gv.y, s, 2.f * q * av.x)), fmaf(gv.y, c, fmaf(-gv.x, s, 2.f * q * av.y)));
+  // q and ga on hQ: Q index i <-> G/C index i + kappa, A index i + 2 kappa
+  for (int o0 = threadIdx.x * kEQ; o0 < nQ; o0 += kEssmThreads * kEQ) {
+    float qv[kEQ];
+    essm_rfilt(C, o0 + kap, kap, tt_b, qv);  // sum_k eta_k c_{m+k}
+#pragma unroll
+    for (int q = 0; q < kEQ; ++q) {
+      const int i = o0 + q;
+      if (i >= nQ) break;
+      const float qq = gam * qv[q];
+      float s, c;
+      sincos_phase<FAST>(gam * PSI[pfl(i + kap)], &s, &c);
+      const float2 gv = upk(G[pcx(i + kap)]), av = upk(A[pcx(i + 2 * kap)]);
+      GA[pcx(i)] = pk(fmaf(gv.x, c, fmaf(gv.y, s, 2.f * qq * av.x)), fmaf(gv.y, c, fmaf(-gv.x, s, 2.f * qq * av.y)));
+    }
   }
   __syncthreads();
-  // gu on owned
+  // gu on owned: sum_j conj(h_j) ga_{s+j}, GA index of s is i + KH
   if (a.out) {
     f2x* ob = reinterpret_cast<f2x*>(a.out) + (int64_t)b * a.n;
-    for (int i = threadIdx.x; i < own; i += kEssmThreads) {
-      f2x acc = 0ull;
-      for (int jj = 0; jj < a.T; ++jj) acc = essm_mac_conj(acc, sh_h[jj], GA[i + hQ + (jj - kh)]);  // ga_{s+j}
-      ob[t0 + i] = acc;
+    for (int o0 = threadIdx.x * kEQ; o0 < own; o0 += kEssmThreads * kEQ) {
+      f2x acc[kEQ];
+      essm_cfir<KH, true>(GA, o0 + KH, sh_h, acc);
+#pragma unroll
+      for (int q = 0; q < kEQ; ++q)
+        if (o0 + q < own) ob[t0 + o0 + q] = acc[q];
     }
   }
-  // gradient sums over owned t: component v in [0, V), group r: thread = v * ngroups + r
-  const int ngroups = kEssmThreads / V > 0 ? kEssmThreads / V : 1;
-  const int comp = threadIdx.x / ngroups, grp = threadIdx.x % ngroups;
-  double part = 0.0;
-  if (comp < V) {
-    float acc = 0.f;
-    for (int i = grp; i < own; i += ngroups) {
-      const int ig = i + hG, ia = i + hA, iu = i + hU, iq = i + hQ;
-      if (comp == 0) {
-        acc = fmaf(C[ig], PSI[ig], acc);  // dgamma'
-      } else if (comp == 1) {
-        acc = 0.f;  // loss handled below
-      } else if (comp < 2 + 2 * a.T) {
-        const int jj = (comp - 2) >> 1, im = (comp - 2) & 1;
-        const float2 g = upk(GA[iq]), w = upk(U[iu - (jj - kh)]);  // ga_t conj(u_{t-j})
-        acc += im ? (g.y * w.x - g.x * w.y) : (g.x * w.x + g.y * w.y);
-      } else {
-        const int k = comp - 2 - 2 * a.T - kap;
-        acc = fmaf(C[ig], P[ia - k], acc);  // c_t p_{t-k}
-      }
-    }
-    part = comp >= 2 + 2 * a.T ? (double)gam * acc : (double)acc;
-  }
-  // loss partial: warp sums into the comp == 1 slot
+  // gradient sums over owned t: warp w takes components v = w, w + 8, ... (warp-uniform
+  // branches); its lanes stride over the owned samples, then a fixed-order warp reduction.
   lsum = warp_sum(lsum);
-  __shared__ float lred[kEssmThreads / 32];
-  if ((threadIdx.x & 31) == 0) lred[threadIdx.x >> 5] = lsum;
-  red[threadIdx.x] = part;
-  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cta = blockIdx.y * gridDim.x + blockIdx.x;
-  for (int v = threadIdx.x; v < V; v += kEssmThreads) {
-    double s = 0.0;
-    if (v == 1) {
-      for (int w = 0; w < kEssmThreads / 32; ++w) s += (double)lred[w];
+  double* outp = a.partials + (int64_t)cta * V;
+  __shared__ float lred[kEssmThreads / 32];
+  if (lane == 0) lred[warp] = lsum;
+  for (int comp = warp; comp < V; comp += kEssmThreads / 32) {
+    float acc = 0.f;
+    if (comp == 0) {
+#pragma unroll 4
+      for (int i = lane; i < own; i += 32) acc = fmaf(C[pfl(i + hG)], PSI[pfl(i + hG)], acc);  // dgamma'
+    } else if (comp == 1) {
+      // loss: filled below from lred
+    } else if (comp < 2 + 2 * T) {
+      const int jj = (comp - 2) >> 1, im = (comp - 2) & 1;
+      const int du = hU - (jj - KH);
+      if (im) {
+#pragma unroll 4
+        for (int i = lane; i < own; i += 32) {
+          const float2 g = upk(GA[pcx(i + hQ)]), w = upk(U[pcx(i + du)]);
+          acc = fmaf(g.y, w.x, fmaf(-g.x, w.y, acc));
+        }
+      } else {
+#pragma unroll 4
+        for (int i = lane; i < own; i += 32) {
+          const float2 g = upk(GA[pcx(i + hQ)]), w = upk(U[pcx(i + du)]);
+          acc = fmaf(g.x, w.x, fmaf(g.y, w.y, acc));
+        }
+      }
     } else {
-      for (int r = 0; r < ngroups; ++r) s += red[v * ngroups + r];
+      const int k = comp - 2 - 2 * T - kap;
+      const int dp = hA - k;
+#pragma unroll 4
+      for (int i = lane; i < own; i += 32) acc = fmaf(C[pfl(i + hG)], P[pfl(i + dp)], acc);  // c_t p_{t-k}
     }
-    a.partials[(int64_t)cta * V + v] = s;
+    acc = warp_sum(acc);
+    if (lane == 0 && comp != 1) outp[comp] = comp >= 2 + 2 * T ? (double)gam * acc : (double)acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kEssmThreads / 32; ++w) t += (double)lred[w];
+    outp[1] = t;
   }
 }
 
