@@ -211,6 +211,27 @@ int ldbp_essm_loss_grad(const ldbp_dims* d, int32_t kappa, const void* x, const 
                         void* ws, size_t ws_bytes, void* cuda_stream);
 
 /*
+ * GPU split-step Fourier channel generator (§IV-A): the link
+ * the oracle simulates, per block of n samples (power of two, n <= 16384), in one launch:
+ *   for each of `spans` spans: for each step delta_s (s < steps_per_span, deltas_km_host[s]):
+ *     u <- u e^{j gamma L_eff(delta_s) |u|^2}                     (Kerr at the segment start, G5)
+ *     U_k <- U_k e^{-alpha delta_s / 2} e^{j beta2/2 omega_k^2 delta_s}   (Eqs. (4)-(6))
+ *   then the EDFA: u <- e^{alpha span_km / 2} u + ase_sigma * noise[span]
+ *   omega_k = 2 pi fftfreq(n) fs_hz;  beta2 in s^2/km, alpha in 1/km (nepers), gamma in 1/(W km)
+ * decim == 0: u is overwritten with the channel output;  decim > 0: r [B][n/decim] receives the
+ * brick-wall low-pass (|fftfreq| <= cutoff) output sampled every decim samples (G8).
+ *   noise: [spans][B][n] complex64 CN(0,1) draws (inputs), or NULL (noiseless).
+ * deltas_km_host is a HOST array (copied; the call synchronises the stream once for it).
+ * fp32 in shared memory (radix-2 FFTs with fp64-accurate twiddles and dispersion factors).
+ */
+int ldbp_ssfm_workspace_bytes(int64_t n, int32_t steps_per_span, size_t* bytes);
+int ldbp_ssfm_link(int64_t batch, int64_t n, int32_t spans, int32_t steps_per_span,
+                   const double* deltas_km_host, double span_km, double alpha_np, double beta2,
+                   double gamma, double fs_hz, double ase_sigma, const void* noise_or_null, void* u,
+                   void* r_or_null, int32_t decim, double cutoff, void* ws, size_t ws_bytes,
+                   void* cuda_stream);
+
+/*
  * Launch tracing (profiling aid; off by default; per calling thread).
  * ldbp_trace_begin(capacity) makes every kernel launch of later calls on this thread be
  * bracketed by two CUDA events recorded on the call's stream (events are created here, not
@@ -227,7 +248,8 @@ typedef enum ldbp_kernel_kind {
   LDBP_K_ADAM = 4,      /* Adam + mask (row a10)                                   */
   LDBP_K_REVERSE = 5,   /* store-all reverse tile kernel (rows a5, a6, a8)         */
   LDBP_K_RX = 6,        /* receiver-chain loss kernels (NEXT-1)                    */
-  LDBP_K_ESSM = 7       /* ESSM step kernels (NEXT-4)                              */
+  LDBP_K_ESSM = 7,      /* ESSM step kernels (NEXT-4)                              */
+  LDBP_K_SSFM = 8       /* SSFM channel generator kernels (NEXT-2)                 */
 } ldbp_kernel_kind;
 
 typedef struct ldbp_trace_record {

@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     ldbp_loss_grad,
     ldbp_rx_loss_grad,
     ldbp_rx_train_grad,
+    ldbp_ssfm_link,
     ldbp_train_step,
     make_dims,
     workspace_bytes,

@@ -36,9 +36,11 @@ EXPORTED = (
     "ldbp_essm_workspace_bytes",
     "ldbp_essm_forward",
     "ldbp_essm_loss_grad",
+    "ldbp_ssfm_workspace_bytes",
+    "ldbp_ssfm_link",
 )
 
-K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM, K_REVERSE, K_RX, K_ESSM = 1, 2, 3, 4, 5, 6, 7
+K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM, K_REVERSE, K_RX, K_ESSM, K_SSFM = 1, 2, 3, 4, 5, 6, 7, 8
 
 
 class LdbpDims(ctypes.Structure):
@@ -101,6 +103,10 @@ def _load():
         "ldbp_essm_workspace_bytes": (ctypes.c_int, [D, ctypes.c_int32, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
         "ldbp_essm_forward": (ctypes.c_int, [D, ctypes.c_int32, P, P, P, P, P, P, ctypes.c_size_t, P]),
         "ldbp_essm_loss_grad": (ctypes.c_int, [D, ctypes.c_int32, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
+        "ldbp_ssfm_workspace_bytes": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]),
+        "ldbp_ssfm_link": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.POINTER(ctypes.c_double), dbl, dbl, dbl, dbl, dbl, dbl, P, P, P,
+                                          ctypes.c_int32, dbl, P, ctypes.c_size_t, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -19,6 +19,7 @@
 #include "ldbp_kernels.cuh"
 #include "ldbp_rx.cuh"
 #include "ldbp_essm.cuh"
+#include "ldbp_ssfm.cuh"
 
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
@@ -1358,6 +1359,84 @@ int ldbp_essm_loss_grad(const ldbp_dims* d, int32_t kappa, const void* x, const 
     ldbp::essm_reduce_kernel<<<(M * w.V + 255) / 256, 256, 0, st>>>(r);
   }
   return cuda_check("essm_reduce_kernel launch");
+}
+
+// ---- GPU SSFM channel generator (§8(f) NEXT-2), ldbp_ssfm.cuh ----
+static size_t ssfm_ws_bytes(int64_t n, int S) {
+  return align256(sizeof(float2) * (size_t)S * n) + align256(sizeof(double) * S) + align256(sizeof(float) * S);
+}
+
+int ldbp_ssfm_workspace_bytes(int64_t n, int32_t steps_per_span, size_t* bytes) {
+  g_err[0] = 0;
+  if (!bytes) return fail(LDBP_EINVAL, "bytes is NULL");
+  if (n < 2 || (n & (n - 1)) || n > (1 << ldbp::kSsfmMaxLog2))
+    return fail(LDBP_ESHAPE, "n %lld must be a power of two in [2, %d]", (long long)n, 1 << ldbp::kSsfmMaxLog2);
+  if (steps_per_span < 1) return fail(LDBP_ESHAPE, "steps_per_span %d < 1", steps_per_span);
+  *bytes = ssfm_ws_bytes(n, steps_per_span);
+  return LDBP_OK;
+}
+
+int ldbp_ssfm_link(int64_t batch, int64_t n, int32_t spans, int32_t steps_per_span, const double* deltas_km_host,
+                   double span_km, double alpha_np, double beta2, double gamma, double fs_hz, double ase_sigma,
+                   const void* noise_or_null, void* u, void* r_or_null, int32_t decim, double cutoff, void* ws,
+                   size_t ws_bytes, void* cuda_stream) {
+  g_err[0] = 0;
+  size_t need = 0;
+  LDBP_TRY(ldbp_ssfm_workspace_bytes(n, steps_per_span, &need));
+  if (batch < 0 || spans < 0) return fail(LDBP_ESHAPE, "batch and spans must be >= 0");
+  if (batch == 0) return LDBP_OK;
+  if (!deltas_km_host) return fail(LDBP_EINVAL, "deltas_km_host is NULL");
+  LDBP_TRY(check_ptr(u, "u", 8));
+  if (noise_or_null) LDBP_TRY(check_ptr(noise_or_null, "noise", 8));
+  if (decim > 0) {
+    LDBP_TRY(check_ptr(r_or_null, "r", 8));
+    if (n % decim) return fail(LDBP_ESHAPE, "n %% decim != 0");
+  }
+  if (!ws || ws_bytes < need) return fail(LDBP_EWORKSPACE, "ssfm needs %zu workspace bytes, got %zu", need, ws_bytes);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int S = steps_per_span;
+  unsigned char* wb = (unsigned char*)ws;
+  float2* H = reinterpret_cast<float2*>(wb);
+  double* dd = reinterpret_cast<double*>(wb + align256(sizeof(float2) * (size_t)S * n));
+  float* kp = reinterpret_cast<float*>(wb + align256(sizeof(float2) * (size_t)S * n) + align256(sizeof(double) * S));
+  std::vector<float> kph(S);
+  for (int s = 0; s < S; ++s) {
+    const double d = deltas_km_host[s];
+    const double leff = alpha_np == 0.0 ? d : (1.0 - exp(-alpha_np * d)) / alpha_np;
+    kph[s] = (float)(gamma * leff);
+  }
+  if (cudaMemcpyAsync(dd, deltas_km_host, sizeof(double) * S, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(kp, kph.data(), sizeof(float) * S, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return fail(LDBP_ECUDA, "cudaMemcpyAsync: %s", cudaGetErrorString(cudaGetLastError()));
+  if (cudaStreamSynchronize(st) != cudaSuccess)  // kph lives on this host stack frame
+    return fail(LDBP_ECUDA, "cudaStreamSynchronize: %s", cudaGetErrorString(cudaGetLastError()));
+  {
+    TraceScope ts(LDBP_K_SSFM, S, 0, st);
+    ldbp::ssfm_htable_kernel<<<256, 256, 0, st>>>(H, dd, S, n, alpha_np, beta2, fs_hz);
+  }
+  LDBP_TRY(cuda_check("ssfm_htable_kernel launch"));
+  ldbp::SsfmArgs a;
+  a.u = (float2*)u;
+  a.r = (float2*)r_or_null;
+  a.H = H;
+  a.noise = (const float2*)noise_or_null;
+  a.kerr_phase = kp;
+  a.n = n;
+  a.log2n = 0;
+  while ((int64_t(1) << a.log2n) < n) ++a.log2n;
+  a.spans = spans;
+  a.S = S;
+  a.decim = decim;
+  a.span_gain = (float)exp(0.5 * alpha_np * span_km);
+  a.ase_sigma = (float)ase_sigma;
+  a.cutoff = (float)cutoff;
+  const size_t smem = sizeof(float2) * (size_t)n * 3 / 2;
+  cudaFuncSetAttribute((const void*)ldbp::ssfm_link_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    TraceScope ts(LDBP_K_SSFM, spans * S, batch * n, st);
+    ldbp::ssfm_link_kernel<<<(unsigned)batch, ldbp::kSsfmThreads, smem, st>>>(a);
+  }
+  return cuda_check("ssfm_link_kernel launch");
 }
 
 int ldbp_trace_begin(int capacity) {
