@@ -283,10 +283,11 @@ struct FwdPlan {
   int steps_per = 1;  // steps per launch (last may be shorter)
 };
 
-FwdPlan plan_fwd_segments(int M, int kh) {
+FwdPlan plan_fwd_segments(int M, int kh, int R = 0) {
+  if (R == 0) R = ldbp::fwd_r(kh);
   FwdPlan p;
   if (M <= 0) return p;
-  const int cap = std::min(env_int("LDBP_FWD_THREADS", kFwdMaxThreads), ldbp::fwd_max_threads(kh)) * kFwdR;
+  const int cap = std::min(env_int("LDBP_FWD_THREADS", kFwdMaxThreads), ldbp::fwd_max_threads(kh)) * R;
   int cmax = kh > 0 ? std::max(1, cap / (16 * kh)) : M;
   cmax = std::min(cmax, env_int("LDBP_FWD_MAX_STEPS", 1 << 30));
   p.segs = (int)cdiv(M, cmax);
@@ -355,7 +356,8 @@ Tile plan_fwd_tile(const ldbp_dims* d, int steps, bool query_device, bool staged
     sms = device_sms();
     occ = fwd_occupancy(staged ? get_fwd_store(kh, sym) : get_fwd(kh, sym, !(d->flags & LDBP_PRECISE)), maxthr, smem);
   }
-  Tile t = plan_tiles(d->batch, d->n, steps * kh, kFwdR, maxthr, occ, sms, /*align_r=*/staged);
+  Tile t = plan_tiles(d->batch, d->n, steps * kh, staged ? kFwdR : ldbp::fwd_r(kh), maxthr, occ, sms,
+                      /*align_r=*/staged);
   t.smem = fwd_smem(kh, sym, steps, t.nthreads, 0, staged);
   return t;
 }
@@ -726,7 +728,7 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
   auto gb = [&](int k) -> float2* { return reinterpret_cast<float2*>(ws + w.g_off + (size_t)(k & 1) * w.g_each); };
   const int64_t stride = (int64_t)(w.act_each / sizeof(float2));
   if (!skip_forward) {
-    const FwdPlan fp = plan_fwd_segments(M, kh);
+    const FwdPlan fp = plan_fwd_segments(M, kh, kFwdR);  // store-all forward: R = LDBP_FWD_R
     for (int k = 0; k < fp.segs; ++k) {
       const int s0 = k * fp.steps_per, s1 = std::min(M, s0 + fp.steps_per);
       LDBP_TRY(launch_fwd(d, s0 == 0 ? x : act(s0), act(s1), taps, gamma, mask, s0, s1, st,
@@ -999,7 +1001,8 @@ int ldbp_launch_count(const ldbp_dims* d, int op, int* launches) {
   if (op == LDBP_OP_FORWARD) { *launches = plan_fwd_segments(d->steps, (d->taps - 1) / 2).segs; return LDBP_OK; }
   if (use_store_all(d)) {
     const RevPlan rp = plan_rev(d, true);
-    int n = plan_fwd_segments(d->steps, (d->taps - 1) / 2).segs + rp.Kr + 1 + (reduce_chunks(rp.tile.grid) > 0 ? 1 : 0);
+    int n = plan_fwd_segments(d->steps, (d->taps - 1) / 2, kFwdR).segs + rp.Kr + 1 +
+            (reduce_chunks(rp.tile.grid) > 0 ? 1 : 0);
     if (op == LDBP_OP_TRAIN_STEP) n += 1;
     *launches = n;
     return LDBP_OK;

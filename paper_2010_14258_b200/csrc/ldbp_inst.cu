@@ -14,7 +14,7 @@ using RevFn = void (*)(const ldbp::RevArgs);
 #define LDBP_CAT(a, b) LDBP_CAT2(a, b)
 
 FwdFn LDBP_CAT(ldbp_get_fwd_, LDBP_KH)(bool sym, bool fast) {
-  constexpr int K = LDBP_KH, R = LDBP_FWD_R;
+  constexpr int K = LDBP_KH, R = ldbp::fwd_r(LDBP_KH);
   if (sym) return fast ? ldbp::fwd_tile_kernel<K, R, true, true> : ldbp::fwd_tile_kernel<K, R, true, false>;
   return fast ? ldbp::fwd_tile_kernel<K, R, false, true> : ldbp::fwd_tile_kernel<K, R, false, false>;
 }

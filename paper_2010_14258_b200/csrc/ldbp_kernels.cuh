@@ -827,6 +827,13 @@ struct FwdArgs {
 #ifndef LDBP_FWD_WIDE_THREADS
 #define LDBP_FWD_WIDE_THREADS 256
 #endif
+// Samples per thread of the inference / checkpoint forward tile kernel: 32 for wide filters
+// (per-step overhead halved; measured C4 Kh = 7: 0.72 vs 0.63 of peak), 16 otherwise (C2 Kh = 2:
+// 0.49 vs 0.40).  The store-all forward (training) keeps LDBP_FWD_R: its stage is R-sized.
+#ifndef LDBP_FWD_R32_KH
+#define LDBP_FWD_R32_KH 5
+#endif
+__host__ __device__ constexpr int fwd_r(int kh) { return kh >= LDBP_FWD_R32_KH ? 32 : LDBP_FWD_R; }
 // register target per thread for each Kh (packed taps cost 4 registers each)
 __host__ __device__ constexpr int fwd_regs(int kh) { return kh <= 2 ? 64 : kh <= 5 ? 80 : 128; }
 #ifdef LDBP_FWD_NTHR  // tuning override: fixed CTA size, residency from the register target
@@ -843,8 +850,11 @@ __host__ __device__ constexpr int fwd_stage_elems(int kh, int r) { return fwd_ma
 #ifdef LDBP_FWD_NTHR
 __host__ __device__ constexpr int fwd_min_blocks(int kh) { return 65536 / (LDBP_FWD_NTHR * fwd_regs(kh)); }
 #else
+#ifndef LDBP_FWD_SMALL_MINB
+#define LDBP_FWD_SMALL_MINB 8  // Kh <= 2: resident 128-thread CTAs per SM (register budget 64)
+#endif
 __host__ __device__ constexpr int fwd_min_blocks(int kh) {
-  return kh <= 2 ? 8 : kh <= 4 ? 3 : (LDBP_FWD_WIDE_THREADS >= 512 && kh >= 6) ? 1 : 2;
+  return kh <= 2 ? LDBP_FWD_SMALL_MINB : kh <= 4 ? 3 : (LDBP_FWD_WIDE_THREADS >= 512 && kh >= 6) ? 1 : 2;
 }
 #endif
 
