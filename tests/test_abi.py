@@ -73,3 +73,51 @@ def test_forward_workspace_and_launch_plan(L):
     assert out.value >= 4096 * 16384 * 8  # chained launches need one ping-pong buffer
     assert lib.ldbp_launch_count(ctypes.byref(d), 0, ctypes.byref(nl)) == 0 and nl.value >= 2
     assert lib.ldbp_workspace_bytes(ctypes.byref(d), 9, ctypes.byref(out)) == -1
+
+
+def test_store_all_schedule_workspace(L):
+    """Backward / loss_grad / train use the store-all schedule when B*n >= 2^20 and the
+    activations fit the budget: the workspace holds all M activations; tiny or over-budget
+    problems use the checkpoint schedule (ldbp.h)."""
+    lib = L.lib
+    out = ctypes.c_size_t(0)
+    d = L.dims(512, 16384, 50, 9, 1)  # C3
+    assert lib.ldbp_workspace_bytes(ctypes.byref(d), 2, ctypes.byref(out)) == 0
+    assert out.value >= 50 * 512 * 16384 * 8
+    d1 = L.dims(4, 1024, 4, 3, 1)  # C1: segments
+    assert lib.ldbp_workspace_bytes(ctypes.byref(d1), 2, ctypes.byref(out)) == 0
+    assert out.value < 4 * 4 * 1024 * 8
+    os.environ["LDBP_BWD_MODE"] = "0"
+    try:
+        assert lib.ldbp_workspace_bytes(ctypes.byref(d), 2, ctypes.byref(out)) == 0
+        assert out.value < 50 * 512 * 16384 * 8 // 4
+    finally:
+        del os.environ["LDBP_BWD_MODE"]
+
+
+def test_rx_essm_ssfm_validation(L):
+    """The NEXT-row entry points validate shapes and pointers before any launch."""
+    lib = L.lib
+    P = ctypes.c_void_p
+    f = P(0x10000)
+    out = ctypes.c_size_t(0)
+    # receiver chain: n % sps, MF length, sps range
+    assert lib.ldbp_rx_workspace_bytes(2, 1001, 2, ctypes.byref(out)) == -2
+    assert lib.ldbp_rx_workspace_bytes(2, 1024, 5, ctypes.byref(out)) == -2
+    assert lib.ldbp_rx_workspace_bytes(2, 1024, 2, ctypes.byref(out)) == 0 and out.value > 0
+    assert lib.ldbp_rx_loss_grad(2, 1024, 2, 600, f, f, f, f, f, None, f, 1 << 20, None) == -2  # 2L+1 > n
+    assert lib.ldbp_rx_loss_grad(2, 1024, 2, 64, None, f, f, f, f, None, f, 1 << 20, None) == -1
+    assert lib.ldbp_rx_loss_grad(2, 1024, 2, 64, f, f, f, f, f, f, f, 1 << 20, None) == -1  # gy aliases y
+    assert lib.ldbp_rx_loss_grad(2, 1024, 2, 64, f, f, f, f, f, None, f, 0, None) == -4   # workspace
+    assert lib.ldbp_rx_loss_grad(0, 1024, 2, 64, None, None, None, None, None, None, None, 0, None) == 0
+    # ESSM: kappa range and filter length
+    d = L.dims(2, 32, 3, 5, 1)
+    assert lib.ldbp_essm_workspace_bytes(ctypes.byref(d), 33, 0, ctypes.byref(out)) == -2
+    assert lib.ldbp_essm_workspace_bytes(ctypes.byref(d), 16, 0, ctypes.byref(out)) == -2  # 33 > n
+    assert lib.ldbp_essm_workspace_bytes(ctypes.byref(d), 4, 2, ctypes.byref(out)) == 0
+    assert out.value >= 3 * 2 * 32 * 8
+    assert lib.ldbp_essm_workspace_bytes(ctypes.byref(d), 4, 1, ctypes.byref(out)) == -1  # no BACKWARD op
+    # SSFM: power-of-two n <= 2^14
+    assert lib.ldbp_ssfm_workspace_bytes(1000, 4, ctypes.byref(out)) == -2
+    assert lib.ldbp_ssfm_workspace_bytes(1 << 15, 4, ctypes.byref(out)) == -2
+    assert lib.ldbp_ssfm_workspace_bytes(1 << 14, 4, ctypes.byref(out)) == 0 and out.value >= 4 * (1 << 14) * 8
