@@ -31,7 +31,7 @@
 #define LDBP_BWD_R 8   // samples per thread, backward kernels
 #endif
 #ifndef LDBP_REV_R
-#define LDBP_REV_R 16  // samples per thread, store-all reverse kernel
+#define LDBP_REV_R 12  // samples per thread, store-all reverse kernel (measured: 12 >= 16 > 8)
 #endif
 
 #ifndef LDBP_NORM
