@@ -1415,7 +1415,9 @@ int ldbp_ssfm_link(int64_t batch, int64_t n, int32_t spans, int32_t steps_per_sp
     return fail(LDBP_ECUDA, "cudaStreamSynchronize: %s", cudaGetErrorString(cudaGetLastError()));
   {
     TraceScope ts(LDBP_K_SSFM, S, 0, st);
-    ldbp::ssfm_htable_kernel<<<256, 256, 0, st>>>(H, dd, S, n, alpha_np, beta2, fs_hz);
+    int lg = 0;
+    while ((int64_t(1) << lg) < n) ++lg;
+    ldbp::ssfm_htable_kernel<<<256, 256, 0, st>>>(H, dd, S, n, alpha_np, beta2, fs_hz, lg);
   }
   LDBP_TRY(cuda_check("ssfm_htable_kernel launch"));
   ldbp::SsfmArgs a;
@@ -1433,7 +1435,7 @@ int ldbp_ssfm_link(int64_t batch, int64_t n, int32_t spans, int32_t steps_per_sp
   a.span_gain = (float)exp(0.5 * alpha_np * span_km);
   a.ase_sigma = (float)ase_sigma;
   a.cutoff = (float)cutoff;
-  const size_t smem = sizeof(float2) * (size_t)n * 3 / 2;
+  const size_t smem = sizeof(float2) * ((size_t)n + n / 16 + 1 + n / 2);
   cudaFuncSetAttribute((const void*)ldbp::ssfm_link_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   {
     TraceScope ts(LDBP_K_SSFM, spans * S, batch * n, st);
