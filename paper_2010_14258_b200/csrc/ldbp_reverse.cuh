@@ -58,6 +58,20 @@ __device__ __forceinline__ const float2* rev_src(const RevArgs& a, int i) {
 #define LDBP_REV_VARK 0  // per-step active tap length in the reverse (off: the alternating code
                          // variants cost more in instruction fetch than the skipped taps save)
 #endif
+#ifndef LDBP_REV_TAPS_SMEM
+#define LDBP_REV_TAPS_SMEM 0  // 1: read the packed adjoint taps from shared memory at every use
+#endif
+template <int N>
+__device__ __forceinline__ TapP rev_tap(const TapP (&hs)[N], const TapP* hs_sm, int j) {
+  if constexpr (LDBP_REV_TAPS_SMEM) {
+    TapP t;  // asm volatile: one LDS.128 (broadcast) per use, not hoisted into registers
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(t.a), "=l"(t.b) : "r"(smem_u32(hs_sm + j)));
+    return t;
+  } else {
+    (void)hs_sm;
+    return hs[j];
+  }
+}
 template <int KH, bool SYM, bool NORM, bool FAST>
 __device__ __forceinline__ constexpr bool rev_vark() { return LDBP_REV_VARK && SYM && NORM && FAST && KH >= 1; }
 #ifndef LDBP_NB_WAIT
@@ -143,7 +157,7 @@ template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL, i
           int S0 = SB>
 __device__ __forceinline__ void rev_range(const f2x (&g)[R], const f2x (&gl)[KH > 0 ? KH : 1],
                                           const f2x (&gr)[KH > 0 ? KH : 1], const f2x* __restrict__ ub_mine,
-                                          const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1],
+                                          const TapP (&hs)[SYM ? KH + 1 : 2 * KH + 1], const TapP* hs_sm,
                                           f2x (&A)[SYM ? KH + 1 : 2 * KH + 1], f2x (&Bq)[SYM ? KH + 1 : 2 * KH + 1],
                                           f2x (&ng)[R], uint32_t own, float gmn, float& dgam_next) {
   if constexpr (S0 < SE) {
@@ -154,12 +168,12 @@ __device__ __forceinline__ void rev_range(const f2x (&g)[R], const f2x (&gl)[KH 
     f2x acc;
     if constexpr (SYM) {
       const f2x g0 = g[s];
-      acc = NORM ? g0 : tmul(hs[0], g0);
+      acc = NORM ? g0 : tmul(rev_tap(hs, hs_sm, 0), g0);
       if (mine) { A[0] = fma2(ux, g0, A[0]); Bq[0] = fma2(uy, g0, Bq[0]); }
 #pragma unroll
       for (int j = 1; j <= KJ; ++j) {
         const f2x P = add2(LDBP_WIN(g, gl, gr, s - j), LDBP_WIN(g, gl, gr, s + j));
-        acc = tmac(acc, hs[j], P);
+        acc = tmac(acc, rev_tap(hs, hs_sm, j), P);
         if (mine) { A[j] = fma2(ux, P, A[j]); Bq[j] = fma2(uy, P, Bq[j]); }
       }
     } else {
@@ -167,14 +181,14 @@ __device__ __forceinline__ void rev_range(const f2x (&g)[R], const f2x (&gl)[KH 
 #pragma unroll
       for (int jj = 0; jj < 2 * KH + 1; ++jj) {
         const f2x P = LDBP_WIN(g, gl, gr, s + (jj - KH));
-        acc = tmac(acc, hs[jj], P);
+        acc = tmac(acc, rev_tap(hs, hs_sm, jj), P);
         if (mine) { A[jj] = fma2(ux, P, A[jj]); Bq[jj] = fma2(uy, P, Bq[jj]); }
       }
     }
     if constexpr (NL) nl_adjoint<FAST, MASKED>(acc, us, gmn, 2.f * gmn, (own >> s) & 1u, dgam_next);
     ng[s] = acc;
-    rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, SB, SE, KJ, S0 + 1>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn,
-                                                                      dgam_next);
+    rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, SB, SE, KJ, S0 + 1>(g, gl, gr, ub_mine, hs, hs_sm, A, Bq, ng, own,
+                                                                      gmn, dgam_next);
   }
 }
 
@@ -190,14 +204,14 @@ __device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub
   constexpr int KI = KJ < R - KJ ? KJ : R / 2;  // interior [KI, R-KI)
   TapP hs[NTU];
 #pragma unroll
-  for (int j = 0; j < NTU; ++j) hs[j] = hs_sm[j];
+  for (int j = 0; j < NTU; ++j) hs[j] = LDBP_REV_TAPS_SMEM ? TapP{0ull, 0ull} : hs_sm[j];
   f2x A[NTU], Bq[NTU], ng[R];
 #pragma unroll
   for (int j = 0; j < NTU; ++j) A[j] = Bq[j] = 0ull;
   f2x gl[KH > 0 ? KH : 1], gr[KH > 0 ? KH : 1];
 #pragma unroll
   for (int j = 0; j < (KH > 0 ? KH : 1); ++j) gl[j] = gr[j] = 0ull;
-  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, KI, R - KI, KJ>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn,
+  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, KI, R - KI, KJ>(g, gl, gr, ub_mine, hs, hs_sm, A, Bq, ng, own, gmn,
                                                                  dgam_next);
   if constexpr (KH > 0) {
     if constexpr (LDBP_NB_WAIT) {
@@ -220,8 +234,8 @@ __device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub
       gr[j] = right_edge[eoff + j * NT];
     }
   }
-  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, 0, KI, KJ>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn, dgam_next);
-  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, R - KI, R, KJ>(g, gl, gr, ub_mine, hs, A, Bq, ng, own, gmn,
+  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, 0, KI, KJ>(g, gl, gr, ub_mine, hs, hs_sm, A, Bq, ng, own, gmn, dgam_next);
+  rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, R - KI, R, KJ>(g, gl, gr, ub_mine, hs, hs_sm, A, Bq, ng, own, gmn,
                                                                dgam_next);
 #pragma unroll
   for (int j = 0; j < NTU; ++j) {
@@ -416,8 +430,17 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   }
 }
 
+// Register budget per thread (occupancy 65536 / (threads * regs) CTAs/SM).  Measured: Kh >= 2
+// needs 128 (tighter budgets spill: C3 reverse 2.02 ms at 128 vs 2.30 at 96); Kh <= 1 fits 80
+// (C5 reverse 18.3 vs 19.3 ms).  Taps stay in registers (LDBP_REV_TAPS_SMEM=1 was slower).
+#ifdef LDBP_REV_REGS
+__host__ __device__ constexpr int rev_regs(int) { return LDBP_REV_REGS; }
+#else
+__host__ __device__ constexpr int rev_regs(int kh) { return kh <= 1 ? 80 : 128; }
+#endif
 template <int KH, int R, bool SYM, bool FAST>
-__global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * 128)) rev_tile_kernel(const RevArgs a) {
+__global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * rev_regs(KH)))
+    rev_tile_kernel(const RevArgs a) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   constexpr int V = 1 + 2 * NTU;
   constexpr int NT = rev_threads(KH), NW = NT / 32;
