@@ -311,6 +311,51 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
                 B=B, n=n, wall_s=t_wall1 - t_wall0)
 
 
+def graph_latency(cfg, reps=50):
+    """Per-step device time with the whole step (forward, or loss_grad + Adam) captured in one CUDA
+    graph and replayed back to back (graphs hide the launch cost of C1/C2)."""
+    import torch
+
+    import paper_2010_14258_b200 as P
+
+    taps, gamma = make_model(cfg)
+    x, tgt = make_inputs(cfg, 0)
+    st = P.TrainState.create(taps, gamma)
+    ws = P.Workspace()
+    train = cfg["mode"] == "train"
+    M, T = taps.shape
+    buf = torch.empty(1 + M + 2 * M * T, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+
+    def step():
+        if train:
+            P.ldbp_loss_grad(x, tgt, st.taps, st.gamma, buf=buf, ws=ws)
+            P.ldbp_adam_update(st, buf, cfg["B"] * cfg["n"])
+        else:
+            P.ldbp_forward(x, st.taps, st.gamma, out=y, ws=ws)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3  # us
+
+
 def traffic_from_profiles(cfg_name, kernel):
     """dram bytes per launch from a committed `ncu --set full` summary, if one exists."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
@@ -452,6 +497,12 @@ def main():
             extra[nm] = {"workload": WORKLOAD[nm], "mode": c["mode"], "value": rr["value"], "unit": UNIT,
                          "ms_per_step": rr["ms_per_step"], "roofline": rr["roof"], "step_roofline": rr["step_roof"],
                          "kernel_shares": rr["kernel_shares"]}
+            if nm in ("C1", "C2"):  # launch-latency-sensitive: the step as one CUDA graph, replayed
+                us = graph_latency(c)
+                M = len(make_model(c)[1])
+                extra[nm]["cuda_graph"] = {"us_per_step": us, "value": c["B"] * c["n"] * M / (us * 1e-6) / 1e9,
+                                           "unit": UNIT, "note": "whole step in one CUDA graph, back-to-back "
+                                           "replays, inputs L2-resident (C1 is latency-bound)"}
             torch.cuda.empty_cache()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

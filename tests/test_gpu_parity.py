@@ -430,3 +430,29 @@ def test_variable_tap_lengths(P, monkeypatch, mode, B, n, M, T, kh_steps):
     for i in range(M):
         assert rel(dt[i], rdt[i]) <= GRAD_TOL, i
     assert np.all(dt[mask == 0] == 0)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_sharding_bit_identity(P, monkeypatch, mode):
+    """§8(e): forward outputs are bit-identical for any partition of the blocks across ranks (each
+    output sample's arithmetic does not depend on the tiling), and the unreduced gradient buffers
+    of the shards sum to the full buffer up to the grouping of the per-CTA fp32 partial sums (the
+    tiles differ between shardings; every grouping is a valid fp32 sum, ~1e-9 apart)."""
+    monkeypatch.setenv("LDBP_BWD_MODE", mode)
+    monkeypatch.setenv("LDBP_STORE_ALL_MIN_SAMPLES", "0")
+    B, n, M, T = 8, 6000, 10, 9
+    x = dev(li.gaussian_blocks(95, range(B), n, 1e-3))
+    tgt = dev(li.gaussian_blocks(95, range(B), n, 1e-3, purpose="target"))
+    taps, gamma = model(95, M, T, True)
+    ht, gt = dev(taps), dev(gamma, np.float32)
+    y = P.ldbp_forward(x, ht, gt)
+    for parts in ((4, 4), (2, 2, 2, 2), (1, 7), (3, 5)):
+        o = 0
+        for p in parts:
+            ys = P.ldbp_forward(x[o:o + p].contiguous(), ht, gt)
+            assert torch.equal(ys, y[o:o + p]), (parts, o)
+            o += p
+    full = P.ldbp_loss_grad(x, tgt, ht, gt).cpu().numpy()
+    sh = sum(P.ldbp_loss_grad(x[o:o + 4].contiguous(), tgt[o:o + 4].contiguous(), ht, gt).cpu().numpy()
+             for o in (0, 4))
+    assert rel(sh, full) <= 1e-7
