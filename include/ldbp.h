@@ -58,7 +58,14 @@ enum ldbp_flags {
      return tied-parameter gradients: dtaps[j] = dtaps[-j] = g_j + g_{-j}. */
   LDBP_SYMMETRIC = 1u,
   /* Use IEEE-accurate sincosf for the Kerr rotation instead of the MUFU approximation. */
-  LDBP_PRECISE = 2u
+  LDBP_PRECISE = 2u,
+  /* Check every step's activations for non-finite values (SPEC "NaN in activations -> error with
+     layer index"): the forward kernels flag the first step whose output holds a NaN/Inf;
+     the call then synchronises its stream once and returns LDBP_ENONFINITE with the 1-based step
+     in ldbp_last_error().  Applies to ldbp_forward/backward/loss_grad/train_step/rx_train_grad
+     (the training calls then use the store-all schedule, so every step is checked); it adds
+     256 workspace bytes. */
+  LDBP_CHECK_FINITE = 4u
 };
 
 typedef enum ldbp_status {
@@ -67,7 +74,8 @@ typedef enum ldbp_status {
   LDBP_ESHAPE = -2,      /* T even, T > LDBP_MAX_TAPS, T > n, M < 1, n < 1, B < 0          */
   LDBP_EALIGN = -3,      /* a complex pointer is not 8-byte aligned, a double one not 8-byte */
   LDBP_EWORKSPACE = -4,  /* ws_bytes < ldbp_workspace_bytes(...) or ws == NULL when needed  */
-  LDBP_ECUDA = -5        /* a CUDA runtime error (detail in ldbp_last_error())               */
+  LDBP_ECUDA = -5,       /* a CUDA runtime error (detail in ldbp_last_error())               */
+  LDBP_ENONFINITE = -6   /* LDBP_CHECK_FINITE: a step produced NaN/Inf (step in ldbp_last_error()) */
 } ldbp_status;
 
 typedef enum ldbp_op {

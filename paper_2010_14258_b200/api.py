@@ -11,7 +11,8 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib
-from ._lib import LDBP_PRECISE, LDBP_SYMMETRIC, OP_BACKWARD, OP_FORWARD, OP_LOSS_GRAD, OP_TRAIN_STEP, check, lib
+from ._lib import (LDBP_CHECK_FINITE, LDBP_PRECISE, LDBP_SYMMETRIC, OP_BACKWARD, OP_FORWARD, OP_LOSS_GRAD,
+                   OP_TRAIN_STEP, check, lib)
 
 _VP = ctypes.c_void_p
 
@@ -25,8 +26,9 @@ def _stream_handle(stream=None):
     return _VP(s.cuda_stream)
 
 
-def _flags(symmetric: bool, precise: bool) -> int:
-    return (LDBP_SYMMETRIC if symmetric else 0) | (LDBP_PRECISE if precise else 0)
+def _flags(symmetric: bool, precise: bool, check_finite: bool = False) -> int:
+    return ((LDBP_SYMMETRIC if symmetric else 0) | (LDBP_PRECISE if precise else 0)
+            | (LDBP_CHECK_FINITE if check_finite else 0))
 
 
 def _need(t, name, dtype, shape=None):
@@ -42,8 +44,8 @@ def _need(t, name, dtype, shape=None):
         raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
 
 
-def make_dims(B, n, M, T, symmetric=True, precise=False):
-    return _lib.dims(B, n, M, T, _flags(symmetric, precise))
+def make_dims(B, n, M, T, symmetric=True, precise=False, check_finite=False):
+    return _lib.dims(B, n, M, T, _flags(symmetric, precise, check_finite))
 
 
 def workspace_bytes(d, op: int) -> int:
@@ -95,10 +97,12 @@ def _check_model(x, taps, gamma):
     return x.shape[0], x.shape[1], M, T
 
 
-def ldbp_forward(x, taps, gamma, *, symmetric=True, precise=False, out=None, ws=None, stream=None):
-    """y = f_theta(x) (Eq. 7) for complex64 x [B][n], taps [M][T], gamma [M]."""
+def ldbp_forward(x, taps, gamma, *, symmetric=True, precise=False, check_finite=False, out=None, ws=None,
+                 stream=None):
+    """y = f_theta(x) (Eq. 7) for complex64 x [B][n], taps [M][T], gamma [M].  check_finite:
+    raise LdbpError (LDBP_ENONFINITE, with the first failing step) on NaN/Inf activations."""
     B, n, M, T = _check_model(x, taps, gamma)
-    d = make_dims(B, n, M, T, symmetric, precise)
+    d = make_dims(B, n, M, T, symmetric, precise, check_finite)
     y = torch.empty_like(x) if out is None else out
     _need(y, "out", torch.complex64, x.shape)
     nb = workspace_bytes(d, OP_FORWARD)
@@ -123,14 +127,14 @@ def ldbp_backward(x, gy, taps, gamma, *, symmetric=True, precise=False, need_gx=
     return torch.view_as_complex(dt), dg, gx
 
 
-def ldbp_loss_grad(x, target, taps, gamma, *, mask=None, symmetric=True, precise=False, buf=None, ws=None,
-                   stream=None):
+def ldbp_loss_grad(x, target, taps, gamma, *, mask=None, symmetric=True, precise=False, check_finite=False,
+                   buf=None, ws=None, stream=None):
     """[sum|e|^2 | dgamma[M] | dtaps[M][T][2]] (float64, unscaled, this device's blocks only)."""
     B, n, M, T = _check_model(x, taps, gamma)
     _need(target, "target", torch.complex64, x.shape)
     if mask is not None:
         _need(mask, "mask", torch.uint8, (M, T))
-    d = make_dims(B, n, M, T, symmetric, precise)
+    d = make_dims(B, n, M, T, symmetric, precise, check_finite)
     out = torch.empty(1 + M + 2 * M * T, dtype=torch.float64, device=x.device) if buf is None else buf
     nb = workspace_bytes(d, OP_LOSS_GRAD)
     w, nb = _ws(x.device, nb, ws)

@@ -28,6 +28,9 @@ using RevFn = void (*)(const ldbp::RevArgs);
 namespace {
 
 thread_local char g_err[1024] = "";
+thread_local int* g_nonfinite = nullptr;  // LDBP_CHECK_FINITE slot of the current call (device int)
+constexpr size_t kCheckBytes = 256;
+constexpr int kFiniteInit = 0x7f7f7f7f;  // memset(0x7f) pattern: no non-finite step seen
 
 int fail(int status, const char* fmt, ...) {
   va_list ap;
@@ -101,8 +104,8 @@ int ntaps_used(int kh, bool sym) { return sym ? kh + 1 : 2 * kh + 1; }
 
 // Kernel instantiations live in ldbp_inst.cu, compiled once per Kh (parallel build).
 #define LDBP_DECL_GETTERS(K)                        \
-  FwdFn ldbp_get_fwd_##K(bool sym, bool fast);      \
-  FwdFn ldbp_get_fwd_store_##K(bool sym);           \
+  FwdFn ldbp_get_fwd_##K(bool sym, bool fast, bool chk); \
+  FwdFn ldbp_get_fwd_store_##K(bool sym, bool chk); \
   BwdFn ldbp_get_bwd_##K(bool sym, bool fast);      \
   RevFn ldbp_get_rev_##K(bool sym, bool fast);
 }  // namespace
@@ -116,16 +119,16 @@ LDBP_DECL_GETTERS(6)
 LDBP_DECL_GETTERS(7)
 namespace {
 
-FwdFn get_fwd(int kh, bool sym, bool fast) {
+FwdFn get_fwd(int kh, bool sym, bool fast, bool chk = false) {
   switch (kh) {
-    case 0: return ldbp_get_fwd_0(sym, fast);
-    case 1: return ldbp_get_fwd_1(sym, fast);
-    case 2: return ldbp_get_fwd_2(sym, fast);
-    case 3: return ldbp_get_fwd_3(sym, fast);
-    case 4: return ldbp_get_fwd_4(sym, fast);
-    case 5: return ldbp_get_fwd_5(sym, fast);
-    case 6: return ldbp_get_fwd_6(sym, fast);
-    case 7: return ldbp_get_fwd_7(sym, fast);
+    case 0: return ldbp_get_fwd_0(sym, fast, chk);
+    case 1: return ldbp_get_fwd_1(sym, fast, chk);
+    case 2: return ldbp_get_fwd_2(sym, fast, chk);
+    case 3: return ldbp_get_fwd_3(sym, fast, chk);
+    case 4: return ldbp_get_fwd_4(sym, fast, chk);
+    case 5: return ldbp_get_fwd_5(sym, fast, chk);
+    case 6: return ldbp_get_fwd_6(sym, fast, chk);
+    case 7: return ldbp_get_fwd_7(sym, fast, chk);
   }
   return nullptr;
 }
@@ -143,16 +146,16 @@ BwdFn get_bwd(int kh, bool sym, bool fast) {
   return nullptr;
 }
 
-FwdFn get_fwd_store(int kh, bool sym) {
+FwdFn get_fwd_store(int kh, bool sym, bool chk = false) {
   switch (kh) {
-    case 0: return ldbp_get_fwd_store_0(sym);
-    case 1: return ldbp_get_fwd_store_1(sym);
-    case 2: return ldbp_get_fwd_store_2(sym);
-    case 3: return ldbp_get_fwd_store_3(sym);
-    case 4: return ldbp_get_fwd_store_4(sym);
-    case 5: return ldbp_get_fwd_store_5(sym);
-    case 6: return ldbp_get_fwd_store_6(sym);
-    case 7: return ldbp_get_fwd_store_7(sym);
+    case 0: return ldbp_get_fwd_store_0(sym, chk);
+    case 1: return ldbp_get_fwd_store_1(sym, chk);
+    case 2: return ldbp_get_fwd_store_2(sym, chk);
+    case 3: return ldbp_get_fwd_store_3(sym, chk);
+    case 4: return ldbp_get_fwd_store_4(sym, chk);
+    case 5: return ldbp_get_fwd_store_5(sym, chk);
+    case 6: return ldbp_get_fwd_store_6(sym, chk);
+    case 7: return ldbp_get_fwd_store_7(sym, chk);
   }
   return nullptr;
 }
@@ -354,7 +357,7 @@ Tile plan_fwd_tile(const ldbp_dims* d, int steps, bool query_device, bool staged
   const size_t smem = fwd_smem(kh, sym, steps, maxthr, staged ? d->steps : 0, staged);
   if (query_device) {
     sms = device_sms();
-    occ = fwd_occupancy(staged ? get_fwd_store(kh, sym) : get_fwd(kh, sym, !(d->flags & LDBP_PRECISE)), maxthr, smem);
+    occ = fwd_occupancy(staged ? get_fwd_store(kh, sym, g_nonfinite) : get_fwd(kh, sym, !(d->flags & LDBP_PRECISE), g_nonfinite), maxthr, smem);
   }
   Tile t = plan_tiles(d->batch, d->n, steps * kh, staged ? kFwdR : ldbp::fwd_r(kh), maxthr, occ, sms,
                       /*align_r=*/staged);
@@ -420,6 +423,7 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
 // Which training path: 1 = store-all activations + fused reverse (default when the activations
 // fit the budget), 0 = checkpoint + recompute segments (memory-lean fallback).
 bool use_store_all(const ldbp_dims* d) {
+  if (d->flags & LDBP_CHECK_FINITE) return true;  // every step's activation is produced and checked
   const int mode = env_int("LDBP_BWD_MODE", -1);
   if (mode == 0) return false;
   if (mode == 1) return true;
@@ -435,7 +439,8 @@ bool use_store_all(const ldbp_dims* d) {
 int validate_dims(const ldbp_dims* d) {
   if (!d) return fail(LDBP_EINVAL, "dims is NULL");
   if (d->reserved != 0) return fail(LDBP_EINVAL, "dims.reserved must be 0");
-  if (d->flags & ~(uint32_t)(LDBP_SYMMETRIC | LDBP_PRECISE)) return fail(LDBP_EINVAL, "unknown flag bits 0x%x", d->flags);
+  if (d->flags & ~(uint32_t)(LDBP_SYMMETRIC | LDBP_PRECISE | LDBP_CHECK_FINITE))
+    return fail(LDBP_EINVAL, "unknown flag bits 0x%x", d->flags);
   if (d->batch < 0) return fail(LDBP_ESHAPE, "batch %lld < 0", (long long)d->batch);
   if (d->n < 1) return fail(LDBP_ESHAPE, "n %lld < 1", (long long)d->n);
   if (d->steps < 1) return fail(LDBP_ESHAPE, "steps %d < 1", d->steps);
@@ -469,7 +474,7 @@ FwdWs fwd_ws(const ldbp_dims* d) {
   FwdWs w;
   const FwdPlan p = plan_fwd_segments(d->steps, (d->taps - 1) / 2);
   if (p.segs >= 2) w.pingpong = align256(sizeof(float2) * d->batch * d->n);
-  w.total = w.pingpong;
+  w.total = w.pingpong + ((d->flags & LDBP_CHECK_FINITE) ? kCheckBytes : 0);
   return w;
 }
 
@@ -535,9 +540,33 @@ RevWs rev_ws(const ldbp_dims* d, const RevPlan& p) {
   off += align256(sizeof(double) * (size_t)nch * d->steps * p.V);
   w.loss2_off = off;
   off += align256(sizeof(double) * (size_t)nch);
+  if (d->flags & LDBP_CHECK_FINITE) off += kCheckBytes;  // the check slot (last 256 bytes)
   w.total = off;
   return w;
 }
+
+// LDBP_CHECK_FINITE: arm the slot (the last kCheckBytes of the workspace) before the launches, then
+// read it back (one stream synchronisation) and report the first non-finite step.
+struct FiniteCheck {
+  int* slot = nullptr;
+  FiniteCheck(const ldbp_dims* d, void* ws, size_t total, cudaStream_t st) {
+    if (!(d->flags & LDBP_CHECK_FINITE) || !ws) return;
+    slot = reinterpret_cast<int*>((unsigned char*)ws + total - kCheckBytes);
+    cudaMemsetAsync(slot, 0x7f, sizeof(int), st);
+    g_nonfinite = slot;
+  }
+  ~FiniteCheck() { g_nonfinite = nullptr; }
+  int finish(int status, cudaStream_t st) {
+    g_nonfinite = nullptr;
+    if (!slot || status != LDBP_OK) return status;
+    int v = kFiniteInit;
+    if (cudaMemcpyAsync(&v, slot, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return fail(LDBP_ECUDA, "finite check: %s", cudaGetErrorString(cudaGetLastError()));
+    if (v != kFiniteInit) return fail(LDBP_ENONFINITE, "non-finite activation after step %d (1-based)", v);
+    return LDBP_OK;
+  }
+};
 
 // ----------------------------------------------------------------------------------------
 // Launch helpers
@@ -551,12 +580,14 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   const bool staged = global_norm && ckpt && ckpt_every == 1 && fast && env_int("LDBP_FWD_STAGED", 1);
   Tile t = plan_fwd_tile(d, s1 - s0, true, staged);
   if (global_norm) t.smem = fwd_smem(kh, sym, s1 - s0, t.nthreads, d->steps, staged);
-  FwdFn fn = staged ? get_fwd_store(kh, sym) : get_fwd(kh, sym, fast);
+  const bool chk = g_nonfinite != nullptr;
+  FwdFn fn = staged ? get_fwd_store(kh, sym, chk) : get_fwd(kh, sym, fast, chk);
   ldbp::FwdArgs a;
   a.src = src;
   a.dst = dst;
   a.ckpt = ckpt;
   a.y_out = y_out;
+  a.nonfinite = g_nonfinite;
   a.ckpt_stride = ckpt_stride;
   a.ckpt_every = ckpt_every > 0 ? ckpt_every : 1;
   a.taps = taps;
@@ -965,6 +996,7 @@ const char* ldbp_status_string(int s) {
     case LDBP_EALIGN: return "LDBP_EALIGN: misaligned pointer";
     case LDBP_EWORKSPACE: return "LDBP_EWORKSPACE: workspace too small";
     case LDBP_ECUDA: return "LDBP_ECUDA: CUDA runtime error";
+    case LDBP_ENONFINITE: return "LDBP_ENONFINITE: non-finite activation";
   }
   return "LDBP: unknown status";
 }
@@ -1035,8 +1067,10 @@ int ldbp_forward(const ldbp_dims* d, const void* x, void* y, const void* taps, c
     if (!ws || ws_bytes < w.total) return fail(LDBP_EWORKSPACE, "forward needs %zu workspace bytes, got %zu", w.total, ws_bytes);
     LDBP_TRY(check_ptr(ws, "ws", 8));
   }
-  return run_forward_chain(d, (const float2*)x, (float2*)y, (const float2*)taps, gamma, nullptr, (float2*)ws,
-                           (cudaStream_t)cuda_stream);
+  FiniteCheck fc(d, ws, w.total, (cudaStream_t)cuda_stream);
+  return fc.finish(run_forward_chain(d, (const float2*)x, (float2*)y, (const float2*)taps, gamma, nullptr,
+                                     (float2*)ws, (cudaStream_t)cuda_stream),
+                   (cudaStream_t)cuda_stream);
 }
 
 int ldbp_backward(const ldbp_dims* d, const void* x, const void* gy, const void* taps, const float* gamma,
@@ -1062,8 +1096,11 @@ int ldbp_backward(const ldbp_dims* d, const void* x, const void* gy, const void*
     if (!ws || ws_bytes < rw.total)
       return fail(LDBP_EWORKSPACE, "backward needs %zu workspace bytes, got %zu", rw.total, ws_bytes);
     LDBP_TRY(check_ptr(ws, "ws", 16));
-    return run_rev_chain(d, (const float2*)x, (const float2*)gy, nullptr, (const float2*)taps, gamma, nullptr,
-                         (float2*)gx_or_null, (unsigned char*)ws, rp, rw, st, nullptr, dtaps, dgamma);
+    FiniteCheck fc(d, ws, rw.total, st);
+    return fc.finish(run_rev_chain(d, (const float2*)x, (const float2*)gy, nullptr, (const float2*)taps, gamma,
+                                   nullptr, (float2*)gx_or_null, (unsigned char*)ws, rp, rw, st, nullptr, dtaps,
+                                   dgamma),
+                     st);
   }
   BwdPlan p = plan_bwd(d, true);
   BwdWs w = bwd_ws(d, p);
@@ -1091,8 +1128,10 @@ int ldbp_loss_grad(const ldbp_dims* d, const void* x, const void* target, const 
     if (!ws || ws_bytes < rw.total)
       return fail(LDBP_EWORKSPACE, "loss_grad needs %zu workspace bytes, got %zu", rw.total, ws_bytes);
     LDBP_TRY(check_ptr(ws, "ws", 16));
-    return run_rev_chain(d, (const float2*)x, nullptr, (const float2*)target, (const float2*)taps, gamma, mask,
-                         nullptr, (unsigned char*)ws, rp, rw, st, buf, nullptr, nullptr);
+    FiniteCheck fc(d, ws, rw.total, st);
+    return fc.finish(run_rev_chain(d, (const float2*)x, nullptr, (const float2*)target, (const float2*)taps, gamma,
+                                   mask, nullptr, (unsigned char*)ws, rp, rw, st, buf, nullptr, nullptr),
+                     st);
   }
   BwdPlan p = plan_bwd(d, true);
   BwdWs w = bwd_ws(d, p);
@@ -1254,8 +1293,10 @@ int ldbp_rx_train_grad(const ldbp_dims* d, const void* x, const void* symbols, c
   if (w.store_all) {
     const RevPlan rp = plan_rev(d, true);
     const RevWs rw = rev_ws(d, rp);
-    LDBP_TRY(run_rev_chain(d, (const float2*)x, nullptr, nullptr, (const float2*)taps, gamma, mask, nullptr, wb, rp,
-                           rw, st, nullptr, nullptr, nullptr, ybuf, /*forward_only=*/true));
+    FiniteCheck fc(d, ws, rw.total, st);
+    LDBP_TRY(fc.finish(run_rev_chain(d, (const float2*)x, nullptr, nullptr, (const float2*)taps, gamma, mask, nullptr,
+                                     wb, rp, rw, st, nullptr, nullptr, nullptr, ybuf, /*forward_only=*/true),
+                       st));
     LDBP_TRY(launch_rx(d->batch, d->n, sps, mf_half, ybuf, (const float2*)symbols, power_w, h_mf, errs, gybuf,
                        wb + w.rx_off, st));
     LDBP_TRY(run_rev_chain(d, (const float2*)x, gybuf, nullptr, (const float2*)taps, gamma, mask, nullptr, wb, rp, rw,

@@ -13,14 +13,19 @@ using RevFn = void (*)(const ldbp::RevArgs);
 #define LDBP_CAT2(a, b) a##b
 #define LDBP_CAT(a, b) LDBP_CAT2(a, b)
 
-FwdFn LDBP_CAT(ldbp_get_fwd_, LDBP_KH)(bool sym, bool fast) {
+FwdFn LDBP_CAT(ldbp_get_fwd_, LDBP_KH)(bool sym, bool fast, bool chk) {
   constexpr int K = LDBP_KH, R = ldbp::fwd_r(LDBP_KH);
+  if (chk) {  // LDBP_CHECK_FINITE instantiations
+    if (sym) return fast ? ldbp::fwd_tile_kernel<K, R, true, true, true> : ldbp::fwd_tile_kernel<K, R, true, false, true>;
+    return fast ? ldbp::fwd_tile_kernel<K, R, false, true, true> : ldbp::fwd_tile_kernel<K, R, false, false, true>;
+  }
   if (sym) return fast ? ldbp::fwd_tile_kernel<K, R, true, true> : ldbp::fwd_tile_kernel<K, R, true, false>;
   return fast ? ldbp::fwd_tile_kernel<K, R, false, true> : ldbp::fwd_tile_kernel<K, R, false, false>;
 }
 
-FwdFn LDBP_CAT(ldbp_get_fwd_store_, LDBP_KH)(bool sym) {
+FwdFn LDBP_CAT(ldbp_get_fwd_store_, LDBP_KH)(bool sym, bool chk) {
   constexpr int K = LDBP_KH, R = LDBP_FWD_R;
+  if (chk) return sym ? ldbp::fwd_store_kernel<K, R, true, true> : ldbp::fwd_store_kernel<K, R, false, true>;
   return sym ? ldbp::fwd_store_kernel<K, R, true> : ldbp::fwd_store_kernel<K, R, false>;
 }
 

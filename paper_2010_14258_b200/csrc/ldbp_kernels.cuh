@@ -816,6 +816,7 @@ struct FwdArgs {
   int scale_dst;
   int staged;  // store-all mode (ckpt_every == 1, global): coalesced stores through a smem stage
   float2* y_out;  // optional second output: the final state in the original scale (y)
+  int* nonfinite; // LDBP_CHECK_FINITE: atomicMin of the first (1-based) step with a NaN/Inf output
   Geo g;
 };
 
@@ -971,7 +972,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity)
 template <int R>
 __device__ __forceinline__ constexpr int stage_rs() { return R + 2; }
 
-template <int KH, int R, bool SYM, bool FAST, bool NORM, bool STG, bool VARK = false>
+template <int KH, int R, bool SYM, bool FAST, bool NORM, bool STG, bool VARK = false, bool CHK = false>
 __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], const TapP* sh_taps,
                                                 const float* sh_gamma, const StepNorm* sh_norm, f2x* sh_edge,
                                                 uint64_t* bar, const StoreMap& smap, int64_t e0, int lane) {
@@ -1083,6 +1084,15 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
 #pragma unroll
     for (int k = 0; k < R; ++k) u[k] = nu[k];
     const int gs = a.s0 + s + 1;  // global step count reached
+    if constexpr (CHK) {  // LDBP_CHECK_FINITE: separate instantiation, the hot path carries no check code
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const float2 v = upk(u[k]);
+        bad |= !(isfinite(v.x) && isfinite(v.y));
+      }
+      if (__any_sync(kFull, bad) && lane == 0 && a.nonfinite) atomicMin(a.nonfinite, gs);
+    }
     if (gs < a.s1) publish((s + 1) & 1);
     if (STG) {
       if (gs < a.s1 && smap.off < 0 && smap.mask) store_mapped<R>(ck_ptr, smap, e0, a.g, u);  // irregular run
@@ -1115,7 +1125,7 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
 #define LDBP_FWD_SPLIT 1
 #endif
 
-template <int KH, int R, bool SYM, bool FAST, bool STG>
+template <int KH, int R, bool SYM, bool FAST, bool STG, bool CHK = false>
 __device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1156,7 +1166,14 @@ __device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
       pruned |= (lof(t.a) == 0.f && hif(t.a) == 0.f);
     }
   }
-  if constexpr (STG) {
+  if constexpr (CHK) {  // LDBP_CHECK_FINITE: per-step check, plain loop (pruned taps are zeros, still exact)
+    if (SYM && *sh_flag)
+      fwd_steps_split<KH, R, SYM, FAST, true, STG, false, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap,
+                                                                 e0, lane);
+    else
+      fwd_steps_split<KH, R, SYM, FAST, false, STG, false, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap,
+                                                                  e0, lane);
+  } else if constexpr (STG) {
     if (SYM && *sh_flag) {
       if (pruned)
         fwd_steps_split<KH, R, SYM, FAST, true, true, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap, e0,
@@ -1183,17 +1200,17 @@ __device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
 }
 
 // Forward tile kernel (inference, checkpoints): register budget for fwd_min_blocks CTAs per SM.
-template <int KH, int R, bool SYM, bool FAST>
+template <int KH, int R, bool SYM, bool FAST, bool CHK = false>
 __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_tile_kernel(const FwdArgs a) {
-  fwd_tile_body<KH, R, SYM, FAST, false>(a);
+  fwd_tile_body<KH, R, SYM, FAST, false, CHK>(a);
 }
 
 // Store-all forward (training): the smem stage limits residency anyway, so the register budget
 // is raised to 1-2 CTAs per SM (no spills in the step loop).
-template <int KH, int R, bool SYM>
+template <int KH, int R, bool SYM, bool CHK = false>
 __global__ void __launch_bounds__(fwd_max_threads(KH), 65536 / (fwd_max_threads(KH) * 128))
     fwd_store_kernel(const FwdArgs a) {
-  fwd_tile_body<KH, R, SYM, true, true>(a);
+  fwd_tile_body<KH, R, SYM, true, true, CHK>(a);
 }
 
 struct BwdArgs {

@@ -456,3 +456,28 @@ def test_sharding_bit_identity(P, monkeypatch, mode):
     sh = sum(P.ldbp_loss_grad(x[o:o + 4].contiguous(), tgt[o:o + 4].contiguous(), ht, gt).cpu().numpy()
              for o in (0, 4))
     assert rel(sh, full) <= 1e-7
+
+
+def test_check_finite_reports_first_step(P, monkeypatch):
+    """LDBP_CHECK_FINITE (§8(b)): finite runs pass and give the unchecked result; a
+    model whose step 3 overflows fp32 (taps 1e25 there) fails with LDBP_ENONFINITE naming step 3,
+    for the forward and for the training gradient."""
+    from paper_2010_14258_b200 import LdbpError
+
+    B, n, M, T = 2, 2048, 6, 5
+    x = dev(li.gaussian_blocks(97, range(B), n, 1e-3))
+    tgt = dev(li.gaussian_blocks(97, range(B), n, 1e-3, purpose="target"))
+    taps, gamma = model(97, M, T, True)
+    ht, gt = dev(taps), dev(gamma, np.float32)
+    assert torch.equal(P.ldbp_forward(x, ht, gt, check_finite=True), P.ldbp_forward(x, ht, gt))
+    monkeypatch.setenv("LDBP_BWD_MODE", "1")  # checked training calls run the store-all schedule
+    assert torch.equal(P.ldbp_loss_grad(x, tgt, ht, gt, check_finite=True), P.ldbp_loss_grad(x, tgt, ht, gt))
+    bad = taps.copy()
+    bad[2] *= 1e25  # |a| ~ 1e22 after step 3: |a|^2 overflows -> NaN phase
+    hb = dev(bad)
+    with pytest.raises(LdbpError) as e:
+        P.ldbp_forward(x, hb, gt, check_finite=True)
+    assert e.value.status == -6 and "step 3" in str(e.value)
+    with pytest.raises(LdbpError) as e:
+        P.ldbp_loss_grad(x, tgt, hb, gt, check_finite=True)
+    assert e.value.status == -6 and "step 3" in str(e.value)
