@@ -847,7 +847,14 @@ __host__ __device__ constexpr int fwd_max_threads(int kh) {
 }
 #endif
 // f2x elements of the store-all stage region: 2 buffers of ST runs of RS, plus run_off[ST] (int64)
-__host__ __device__ constexpr int fwd_stage_elems(int kh, int r) { return fwd_max_threads(kh) * (2 * (r + 2) + 1); }
+#ifndef LDBP_FWD_WSTAGE
+#define LDBP_FWD_WSTAGE 1  // store-all forward: 1 = halos through the edge arrays + per-warp store stage,
+                           // 0 = one CTA-wide double-buffered stage for halos and stores
+#endif
+__host__ __device__ constexpr int fwd_stage_elems(int kh, int r) {
+  return LDBP_FWD_WSTAGE ? fwd_max_threads(kh) * (4 * (kh > 0 ? kh : 1) + (r + 2) + 1)
+                         : fwd_max_threads(kh) * (2 * (r + 2) + 1);
+}
 #ifdef LDBP_FWD_NTHR
 __host__ __device__ constexpr int fwd_min_blocks(int kh) { return 65536 / (LDBP_FWD_NTHR * fwd_regs(kh)); }
 #else
@@ -991,10 +998,19 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
   const f2x* const right_edge = sh_edge + right;
   // STG: stage[2][ST*RS] f2x, then run_off[ST] (int64: HBM element offset of run t, -1 = not an
   // owned real run, -2 = owned but irregular: the owner stores it itself)
+  // WSTAGE: edges[2][2*KE][ST] as in the plain kernel, then wstage[ST/32 warps][32][RS] f2x, then
+  // run_off[ST]
+  constexpr int KE = KH > 0 ? KH : 1;
+  constexpr bool WST = STG && LDBP_FWD_WSTAGE;
   f2x* const stage = sh_edge;
-  int64_t* const run_off = reinterpret_cast<int64_t*>(sh_edge + 2 * ST * RS);
+  int64_t* const run_off = reinterpret_cast<int64_t*>(sh_edge + (WST ? 4 * KE * ST + ST * RS : 2 * ST * RS));
+  f2x* const wstage = sh_edge + 4 * KE * ST + (tid >> 5) * 32 * RS;
+  const int64_t* const wrun_off = run_off + (tid & ~31);
   int t_lo = 0, t_hi = 0;
-  if constexpr (STG) {
+  if constexpr (WST) {
+    static_assert(R % 2 == 0 && 32 % (R / 2) == 0, "warp store stage: R/2 must divide 32");
+    run_off[tid] = smap.off >= 0 ? smap.off : -1;  // warp-local: ordered by the __syncwarp of the first store
+  } else if constexpr (STG) {
     const bool fullrun = smap.off >= 0;
     run_off[tid] = fullrun ? smap.off : (smap.mask ? -2 : -1);
     const int64_t lo = tile_lo(a.g, blockIdx.x);
@@ -1004,7 +1020,7 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
     __syncthreads();  // run_off visible before the first copy
   }
   auto publish = [&](int buf) {
-    if constexpr (STG) {
+    if constexpr (STG && !WST) {
       f2x* st = stage + buf * ST * RS + tid * RS;
 #pragma unroll
       for (int m = 0; m < R / 2; ++m)
@@ -1046,7 +1062,7 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
     constexpr int KJ = decltype(kjc)::value;
     constexpr int KI2 = KJ < R - KJ ? KJ : R / 2;
     step_range<KH, R, SYM, FAST, NORM, KI2, R - KI2, KJ>(u, hl, hr, hs, gm, acc, nu);
-    if constexpr (STG) {
+    if constexpr (STG && !WST) {
       mbar_wait_parity(bar, s & 1);
       const f2x* st = stage + (s & 1) * ST * RS;
 #pragma unroll
@@ -1056,13 +1072,14 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
       }
       // coalesced copy of u^(s0+s) (computed by this launch when s >= 1) to its activation slot
       if (s >= 1) {
-        float2* dstp = a.ckpt + (int64_t)(a.s0 + s - 1) * a.ckpt_stride;
-        const int units = (t_hi - t_lo) * (R / 2);
-        for (int uu = tid; uu < units; uu += nthr) {
-          const int t = t_lo + uu / (R / 2), p2 = uu % (R / 2);
+        // thread tid always moves pair p2 = tid % (R/2) of runs t = t_lo + tid / (R/2) + k * nthr / (R/2)
+        float2* const dstp = a.ckpt + (int64_t)(a.s0 + s - 1) * a.ckpt_stride + 2 * (tid % (R / 2));
+        const f2x* const stp = st + 2 * (tid % (R / 2));
+#pragma unroll 2
+        for (int t = t_lo + tid / (R / 2); t < t_hi; t += nthr / (R / 2)) {
           const int64_t off = run_off[t];
           if (off >= 0)
-            *reinterpret_cast<ulonglong2*>(dstp + off + 2 * p2) = *reinterpret_cast<const ulonglong2*>(st + t * RS + 2 * p2);
+            *reinterpret_cast<ulonglong2*>(dstp + off) = *reinterpret_cast<const ulonglong2*>(stp + t * RS);
         }
       }
     } else if constexpr (KH > 0) {
@@ -1094,6 +1111,25 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
       if (__any_sync(kFull, bad) && lane == 0 && a.nonfinite) atomicMin(a.nonfinite, gs);
     }
     if (gs < a.s1) publish((s + 1) & 1);
+    if constexpr (WST) {
+      // u^(gs) -> activation slot gs-1: the warp's 32 runs through its stage, 16-byte lane-consecutive
+      // stores (R/2 lanes per run); irregular runs are stored by their owners below
+      if (gs < a.s1) {
+#pragma unroll
+        for (int m = 0; m < R / 2; ++m)
+          *reinterpret_cast<ulonglong2*>(wstage + lane * RS + 2 * m) = make_ulonglong2(u[2 * m], u[2 * m + 1]);
+        __syncwarp();
+        float2* const dstp = a.ckpt + (int64_t)(gs - 1) * a.ckpt_stride + 2 * (lane % (R / 2));
+        const f2x* const sp = wstage + 2 * (lane % (R / 2));
+#pragma unroll
+        for (int k = 0; k < R / 2; ++k) {
+          const int t = lane / (R / 2) + k * (64 / R);
+          const int64_t off = wrun_off[t];
+          if (off >= 0) *reinterpret_cast<ulonglong2*>(dstp + off) = *reinterpret_cast<const ulonglong2*>(sp + t * RS);
+        }
+        __syncwarp();
+      }
+    }
     if (STG) {
       if (gs < a.s1 && smap.off < 0 && smap.mask) store_mapped<R>(ck_ptr, smap, e0, a.g, u);  // irregular run
       ck_ptr += a.ckpt_stride;
@@ -1207,8 +1243,11 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
 
 // Store-all forward (training): the smem stage limits residency anyway, so the register budget
 // is raised to 1-2 CTAs per SM (no spills in the step loop).
+#ifndef LDBP_FWD_STORE_REGS
+#define LDBP_FWD_STORE_REGS 128
+#endif
 template <int KH, int R, bool SYM, bool CHK = false>
-__global__ void __launch_bounds__(fwd_max_threads(KH), 65536 / (fwd_max_threads(KH) * 128))
+__global__ void __launch_bounds__(fwd_max_threads(KH), 65536 / (fwd_max_threads(KH) * LDBP_FWD_STORE_REGS))
     fwd_store_kernel(const FwdArgs a) {
   fwd_tile_body<KH, R, SYM, true, true, CHK>(a);
 }
