@@ -24,6 +24,7 @@
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
 using RevFn = void (*)(const ldbp::RevArgs);
+using ParFn = void (*)(const float2*, const float*, const uint8_t*, int, int, void*);
 
 namespace {
 
@@ -107,7 +108,8 @@ int ntaps_used(int kh, bool sym) { return sym ? kh + 1 : 2 * kh + 1; }
   FwdFn ldbp_get_fwd_##K(bool sym, bool fast, bool chk); \
   FwdFn ldbp_get_fwd_store_##K(bool sym, bool chk); \
   BwdFn ldbp_get_bwd_##K(bool sym, bool fast);      \
-  RevFn ldbp_get_rev_##K(bool sym, bool fast);
+  RevFn ldbp_get_rev_##K(bool sym, bool fast);      \
+  ParFn ldbp_get_params_##K(bool sym);
 }  // namespace
 LDBP_DECL_GETTERS(0)
 LDBP_DECL_GETTERS(1)
@@ -170,6 +172,20 @@ RevFn get_rev(int kh, bool sym, bool fast) {
     case 5: return ldbp_get_rev_5(sym, fast);
     case 6: return ldbp_get_rev_6(sym, fast);
     case 7: return ldbp_get_rev_7(sym, fast);
+  }
+  return nullptr;
+}
+
+ParFn get_params(int kh, bool sym) {
+  switch (kh) {
+    case 0: return ldbp_get_params_0(sym);
+    case 1: return ldbp_get_params_1(sym);
+    case 2: return ldbp_get_params_2(sym);
+    case 3: return ldbp_get_params_3(sym);
+    case 4: return ldbp_get_params_4(sym);
+    case 5: return ldbp_get_params_5(sym);
+    case 6: return ldbp_get_params_6(sym);
+    case 7: return ldbp_get_params_7(sym);
   }
   return nullptr;
 }
@@ -519,6 +535,7 @@ struct RevWs {
   size_t act_off = 0, act_each = 0;  // M activation buffers u_hat^(1..M)
   size_t g_off = 0, g_each = 0;      // 2 adjoint ping-pong buffers (when Kr >= 2)
   size_t part_off = 0, loss_off = 0, part2_off = 0, loss2_off = 0;
+  size_t ptab_off = 0;               // parameter table (params_kernel)
   size_t total = 0;
 };
 
@@ -540,6 +557,8 @@ RevWs rev_ws(const ldbp_dims* d, const RevPlan& p) {
   off += align256(sizeof(double) * (size_t)nch * d->steps * p.V);
   w.loss2_off = off;
   off += align256(sizeof(double) * (size_t)nch);
+  w.ptab_off = off;
+  off += align256(ldbp::ptab_bytes(d->steps, ntaps_used((d->taps - 1) / 2, d->flags & LDBP_SYMMETRIC)));
   if (d->flags & LDBP_CHECK_FINITE) off += kCheckBytes;  // the check slot (last 256 bytes)
   w.total = off;
   return w;
@@ -573,7 +592,8 @@ struct FiniteCheck {
 // ----------------------------------------------------------------------------------------
 int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2* taps, const float* gamma,
                const uint8_t* mask, int s0, int s1, cudaStream_t st, float2* ckpt = nullptr, int ckpt_every = 0,
-               int64_t ckpt_stride = 0, bool global_norm = false, bool scale_dst = false, float2* y_out = nullptr) {
+               int64_t ckpt_stride = 0, bool global_norm = false, bool scale_dst = false, float2* y_out = nullptr,
+               const void* ptab = nullptr) {
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const bool fast = !(d->flags & LDBP_PRECISE);
@@ -588,6 +608,7 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   a.ckpt = ckpt;
   a.y_out = y_out;
   a.nonfinite = g_nonfinite;
+  a.ptab = global_norm ? ptab : nullptr;
   a.ckpt_stride = ckpt_stride;
   a.ckpt_every = ckpt_every > 0 ? ckpt_every : 1;
   a.taps = taps;
@@ -758,12 +779,23 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
   auto act = [&](int i) -> float2* { return reinterpret_cast<float2*>(ws + w.act_off + (size_t)(i - 1) * w.act_each); };
   auto gb = [&](int k) -> float2* { return reinterpret_cast<float2*>(ws + w.g_off + (size_t)(k & 1) * w.g_each); };
   const int64_t stride = (int64_t)(w.act_each / sizeof(float2));
+  // parameter table for every launch below (one tiny kernel; skip_forward recomputes it too)
+  void* ptab = ws + w.ptab_off;
+  {
+    TraceScope ts(LDBP_K_REDUCE, M, 0, st);
+    const size_t psm = M <= ldbp::kParamsSmemSteps ? 16 + sizeof(ldbp::StepNorm) * (size_t)M : 0;
+    if (psm > 48 * 1024)
+      cudaFuncSetAttribute((const void*)get_params(kh, sym), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+    get_params(kh, sym)<<<1, 256, psm, st>>>(taps, gamma, mask, d->taps, M, ptab);
+  }
+  LDBP_TRY(cuda_check("params_kernel launch"));
   if (!skip_forward) {
     const FwdPlan fp = plan_fwd_segments(M, kh, kFwdR);  // store-all forward: R = LDBP_FWD_R
     for (int k = 0; k < fp.segs; ++k) {
       const int s0 = k * fp.steps_per, s1 = std::min(M, s0 + fp.steps_per);
       LDBP_TRY(launch_fwd(d, s0 == 0 ? x : act(s0), act(s1), taps, gamma, mask, s0, s1, st,
-                          s1 - s0 >= 2 ? act(1) : nullptr, 1, stride, true, false, s1 == M ? y_out : nullptr));
+                          s1 - s0 >= 2 ? act(1) : nullptr, 1, stride, true, false, s1 == M ? y_out : nullptr,
+                          ptab));
     }
   }
   if (forward_only) return LDBP_OK;
@@ -784,6 +816,7 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
     a.mask = mask;
     a.partials = partials;
     a.loss_partials = lossp;
+    a.ptab = ptab;
     a.seed_scale = 2.0f;
     a.T = d->taps;
     a.M = M;

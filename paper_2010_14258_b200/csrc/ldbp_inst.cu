@@ -9,6 +9,7 @@
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
 using RevFn = void (*)(const ldbp::RevArgs);
+using ParFn = void (*)(const float2*, const float*, const uint8_t*, int, int, void*);
 
 #define LDBP_CAT2(a, b) a##b
 #define LDBP_CAT(a, b) LDBP_CAT2(a, b)
@@ -39,4 +40,9 @@ RevFn LDBP_CAT(ldbp_get_rev_, LDBP_KH)(bool sym, bool fast) {
   constexpr int K = LDBP_KH, R = LDBP_REV_R;
   if (sym) return fast ? ldbp::rev_tile_kernel<K, R, true, true> : ldbp::rev_tile_kernel<K, R, true, false>;
   return fast ? ldbp::rev_tile_kernel<K, R, false, true> : ldbp::rev_tile_kernel<K, R, false, false>;
+}
+
+ParFn LDBP_CAT(ldbp_get_params_, LDBP_KH)(bool sym) {
+  constexpr int K = LDBP_KH;
+  return sym ? ldbp::params_kernel<K, true> : ldbp::params_kernel<K, false>;
 }

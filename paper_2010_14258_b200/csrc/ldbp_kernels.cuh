@@ -794,6 +794,98 @@ __device__ __forceinline__ void stage_params(const float2* __restrict__ taps, co
   }
 }
 
+// Model parameter table of the store-all training step (global normalisation): computed once
+// per call by params_kernel, then copied by every CTA of the storing forward and the reverse
+// launches with one round of asynchronous 16-/4-byte copies, instead of each CTA re-deriving the
+// prefix products P_i (a serial fp64 chain over M steps behind three barriers) and re-packing
+// the taps from global memory.
+//   [flag int, 16 B][norm StepNorm[M]][gamma_hat float[M], 16 B-rounded][fwd TapP[M][NTU]]
+//   [adj TapP[M][NTU]][kj int[M]]
+struct PTab {
+  int* flag;
+  StepNorm* norm;
+  float* gamma;
+  TapP* fwd;
+  TapP* adj;
+  int* kj;
+};
+__host__ __device__ inline size_t ptab_bytes(int M, int ntu) {
+  return 16 + 16 * (size_t)M + 16 * (((size_t)M + 3) / 4) + 32 * (size_t)M * ntu + 4 * (size_t)M;
+}
+__host__ __device__ inline PTab ptab_view(const void* base, int M, int ntu) {
+  unsigned char* b = reinterpret_cast<unsigned char*>(const_cast<void*>(base));
+  PTab p;
+  p.flag = reinterpret_cast<int*>(b);
+  b += 16;
+  p.norm = reinterpret_cast<StepNorm*>(b);
+  b += 16 * (size_t)M;
+  p.gamma = reinterpret_cast<float*>(b);
+  b += 16 * (((size_t)M + 3) / 4);
+  p.fwd = reinterpret_cast<TapP*>(b);
+  b += 16 * (size_t)M * ntu;
+  p.adj = reinterpret_cast<TapP*>(b);
+  b += 16 * (size_t)M * ntu;
+  p.kj = reinterpret_cast<int*>(b);
+  return p;
+}
+
+// One CTA: the same staging functions the kernels use, with the table in global memory as target.
+constexpr int kParamsSmemSteps = 3072;
+template <int KH, bool SYM>
+__global__ void __launch_bounds__(256) params_kernel(const float2* __restrict__ taps, const float* __restrict__ gamma,
+                                                     const uint8_t* __restrict__ mask, int T, int M, void* tab) {
+  constexpr int NTU = ntaps_used<SYM, KH>();
+  const PTab p = ptab_view(tab, M, NTU);
+  // the prefix-product chain runs on shared memory (launched with M * 16 + 16 bytes of dynamic
+  // shared memory when that fits, else on the table in global memory)
+  extern __shared__ __align__(16) unsigned char par_smem[];
+  const bool in_smem = M <= kParamsSmemSteps;
+  StepNorm* nrm = in_smem ? reinterpret_cast<StepNorm*>(par_smem + 16) : p.norm;
+  int* flag = in_smem ? reinterpret_cast<int*>(par_smem) : p.flag;
+  norm_range<KH, SYM>(taps, mask, T, 0, M, nrm, flag);  // ends with a barrier
+  const bool norm = SYM && *flag;
+  if (in_smem) {
+    for (int i = threadIdx.x; i < M; i += blockDim.x) p.norm[i] = nrm[i];
+    if (threadIdx.x == 0) *p.flag = *flag;
+  }
+  stage_range<KH, SYM, true, true>(taps, gamma, mask, T, 0, M, 0, p.fwd, p.adj, p.gamma, nrm, norm);
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {  // outermost unmasked folded tap per step
+    int kj = KH;
+    if (mask && SYM) {
+      const uint8_t* mrow = mask + (int64_t)i * T + KH;
+      kj = 0;
+      for (int j = 1; j <= KH; ++j)
+        if (mrow[j] || mrow[-j]) kj = j;
+    }
+    p.kj[i] = kj;
+  }
+}
+
+__device__ __forceinline__ void ptab_cp16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void ptab_cp4(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
+// Copy the slices a CTA needs (norm: all M; taps, gamma_hat, kj: steps [s0, s1)) into shared
+// memory; all copies in flight at once.  Followed by the caller's __syncthreads.
+template <int NTU>
+__device__ __forceinline__ void load_ptab(const void* tab, int M, int s0, int s1, StepNorm* norm, TapP* fwd,
+                                          TapP* adj, float* gam, int* kj, int* flag) {
+  const PTab p = ptab_view(tab, M, NTU);
+  const int S = s1 - s0, tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < M; i += nt) ptab_cp16(norm + i, p.norm + i);
+  if (fwd)
+    for (int i = tid; i < S * NTU; i += nt) ptab_cp16(fwd + i, p.fwd + (size_t)s0 * NTU + i);
+  if (adj)
+    for (int i = tid; i < S * NTU; i += nt) ptab_cp16(adj + i, p.adj + (size_t)s0 * NTU + i);
+  for (int i = tid; i < S; i += nt) ptab_cp4(gam + i, p.gamma + s0 + i);
+  if (kj)
+    for (int i = tid; i < S; i += nt) ptab_cp4(kj + i, p.kj + s0 + i);
+  if (tid == 0) ptab_cp4(flag, p.flag);
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+}
+
 // P * v for a staged complex scale P.
 __device__ __forceinline__ f2x cscale(float2 P, f2x v) { return tmul(tap_fwd(P), v); }
 
@@ -816,6 +908,7 @@ struct FwdArgs {
   int scale_dst;
   int staged;  // store-all mode (ckpt_every == 1, global): coalesced stores through a smem stage
   float2* y_out;  // optional second output: the final state in the original scale (y)
+  const void* ptab;  // store-all training: parameter table (params_kernel), or nullptr
   int* nonfinite; // LDBP_CHECK_FINITE: atomicMin of the first (1-based) step with a NaN/Inf output
   Geo g;
 };
@@ -1184,7 +1277,9 @@ __device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
   const int64_t e0 = thread_e0(a.g, R);
   load_window<R>(a.src, e0, a.g, u);
   const StoreMap smap = store_map<R>(e0, a.g);
-  if (a.global_norm) {
+  if (a.global_norm && a.ptab) {
+    load_ptab<NTU>(a.ptab, a.nM, a.s0, a.s1, sh_norm, sh_taps, nullptr, sh_gamma, nullptr, sh_flag);
+  } else if (a.global_norm) {
     norm_range<KH, SYM>(a.taps, a.mask, a.T, a.n0, a.nM, sh_norm, sh_flag);
     stage_range<KH, SYM, true, false>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, a.n0, sh_taps, nullptr, sh_gamma,
                                       sh_norm, *sh_flag != 0);

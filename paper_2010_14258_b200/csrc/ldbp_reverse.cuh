@@ -36,6 +36,7 @@ struct RevArgs {
   const uint8_t* mask;
   double* partials;        // [gridDim.x][M][V]
   double* loss_partials;   // [gridDim.x] (seed mode)
+  const void* ptab;        // parameter table (params_kernel), or nullptr -> derive in the prologue
   float seed_scale;        // seed g = seed_scale * (y - target)
   int T, M, s0, s1;
   Geo g;
@@ -469,10 +470,14 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * re
                  "r"(LDBP_NB_WAIT ? 1 : NT / 32)
                  : "memory");
   }
+  if (a.ptab) {
+    load_ptab<NTU>(a.ptab, a.M, a.s0, a.s1, sm.norm, nullptr, sm.taps_adj, sm.gamma, sm.kj, sm.flag);
+    __syncthreads();
+  } else {
   norm_range<KH, SYM>(a.taps, a.mask, a.T, 0, a.M, sm.norm, sm.flag);
-  const bool norm = SYM && *sm.flag;
+  const bool norm0 = SYM && *sm.flag;
   stage_range<KH, SYM, false, true>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, 0, nullptr, sm.taps_adj, sm.gamma,
-                                    sm.norm, norm);
+                                    sm.norm, norm0);
   for (int i = threadIdx.x; i < S; i += NT) {
     int kj = KH;
     if (a.mask && SYM) {
@@ -484,6 +489,8 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * re
     sm.kj[i] = kj;
   }
   __syncthreads();
+  }
+  const bool norm = SYM && *sm.flag;
   if (norm)
     rev_body<KH, R, SYM, FAST, true>(a, sm, e0, fast_off, own, lane, warp);
   else
