@@ -286,8 +286,11 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
     roof = None
     kernel_shares = {}
     tot_ms = sum(v["ms"] for v in per_kind.values()) or 1.0
-    names = {_lib.K_FORWARD: "fwd_tile_kernel", _lib.K_BACKWARD: "bwd_segment_kernel",
-             _lib.K_REDUCE: "reduce_partials_kernel", _lib.K_ADAM: "adam_kernel", _lib.K_REVERSE: "rev_tile_kernel"}
+    store_all = train and _lib.K_REVERSE in per_kind  # the storing forward of the store-all schedule
+    names = {_lib.K_FORWARD: "fwd_store_kernel" if store_all else "fwd_tile_kernel",
+             _lib.K_BACKWARD: "bwd_segment_kernel",
+             _lib.K_REDUCE: "reduce_partials_kernel+params_kernel" if store_all else "reduce_partials_kernel",
+             _lib.K_ADAM: "adam_kernel", _lib.K_REVERSE: "rev_tile_kernel"}
     for k, v in per_kind.items():
         kernel_shares[names[k]] = {"share": v["ms"] / tot_ms, "avg_ms": v["ms"] / v["launches"],
                                    "launches": v["launches"]}

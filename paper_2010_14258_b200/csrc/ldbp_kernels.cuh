@@ -1277,8 +1277,14 @@ __device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
   const int64_t e0 = thread_e0(a.g, R);
   load_window<R>(a.src, e0, a.g, u);
   const StoreMap smap = store_map<R>(e0, a.g);
-  if (a.global_norm && a.ptab) {
-    load_ptab<NTU>(a.ptab, a.nM, a.s0, a.s1, sh_norm, sh_taps, nullptr, sh_gamma, nullptr, sh_flag);
+  bool from_table = false;
+  if constexpr (STG) {  // the storing forward only: keeps the inference kernel's prologue (and registers) lean
+    if (a.global_norm && a.ptab) {
+      load_ptab<NTU>(a.ptab, a.nM, a.s0, a.s1, sh_norm, sh_taps, nullptr, sh_gamma, nullptr, sh_flag);
+      from_table = true;
+    }
+  }
+  if (from_table) {
   } else if (a.global_norm) {
     norm_range<KH, SYM>(a.taps, a.mask, a.T, a.n0, a.nM, sh_norm, sh_flag);
     stage_range<KH, SYM, true, false>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, a.n0, sh_taps, nullptr, sh_gamma,
