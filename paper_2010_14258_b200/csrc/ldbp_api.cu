@@ -1066,7 +1066,7 @@ int ldbp_launch_count(const ldbp_dims* d, int op, int* launches) {
   if (op == LDBP_OP_FORWARD) { *launches = plan_fwd_segments(d->steps, (d->taps - 1) / 2).segs; return LDBP_OK; }
   if (use_store_all(d)) {
     const RevPlan rp = plan_rev(d, true);
-    int n = plan_fwd_segments(d->steps, (d->taps - 1) / 2, kFwdR).segs + rp.Kr + 1 +
+    int n = 1 /* params_kernel */ + plan_fwd_segments(d->steps, (d->taps - 1) / 2, kFwdR).segs + rp.Kr + 1 +
             (reduce_chunks(rp.tile.grid) > 0 ? 1 : 0);
     if (op == LDBP_OP_TRAIN_STEP) n += 1;
     *launches = n;

@@ -390,6 +390,26 @@ def test_train_step_cuda_graph_capture(P):
             assert torch.equal(eager.master, graphed.master)
 
 
+@pytest.mark.parametrize("mode", MODES)
+def test_launch_count_matches_traced_launches(P, monkeypatch, mode):
+    """ldbp_launch_count (the bench's gpu_launches claim) equals the launches the library actually
+    makes for one loss_grad + Adam step, in both schedules (store-all adds params_kernel)."""
+    set_mode(monkeypatch, mode, None)
+    B, n, M, T = 64, 16384, 6, 9  # B*n = 2^20: store-all eligible
+    x = dev(li.gaussian_blocks(91, range(B), n, 1e-3))
+    tgt = dev(li.gaussian_blocks(91, range(B), n, 1e-3, purpose="target"))
+    taps, gamma = model(91, M, T, True)
+    st = P.TrainState.create(taps, gamma)
+    buf = P.ldbp_loss_grad(x, tgt, st.taps, st.gamma)  # warm-up (workspace)
+    torch.cuda.synchronize()
+    with P.api.trace() as tr:
+        buf = P.ldbp_loss_grad(x, tgt, st.taps, st.gamma)
+        P.ldbp_adam_update(st, buf, B * n)
+        torch.cuda.synchronize()
+    d = P.make_dims(B, n, M, T)
+    assert len(tr.records) == P.launch_count(d, P._lib.OP_TRAIN_STEP)
+
+
 # ---- §8(f) NEXT-3: per-step variable filter lengths (pruned outer taps are not computed) ----
 def pruned_model(seed, M, T, kh_steps):
     """Symmetric taps whose step i keeps only |j| <= kh_steps[i] (progressive pruning
