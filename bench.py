@@ -230,8 +230,10 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
             ht[i].copy_(tgt)
         dx = [torch.empty_like(x) for _ in range(2)]
         dt = [torch.empty_like(tgt) for _ in range(2)]
-        res = torch.empty(1 if train else y.numel(), dtype=torch.float64 if train else torch.complex64,
-                          pin_memory=True)
+        res = [torch.empty(1 if train else y.numel(), dtype=torch.float64 if train else torch.complex64,
+                           pin_memory=True) for _ in range(2)]
+        read_ev = [torch.cuda.Event() for _ in range(2)]
+        seen = []
         cstream = torch.cuda.Stream(device=dev)
         copied = [torch.cuda.Event() for _ in range(2)]
         freed = [torch.cuda.Event() for _ in range(2)]
@@ -260,13 +262,17 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
             freed[b].record(stream)
             if i + 1 < e2e_steps:
                 issue_copy(i + 1)  # overlaps this step's compute
-            if train:
-                res.copy_(out[:1], non_blocking=True)
-            else:
-                res.copy_(out.view(-1), non_blocking=True)
-            stream.synchronize()  # the host reads the step's result
+            with torch.cuda.stream(stream):
+                res[b].copy_(out[:1] if train else out.view(-1), non_blocking=True)
+            read_ev[b].record(stream)
+            if i >= 1:  # the host reads step i-1's result while step i runs (no launch bubble)
+                read_ev[1 - b].synchronize()
+                seen.append(float(res[1 - b][0].real))
+        read_ev[(e2e_steps - 1) % 2].synchronize()
+        seen.append(float(res[(e2e_steps - 1) % 2][0].real))
         e1.record(stream)
         torch.cuda.synchronize()
+        assert len(seen) == e2e_steps
         e_ms = e0.elapsed_time(e1) / e2e_steps
         if dist.is_initialized():
             t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
@@ -276,7 +282,8 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
         bo = 8 if train else y.numel() * 8
         e2e = {"value": samples_global * M / (e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": bi,
                "d2h_bytes_per_step": bo, "ms_per_step": e_ms,
-               "pipeline": "inputs of step i+1 copied H2D (pinned, copy stream) during step i; result read every step"}
+               "pipeline": "inputs of step i+1 copied H2D (pinned, copy stream) during step i; every step's result "
+               "copied D2H (pinned) and read by the host while the next step runs"}
 
     # roofline of the dominant kernel (largest total time)
     sm_mhz = (clk or {}).get("sm_mhz") or 1965.0

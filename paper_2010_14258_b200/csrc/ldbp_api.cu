@@ -49,7 +49,6 @@ int cuda_check(const char* what) {
 
 constexpr int kFwdR = LDBP_FWD_R;
 constexpr int kBwdR = LDBP_BWD_R;
-constexpr int kRevR = LDBP_REV_R;
 constexpr int kFwdMaxThreads = 512;
 constexpr int kBwdMaxThreads = 256;
 
@@ -222,7 +221,7 @@ size_t rev_smem(int kh, bool sym, int steps, int M) {
   const int NT = ldbp::rev_threads(kh), nw = NT / 32;
   const int V = 1 + 2 * ntaps_used(kh, sym);
   size_t s = 16 * (size_t)nw;                                         // split-barrier mbarriers
-  s += sizeof(float2) * 2 * (size_t)kRevR * NT;                       // u window copies
+  s += sizeof(float2) * 2 * (size_t)rev_r(kh) * NT;                       // u window copies
   s += sizeof(float2) * 4 * (size_t)std::max(kh, 1) * NT;             // ga edges
   s += sizeof(ldbp::TapP) * (size_t)steps * ntaps_used(kh, sym);      // adjoint taps
   s += sizeof(ldbp::StepNorm) * (size_t)M;                            // global normalisation
@@ -407,7 +406,7 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
   // cost model in step units: a launch of S steps costs S * window / (window - 2*S*kh) plus a
   // fixed ~2 steps (prologue: staging, first load, seed); pick the number of launches minimising
   // it, subject to the shared-memory budget (2 CTAs per SM)
-  const double window = (double)nthr * kRevR;
+  const double window = (double)nthr * rev_r(kh);
   const double fixed = 2.0;
   const size_t budget = (size_t)env_int("LDBP_REV_SMEM_KB", 113) * 1024;
   int best_k = 0;
@@ -431,7 +430,7 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
     sms = device_sms();
     occ = rev_occupancy(get_rev(kh, sym, !(d->flags & LDBP_PRECISE)), nthr, rev_smem(kh, sym, p.Cr, M));
   }
-  p.tile = plan_tiles(d->batch, d->n, p.Cr * kh, kRevR, nthr, occ, sms, /*align_r=*/true);
+  p.tile = plan_tiles(d->batch, d->n, p.Cr * kh, rev_r(kh), nthr, occ, sms, /*align_r=*/true);
   p.tile.nthreads = nthr;  // the kernel's layout is compiled for exactly rev_threads(kh) threads
   return p;
 }

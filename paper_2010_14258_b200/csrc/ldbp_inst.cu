@@ -37,7 +37,7 @@ BwdFn LDBP_CAT(ldbp_get_bwd_, LDBP_KH)(bool sym, bool fast) {
 }
 
 RevFn LDBP_CAT(ldbp_get_rev_, LDBP_KH)(bool sym, bool fast) {
-  constexpr int K = LDBP_KH, R = LDBP_REV_R;
+  constexpr int K = LDBP_KH, R = rev_r(LDBP_KH);
   if (sym) return fast ? ldbp::rev_tile_kernel<K, R, true, true> : ldbp::rev_tile_kernel<K, R, true, false>;
   return fast ? ldbp::rev_tile_kernel<K, R, false, true> : ldbp::rev_tile_kernel<K, R, false, false>;
 }

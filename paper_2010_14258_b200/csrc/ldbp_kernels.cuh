@@ -33,6 +33,10 @@
 #ifndef LDBP_REV_R
 #define LDBP_REV_R 12  // samples per thread, store-all reverse kernel (measured: 12 >= 16 > 8)
 #endif
+#ifndef LDBP_REV_R_SMALL
+#define LDBP_REV_R_SMALL LDBP_REV_R  // samples per thread of the reverse kernel for Kh <= 1
+#endif
+__host__ __device__ constexpr int rev_r(int kh) { return kh <= 1 ? LDBP_REV_R_SMALL : LDBP_REV_R; }
 
 #ifndef LDBP_NORM
 #define LDBP_NORM 1  // h0-normalised FIR when well conditioned (saves one complex multiply per FIR)
