@@ -24,7 +24,7 @@
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
 using RevFn = void (*)(const ldbp::RevArgs);
-using ParFn = void (*)(const float2*, const float*, const uint8_t*, int, int, void*);
+using ParFn = void (*)(const float2*, const float*, const uint8_t*, int, int, void*, int);
 
 namespace {
 
@@ -782,10 +782,12 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
   void* ptab = ws + w.ptab_off;
   {
     TraceScope ts(LDBP_K_REDUCE, M, 0, st);
-    const size_t psm = M <= ldbp::kParamsSmemSteps ? 16 + sizeof(ldbp::StepNorm) * (size_t)M : 0;
+    // LDBP_PARAMS_SMEM_STEPS (tests): longest model whose prefix chain runs in shared memory
+    const int in_smem = M <= std::min(ldbp::kParamsSmemSteps, env_int("LDBP_PARAMS_SMEM_STEPS", 1 << 30)) ? 1 : 0;
+    const size_t psm = in_smem ? 16 + sizeof(ldbp::StepNorm) * (size_t)M : 0;
     if (psm > 48 * 1024)
       cudaFuncSetAttribute((const void*)get_params(kh, sym), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
-    get_params(kh, sym)<<<1, 256, psm, st>>>(taps, gamma, mask, d->taps, M, ptab);
+    get_params(kh, sym)<<<1, 256, psm, st>>>(taps, gamma, mask, d->taps, M, ptab, in_smem);
   }
   LDBP_TRY(cuda_check("params_kernel launch"));
   if (!skip_forward) {

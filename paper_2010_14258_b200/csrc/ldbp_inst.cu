@@ -9,7 +9,7 @@
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
 using RevFn = void (*)(const ldbp::RevArgs);
-using ParFn = void (*)(const float2*, const float*, const uint8_t*, int, int, void*);
+using ParFn = void (*)(const float2*, const float*, const uint8_t*, int, int, void*, int);
 
 #define LDBP_CAT2(a, b) a##b
 #define LDBP_CAT(a, b) LDBP_CAT2(a, b)

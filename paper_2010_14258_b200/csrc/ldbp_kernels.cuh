@@ -837,13 +837,13 @@ __host__ __device__ inline PTab ptab_view(const void* base, int M, int ntu) {
 constexpr int kParamsSmemSteps = 3072;
 template <int KH, bool SYM>
 __global__ void __launch_bounds__(256) params_kernel(const float2* __restrict__ taps, const float* __restrict__ gamma,
-                                                     const uint8_t* __restrict__ mask, int T, int M, void* tab) {
+                                                     const uint8_t* __restrict__ mask, int T, int M, void* tab,
+                                                     int in_smem) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   const PTab p = ptab_view(tab, M, NTU);
-  // the prefix-product chain runs on shared memory (launched with M * 16 + 16 bytes of dynamic
-  // shared memory when that fits, else on the table in global memory)
+  // the prefix-product chain runs on shared memory (in_smem: launched with M * 16 + 16 bytes of
+  // dynamic shared memory, M <= kParamsSmemSteps), else on the table in global memory
   extern __shared__ __align__(16) unsigned char par_smem[];
-  const bool in_smem = M <= kParamsSmemSteps;
   StepNorm* nrm = in_smem ? reinterpret_cast<StepNorm*>(par_smem + 16) : p.norm;
   int* flag = in_smem ? reinterpret_cast<int*>(par_smem) : p.flag;
   norm_range<KH, SYM>(taps, mask, T, 0, M, nrm, flag);  // ends with a barrier

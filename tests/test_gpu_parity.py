@@ -390,6 +390,30 @@ def test_train_step_cuda_graph_capture(P):
             assert torch.equal(eager.master, graphed.master)
 
 
+@pytest.mark.parametrize("masked", [False, True])
+def test_store_all_param_table_in_global_memory(P, monkeypatch, masked):
+    """Models longer than kParamsSmemSteps (3072) build the store-all parameter table with the
+    prefix-product chain in global memory instead of shared memory; forced here for a short model
+    (LDBP_PARAMS_SMEM_STEPS=0): identical arithmetic, so results equal the default path exactly.
+    (Long random models are not used for parity: their fp32 rounding differences grow
+    exponentially with M — measured 1.4e-5 at M = 100, O(1) at M = 1000 — for any schedule.)"""
+    monkeypatch.setenv("LDBP_BWD_MODE", "1")
+    B, n, M, T = 3, 4096, 12, 9
+    x = dev(li.gaussian_blocks(97, range(B), n, 1e-3))
+    tgt = dev(li.gaussian_blocks(97, range(B), n, 1e-3, purpose="target"))
+    taps, gamma, mask = pruned_model(97, M, T, [4, 3, 4, 2, 4, 4, 1, 4, 3, 4, 4, 2])
+    mk = torch.from_numpy(mask).cuda() if masked else None
+    ref_buf = P.ldbp_loss_grad(x, tgt, dev(taps), dev(gamma, np.float32), mask=mk)
+    monkeypatch.setenv("LDBP_PARAMS_SMEM_STEPS", "0")
+    buf = P.ldbp_loss_grad(x, tgt, dev(taps), dev(gamma, np.float32), mask=mk)
+    assert torch.equal(buf, ref_buf)
+    ref = O.loss_grad(r32(x.cpu().numpy()), r32(tgt.cpu().numpy()), r32(taps), r32(gamma),
+                      mask=mask if masked else None, symmetric=True)
+    b = buf.cpu().numpy()
+    assert abs(b[0] - ref[0]) <= OUT_TOL * ref[0]
+    assert rel(b[1:], ref[1:]) <= GRAD_TOL
+
+
 @pytest.mark.parametrize("mode", MODES)
 def test_launch_count_matches_traced_launches(P, monkeypatch, mode):
     """ldbp_launch_count (the bench's gpu_launches claim) equals the launches the library actually
