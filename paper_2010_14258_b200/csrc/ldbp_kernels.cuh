@@ -1044,6 +1044,11 @@ __device__ __forceinline__ void dispatch_kj(int kj, F&& f) {
 #define LDBP_FWD_UNROLL 1
 #endif
 constexpr int kFwdUnroll = LDBP_FWD_UNROLL;
+#ifndef LDBP_FWD_STORE_UNROLL
+#define LDBP_FWD_STORE_UNROLL 2  // storing forward: two steps per loop iteration (C3 -1.3 %, measured;
+                                 // the inference kernel is faster without: C2 +3 %, C4 +4 %)
+#endif
+constexpr int kFwdStoreUnroll = LDBP_FWD_STORE_UNROLL;
 // mbarrier helpers for the split (arrive early / wait late) step barrier.
 __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) { mbar_arrive(bar); }
 #ifndef LDBP_MBAR_SUSPEND_NS
@@ -1140,7 +1145,8 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
   // checkpoint schedule without a per-step modulo: next global step count to store
   int next_ck = a.ckpt ? (a.s0 / a.ckpt_every + 1) * a.ckpt_every : 0x7fffffff;
   float2* ck_ptr = a.ckpt ? a.ckpt + (int64_t)(next_ck / a.ckpt_every - 1) * a.ckpt_stride : nullptr;
-#pragma unroll kFwdUnroll
+  constexpr int kUnroll = STG ? kFwdStoreUnroll : kFwdUnroll;
+#pragma unroll kUnroll
   for (int s = 0; s < a.s1 - a.s0; ++s) {
     TapP hs[NTU];
 #pragma unroll
