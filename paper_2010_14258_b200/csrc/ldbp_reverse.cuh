@@ -75,6 +75,9 @@ __device__ __forceinline__ TapP rev_tap(const TapP (&hs)[N], const TapP* hs_sm, 
 }
 template <int KH, bool SYM, bool NORM, bool FAST>
 __device__ __forceinline__ constexpr bool rev_vark() { return LDBP_REV_VARK && SYM && NORM && FAST && KH >= 1; }
+#ifndef LDBP_REV_PIPE
+#define LDBP_REV_PIPE 2  // window-copy buffers of the reverse: 2 = prefetch one step ahead, 3 = two
+#endif
 #ifndef LDBP_NB_WAIT
 #define LDBP_NB_WAIT 0  // split step barrier: 1 = wait only for the neighbouring warps, 0 = CTA-wide phase
 #endif
@@ -267,8 +270,12 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   const bool none = own == 0;
   uint64_t* bar = sm.bar;
 
-  // prefetch u^(s1-1) (own slots only: no barrier is needed to consume it)
-  async_window<R, NT>(rev_src(a, s1 - 1), e0, a.g, sm.ubuf + (size_t)((s1 - 1) & 1) * R * NT, fast_off);
+  // prefetch u^(s1-1) (own slots only: no barrier is needed to consume it); LDBP_REV_PIPE = 3:
+  // also u^(s1-2) (two steps ahead, three buffers)
+  constexpr int PIPE = LDBP_REV_PIPE;
+  async_window<R, NT>(rev_src(a, s1 - 1), e0, a.g, sm.ubuf + (size_t)((s1 - 1) % PIPE) * R * NT, fast_off);
+  if (PIPE == 3 && s1 - 2 >= s0)
+    async_window<R, NT>(rev_src(a, s1 - 2), e0, a.g, sm.ubuf + (size_t)((s1 - 2) % PIPE) * R * NT, fast_off);
   f2x v[R], g[R];
   load_window<R>(rev_src(a, s1), e0, a.g, v);
   const float2 Pend = sm.norm[a.M - 1].P;
@@ -335,11 +342,15 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   for (int l = s1 - 1; l >= s0; --l) {
     const int li = l - s0;
     const int ph = s1 - 1 - l;  // barrier phase of this step
-    cp_async_wait_all();        // own u^(l) slots landed
-    // prefetch u^(l-1) into the other buffer (this thread's own slots, consumed in step l+1)
-    if (l > s0)
-      async_window<R, NT>(rev_src(a, l - 1), e0, a.g, sm.ubuf + (size_t)((l - 1) & 1) * R * NT, fast_off);
-    const f2x* ub_mine = sm.ubuf + (size_t)(l & 1) * R * NT + ubuf_idx<NT>(0, tid);
+    if (PIPE == 3 && l > s0)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // u^(l) landed, u^(l-1) may be in flight
+    else
+      cp_async_wait_all();  // own u^(l) slots landed
+    // prefetch u^(l-PIPE+1) into a free buffer (this thread's own slots, consumed later)
+    if (l - (PIPE - 1) >= s0)
+      async_window<R, NT>(rev_src(a, l - (PIPE - 1)), e0, a.g,
+                          sm.ubuf + (size_t)((l - (PIPE - 1)) % PIPE) * R * NT, fast_off);
+    const f2x* ub_mine = sm.ubuf + (size_t)(l % PIPE) * R * NT + ubuf_idx<NT>(0, tid);
     const int eoff = (ph & 1) * 2 * KE * NT;
     float dh[2 * NTU];
     float dgam_next = 0.f;
@@ -452,7 +463,7 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * re
   RevSmem sm;
   sm.bar = reinterpret_cast<uint64_t*>(smem_raw);                                    // 2*NW words
   sm.ubuf = reinterpret_cast<f2x*>(smem_raw) + 2 * NW;                               // 2*R*NT
-  sm.edge = sm.ubuf + (size_t)2 * R * NT;                                            // 4*KH*NT
+  sm.edge = sm.ubuf + (size_t)LDBP_REV_PIPE * R * NT;                                           // 4*KH*NT
   sm.taps_adj = reinterpret_cast<TapP*>(sm.edge + (size_t)4 * (KH > 0 ? KH : 1) * NT);  // S*NTU
   sm.norm = reinterpret_cast<StepNorm*>(sm.taps_adj + S * NTU);                      // M
   sm.red = reinterpret_cast<float*>(sm.norm + a.M);                                  // S*NW*V
