@@ -170,8 +170,14 @@ __device__ __forceinline__ uint32_t owned_mask(int64_t e0, const Geo& g) {
   const int64_t lo = tile_lo(g, blockIdx.x);
   const int64_t hi = min(lo + ((int64_t)blockIdx.x < g.NS ? g.Wh : g.W), g.E);
   const Span sp = make_span(e0, g);
-  if (span_fast<R>(sp, g, e0) && e0 >= lo && e0 + R <= hi) return R >= 32 ? 0xffffffffu : ((1u << R) - 1u);
+  constexpr uint32_t FULL = R >= 32 ? 0xffffffffu : ((1u << R) - 1u);
   if (e0 + R <= lo || e0 >= hi) return 0u;
+  if (span_fast<R>(sp, g, e0)) {  // R real samples of one block: only the tile edges cut the run
+    uint32_t m = FULL;
+    if (e0 < lo) m &= FULL << (int)(lo - e0);
+    if (e0 + R > hi) m &= FULL >> (int)(e0 + R - hi);
+    return m;
+  }
   uint32_t m = 0;
 #pragma unroll
   for (int k = 0; k < R; ++k) {
@@ -620,7 +626,10 @@ __device__ __forceinline__ void norm_range(const float2* __restrict__ taps, cons
                                            int n0, int nM, StepNorm* sh_norm, int* sh_flag) {
   constexpr int NT = ntaps_used<SYM, KH>();
   const int S = nM - n0;
-  if (threadIdx.x == 0) *sh_flag = (SYM && LDBP_NORM) ? 1 : 0;
+  if (threadIdx.x == 0) {
+    sh_flag[0] = (SYM && LDBP_NORM) ? 1 : 0;
+    sh_flag[1] = 0;  // set by stage_range when a step's outermost tap is zero (pruned)
+  }
   __syncthreads();
   if (SYM && LDBP_NORM)
     for (int i = threadIdx.x; i < S; i += blockDim.x) {
@@ -669,7 +678,7 @@ template <int KH, bool SYM, bool FWD, bool ADJ>
 __device__ __forceinline__ void stage_range(const float2* __restrict__ taps, const float* __restrict__ gamma,
                                             const uint8_t* __restrict__ mask, int T, int s0, int s1, int n0,
                                             TapP* sh_taps, TapP* sh_taps_adj, float* sh_gamma,
-                                            const StepNorm* sh_norm, bool norm) {
+                                            const StepNorm* sh_norm, bool norm, int* pruned = nullptr) {
   constexpr int NT = ntaps_used<SYM, KH>();
   const int S = s1 - s0;
   for (int i = threadIdx.x; i < S; i += blockDim.x) {
@@ -685,6 +694,7 @@ __device__ __forceinline__ void stage_range(const float2* __restrict__ taps, con
     const int t = (i % NT) + (SYM ? KH : 0);
     float2 h = taps[(int64_t)s * T + t];
     if (mask && !mask[(int64_t)s * T + t]) h = make_float2(0.f, 0.f);
+    if (SYM && KH >= 1 && pruned && t == 2 * KH && h.x == 0.f && h.y == 0.f) *pruned = 1;
     if (norm) {
       const float2 c = sh_norm[s - n0].c;
       const float inv = 1.f / (c.x * c.x + c.y * c.y);
@@ -722,7 +732,10 @@ __device__ __forceinline__ void stage_params(const float2* __restrict__ taps, co
     raw[i] = h;
   }
   for (int i = threadIdx.x; i < S; i += blockDim.x) sh_gamma[i] = gamma[s0 + i];
-  if (threadIdx.x == 0) *sh_flag = (SYM && LDBP_NORM) ? 1 : 0;
+  if (threadIdx.x == 0) {
+    sh_flag[0] = (SYM && LDBP_NORM) ? 1 : 0;
+    sh_flag[1] = 0;  // any step with a zero outermost tap (pruned), set by pack()
+  }
   __syncthreads();
   // Phase A (parallel over steps): c_i = h0 and its conditioning (SYM stores h_0..h_Kh; the
   // energy of the full symmetric filter is |h0|^2 + 2 sum_{j>0} |h_j|^2).
@@ -775,6 +788,7 @@ __device__ __forceinline__ void stage_params(const float2* __restrict__ taps, co
   __syncthreads();
   auto pack = [&](int i, float2 h) {
     const int t = (i % NT) + (SYM ? KH : 0);
+    if (SYM && KH >= 1 && t == 2 * KH && h.x == 0.f && h.y == 0.f) sh_flag[1] = 1;
     if (norm) {  // h / c = h conj(c) / |c|^2
       const float2 c = sh_norm[i / NT].c;
       const float inv = 1.f / (c.x * c.x + c.y * c.y);
@@ -846,13 +860,14 @@ __global__ void __launch_bounds__(256) params_kernel(const float2* __restrict__ 
   extern __shared__ __align__(16) unsigned char par_smem[];
   StepNorm* nrm = in_smem ? reinterpret_cast<StepNorm*>(par_smem + 16) : p.norm;
   int* flag = in_smem ? reinterpret_cast<int*>(par_smem) : p.flag;
+  if (threadIdx.x == 0) p.flag[1] = 0;                 // pruned flag (ordered by norm_range's barriers)
   norm_range<KH, SYM>(taps, mask, T, 0, M, nrm, flag);  // ends with a barrier
   const bool norm = SYM && *flag;
   if (in_smem) {
     for (int i = threadIdx.x; i < M; i += blockDim.x) p.norm[i] = nrm[i];
     if (threadIdx.x == 0) *p.flag = *flag;
   }
-  stage_range<KH, SYM, true, true>(taps, gamma, mask, T, 0, M, 0, p.fwd, p.adj, p.gamma, nrm, norm);
+  stage_range<KH, SYM, true, true>(taps, gamma, mask, T, 0, M, 0, p.fwd, p.adj, p.gamma, nrm, norm, p.flag + 1);
   for (int i = threadIdx.x; i < M; i += blockDim.x) {  // outermost unmasked folded tap per step
     int kj = KH;
     if (mask && SYM) {
@@ -886,7 +901,10 @@ __device__ __forceinline__ void load_ptab(const void* tab, int M, int s0, int s1
   for (int i = tid; i < S; i += nt) ptab_cp4(gam + i, p.gamma + s0 + i);
   if (kj)
     for (int i = tid; i < S; i += nt) ptab_cp4(kj + i, p.kj + s0 + i);
-  if (tid == 0) ptab_cp4(flag, p.flag);
+  if (tid == 0) {
+    ptab_cp4(flag, p.flag);
+    ptab_cp4(flag + 1, p.flag + 1);
+  }
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
 }
 
@@ -1298,7 +1316,7 @@ __device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
   } else if (a.global_norm) {
     norm_range<KH, SYM>(a.taps, a.mask, a.T, a.n0, a.nM, sh_norm, sh_flag);
     stage_range<KH, SYM, true, false>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, a.n0, sh_taps, nullptr, sh_gamma,
-                                      sh_norm, *sh_flag != 0);
+                                      sh_norm, *sh_flag != 0, sh_flag + 1);
   } else {
     stage_params<KH, SYM, false>(a.taps, a.gamma, a.mask, a.T, a.s0, a.s1, sh_taps, nullptr, sh_gamma, sh_norm,
                                  sh_flag);
@@ -1307,12 +1325,7 @@ __device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
   // NEXT-3: does any step of this launch have zero outer taps?  (then the per-step active-length
   // loop runs; otherwise the plain loop, identical code to the unpruned kernel)
   bool pruned = false;
-  if constexpr (SYM && FAST && KH >= 1) {
-    for (int i = 0; i < S; ++i) {
-      const TapP t = sh_taps[i * NTU + KH];
-      pruned |= (lof(t.a) == 0.f && hif(t.a) == 0.f);
-    }
-  }
+  if constexpr (SYM && FAST && KH >= 1) pruned = sh_flag[1] != 0;  // set during staging
   if constexpr (CHK) {  // LDBP_CHECK_FINITE: per-step check, plain loop (pruned taps are zeros, still exact)
     if (SYM && *sh_flag)
       fwd_steps_split<KH, R, SYM, FAST, true, STG, false, true>(a, u, sh_taps, sh_gamma, sh_norm, sh_edge, bars, smap,
