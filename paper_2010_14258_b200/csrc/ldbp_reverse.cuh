@@ -75,6 +75,9 @@ __device__ __forceinline__ TapP rev_tap(const TapP (&hs)[N], const TapP* hs_sm, 
 }
 template <int KH, bool SYM, bool NORM, bool FAST>
 __device__ __forceinline__ constexpr bool rev_vark() { return LDBP_REV_VARK && SYM && NORM && FAST && KH >= 1; }
+#ifndef LDBP_REV_DEFER_RED
+#define LDBP_REV_DEFER_RED 0
+#endif
 #ifndef LDBP_REV_PIPE
 #define LDBP_REV_PIPE 2  // window-copy buffers of the reverse: 2 = prefetch one step ahead, 3 = two
 #endif
@@ -198,11 +201,15 @@ __device__ __forceinline__ void rev_range(const f2x (&g)[R], const f2x (&gl)[KH 
 
 // One full reverse step with the split barrier: interior outputs (no halo needed) before the
 // wait on the ga-edge mbarrier phase, boundary outputs after it.
-template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL, int KJ = KH>
+struct NoMid {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <int KH, int R, bool SYM, bool FAST, bool NORM, bool MASKED, bool NL, int KJ = KH, class Mid = NoMid>
 __device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub_mine, const f2x* left_edge,
                                          const f2x* right_edge, int eoff, uint64_t* bar, unsigned parity,
                                          const TapP* __restrict__ hs_sm, uint32_t own, float gmn,
-                                         float (&dh)[2 * (SYM ? KH + 1 : 2 * KH + 1)], float& dgam_next) {
+                                         float (&dh)[2 * (SYM ? KH + 1 : 2 * KH + 1)], float& dgam_next,
+                                         const Mid& mid = Mid{}) {
   constexpr int NTU = ntaps_used<SYM, KH>();
   constexpr int NT = rev_threads(KH);
   constexpr int KI = KJ < R - KJ ? KJ : R / 2;  // interior [KI, R-KI)
@@ -217,6 +224,7 @@ __device__ __forceinline__ void rev_step(f2x (&g)[R], const f2x* __restrict__ ub
   for (int j = 0; j < (KH > 0 ? KH : 1); ++j) gl[j] = gr[j] = 0ull;
   rev_range<KH, R, SYM, FAST, NORM, MASKED, NL, KI, R - KI, KJ>(g, gl, gr, ub_mine, hs, hs_sm, A, Bq, ng, own, gmn,
                                                                  dgam_next);
+  mid();  // LDBP_REV_DEFER_RED: the previous step's warp reduction, inside the barrier window
   if constexpr (KH > 0) {
     if constexpr (LDBP_NB_WAIT) {
       // neighbour-only wait: within the warp the edges are ordered by the publisher's __syncwarp;
@@ -339,6 +347,23 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   };
   publish(0);
 
+  // per-warp reduction of one step's partials -> red[li][warp][.]
+  constexpr int VP = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
+  auto reduce_step = [&](float (&vals)[VP], int rli) {
+    const float r = warp_reduce_scatter<VP>(vals, lane);
+    constexpr int SH = VP == 2 ? 4 : VP == 4 ? 3 : VP == 8 ? 2 : VP == 16 ? 1 : 0;
+    const int idx = lane >> SH;
+    float* red = sm.red + ((size_t)rli * NW + warp) * V;
+    if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
+  };
+  // LDBP_REV_DEFER_RED: step l's reduction runs inside step l-1's barrier window (after its
+  // interior outputs, before the wait), off the path between publish and the next wait
+  float pend[VP];
+  int pend_li = -1;
+  auto mid = [&]() {
+    if (LDBP_REV_DEFER_RED && pend_li >= 0) reduce_step(pend, pend_li);
+  };
+
   for (int l = s1 - 1; l >= s0; --l) {
     const int li = l - s0;
     const int ph = s1 - 1 - l;  // barrier phase of this step
@@ -369,17 +394,17 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
           });
       } else if (full)
         rev_step<KH, R, SYM, FAST, NORM, false, true>(g, ub_mine, left_edge, right_edge, eoff, bar, LDBP_NB_WAIT ? ph : (ph & 1), hs_sm,
-                                                      own, gmn, dh, dgam_next);
+                                                      own, gmn, dh, dgam_next, mid);
       else
         rev_step<KH, R, SYM, FAST, NORM, true, true>(g, ub_mine, left_edge, right_edge, eoff, bar, LDBP_NB_WAIT ? ph : (ph & 1), hs_sm,
-                                                     own, gmn, dh, dgam_next);
+                                                     own, gmn, dh, dgam_next, mid);
     } else {
       if (full)
         rev_step<KH, R, SYM, FAST, NORM, false, false>(g, ub_mine, left_edge, right_edge, eoff, bar, LDBP_NB_WAIT ? ph : (ph & 1), hs_sm,
-                                                       own, gmn, dh, dgam_next);
+                                                       own, gmn, dh, dgam_next, mid);
       else
         rev_step<KH, R, SYM, FAST, NORM, true, false>(g, ub_mine, left_edge, right_edge, eoff, bar, LDBP_NB_WAIT ? ph : (ph & 1), hs_sm,
-                                                      own, gmn, dh, dgam_next);
+                                                      own, gmn, dh, dgam_next, mid);
     }
     if (l > s0) publish(ph + 1);
     if (none) {
@@ -387,23 +412,25 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
 #pragma unroll
       for (int i = 0; i < 2 * NTU; ++i) dh[i] = 0.f;
     }
-    // ---- per-warp reduction of this step's partials -> red[li][warp][.] ----
+    // ---- per-warp reduction of this step's partials (now, or deferred into the next step) ----
     {
-      constexpr int VP = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
       float vals[VP];
       vals[0] = dgam;
 #pragma unroll
       for (int i = 0; i < 2 * NTU; ++i) vals[1 + i] = dh[i];
 #pragma unroll
       for (int i = V; i < VP; ++i) vals[i] = 0.f;
-      const float r = warp_reduce_scatter<VP>(vals, lane);
-      constexpr int SH = VP == 2 ? 4 : VP == 4 ? 3 : VP == 8 ? 2 : VP == 16 ? 1 : 0;
-      const int idx = lane >> SH;
-      float* red = sm.red + ((size_t)li * NW + warp) * V;
-      if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
+      if (LDBP_REV_DEFER_RED) {
+#pragma unroll
+        for (int i = 0; i < VP; ++i) pend[i] = vals[i];
+        pend_li = li;
+      } else {
+        reduce_step(vals, li);
+      }
     }
     dgam = dgam_next;
   }
+  if (LDBP_REV_DEFER_RED && pend_li >= 0) reduce_step(pend, pend_li);
   if (a.gout) store_owned<R>(a.gout, e0, a.g, g);
   __syncthreads();
   // CTA reduction in fp64, fixed order over warps, mapped back to the original parameters:
