@@ -93,21 +93,62 @@ __host__ __device__ constexpr int rev_threads(int) { return LDBP_REV_NTHR; }
 __host__ __device__ constexpr int rev_threads(int kh) { return kh <= 1 ? 64 : 128; }
 #endif
 
-// Shared-memory window copy: sample k of thread t at f2x index ((k >> 1) * NT + t) * 2 + (k & 1)
-// (16-byte pairs, lane-consecutive -> conflict-free LDS.128 / LDGSTS.128).
-template <int NT>
-__device__ __forceinline__ constexpr int ubuf_idx(int k, int t) { return ((k >> 1) * NT + t) * 2 + (k & 1); }
+#ifndef LDBP_REV_COALESCED
+#define LDBP_REV_COALESCED 1  // warp-cooperative coalesced window copies into a padded thread-major
+                              // layout: 1 = for Kh <= 1 (C5 reverse -6 %; C3 (Kh = 4) +1 %, measured),
+                              // 2 = always, 0 = never
+#endif
+__host__ __device__ constexpr bool rev_coal(int kh) {
+  return LDBP_REV_COALESCED == 2 || (LDBP_REV_COALESCED == 1 && kh <= 1);
+}
+// Shared-memory window copy of u^(l).  LDBP_REV_COALESCED: sample k of thread t at f2x index
+// t*(R+2) + k (one pad pair per thread: a thread's own 16-byte LDS.128 reads, 8 lanes apart by
+// (R+2)*8 bytes, hit distinct banks for R = 12); the copies are issued warp-cooperatively, lane L
+// moving 16-byte chunk m*32+L of the warp's contiguous 32*R-sample run, so every LDGSTS is a
+// coalesced 512-byte read (the per-thread copies read 16 bytes per lane at an R*8-byte stride:
+// 32 sectors and 32 shared-memory wavefronts per instruction).  Otherwise: ((k >> 1)*NT + t)*2 +
+// (k & 1) with per-thread copies.
+template <bool COAL, int R>
+__host__ __device__ constexpr int rev_rs() { return COAL ? R + 2 : R; }
+template <bool COAL, int R, int NT>
+__device__ __forceinline__ constexpr int ubuf_idx(int k, int t) {
+  return COAL ? t * (R + 2) + k : ((k >> 1) * NT + t) * 2 + (k & 1);
+}
+template <bool COAL, int R, int NT>
+__device__ __forceinline__ constexpr int ubuf_off(int k) {  // offset of sample k from the thread's slot 0
+  return COAL ? k : (k >> 1) * 2 * NT + (k & 1);
+}
 
 // Issue the asynchronous copy of this thread's R window samples of `src` (zeros outside [0, E)).
-template <int R, int NT>
+// With COAL a lane may copy other lanes' samples of its warp: consumers order the copies with
+// cp.async.wait_all + __syncwarp.
+template <bool COAL, int R, int NT>
 __device__ __forceinline__ void async_window(const float2* __restrict__ src, int64_t e0, const Geo& g, f2x* buf,
                                              int64_t fast_off) {
   const int t = threadIdx.x;
-  f2x* mine = buf + ubuf_idx<NT>(0, t);
-  const f2x* p = reinterpret_cast<const f2x*>(src) + fast_off;
-  if (fast_off >= 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+  f2x* mine = buf + ubuf_idx<COAL, R, NT>(0, t);
+  const f2x* src2 = reinterpret_cast<const f2x*>(src);
+  const f2x* p = src2 + fast_off;
+  const bool fast = fast_off >= 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+  if constexpr (COAL) {
+    static_assert(NT % 32 == 0, "warp-cooperative copies need whole warps");
+    const int lane = t & 31;
+    const int64_t off0 = __shfl_sync(kFull, fast_off, 0);
+    if (__all_sync(kFull, fast && fast_off == off0 + (int64_t)lane * R)) {
+      const f2x* base = src2 + off0;
+      f2x* wbuf = buf + ubuf_idx<COAL, R, NT>(0, t & ~31);
 #pragma unroll
-    for (int m = 0; m < R / 2; ++m) cp_async16(mine + m * 2 * NT, p + 2 * m);
+      for (int m = 0; m < R / 2; ++m) {
+        const int c = m * 32 + lane, tt = c / (R / 2), k2 = c - tt * (R / 2);
+        cp_async16(wbuf + tt * (R + 2) + 2 * k2, base + 2 * c);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      return;
+    }
+  }
+  if (fast) {
+#pragma unroll
+    for (int m = 0; m < R / 2; ++m) cp_async16(mine + ubuf_off<COAL, R, NT>(2 * m), p + 2 * m);
   } else {  // irregular or 8-byte aligned runs (rare): per-sample copies with zero fill
     const Span sp = make_span(e0, g);
 #pragma unroll
@@ -115,7 +156,7 @@ __device__ __forceinline__ void async_window(const float2* __restrict__ src, int
       int64_t b, pos;
       int q;
       const bool ok = span_at<R>(sp, k, g, e0, &b, &pos, &q);
-      cp_async8_zfill(mine + (k >> 1) * 2 * NT + (k & 1), ok ? (const void*)(src + b * g.n + pos) : (const void*)src,
+      cp_async8_zfill(mine + ubuf_off<COAL, R, NT>(k), ok ? (const void*)(src + b * g.n + pos) : (const void*)src,
                       ok ? 8 : 0);
     }
   }
@@ -169,7 +210,7 @@ __device__ __forceinline__ void rev_range(const f2x (&g)[R], const f2x (&gl)[KH 
                                           f2x (&ng)[R], uint32_t own, float gmn, float& dgam_next) {
   if constexpr (S0 < SE) {
     constexpr int s = S0;
-    const f2x us = ub_mine[(s >> 1) * 2 * rev_threads(KH) + (s & 1)];
+    const f2x us = ub_mine[ubuf_off<rev_coal(KH), R, rev_threads(KH)>(s)];
     const bool mine = !MASKED || ((own >> s) & 1u);
     const f2x ux = bcast(lof(us)), uy = bcast(hif(us));
     f2x acc;
@@ -281,9 +322,11 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   // prefetch u^(s1-1) (own slots only: no barrier is needed to consume it); LDBP_REV_PIPE = 3:
   // also u^(s1-2) (two steps ahead, three buffers)
   constexpr int PIPE = LDBP_REV_PIPE;
-  async_window<R, NT>(rev_src(a, s1 - 1), e0, a.g, sm.ubuf + (size_t)((s1 - 1) % PIPE) * R * NT, fast_off);
+  constexpr bool COAL = rev_coal(KH);
+  constexpr int UB = rev_rs<COAL, R>() * NT;  // f2x per window buffer
+  async_window<COAL, R, NT>(rev_src(a, s1 - 1), e0, a.g, sm.ubuf + (size_t)((s1 - 1) % PIPE) * UB, fast_off);
   if (PIPE == 3 && s1 - 2 >= s0)
-    async_window<R, NT>(rev_src(a, s1 - 2), e0, a.g, sm.ubuf + (size_t)((s1 - 2) % PIPE) * R * NT, fast_off);
+    async_window<COAL, R, NT>(rev_src(a, s1 - 2), e0, a.g, sm.ubuf + (size_t)((s1 - 2) % PIPE) * UB, fast_off);
   f2x v[R], g[R];
   load_window<R>(rev_src(a, s1), e0, a.g, v);
   const float2 Pend = sm.norm[a.M - 1].P;
@@ -371,11 +414,12 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // u^(l) landed, u^(l-1) may be in flight
     else
       cp_async_wait_all();  // own u^(l) slots landed
+    if (COAL) __syncwarp();  // ... and the warp's cooperative copies (and WAR on reuse)
     // prefetch u^(l-PIPE+1) into a free buffer (this thread's own slots, consumed later)
     if (l - (PIPE - 1) >= s0)
-      async_window<R, NT>(rev_src(a, l - (PIPE - 1)), e0, a.g,
-                          sm.ubuf + (size_t)((l - (PIPE - 1)) % PIPE) * R * NT, fast_off);
-    const f2x* ub_mine = sm.ubuf + (size_t)(l % PIPE) * R * NT + ubuf_idx<NT>(0, tid);
+      async_window<COAL, R, NT>(rev_src(a, l - (PIPE - 1)), e0, a.g,
+                          sm.ubuf + (size_t)((l - (PIPE - 1)) % PIPE) * UB, fast_off);
+    const f2x* ub_mine = sm.ubuf + (size_t)(l % PIPE) * UB + ubuf_idx<COAL, R, NT>(0, tid);
     const int eoff = (ph & 1) * 2 * KE * NT;
     float dh[2 * NTU];
     float dgam_next = 0.f;
@@ -489,8 +533,8 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * re
   // carve-up (16-byte aligned regions; mirrored by rev_smem() on the host)
   RevSmem sm;
   sm.bar = reinterpret_cast<uint64_t*>(smem_raw);                                    // 2*NW words
-  sm.ubuf = reinterpret_cast<f2x*>(smem_raw) + 2 * NW;                               // 2*R*NT
-  sm.edge = sm.ubuf + (size_t)LDBP_REV_PIPE * R * NT;                                           // 4*KH*NT
+  sm.ubuf = reinterpret_cast<f2x*>(smem_raw) + 2 * NW;                               // PIPE*RS*NT
+  sm.edge = sm.ubuf + (size_t)LDBP_REV_PIPE * rev_rs<rev_coal(KH), R>() * NT;                                           // 4*KH*NT
   sm.taps_adj = reinterpret_cast<TapP*>(sm.edge + (size_t)4 * (KH > 0 ? KH : 1) * NT);  // S*NTU
   sm.norm = reinterpret_cast<StepNorm*>(sm.taps_adj + S * NTU);                      // M
   sm.red = reinterpret_cast<float*>(sm.norm + a.M);                                  // S*NW*V
