@@ -86,11 +86,12 @@ __device__ __forceinline__ constexpr bool rev_vark() { return LDBP_REV_VARK && S
 #endif
 // Threads per reverse CTA, compile time (every smem offset is an immediate).  Small CTAs (4 warps,
 // 4 CTAs/SM at 128 registers) keep the per-step barrier among few warps (measured on C3: 128
-// threads 2.05 ms, 256: 2.20, 96: 2.23); Kh <= 1 has tiny halos and prefers 64 (C5: 18.7 vs 19.3).
+// threads 2.05 ms, 256: 2.20, 96: 2.23).  Kh <= 1: 64-thread CTAs were faster with per-thread window
+// copies (C5 18.7 vs 19.3 ms); with the coalesced copies 128 is (C5 reverse 17.6 -> 15.2 ms; 256: 15.4).
 #ifdef LDBP_REV_NTHR
 __host__ __device__ constexpr int rev_threads(int) { return LDBP_REV_NTHR; }
 #else
-__host__ __device__ constexpr int rev_threads(int kh) { return kh <= 1 ? 64 : 128; }
+__host__ __device__ constexpr int rev_threads(int) { return 128; }
 #endif
 
 #ifndef LDBP_REV_COALESCED
@@ -514,12 +515,12 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
 }
 
 // Register budget per thread (occupancy 65536 / (threads * regs) CTAs/SM).  Measured: Kh >= 2
-// needs 128 (tighter budgets spill: C3 reverse 2.02 ms at 128 vs 2.30 at 96); Kh <= 1 fits 80
-// (C5 reverse 18.3 vs 19.3 ms).  Taps stay in registers (LDBP_REV_TAPS_SMEM=1 was slower).
+// needs 128 (tighter budgets spill: C3 reverse 2.02 ms at 128 vs 2.30 at 96); Kh <= 1: 96 at 128
+// threads (C5 reverse 15.0 vs 15.2 ms at 80).  Taps stay in registers (LDBP_REV_TAPS_SMEM=1 was slower).
 #ifdef LDBP_REV_REGS
 __host__ __device__ constexpr int rev_regs(int) { return LDBP_REV_REGS; }
 #else
-__host__ __device__ constexpr int rev_regs(int kh) { return kh <= 1 ? 80 : 128; }
+__host__ __device__ constexpr int rev_regs(int kh) { return kh <= 1 ? 96 : 128; }
 #endif
 template <int KH, int R, bool SYM, bool FAST>
 __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * rev_regs(KH)))
