@@ -974,7 +974,7 @@ __host__ __device__ constexpr int fwd_stage_elems(int kh, int r) {
 __host__ __device__ constexpr int fwd_min_blocks(int kh) { return 65536 / (LDBP_FWD_NTHR * fwd_regs(kh)); }
 #else
 #ifndef LDBP_FWD_SMALL_MINB
-#define LDBP_FWD_SMALL_MINB 8  // Kh <= 2: resident 128-thread CTAs per SM (register budget 64)
+#define LDBP_FWD_SMALL_MINB 7  // Kh <= 2: resident 128-thread CTAs per SM (72 registers; C2: 7 0.503, 8 0.497, 6 0.46)
 #endif
 __host__ __device__ constexpr int fwd_min_blocks(int kh) {
   return kh <= 2 ? LDBP_FWD_SMALL_MINB : kh <= 4 ? 3 : (LDBP_FWD_WIDE_THREADS >= 512 && kh >= 6) ? 1 : 2;
