@@ -267,51 +267,92 @@ __global__ void __launch_bounds__(kEssmThreads) essm_bwd_step_kernel(const EssmA
         if (o0 + q < own) ob[t0 + o0 + q] = acc[q];
     }
   }
-  // gradient sums over owned t: warp w takes components v = w, w + 8, ... (warp-uniform
-  // branches); its lanes stride over the owned samples, then a fixed-order warp reduction.
+  // gradient sums over owned t, register-blocked: thread tid owns samples i = 4 tid + q (q < 4,
+  // W = 4 * threads) and forms its partial of every component from register windows (dh: the
+  // T-tap correlation of ga with conj(u); deta: the (2 kappa + 1)-tap correlation of c with p, in
+  // chunks of 8 taps); each chunk of 8 partials is reduced across the warp with the transposing
+  // butterfly into red[warp][v]; the CTA then sums the 8 warps in fixed order.
   lsum = warp_sum(lsum);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cta = blockIdx.y * gridDim.x + blockIdx.x;
   double* outp = a.partials + (int64_t)cta * V;
   __shared__ float lred[kEssmThreads / 32];
+  __shared__ float red[kEssmThreads / 32][2 + 2 * kEssmMaxT + 2 * kEssmMaxKappa + 1 + 8];
   if (lane == 0) lred[warp] = lsum;
-  for (int comp = warp; comp < V; comp += kEssmThreads / 32) {
-    float acc = 0.f;
-    if (comp == 0) {
-#pragma unroll 4
-      for (int i = lane; i < own; i += 32) acc = fmaf(C[pfl(i + hG)], PSI[pfl(i + hG)], acc);  // dgamma'
-    } else if (comp == 1) {
-      // loss: filled below from lred
-    } else if (comp < 2 + 2 * T) {
-      const int jj = (comp - 2) >> 1, im = (comp - 2) & 1;
-      const int du = hU - (jj - KH);
-      if (im) {
-#pragma unroll 4
-        for (int i = lane; i < own; i += 32) {
-          const float2 g = upk(GA[pcx(i + hQ)]), w = upk(U[pcx(i + du)]);
-          acc = fmaf(g.y, w.x, fmaf(-g.x, w.y, acc));
-        }
-      } else {
-#pragma unroll 4
-        for (int i = lane; i < own; i += 32) {
-          const float2 g = upk(GA[pcx(i + hQ)]), w = upk(U[pcx(i + du)]);
-          acc = fmaf(g.x, w.x, fmaf(g.y, w.y, acc));
-        }
+  static_assert(kEssmW == 4 * kEssmThreads, "4 owned samples per thread");
+  constexpr int QN = 4;
+  const int i0 = QN * threadIdx.x;
+  float cq[QN];
+#pragma unroll
+  for (int q = 0; q < QN; ++q) cq[q] = i0 + q < own ? C[pfl(i0 + q + hG)] : 0.f;
+  auto flush8 = [&](float (&v)[8], int comp0, int lim) {  // warp-reduce 8 partials -> red[warp][comp0 + .]
+    const float r = warp_reduce_scatter<8>(v, lane);
+    const int idx = lane >> 2;
+    if ((lane & 3) == 0 && comp0 + idx < lim) red[warp][comp0 + idx] = r;
+  };
+  {  // comp 0 (dgamma') and the T complex tap correlations, comps 2 .. 2 + 2T
+    float vals[2 + 2 * kEssmMaxT + 6];  // padded to a multiple of 8
+#pragma unroll
+    for (int v = 0; v < 2 + 2 * kEssmMaxT + 6; ++v) vals[v] = 0.f;
+#pragma unroll
+    for (int q = 0; q < QN; ++q) vals[0] = fmaf(cq[q], i0 + q < own ? PSI[pfl(i0 + q + hG)] : 0.f, vals[0]);
+    float2 gq[QN];
+#pragma unroll
+    for (int q = 0; q < QN; ++q) gq[q] = i0 + q < own ? upk(GA[pcx(i0 + q + hQ)]) : make_float2(0.f, 0.f);
+    // u window: U index i + du, du = hU - (jj - KH) for jj in [0, T): i0 + q + hU + KH - jj
+    float2 uw[QN + 2 * KH];
+#pragma unroll
+    for (int w = 0; w < QN + 2 * KH; ++w) uw[w] = upk(U[pcx(i0 + hU - KH + w)]);
+#pragma unroll
+    for (int jj = 0; jj < 2 * KH + 1; ++jj) {
+      float re = 0.f, im = 0.f;
+#pragma unroll
+      for (int q = 0; q < QN; ++q) {
+        const float2 g = gq[q], w = uw[q + 2 * KH - jj];  // U[i0 + q + hU - (jj - KH)]
+        re = fmaf(g.x, w.x, fmaf(g.y, w.y, re));
+        im = fmaf(g.y, w.x, fmaf(-g.x, w.y, im));
       }
-    } else {
-      const int k = comp - 2 - 2 * T - kap;
-      const int dp = hA - k;
-#pragma unroll 4
-      for (int i = lane; i < own; i += 32) acc = fmaf(C[pfl(i + hG)], P[pfl(i + dp)], acc);  // c_t p_{t-k}
+      vals[2 + 2 * jj] = re;
+      vals[3 + 2 * jj] = im;
     }
-    acc = warp_sum(acc);
-    if (lane == 0 && comp != 1) outp[comp] = comp >= 2 + 2 * T ? (double)gam * acc : (double)acc;
+    constexpr int NV = ((2 + 2 * (2 * KH + 1)) + 7) / 8;
+#pragma unroll
+    for (int c8 = 0; c8 < NV; ++c8) {
+      float v8[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v8[t] = vals[8 * c8 + t];
+      flush8(v8, 8 * c8, 2 + 2 * T);  // comps below the deta block only
+    }
+  }
+  {  // deta_k = sum_t c_t p_{t-k}, k = kk - kappa, P index i + dp, dp = hA - k; comps 2 + 2T + kk
+    const int NE = 2 * kap + 1, base = 2 + 2 * T;
+    for (int k0 = 0; k0 < NE; k0 += 8) {
+      // P[i0 + q + hA - (k0 + t - kap)] for t < 8, q < 4: window index w = q - t + 7
+      float pw[QN + 7];
+#pragma unroll
+      for (int w = 0; w < QN + 7; ++w) pw[w] = P[pfl(i0 + hA + kap - k0 - 7 + w)];
+      float v8[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < QN; ++q) acc = fmaf(cq[q], pw[q - t + 7], acc);
+        v8[t] = k0 + t < NE ? acc : 0.f;
+      }
+      flush8(v8, base + k0, V);  // comps base + k0 .. base + k0 + 7
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < kEssmThreads / 32; ++w) t += (double)lred[w];
-    outp[1] = t;
+  for (int comp = threadIdx.x; comp < V; comp += kEssmThreads) {
+    if (comp == 1) {
+      double t = 0.0;
+      for (int w = 0; w < kEssmThreads / 32; ++w) t += (double)lred[w];
+      outp[1] = t;
+    } else {
+      double t = 0.0;
+      for (int w = 0; w < kEssmThreads / 32; ++w) t += (double)red[w][comp];
+      outp[comp] = comp >= 2 + 2 * T ? (double)gam * t : t;
+    }
   }
 }
 
