@@ -41,6 +41,11 @@ __device__ __forceinline__ int64_t essm_mod(int64_t i, int64_t n) {
   i %= n;
   return i < 0 ? i + n : i;
 }
+// Position (s0 + i) mod n for s0 in [0, n) and i >= 0: one conditional wrap when i < n.
+__device__ __forceinline__ int64_t essm_wrap(int64_t s0, int i, int64_t n) {
+  const int64_t j = s0 + i;
+  return j < n ? j : (i < n ? j - n : j % n);
+}
 
 // acc + h*s and acc + conj(h)*s for complex h, s (FFMA2 form, see ldbp_f32x2.cuh)
 __device__ __forceinline__ f2x essm_mac(f2x acc, float2 h, f2x s) {
@@ -127,8 +132,9 @@ __global__ void __launch_bounds__(kEssmThreads) essm_fwd_step_kernel(const EssmA
   for (int i = threadIdx.x; i < 2 * KH + 1; i += kEssmThreads) sh_h[i] = a.taps[i];
   essm_tap_table(a.eta, kap, +1, tt);
   const f2x* ub = reinterpret_cast<const f2x*>(a.u) + (int64_t)b * a.n;
+  const int64_t su = essm_mod(t0 - hu, a.n);
   for (int i = threadIdx.x; i < nu + kESlack; i += kEssmThreads)
-    U[pcx(i)] = i < nu ? ub[essm_mod(t0 - hu + i, a.n)] : 0ull;
+    U[pcx(i)] = i < nu ? ub[essm_wrap(su, i, a.n)] : 0ull;
   for (int i = threadIdx.x; i < kESlack; i += kEssmThreads) P[pfl(na + i)] = 0.f;
   __syncthreads();
   // a_t = sum_j h_j u_{t-j}, A index i <-> t = t0 - kappa + i <-> U index i + KH
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(kEssmThreads) essm_bwd_step_kernel(const EssmA
   essm_tap_table(a.eta, kap, +1, tt_f);
   essm_tap_table(a.eta, kap, -1, tt_b);
   const f2x* ub = reinterpret_cast<const f2x*>(a.u) + (int64_t)b * a.n;
-  for (int i = threadIdx.x; i < nU + kESlack; i += kEssmThreads)
+  for (int i = threadIdx.x; i < nU + kESlack; i += kEssmThreads)  // (essm_wrap here: measured +8 %)
     U[pcx(i)] = i < nU ? ub[essm_mod(t0 - hU + i, a.n)] : 0ull;
   for (int i = threadIdx.x; i < kESlack; i += kEssmThreads) {  // finite slack (zero taps x slack)
     P[pfl(nA + i)] = 0.f;
