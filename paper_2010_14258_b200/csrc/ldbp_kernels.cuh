@@ -949,7 +949,12 @@ struct FwdArgs {
 #ifndef LDBP_FWD_R32_KH
 #define LDBP_FWD_R32_KH 5
 #endif
-__host__ __device__ constexpr int fwd_r(int kh) { return kh >= LDBP_FWD_R32_KH ? 32 : LDBP_FWD_R; }
+#ifndef LDBP_FWD_R_SMALL
+#define LDBP_FWD_R_SMALL 18  // inference forward, Kh <= 2 (C2: 18 0.540, 16 0.503, 20 0.47: 18 fits C2 in two waves)
+#endif
+__host__ __device__ constexpr int fwd_r(int kh) {
+  return kh >= LDBP_FWD_R32_KH ? 32 : (kh <= 2 ? LDBP_FWD_R_SMALL : LDBP_FWD_R);
+}
 // register target per thread for each Kh (packed taps cost 4 registers each)
 __host__ __device__ constexpr int fwd_regs(int kh) { return kh <= 2 ? 64 : kh <= 5 ? 80 : 128; }
 #ifdef LDBP_FWD_NTHR  // tuning override: fixed CTA size, residency from the register target
