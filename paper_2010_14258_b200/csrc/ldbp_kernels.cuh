@@ -949,11 +949,15 @@ struct FwdArgs {
 #ifndef LDBP_FWD_R32_KH
 #define LDBP_FWD_R32_KH 5
 #endif
+#ifndef LDBP_FWD_R_WIDE
+#define LDBP_FWD_R_WIDE 32  // inference forward, Kh >= LDBP_FWD_R32_KH (<= 32: ownership masks are 32-bit)
+#endif
 #ifndef LDBP_FWD_R_SMALL
 #define LDBP_FWD_R_SMALL 18  // inference forward, Kh <= 2 (C2: 18 0.540, 16 0.503, 20 0.47: 18 fits C2 in two waves)
 #endif
+// R <= 32 everywhere: per-thread ownership masks are 32-bit (static_assert in fwd_tile_body).
 __host__ __device__ constexpr int fwd_r(int kh) {
-  return kh >= LDBP_FWD_R32_KH ? 32 : (kh <= 2 ? LDBP_FWD_R_SMALL : LDBP_FWD_R);
+  return kh >= LDBP_FWD_R32_KH ? LDBP_FWD_R_WIDE : (kh <= 2 ? LDBP_FWD_R_SMALL : LDBP_FWD_R);
 }
 // register target per thread for each Kh (packed taps cost 4 registers each)
 __host__ __device__ constexpr int fwd_regs(int kh) { return kh <= 2 ? 64 : kh <= 5 ? 80 : 128; }
@@ -1289,6 +1293,7 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
 
 template <int KH, int R, bool SYM, bool FAST, bool STG, bool CHK = false>
 __device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
+  static_assert(R % 2 == 0 && R <= 32, "R samples per thread: even, at most 32 (32-bit ownership masks)");
   constexpr int NTU = ntaps_used<SYM, KH>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int S = a.s1 - a.s0;

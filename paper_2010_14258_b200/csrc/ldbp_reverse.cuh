@@ -308,7 +308,7 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   constexpr int V = 1 + 2 * NTU;
   constexpr int KE = KH > 0 ? KH : 1;
   constexpr uint32_t FULL = R >= 32 ? 0xffffffffu : ((1u << R) - 1u);
-  static_assert(R % 2 == 0 && R >= KH, "window pairs and neighbour halos need even R >= Kh");
+  static_assert(R % 2 == 0 && R >= KH && R <= 32, "window pairs and neighbour halos need even Kh <= R <= 32");
   const int tid = threadIdx.x;
   const int left = tid > 0 ? tid - 1 : 0;
   const int right = tid + 1 < NT ? tid + 1 : tid;
