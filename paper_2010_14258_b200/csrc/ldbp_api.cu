@@ -48,7 +48,6 @@ int cuda_check(const char* what) {
 }
 
 constexpr int kFwdR = LDBP_FWD_R;
-constexpr int kBwdR = LDBP_BWD_R;
 constexpr int kFwdMaxThreads = 512;
 constexpr int kBwdMaxThreads = 256;
 
@@ -241,7 +240,7 @@ size_t bwd_smem(int kh, bool sym, int steps, int nthreads) {
   s += sizeof(ldbp::StepNorm) * steps;                                  // normalisation
   s += sizeof(float) * ((steps + 3) & ~3) + 16;                         // gamma + flag
   s += sizeof(float) * ((steps * nw * V + 3) & ~3);                     // per-warp partials
-  s += sizeof(float2) * size_t(steps + LDBP_BWD_PREFETCH) * kBwdR * nthreads;  // tape (+ prefetch buffer)
+  s += sizeof(float2) * size_t(steps + LDBP_BWD_PREFETCH) * bwd_r(kh) * nthreads;  // tape (+ prefetch buffer)
   return s;
 }
 
@@ -360,7 +359,7 @@ BwdPlan plan_bwd(const ldbp_dims* d, bool query_device) {
     BwdFn fn = get_bwd(kh, sym, !(d->flags & LDBP_PRECISE));
     occ = bwd_occupancy(fn, p.nthreads, bwd_smem(kh, sym, p.C, p.nthreads));
   }
-  p.tile = plan_tiles(d->batch, d->n, H, kBwdR, p.nthreads, occ, sms);
+  p.tile = plan_tiles(d->batch, d->n, H, bwd_r(kh), p.nthreads, occ, sms);
   return p;
 }
 

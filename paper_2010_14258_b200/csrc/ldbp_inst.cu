@@ -31,7 +31,7 @@ FwdFn LDBP_CAT(ldbp_get_fwd_store_, LDBP_KH)(bool sym, bool chk) {
 }
 
 BwdFn LDBP_CAT(ldbp_get_bwd_, LDBP_KH)(bool sym, bool fast) {
-  constexpr int K = LDBP_KH, R = LDBP_BWD_R;
+  constexpr int K = LDBP_KH, R = bwd_r(LDBP_KH);
   if (sym) return fast ? ldbp::bwd_segment_kernel<K, R, true, true> : ldbp::bwd_segment_kernel<K, R, true, false>;
   return fast ? ldbp::bwd_segment_kernel<K, R, false, true> : ldbp::bwd_segment_kernel<K, R, false, false>;
 }

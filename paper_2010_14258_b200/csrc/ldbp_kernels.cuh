@@ -30,6 +30,11 @@
 #ifndef LDBP_BWD_R
 #define LDBP_BWD_R 8   // samples per thread, backward kernels
 #endif
+#ifndef LDBP_BWD_R_SMALL
+#define LDBP_BWD_R_SMALL 4  // segment backward for Kh <= 2 (C1 CUDA-graph step 18.5 -> 14.4 us: half the
+                            // serial per-thread chain of the latency-bound tiny problems)
+#endif
+__host__ __device__ constexpr int bwd_r(int kh) { return kh <= 2 ? LDBP_BWD_R_SMALL : LDBP_BWD_R; }
 #ifndef LDBP_REV_R
 #define LDBP_REV_R 12  // samples per thread, store-all reverse kernel (measured: 12 >= 16 > 8)
 #endif
