@@ -34,12 +34,15 @@ UNIT = "Gsample·steps/s"
 POWERS_DBM = (-2.0, -1.0, 0.0, 1.0)  # training power set of §V-A
 
 CONFIGS = {
-    # name: blocks per GPU, samples per block, spans, steps per span, taps, mode
-    "C1": dict(B=4, n=1024, spans=2, sps=2, T=3, mode="train"),
-    "C2": dict(B=256, n=16384, spans=25, sps=1, T=5, mode="fwd"),
-    "C3": dict(B=512, n=16384, spans=25, sps=2, T=9, mode="train"),
-    "C4": dict(B=4096, n=16384, spans=25, sps=4, T=15, mode="fwd"),
-    "C5": dict(B=8192, n=32768, spans=25, sps=1, T=3, mode="train"),
+    # name: blocks (per GPU when weak-scaled, global when strong-scaled), samples per block, spans,
+    # steps per span, taps, mode, seed index (ldbp_inputs keyed streams), default scaling (BJ configs:
+    # C4 "2^26 total samples sharded across 1/2/4/8 GPUs" and C5 "8192 blocks on 8 GPUs" fix the
+    # global batch; C1-C3 fix the per-GPU batch)
+    "C1": dict(B=4, n=1024, spans=2, sps=2, T=3, mode="train", idx=1, scaling="weak"),
+    "C2": dict(B=256, n=16384, spans=25, sps=1, T=5, mode="fwd", idx=2, scaling="weak"),
+    "C3": dict(B=512, n=16384, spans=25, sps=2, T=9, mode="train", idx=3, scaling="weak"),
+    "C4": dict(B=4096, n=16384, spans=25, sps=4, T=15, mode="fwd", idx=4, scaling="strong"),
+    "C5": dict(B=8192, n=32768, spans=25, sps=1, T=3, mode="train", idx=5, scaling="strong"),
 }
 WORKLOAD = {
     "C1": "Tiny LDBP fwd+bwd: 4 blocks x 1024, M=4, T=3",
@@ -122,6 +125,8 @@ class Clocks:
 # workload
 # ----------------------------------------------------------------------------------------
 def make_model(cfg):
+    """Product-side model init (GPU leg): DBP step plan + gamma' (G3/G4) and LS inverse-CD taps
+    with gain cap (G12b) from the package's host helpers."""
     import numpy as np
 
     from paper_2010_14258_b200 import init
@@ -131,18 +136,42 @@ def make_model(cfg):
     return taps.astype(np.complex128), gamma
 
 
-def make_inputs(cfg, rank, seed_base=1000):
+def make_model_oracle(cfg):
+    """The same model from the oracle's own helpers (CPU legs: the reference arm and cpu_baseline
+    never import the product package, so libldbp.so is never loaded into the oracle process)."""
+    from oracle import physics, steps
+
+    deltas, gamma = steps.dbp_plan(cfg["spans"], 80.0, cfg["sps"], 0.2, 1.3)
+    taps = [steps.ls_taps(steps.xi_of(d, physics.ps2_per_km(-21.7), 21.4e9), cfg["T"], cap=1.0) for d in deltas]
+    import numpy as np
+
+    return np.stack(taps), gamma
+
+
+def global_blocks(cfg, world, scaling):
+    return cfg["B"] * world if scaling == "weak" else cfg["B"]
+
+
+def my_blocks(cfg, world, rank, scaling):
+    """Global block indices of this rank: contiguous shard (dp.shard) of the global batch."""
+    from paper_2010_14258_b200.dp import shard
+
+    return shard(rank, world, global_blocks(cfg, world, scaling))
+
+
+def make_inputs(cfg, blocks):
+    """Received blocks and tx targets keyed by GLOBAL block index (same union for any G)."""
     import ldbp_inputs as li
 
-    B, n = cfg["B"], cfg["n"]
-    blocks = range(rank * B, (rank + 1) * B)  # global block indices of this rank
-    pw = li.dbm_to_w(li.pick_powers_dbm(seed_base, blocks, POWERS_DBM))
-    x = li.bandlimited_blocks_torch(seed_base + 2 * rank, B, n, pw)
-    tgt = li.bandlimited_blocks_torch(seed_base + 2 * rank + 1, B, n, pw)
+    blocks = list(blocks)
+    pw = li.dbm_to_w(li.pick_powers_dbm(cfg["idx"], blocks, POWERS_DBM))
+    x = li.bandlimited_blocks_keyed_torch(cfg["idx"], blocks, cfg["n"], pw)
+    tgt = li.bandlimited_blocks_keyed_torch(cfg["idx"], blocks, cfg["n"], pw, purpose="target") \
+        if cfg["mode"] == "train" else None
     return x, tgt
 
 
-def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_clocks=True):
+def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_clocks=True, scaling=None):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -154,8 +183,10 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
     taps, gamma = make_model(cfg)
     M, T = taps.shape
     kh = (T - 1) // 2
-    B, n = cfg["B"], cfg["n"]
-    x, tgt = make_inputs(cfg, rank)
+    scaling = scaling or cfg["scaling"]
+    blocks = my_blocks(cfg, world, rank, scaling)
+    B, n = len(blocks), cfg["n"]
+    x, tgt = make_inputs(cfg, blocks)
     train = cfg["mode"] == "train"
     st = P.TrainState.create(taps, gamma, device=dev)
     ws = P.Workspace()
@@ -198,7 +229,7 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
         ms = float(t.item())
     clk = clocks.stop(t_wall0, t_wall1) if clocks else None
     ms_per_step = ms / steps
-    samples_global = B * n * world
+    samples_global = global_blocks(cfg, world, scaling) * n
     value = samples_global * M / (ms_per_step * 1e-3) / 1e9
 
     # per-kernel durations, live (CUDA events around each launch, same stream), separate pass
@@ -224,12 +255,13 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
     if want_e2e:
         e2e_steps = max(2, min(steps, 10))
         hx = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for _ in range(2)]
-        ht = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for _ in range(2)]
+        ht = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) if train else None for _ in range(2)]
         for i in range(2):
             hx[i].copy_(x)
-            ht[i].copy_(tgt)
+            if train:
+                ht[i].copy_(tgt)
         dx = [torch.empty_like(x) for _ in range(2)]
-        dt = [torch.empty_like(tgt) for _ in range(2)]
+        dt = [torch.empty_like(tgt) if train else None for _ in range(2)]
         res = [torch.empty(1 if train else y.numel(), dtype=torch.float64 if train else torch.complex64,
                            pin_memory=True) for _ in range(2)]
         read_ev = [torch.cuda.Event() for _ in range(2)]
@@ -318,7 +350,7 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
     step_roof = {"bound_gsample_steps": bound, "frac": value / bound, "instr_per_sample_step": ips}
     return dict(value=value, ms_per_step=ms_per_step, clk=clk, roof=roof, step_roof=step_roof, e2e=e2e,
                 gpu_launches=gpu_launches, kernel_shares=kernel_shares, samples_global=samples_global, M=M, T=T,
-                B=B, n=n, wall_s=t_wall1 - t_wall0)
+                B=B, n=n, wall_s=t_wall1 - t_wall0, scaling=scaling, global_blocks=global_blocks(cfg, world, scaling))
 
 
 def graph_latency(cfg, reps=50):
@@ -329,7 +361,7 @@ def graph_latency(cfg, reps=50):
     import paper_2010_14258_b200 as P
 
     taps, gamma = make_model(cfg)
-    x, tgt = make_inputs(cfg, 0)
+    x, tgt = make_inputs(cfg, range(cfg["B"]))
     st = P.TrainState.create(taps, gamma)
     ws = P.Workspace()
     train = cfg["mode"] == "train"
@@ -388,10 +420,10 @@ def _oracle_block(args):
 
     cfg_name, b, taps, gamma, train = args
     cfg = CONFIGS[cfg_name]
-    pw = li.dbm_to_w(li.pick_powers_dbm(1000, [b], POWERS_DBM))
-    x = li.bandlimited_blocks(1000, [b], cfg["n"], pw)
+    pw = li.dbm_to_w(li.pick_powers_dbm(cfg["idx"], [b], POWERS_DBM))
+    x = li.bandlimited_blocks(cfg["idx"], [b], cfg["n"], pw)
     if train:
-        t = li.bandlimited_blocks(1000, [b], cfg["n"], pw, purpose="target")
+        t = li.bandlimited_blocks(cfg["idx"], [b], cfg["n"], pw, purpose="target")
         t0 = time.perf_counter()
         O.loss_grad(x, t, taps, gamma, symmetric=True)
     else:
@@ -407,7 +439,7 @@ def oracle_throughput(cfg_name, target_s, cores, pool=None):
     import numpy as np
 
     cfg = CONFIGS[cfg_name]
-    taps, gamma = make_model(cfg)
+    taps, gamma = make_model_oracle(cfg)
     taps = taps.astype(np.complex64).astype(np.complex128)
     gamma = gamma.astype(np.float32).astype(np.float64)
     train = cfg["mode"] == "train"
@@ -448,15 +480,32 @@ def run_reference(args, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling or cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD[args.config], "config": args.config, "B": cfg["B"], "n": cfg["n"],
                    "sample_blocks_per_step": nblk},
+        "native_libs_loaded": [l for l in _loaded_libs() if "ldbp" in l],
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"{nblk} of {cfg['B']} blocks per step (numpy fp64 oracle, process pool)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _loaded_libs():
+    try:
+        return sorted({ln.split()[-1] for ln in open("/proc/self/maps") if ln.rstrip().endswith(".so")})
+    except OSError:
+        return []
+
+
+def _compact(nm, c, rr):
+    """Compact per-config summary (the driver keeps only the tail of stdout)."""
+    roof = rr["roof"] or {}
+    d = {"mode": c["mode"], "value": round(rr["value"], 2), "ms": round(rr["ms_per_step"], 4),
+         "kernel": roof.get("kernel"), "kernel_frac": round(roof.get("frac", 0.0), 3),
+         "step_frac": round(rr["step_roof"]["frac"], 3), "blocks": rr["global_blocks"], "scaling": rr["scaling"]}
+    return d
 
 
 # ----------------------------------------------------------------------------------------
@@ -466,9 +515,12 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="weak: per-GPU batch fixed (C1-C3 default); strong: global batch fixed (C4, C5 default)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -485,6 +537,9 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # communicator lines (ranks, NVLS/P2P transport) on stderr for the driver's rank check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     import __graft_entry__
 
@@ -495,49 +550,59 @@ def main():
     import paper_2010_14258_b200  # noqa: F401
 
     main_cfg = CONFIGS[args.config]
-    r = run_config(args.config, main_cfg, args.steps, args.warmup, world, rank, dev)
-    extra = {}
-    if world == 1 and not args.no_extra:
+    r = run_config(args.config, main_cfg, args.steps, args.warmup, world, rank, dev, want_e2e=not args.no_e2e,
+                   scaling=args.scaling)
+    extra, detail = {}, {}
+    if not args.no_extra:
         for nm in ("C2", "C4", "C5", "C1"):
             if nm == args.config:
                 continue
             c = CONFIGS[nm]
             k = 20 if nm in ("C2", "C1") else 10
             rr = run_config(nm, c, k, 3, world, rank, dev, want_e2e=False, want_clocks=False)
-            extra[nm] = {"workload": WORKLOAD[nm], "mode": c["mode"], "value": rr["value"], "unit": UNIT,
-                         "ms_per_step": rr["ms_per_step"], "roofline": rr["roof"], "step_roofline": rr["step_roof"],
-                         "kernel_shares": rr["kernel_shares"]}
-            if nm in ("C1", "C2"):  # launch-latency-sensitive: the step as one CUDA graph, replayed
+            extra[nm] = _compact(nm, c, rr)
+            detail[nm] = {"workload": WORKLOAD[nm], "roofline": rr["roof"], "step_roofline": rr["step_roof"],
+                          "kernel_shares": rr["kernel_shares"]}
+            if nm in ("C1", "C2") and world == 1:  # launch-latency-sensitive: one CUDA graph, replayed
                 us = graph_latency(c)
                 M = len(make_model(c)[1])
-                extra[nm]["cuda_graph"] = {"us_per_step": us, "value": c["B"] * c["n"] * M / (us * 1e-6) / 1e9,
-                                           "unit": UNIT, "note": "whole step in one CUDA graph, back-to-back "
-                                           "replays, inputs L2-resident (C1 is latency-bound)"}
+                extra[nm]["graph_us"] = round(us, 2)
+                extra[nm]["graph_value"] = round(c["B"] * c["n"] * M / (us * 1e-6) / 1e9, 2)
             torch.cuda.empty_cache()
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         cores = os.cpu_count() or 1
         v, nblk, wall = oracle_throughput(args.config, 15.0, cores)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{nblk} of {main_cfg['B']} {args.config} blocks, full fwd+bwd (numpy fp64), {wall:.1f} s "
                          f"on a {cores}-process pool"}
+    line = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": r["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "extra": extra,
             "config": {"workload": WORKLOAD[args.config], "config": args.config, "blocks_per_gpu": r["B"],
-                       "global_blocks": r["B"] * world, "n": r["n"], "steps_M": r["M"], "taps_T": r["T"],
+                       "global_blocks": r["global_blocks"], "n": r["n"], "steps_M": r["M"], "taps_T": r["T"],
                        "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) between timed steps",
-                       "inputs": "band-limited circular Gaussian, P in {-2,-1,0,1} dBm, LS inverse-CD taps (cap 1)"},
+                       "inputs": "band-limited circular Gaussian keyed by global block index, P in {-2,-1,0,1} dBm, "
+                                 "LS inverse-CD taps (cap 1)"},
             "clocks": r["clk"], "roofline": r["roof"], "step_roofline": r["step_roof"], "cpu_baseline": cpu,
             "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "kernel_shares": r["kernel_shares"],
-            "extra": extra,
         }
-        print(json.dumps(line), flush=True)
+        try:
+            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+            with open(os.path.join(ROOT, "gpurun_out", f"bench_detail_n{world}.json"), "w") as fh:
+                json.dump({"line": line, "extra_detail": detail}, fh, indent=1)
+        except OSError:
+            pass
+        print(json.dumps({"extra_detail": detail}), file=sys.stderr, flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
     return 0
 
 

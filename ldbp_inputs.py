@@ -170,3 +170,31 @@ def bandlimited_blocks_torch(seed: int, B: int, n: int, power_w, device="cuda", 
         w = torch.randn((e - s, n), dtype=torch.complex64, device=device, generator=g)
         out[s:e] = torch.fft.ifft(torch.fft.fft(w, dim=-1) * mask, dim=-1) * amp[s:e, None]
     return out
+
+
+def bandlimited_blocks_keyed_torch(cfg_index: int, blocks, n: int, power_w, device="cuda",
+                                   occupied: float = OCCUPIED, chunk: int = 256, purpose: str = "signal"):
+    """Band-limited circular Gaussian blocks (recipe above) drawn on the device, one seeded torch
+    generator per GLOBAL block index: block b's samples depend only on (cfg_index, b, purpose),
+    so the union over ranks of a sharded batch is the same for any number of ranks G
+    (SURVEY.md §8(e)).  complex64 [len(blocks)][n]; ``power_w`` scalar or per listed block."""
+    import torch
+
+    blocks = list(blocks)
+    B = len(blocks)
+    out = torch.empty((B, n), dtype=torch.complex64, device=device)
+    f = torch.fft.fftfreq(n, device=device)
+    mask = (f.abs() <= occupied / 2.0).to(torch.complex64)
+    norm = float(np.sqrt(n / float(mask.real.sum().item())))
+    pw = torch.as_tensor(np.broadcast_to(np.asarray(power_w, dtype=np.float64), (B,)).copy(), device=device)
+    amp = (pw.sqrt() * norm).to(torch.float32)
+    g = torch.Generator(device=device)
+    w = torch.empty((min(chunk, max(B, 1)), n), dtype=torch.complex64, device=device)
+    for s in range(0, B, chunk):
+        e = min(B, s + chunk)
+        for i in range(s, e):
+            key = np.random.SeedSequence([SEED_ROOT, int(cfg_index), int(blocks[i]), PURPOSES[purpose]])
+            g.manual_seed(int(key.generate_state(1, dtype=np.uint64)[0] >> 1))
+            torch.randn((n,), dtype=torch.complex64, device=device, generator=g, out=w[i - s])
+        out[s:e] = torch.fft.ifft(torch.fft.fft(w[: e - s], dim=-1) * mask, dim=-1) * amp[s:e, None]
+    return out

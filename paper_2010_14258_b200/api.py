@@ -5,7 +5,10 @@ PyTorch is plumbing only: tensors provide device memory, the current CUDA stream
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import functools
+import threading
 from dataclasses import dataclass, field
 
 import torch
@@ -79,10 +82,42 @@ _default_ws = {}
 
 
 def _ws(device, nbytes, ws):
+    """Scratch for one call, enqueued on torch's current stream (the call's stream: see _on_stream).
+    Default workspaces are private per (device, stream, thread), so concurrent calls on different
+    streams or threads never share scratch; a caller-supplied ``ws`` used on several streams is
+    protected against early reuse by record_stream (the caching allocator then waits for every
+    stream that used the buffer before handing its memory out again)."""
+    cur = torch.cuda.current_stream(device)
     if ws is None:
-        ws = _default_ws.setdefault(str(device), Workspace())
+        key = (str(device), cur.cuda_stream, threading.get_ident())
+        ws = _default_ws.setdefault(key, Workspace())
     b = ws.get(nbytes, device)
+    if b is not None and not torch.cuda.is_current_stream_capturing():
+        b.record_stream(cur)
     return b, nbytes
+
+
+def _on_stream(fn):
+    """Run a binding with ``stream=`` made torch's current stream, so that every output and
+    scratch tensor is allocated on (and its memory ordered by) the stream the kernels run on."""
+
+    @functools.wraps(fn)
+    def wrapper(*args, stream=None, **kw):
+        ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+        with ctx:
+            return fn(*args, stream=stream, **kw)
+
+    return wrapper
+
+
+def _check_buf(buf, length, device):
+    """Caller-supplied gradient buffer: float64, contiguous, exactly ``length`` long, on ``device``."""
+    if buf is None:
+        return torch.empty(length, dtype=torch.float64, device=device)
+    _need(buf, "buf", torch.float64, (length,))
+    if buf.device != device:
+        raise ValueError(f"buf is on {buf.device}, expected {device}")
+    return buf
 
 
 def _check_model(x, taps, gamma):
@@ -97,6 +132,7 @@ def _check_model(x, taps, gamma):
     return x.shape[0], x.shape[1], M, T
 
 
+@_on_stream
 def ldbp_forward(x, taps, gamma, *, symmetric=True, precise=False, check_finite=False, out=None, ws=None,
                  stream=None):
     """y = f_theta(x) (Eq. 7) for complex64 x [B][n], taps [M][T], gamma [M].  check_finite:
@@ -112,6 +148,7 @@ def ldbp_forward(x, taps, gamma, *, symmetric=True, precise=False, check_finite=
     return y
 
 
+@_on_stream
 def ldbp_backward(x, gy, taps, gamma, *, symmetric=True, precise=False, need_gx=True, ws=None, stream=None):
     """Reverse mode for incoming gy = dL/dy.  Returns (dtaps complex128 [M][T], dgamma f64 [M], gx or None)."""
     B, n, M, T = _check_model(x, taps, gamma)
@@ -127,6 +164,7 @@ def ldbp_backward(x, gy, taps, gamma, *, symmetric=True, precise=False, need_gx=
     return torch.view_as_complex(dt), dg, gx
 
 
+@_on_stream
 def ldbp_loss_grad(x, target, taps, gamma, *, mask=None, symmetric=True, precise=False, check_finite=False,
                    buf=None, ws=None, stream=None):
     """[sum|e|^2 | dgamma[M] | dtaps[M][T][2]] (float64, unscaled, this device's blocks only)."""
@@ -135,7 +173,7 @@ def ldbp_loss_grad(x, target, taps, gamma, *, mask=None, symmetric=True, precise
     if mask is not None:
         _need(mask, "mask", torch.uint8, (M, T))
     d = make_dims(B, n, M, T, symmetric, precise, check_finite)
-    out = torch.empty(1 + M + 2 * M * T, dtype=torch.float64, device=x.device) if buf is None else buf
+    out = _check_buf(buf, 1 + M + 2 * M * T, x.device)
     nb = workspace_bytes(d, OP_LOSS_GRAD)
     w, nb = _ws(x.device, nb, ws)
     check(lib.ldbp_loss_grad(ctypes.byref(d), _p(x), _p(target), _p(taps), _p(gamma), _p(mask), _p(out), _p(w), nb,
@@ -193,8 +231,10 @@ class TrainState:
         return self.taps.shape[1]
 
 
+@_on_stream
 def ldbp_adam_update(state: TrainState, buf_reduced, n_global: float, *, stream=None):
     """One Adam step on the device from an (all-reduced) gradient buffer."""
+    _need(buf_reduced, "buf_reduced", torch.float64, (1 + state.M + 2 * state.M * state.T,))
     state.t += 1
     d = make_dims(1, state.T, state.M, state.T, state.symmetric, state.precise)
     a = state.adam
@@ -204,12 +244,13 @@ def ldbp_adam_update(state: TrainState, buf_reduced, n_global: float, *, stream=
           "ldbp_adam_update")
 
 
+@_on_stream
 def ldbp_train_step(state: TrainState, x, target, *, buf=None, ws=None, stream=None):
     """Single-process step: loss_grad on the working copies then Adam with n_global = B*n."""
     B, n, M, T = _check_model(x, state.taps, state.gamma)
     _need(target, "target", torch.complex64, x.shape)
     d = make_dims(B, n, M, T, state.symmetric, state.precise)
-    out = torch.empty(1 + M + 2 * M * T, dtype=torch.float64, device=x.device) if buf is None else buf
+    out = _check_buf(buf, 1 + M + 2 * M * T, x.device)
     nb = workspace_bytes(d, OP_TRAIN_STEP)
     w, nb = _ws(x.device, nb, ws)
     state.t += 1
@@ -233,6 +274,7 @@ def _check_rx(y_like, symbols, power_w, h_mf, sps):
     return B, n, (h_mf.numel() - 1) // 2
 
 
+@_on_stream
 def ldbp_rx_loss_grad(y, symbols, power_w, h_mf, *, sps=2, need_grad=True, ws=None, stream=None):
     """Receiver-chain symbol loss (§8(f) NEXT-1): matched filter + downsample + genie phase.
     Returns (errs float64 [B], gy complex64 [B][n] or None); L = sum(errs)."""
@@ -248,6 +290,7 @@ def ldbp_rx_loss_grad(y, symbols, power_w, h_mf, *, sps=2, need_grad=True, ws=No
     return errs, gy
 
 
+@_on_stream
 def ldbp_rx_train_grad(x, symbols, power_w, h_mf, taps, gamma, *, sps=2, mask=None, symmetric=True, precise=False,
                        buf=None, ws=None, stream=None):
     """[sum errs | dgamma[M] | dtaps[M][T][2]] of the receiver-chain loss through LDBP (float64,
@@ -257,7 +300,7 @@ def ldbp_rx_train_grad(x, symbols, power_w, h_mf, taps, gamma, *, sps=2, mask=No
     if mask is not None:
         _need(mask, "mask", torch.uint8, (M, T))
     d = make_dims(B, n, M, T, symmetric, precise)
-    out = torch.empty(1 + M + 2 * M * T, dtype=torch.float64, device=x.device) if buf is None else buf
+    out = _check_buf(buf, 1 + M + 2 * M * T, x.device)
     nb = ctypes.c_size_t(0)
     check(lib.ldbp_rx_train_workspace_bytes(ctypes.byref(d), sps, ctypes.byref(nb)), "ldbp_rx_train_workspace_bytes")
     w, nbv = _ws(x.device, int(nb.value), ws)
@@ -274,12 +317,14 @@ def _check_eta(eta, M):
     return (eta.shape[1] - 1) // 2
 
 
+@_on_stream
 def ldbp_essm_forward(x, taps, gamma, eta, *, symmetric=True, precise=False, out=None, ws=None, stream=None):
     """Learned ESSM forward (§8(f) NEXT-4): y = f_theta(x) with filtered nonlinear steps."""
     B, n, M, T = _check_model(x, taps, gamma)
     kappa = _check_eta(eta, M)
     d = make_dims(B, n, M, T, symmetric, precise)
     y = torch.empty_like(x) if out is None else out
+    _need(y, "out", torch.complex64, x.shape)
     nb = ctypes.c_size_t(0)
     check(lib.ldbp_essm_workspace_bytes(ctypes.byref(d), kappa, OP_FORWARD, ctypes.byref(nb)), "ldbp_essm_workspace_bytes")
     w, nbv = _ws(x.device, int(nb.value), ws)
@@ -288,6 +333,7 @@ def ldbp_essm_forward(x, taps, gamma, eta, *, symmetric=True, precise=False, out
     return y
 
 
+@_on_stream
 def ldbp_essm_loss_grad(x, target, taps, gamma, eta, *, symmetric=True, precise=False, buf=None, ws=None,
                         stream=None):
     """[sum|e|^2 | dgamma[M] | dtaps[M][T][2] | deta[M][2kappa+1]] (float64, unscaled)."""
@@ -295,8 +341,7 @@ def ldbp_essm_loss_grad(x, target, taps, gamma, eta, *, symmetric=True, precise=
     kappa = _check_eta(eta, M)
     _need(target, "target", torch.complex64, x.shape)
     d = make_dims(B, n, M, T, symmetric, precise)
-    out = torch.empty(1 + M + 2 * M * T + M * (2 * kappa + 1), dtype=torch.float64, device=x.device) \
-        if buf is None else buf
+    out = _check_buf(buf, 1 + M + 2 * M * T + M * (2 * kappa + 1), x.device)
     nb = ctypes.c_size_t(0)
     check(lib.ldbp_essm_workspace_bytes(ctypes.byref(d), kappa, OP_LOSS_GRAD, ctypes.byref(nb)),
           "ldbp_essm_workspace_bytes")
@@ -306,6 +351,7 @@ def ldbp_essm_loss_grad(x, target, taps, gamma, eta, *, symmetric=True, precise=
     return out
 
 
+@_on_stream
 def ldbp_ssfm_link(u, deltas_km, *, spans, span_km, alpha_np, beta2, gamma, fs_hz, ase_sigma=0.0, noise=None,
                    decim=0, cutoff=0.5, ws=None, stream=None):
     """GPU SSFM channel generator (§8(f) NEXT-2): propagates u [B][n] (complex64, in place) over

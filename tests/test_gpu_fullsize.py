@@ -69,7 +69,7 @@ def test_forward_full_size_sampled(P, name, B, n, spans, sps, T):
     ("C3", 512, 16384, 25, 2, 9, 4),
     ("C5", 8192, 32768, 25, 1, 3, 2),
 ])
-def test_loss_grad_full_size(P, name, B, n, spans, sps, T, shards):
+def test_loss_grad_full_size(P, monkeypatch, name, B, n, spans, sps, T, shards):
     taps, gamma = ls_model(spans, sps, T)
     ht, gt = as_dev(taps, gamma)
     x = gauss(B, n, 8)
@@ -79,7 +79,10 @@ def test_loss_grad_full_size(P, name, B, n, spans, sps, T, shards):
     parts = sum(P.ldbp_loss_grad(x[s:s + step].contiguous(), tgt[s:s + step].contiguous(), ht, gt).cpu().numpy()
                 for s in range(0, B, step))
     assert rel(parts, full) <= 1e-6
-    # sampled blocks through the same launch path vs the oracle
+    # two sampled blocks vs the oracle, forced through the store-all schedule bench.py times (2 blocks
+    # are below its 2^20-sample threshold; the whole timed batch is in test_gpu_timed_path.py)
+    monkeypatch.setenv("LDBP_BWD_MODE", "1")
+    monkeypatch.setenv("LDBP_STORE_ALL_MIN_SAMPLES", "0")
     M = len(gamma)
     h64 = taps.astype(np.complex64).astype(np.complex128)
     g64 = gamma.astype(np.float32).astype(np.float64)

@@ -190,7 +190,8 @@ def test_loss_grad_parity(P, monkeypatch, sym, masked, cmax, mode):
                            mask=None if mask is None else torch.from_numpy(mask).cuda()).cpu().numpy()
     ref = O.loss_grad(r32(x), r32(tgt), r32(taps), r32(gamma), mask=mask, symmetric=sym)
     assert abs(buf[0] - ref[0]) <= OUT_TOL * ref[0]
-    assert rel(buf[1:1 + M], ref[1:1 + M]) <= GRAD_TOL
+    for i in range(M):  # dgamma'_i per step (a scalar each)
+        assert abs(buf[1 + i] - ref[1 + i]) <= GRAD_TOL * abs(ref[1 + i]), (i, buf[1 + i], ref[1 + i])
     dt, rdt = buf[1 + M:].reshape(M, T, 2), ref[1 + M:].reshape(M, T, 2)
     for i in range(M):
         assert rel(dt[i], rdt[i]) <= GRAD_TOL, i
@@ -288,17 +289,18 @@ def _inband_unit_taps(T, band=0.275):
 
 def test_snr_parity_on_simulated_link(P):
     """Effective SNR after LDBP (oracle receiver on both outputs) agrees to 0.01 dB, on seeded
-    SSFM + EDFA blocks of the C2 link (25 x 80 km, 1 StPS) at several launch powers, for the
-    C2 filter length (T = 5) and a working in-band equaliser (T = 15)."""
-    nsym, spans, M = 1024, 25, 25
+    SSFM + EDFA blocks of the C2 link (25 x 80 km, 1 StPS, n = 2^14 samples = 8192 symbols per
+    block) at all 11 launch powers -4..+6 dBm, for the C2 filter length (T = 5)
+    and a working in-band equaliser (T = 15), with and without the nonlinear steps."""
+    nsym, spans, M, nblk = 8192, 25, 25, 2
     link = dict(span_km=80.0, alpha_db=0.2, beta2=physics.ps2_per_km(-21.7), gamma=1.3, baud_hz=10.7e9,
                 rho_a=4, rho_d=2, nf_db=5.0, nu_hz=1.946e14)
     _, gam = steps.dbp_plan(spans, 80.0, 1, 0.2, 1.3)
     snr = {}
-    for pdbm in (-4.0, 2.0, 6.0):
+    for pdbm in [float(p) for p in range(-4, 7)]:
         pw = float(physics.dbm_to_w(pdbm))
         rs, ss = [], []
-        for b in range(4):
+        for b in range(nblk):
             s = li.qam16(li.rng(2, b, "symbols", sub=int(pdbm + 10)), nsym)
             ase = [li.cn(li.rng(2, b, "ase", sub=100 * int(pdbm + 10) + k), nsym * 4) for k in range(spans)]
             r, _ = channel.simulate_link(s, pw, num_spans=spans, steps_per_span=8, ase_draws=ase, **link)
@@ -311,8 +313,8 @@ def test_snr_parity_on_simulated_link(P):
                 g = gam if nl else 0 * gam
                 y = P.ldbp_forward(dev(rs), dev(taps), dev(g, np.float32)).cpu().numpy()
                 yo = O.forward(r32(rs), r32(taps), r32(g))
-                snr_gpu = receiver.evaluate(y.astype(np.complex128), ss, [pw] * 4)
-                snr_ref = receiver.evaluate(yo, ss, [pw] * 4)
+                snr_gpu = receiver.evaluate(y.astype(np.complex128), ss, [pw] * nblk)
+                snr_ref = receiver.evaluate(yo, ss, [pw] * nblk)
                 assert abs(snr_gpu[0] - snr_ref[0]) <= 0.01, (pdbm, T, nl, snr_gpu, snr_ref)
                 assert abs(snr_gpu[1] - snr_ref[1]) <= 0.01, (pdbm, T, nl, snr_gpu, snr_ref)
                 snr[(pdbm, T, nl)] = snr_gpu[0]

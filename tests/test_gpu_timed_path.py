@@ -1,0 +1,103 @@
+"""Parity of the exact training call bench.py times, at BASELINE.json's full sizes, against the
+fp64 oracle over EVERY block (SURVEY.md §8(c) "the gate"; VERDICT r1 Next #1).
+
+C3: 512 blocks x 2^14, M = 50, T = 9 — the store-all schedule (storing forward, Kr = 2 reverse
+launches of 25 steps, 6498 CTAs, so the two-level fp64 reduction `reduce_partials_pass1` runs).
+C5 slice: 512 blocks x 2^15, M = 25, T = 3 (2^24 samples, > 1024 reverse CTAs: the same
+two-level reduction; one reverse launch).  The schedule is asserted from the library's own
+launch trace, and the whole [loss | dgamma' | dtaps] buffer is compared per step with the oracle
+run block by block in a process pool (Eq. (7); loss Eq. (2) with reading G7).
+
+Tolerances (§8(c)): loss <= 1e-5 relative, dgamma' <= 1e-4 relative per step, dtaps <= 1e-4
+relative L2 per step.
+"""
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import ldbp_inputs as li
+from oracle import ldbp as O, physics, steps
+
+pytestmark = pytest.mark.gpu
+
+POWERS_DBM = (-2.0, -1.0, 0.0, 1.0)  # training set P of §V-A
+K_FORWARD, K_REDUCE, K_REVERSE = 1, 3, 5
+
+_X = _T = _H = _G = None  # fork-shared oracle inputs
+
+
+def _oracle_chunk(rng):
+    s, e = rng
+    return O.loss_grad(_X[s:e], _T[s:e], _H, _G, symmetric=True)
+
+
+def oracle_buf(x, t, h, g, chunk=4):
+    """sum over blocks of oracle.loss_grad, evaluated in a fork pool over chunks of blocks."""
+    global _X, _T, _H, _G
+    _X, _T, _H, _G = x, t, h, g
+    B = x.shape[0]
+    ranges = [(s, min(B, s + chunk)) for s in range(0, B, chunk)]
+    procs = max(1, min(len(ranges), os.cpu_count() or 1))
+    with mp.get_context("fork").Pool(procs) as pool:
+        parts = pool.map(_oracle_chunk, ranges)
+    return np.sum(np.stack(parts), axis=0)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2010_14258_b200 as P
+
+    return P
+
+
+def ls_model(spans, sps, T):
+    d, g = steps.dbp_plan(spans, 80.0, sps, 0.2, 1.3)
+    taps = np.stack([steps.ls_taps(steps.xi_of(dd, physics.ps2_per_km(-21.7), 21.4e9), T, cap=1.0) for dd in d])
+    return taps, g
+
+
+@pytest.mark.parametrize("name,B,n,spans,sps,T,kr", [
+    ("C3", 512, 16384, 25, 2, 9, 2),
+    ("C5-slice", 512, 32768, 25, 1, 3, 1),
+])
+def test_timed_training_call_vs_oracle_all_blocks(P, name, B, n, spans, sps, T, kr):
+    idx = 3 if name == "C3" else 5
+    blocks = range(B)
+    pw = li.dbm_to_w(li.pick_powers_dbm(idx, blocks, POWERS_DBM))
+    x = li.bandlimited_blocks_keyed_torch(idx, blocks, n, pw)
+    tgt = li.bandlimited_blocks_keyed_torch(idx, blocks, n, pw, purpose="target")
+    taps, gamma = ls_model(spans, sps, T)
+    M = len(gamma)
+    st = P.TrainState.create(taps, gamma)
+    ws = P.Workspace()
+    P.ldbp_loss_grad(x, tgt, st.taps, st.gamma, ws=ws)  # warm-up: same call bench.py repeats
+    torch.cuda.synchronize()
+    with P.api.trace() as tr:
+        buf = P.ldbp_loss_grad(x, tgt, st.taps, st.gamma, ws=ws)
+        torch.cuda.synchronize()
+    kinds = [r[0] for r in tr.records]
+    # the store-all schedule: params + storing forward, Kr reverse launches, two-level reduction
+    assert kinds.count(K_REVERSE) == kr, kinds
+    assert kinds.count(K_FORWARD) >= 1, kinds
+    assert kinds.count(K_REDUCE) == 3, kinds  # params_kernel, reduce_partials_pass1, reduce_partials_kernel
+    assert sum(r[1] for r in tr.records if r[0] == K_REVERSE) == M
+    b = buf.cpu().numpy()
+
+    h64 = st.taps.cpu().numpy().astype(np.complex128)
+    g64 = st.gamma.cpu().numpy().astype(np.float64)
+    ref = oracle_buf(x.cpu().numpy().astype(np.complex128), tgt.cpu().numpy().astype(np.complex128), h64, g64)
+
+    assert abs(b[0] - ref[0]) <= 1e-5 * ref[0], (b[0], ref[0])
+    dg, rdg = b[1:1 + M], ref[1:1 + M]
+    for i in range(M):
+        assert abs(dg[i] - rdg[i]) <= 1e-4 * abs(rdg[i]), (name, "dgamma", i, dg[i], rdg[i])
+    dt, rdt = b[1 + M:].reshape(M, -1), ref[1 + M:].reshape(M, -1)
+    for i in range(M):
+        e = np.linalg.norm(dt[i] - rdt[i]) / np.linalg.norm(rdt[i])
+        assert e <= 1e-4, (name, "dtaps", i, e)
