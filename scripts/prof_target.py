@@ -21,7 +21,7 @@ if os.environ.get("PROF_B"):
 if os.environ.get("PROF_FWD"):
     cfg["mode"] = "fwd"
 taps, gamma = bench.make_model(cfg)
-x, tgt = bench.make_inputs(cfg, 0)
+x, tgt = bench.make_inputs(cfg, range(cfg["B"]))
 st = P.TrainState.create(taps, gamma)
 for _ in range(reps):
     if cfg["mode"] == "train":
