@@ -107,6 +107,7 @@ int ntaps_used(int kh, bool sym) { return sym ? kh + 1 : 2 * kh + 1; }
   FwdFn ldbp_get_fwd_store_##K(bool sym, bool chk); \
   BwdFn ldbp_get_bwd_##K(bool sym, bool fast);      \
   RevFn ldbp_get_rev_##K(bool sym, bool fast);      \
+  RevFn ldbp_get_rev2_##K(bool fast);               \
   ParFn ldbp_get_params_##K(bool sym);
 }  // namespace
 LDBP_DECL_GETTERS(0)
@@ -170,6 +171,20 @@ RevFn get_rev(int kh, bool sym, bool fast) {
     case 5: return ldbp_get_rev_5(sym, fast);
     case 6: return ldbp_get_rev_6(sym, fast);
     case 7: return ldbp_get_rev_7(sym, fast);
+  }
+  return nullptr;
+}
+
+RevFn get_rev2(int kh, bool fast) {
+  switch (kh) {
+    case 0: return ldbp_get_rev2_0(fast);
+    case 1: return ldbp_get_rev2_1(fast);
+    case 2: return ldbp_get_rev2_2(fast);
+    case 3: return ldbp_get_rev2_3(fast);
+    case 4: return ldbp_get_rev2_4(fast);
+    case 5: return ldbp_get_rev2_5(fast);
+    case 6: return ldbp_get_rev2_6(fast);
+    case 7: return ldbp_get_rev2_7(fast);
   }
   return nullptr;
 }
@@ -395,27 +410,51 @@ int rev_occupancy(RevFn fn, int nthreads, size_t smem) {
   return std::max(occ, 1);
 }
 
+// The warp-overlapped reverse (ldbp_reverse2.cuh, symmetric taps only) is OFF by default:
+// measured slower than rev_tile_kernel on every shape (C3 reverse 2.37 ms at 8 warps/CTA, 2.49 at 4,
+// 3.24 at 2, 3.86 at 1 warp vs 1.95; C5 15.6-20.5 vs 14.9 ms): the refresh barrier every R/Kh
+// steps across 8 warps costs more than the per-step split barrier it replaces (28 % barrier
+// stalls), and barrier-free 1-warp tiles pay 19-25 % halo recompute.  LDBP_REV2=1 selects it.
+bool use_rev2(const ldbp_dims* d) { return (d->flags & LDBP_SYMMETRIC) && env_int("LDBP_REV2", 0) != 0; }
+
+size_t rev_smem_any(const ldbp_dims* d, int steps) {
+  const int kh = (d->taps - 1) / 2;
+  return use_rev2(d) ? ldbp::rev2_smem_bytes(kh, steps, d->steps)
+                     : rev_smem(kh, d->flags & LDBP_SYMMETRIC, steps, d->steps);
+}
+
+RevFn get_rev_any(const ldbp_dims* d) {
+  const int kh = (d->taps - 1) / 2;
+  const bool fast = !(d->flags & LDBP_PRECISE);
+  return use_rev2(d) ? get_rev2(kh, fast) : get_rev(kh, d->flags & LDBP_SYMMETRIC, fast);
+}
+
 RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
   RevPlan p;
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
+  const bool v2 = use_rev2(d);
   const int M = d->steps;
-  const int nthr = ldbp::rev_threads(kh);
+  const int R = v2 ? ldbp::rev2_r(kh) : rev_r(kh);
+  // window slots per CTA (rev2: 30 owned lanes per warp + the two duplicate end lanes)
+  const int slots = v2 ? ldbp::rev2_slots(ldbp::rev2_warps(kh)) : ldbp::rev_threads(kh);
+  const int nthr = v2 ? 32 * ldbp::rev2_warps(kh) : ldbp::rev_threads(kh);
   p.V = 1 + 2 * ntaps_used(kh, sym);
-  // cost model in step units: a launch of S steps costs S * window / (window - 2*S*kh) plus a
-  // fixed ~2 steps (prologue: staging, first load, seed); pick the number of launches minimising
-  // it, subject to the shared-memory budget (2 CTAs per SM)
-  const double window = (double)nthr * rev_r(kh);
+  // cost model in step units: a launch of S steps costs S * window / (window - 2*H) plus a
+  // fixed ~2 steps (prologue: staging, first load, seed), H = S*kh rounded up to whole slots;
+  // pick the number of launches minimising it, subject to the shared-memory budget
+  const double window = (double)slots * R;
   const double fixed = 2.0;
-  const size_t budget = (size_t)env_int("LDBP_REV_SMEM_KB", 113) * 1024;
+  const size_t budget = (size_t)env_int("LDBP_REV_SMEM_KB", v2 ? 150 : 113) * 1024;
   int best_k = 0;
   double best = 1e300;
   const int kmax = std::min(M, env_int("LDBP_REV_MAX_LAUNCHES", 256));
   const int cmax = std::max(1, env_int("LDBP_REV_MAX_STEPS", 1 << 30));
   for (int k = 1; k <= kmax; ++k) {
     const int S = (int)cdiv(M, k);
-    if (S > cmax || rev_smem(kh, sym, S, M) > budget) continue;
-    const double useful = window - 2.0 * S * kh;
+    if (S > cmax || rev_smem_any(d, S) > budget) continue;
+    const double H = (double)cdiv((int64_t)S * kh, R) * R;
+    const double useful = window - 2.0 * H;
     if (useful < window / 4) continue;
     const double cost = k * (S * window / useful + fixed);
     if (cost < best) { best = cost; best_k = k; }
@@ -427,10 +466,12 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
   int occ = 1, sms = 148;
   if (query_device) {
     sms = device_sms();
-    occ = rev_occupancy(get_rev(kh, sym, !(d->flags & LDBP_PRECISE)), nthr, rev_smem(kh, sym, p.Cr, M));
+    occ = rev_occupancy(get_rev_any(d), nthr, rev_smem_any(d, p.Cr));
   }
-  p.tile = plan_tiles(d->batch, d->n, p.Cr * kh, rev_r(kh), nthr, occ, sms, /*align_r=*/true);
-  p.tile.nthreads = nthr;  // the kernel's layout is compiled for exactly rev_threads(kh) threads
+  // rev2: at least one halo slot per side (slot 0 / the last slot are never owned: duplicate lanes)
+  const int H = v2 ? std::max(p.Cr * kh, 1) : p.Cr * kh;
+  p.tile = plan_tiles(d->batch, d->n, H, R, slots, occ, sms, /*align_r=*/true);
+  p.tile.nthreads = nthr;  // the kernel's layout is compiled for exactly this many threads
   return p;
 }
 
@@ -799,7 +840,7 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
     }
   }
   if (forward_only) return LDBP_OK;
-  RevFn fn = get_rev(kh, sym, fast);
+  RevFn fn = get_rev_any(d);
   double* partials = reinterpret_cast<double*>(ws + w.part_off);
   double* lossp = reinterpret_cast<double*>(ws + w.loss_off);
   for (int k = p.Kr - 1; k >= 0; --k) {
@@ -823,7 +864,7 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
     a.s0 = s0;
     a.s1 = s1;
     a.g = p.tile.g;
-    const size_t smem = rev_smem(kh, sym, s1 - s0, M);
+    const size_t smem = rev_smem_any(d, s1 - s0);
     cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     {
       TraceScope ts(LDBP_K_REVERSE, s1 - s0, d->batch * d->n, st);

@@ -46,3 +46,8 @@ ParFn LDBP_CAT(ldbp_get_params_, LDBP_KH)(bool sym) {
   constexpr int K = LDBP_KH;
   return sym ? ldbp::params_kernel<K, true> : ldbp::params_kernel<K, false>;
 }
+
+RevFn LDBP_CAT(ldbp_get_rev2_, LDBP_KH)(bool fast) {
+  constexpr int K = LDBP_KH;
+  return fast ? ldbp::rev2_tile_kernel<K, true> : ldbp::rev2_tile_kernel<K, false>;
+}

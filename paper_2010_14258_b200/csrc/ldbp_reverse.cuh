@@ -164,6 +164,51 @@ __device__ __forceinline__ void async_window(const float2* __restrict__ src, int
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// Loop-invariant part of the warp-cooperative window copy (COAL), computed once per launch: the
+// shared-memory address of each of the lane's R/2 16-byte chunks (relative to buffer 0) and whether
+// the whole warp takes the coalesced path.  Per step only the source base pointer changes, so a copy
+// is R/2 LDGSTS with immediate source offsets (lane*16 + m*512) and one add per chunk — instead of
+// re-deriving the chunk -> (thread, sample) mapping (an integer division per chunk) every step
+// (measured: the copy was ~89 instructions per thread-step, 15 % of the C5 reverse).
+template <int R, int NT>
+struct CoalCopy {
+  uint32_t dst[R / 2];  // smem byte addresses in window buffer 0
+  int64_t off0;         // element offset of the warp's first sample (fast path)
+  bool warp_fast;       // every lane of the warp is on the contiguous fast path
+};
+template <int R, int NT>
+__device__ __forceinline__ CoalCopy<R, NT> coal_setup(f2x* buf0, int64_t fast_off) {
+  CoalCopy<R, NT> cc;
+  const int t = threadIdx.x, lane = t & 31;
+  cc.off0 = __shfl_sync(kFull, fast_off, 0);
+  cc.warp_fast = __all_sync(kFull, fast_off >= 0 && fast_off == cc.off0 + (int64_t)lane * R);
+  f2x* wbuf = buf0 + (t & ~31) * (R + 2);
+#pragma unroll
+  for (int m = 0; m < R / 2; ++m) {
+    const int c = m * 32 + lane, tt = c / (R / 2), k2 = c - tt * (R / 2);
+    cc.dst[m] = smem_u32(wbuf + tt * (R + 2) + 2 * k2);
+  }
+  return cc;
+}
+// Copy of src's window into buffer `buf` (byte offset `boff` from buffer 0).  Falls back to the
+// general per-thread path when the warp is not on the fast path or src is not 16-byte aligned.
+template <int R, int NT>
+__device__ __forceinline__ void async_window_cc(const CoalCopy<R, NT>& cc, const float2* __restrict__ src,
+                                                int64_t e0, const Geo& g, f2x* buf, uint32_t boff,
+                                                int64_t fast_off) {
+  if (cc.warp_fast && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const char* base = reinterpret_cast<const char*>(reinterpret_cast<const f2x*>(src) + cc.off0) +
+                       16 * (threadIdx.x & 31);
+#pragma unroll
+    for (int m = 0; m < R / 2; ++m)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(cc.dst[m] + boff), "l"(base + 512 * m)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    return;
+  }
+  async_window<true, R, NT>(src, e0, g, buf, fast_off);
+}
+
 struct RevSmem {
   uint64_t* bar;    // split step barrier (count = warps), phases = reverse steps
   TapP* taps_adj;   // [S][NTU]
@@ -325,9 +370,17 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   constexpr int PIPE = LDBP_REV_PIPE;
   constexpr bool COAL = rev_coal(KH);
   constexpr int UB = rev_rs<COAL, R>() * NT;  // f2x per window buffer
-  async_window<COAL, R, NT>(rev_src(a, s1 - 1), e0, a.g, sm.ubuf + (size_t)((s1 - 1) % PIPE) * UB, fast_off);
+  CoalCopy<R, NT> cc{};
+  if constexpr (COAL) cc = coal_setup<R, NT>(sm.ubuf, fast_off);
+  auto window = [&](int i, int b) {  // async copy of u^(i) into window buffer b
+    if constexpr (COAL)
+      async_window_cc<R, NT>(cc, rev_src(a, i), e0, a.g, sm.ubuf + (size_t)b * UB, (uint32_t)(b * UB * 8), fast_off);
+    else
+      async_window<COAL, R, NT>(rev_src(a, i), e0, a.g, sm.ubuf + (size_t)b * UB, fast_off);
+  };
+  window(s1 - 1, (s1 - 1) % PIPE);
   if (PIPE == 3 && s1 - 2 >= s0)
-    async_window<COAL, R, NT>(rev_src(a, s1 - 2), e0, a.g, sm.ubuf + (size_t)((s1 - 2) % PIPE) * UB, fast_off);
+    window(s1 - 2, (s1 - 2) % PIPE);
   f2x v[R], g[R];
   load_window<R>(rev_src(a, s1), e0, a.g, v);
   const float2 Pend = sm.norm[a.M - 1].P;
@@ -418,8 +471,7 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
     if (COAL) __syncwarp();  // ... and the warp's cooperative copies (and WAR on reuse)
     // prefetch u^(l-PIPE+1) into a free buffer (this thread's own slots, consumed later)
     if (l - (PIPE - 1) >= s0)
-      async_window<COAL, R, NT>(rev_src(a, l - (PIPE - 1)), e0, a.g,
-                          sm.ubuf + (size_t)((l - (PIPE - 1)) % PIPE) * UB, fast_off);
+      window(l - (PIPE - 1), (l - (PIPE - 1)) % PIPE);
     const f2x* ub_mine = sm.ubuf + (size_t)(l % PIPE) * UB + ubuf_idx<COAL, R, NT>(0, tid);
     const int eoff = (ph & 1) * 2 * KE * NT;
     float dh[2 * NTU];
@@ -581,3 +633,4 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * re
 }
 
 }  // namespace ldbp
+#include "ldbp_reverse2.cuh"

@@ -13,7 +13,7 @@ names = sys.argv[1:] or ["C2", "C4", "C3", "C5"]
 for name in names:
     cfg = bench.CONFIGS[name]
     taps, gamma = bench.make_model(cfg)
-    x, tgt = bench.make_inputs(cfg, 0)
+    x, tgt = bench.make_inputs(cfg, range(cfg["B"]))
     st = P.TrainState.create(taps, gamma)
     M, T = taps.shape
     kh = (T - 1) // 2
