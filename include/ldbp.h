@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define LDBP_ABI_VERSION 1
+#define LDBP_ABI_VERSION 2
 
 /* Problem dimensions. */
 typedef struct ldbp_dims {
@@ -220,24 +220,31 @@ int ldbp_essm_loss_grad(const ldbp_dims* d, int32_t kappa, const void* x, const 
 
 /*
  * GPU split-step Fourier channel generator (§IV-A): the link
- * the oracle simulates, per block of n samples (power of two, n <= 16384), in one launch:
- *   for each of `spans` spans: for each step delta_s (s < steps_per_span, deltas_km_host[s]):
+ * the oracle simulates, per block of n samples (power of two, 2 <= n <= 65536), in one launch:
+ *   for each of `spans` spans: for each step delta_s (s < steps_per_span <= 64, deltas_km_host[s]):
  *     u <- u e^{j gamma L_eff(delta_s) |u|^2}                     (Kerr at the segment start, G5)
  *     U_k <- U_k e^{-alpha delta_s / 2} e^{j beta2/2 omega_k^2 delta_s}   (Eqs. (4)-(6))
- *   then the EDFA: u <- e^{alpha span_km / 2} u + ase_sigma * noise[span]
+ *   then the EDFA: u <- e^{alpha span_km / 2} u + ase_sigma * z[span]
  *   omega_k = 2 pi fftfreq(n) fs_hz;  beta2 in s^2/km, alpha in 1/km (nepers), gamma in 1/(W km)
+ * ASE draws z (CN(0,1)): noise_or_null != NULL: the given [spans][B][n] complex64 array;
+ *   otherwise, if ase_sigma != 0, drawn in the kernel by Philox4x32-10 keyed by
+ *   (ase_seed, global block ase_block0 + b, span, sample) — ldbp_inputs.ase_cn_philox is the same
+ *   generator in numpy, so a batch sharded over ranks draws the same noise for any rank count;
+ *   ase_sigma == 0 and noise NULL: noiseless.
  * decim == 0: u is overwritten with the channel output;  decim > 0: r [B][n/decim] receives the
  * brick-wall low-pass (|fftfreq| <= cutoff) output sampled every decim samples (G8).
- *   noise: [spans][B][n] complex64 CN(0,1) draws (inputs), or NULL (noiseless).
- * deltas_km_host is a HOST array (copied; the call synchronises the stream once for it).
- * fp32 in shared memory (radix-2 FFTs with fp64-accurate twiddles and dispersion factors).
+ * deltas_km_host is a HOST array read during the call (the values travel in kernel parameters:
+ * no copy, no host synchronisation; the call is asynchronous like every other entry point).
+ * fp32 in shared memory: one CTA per block up to n = 16384, a 2- or 4-CTA cluster (distributed
+ * shared memory, four-step split of the DFT) for 32768 / 65536; dispersion factors and twiddles
+ * are fp64-accurate.  Workspace: ldbp_ssfm_workspace_bytes (S x n complex64 dispersion table).
  */
 int ldbp_ssfm_workspace_bytes(int64_t n, int32_t steps_per_span, size_t* bytes);
 int ldbp_ssfm_link(int64_t batch, int64_t n, int32_t spans, int32_t steps_per_span,
                    const double* deltas_km_host, double span_km, double alpha_np, double beta2,
-                   double gamma, double fs_hz, double ase_sigma, const void* noise_or_null, void* u,
-                   void* r_or_null, int32_t decim, double cutoff, void* ws, size_t ws_bytes,
-                   void* cuda_stream);
+                   double gamma, double fs_hz, double ase_sigma, const void* noise_or_null,
+                   uint64_t ase_seed, int64_t ase_block0, void* u, void* r_or_null, int32_t decim,
+                   double cutoff, void* ws, size_t ws_bytes, void* cuda_stream);
 
 /*
  * Launch tracing (profiling aid; off by default; per calling thread).

@@ -198,3 +198,50 @@ def bandlimited_blocks_keyed_torch(cfg_index: int, blocks, n: int, power_w, devi
             torch.randn((n,), dtype=torch.complex64, device=device, generator=g, out=w[i - s])
         out[s:e] = torch.fft.ifft(torch.fft.fft(w[: e - s], dim=-1) * mask, dim=-1) * amp[s:e, None]
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# Counter-based ASE draws (shared generator: the GPU channel kernel implements the same Philox)
+# ---------------------------------------------------------------------------------------
+# Philox4x32-10 (Salmon et al., SC'11): counter (c0, c1, c2, c3), key (k0, k1); per round
+#   (hi0, lo0) = M0 * c0, (hi1, lo1) = M1 * c2,  c <- (hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0),
+#   key <- key + (W0, W1).
+# The ASE draw of sample i of span `span` of global block `block` (SURVEY.md §8(d) seed tree:
+# keyed by global block index, so the union is independent of the number of ranks) is
+#   x = philox((i >> 1, span, block & 0xffffffff, block >> 32), (seed & 0xffffffff, seed >> 32)),
+#   (u1, u2) = ((x0 + 0.5) 2^-32, (x1 + 0.5) 2^-32) for even i, (x2, x3) for odd i,
+#   z = sqrt(-2 ln u1) (cos 2 pi u2 + j sin 2 pi u2) / sqrt(2)     (Box-Muller, CN(0, 1)).
+PHILOX_M0, PHILOX_M1 = 0xD2511F53, 0xCD9E8D57
+PHILOX_W0, PHILOX_W1 = 0x9E3779B9, 0xBB67AE85
+_MASK32 = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_10(c0, c1, c2, c3, k0: int, k1: int):
+    """Vectorised Philox4x32-10 on uint32 counter arrays (numpy), returns four uint32 arrays."""
+    c = [np.asarray(v, dtype=np.uint64) & _MASK32 for v in (c0, c1, c2, c3)]
+    k0, k1 = np.uint64(k0 & 0xFFFFFFFF), np.uint64(k1 & 0xFFFFFFFF)
+    for _ in range(10):
+        p0 = np.uint64(PHILOX_M0) * c[0]
+        p1 = np.uint64(PHILOX_M1) * c[2]
+        hi0, lo0 = p0 >> np.uint64(32), p0 & _MASK32
+        hi1, lo1 = p1 >> np.uint64(32), p1 & _MASK32
+        c = [hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0]
+        k0 = (k0 + np.uint64(PHILOX_W0)) & _MASK32
+        k1 = (k1 + np.uint64(PHILOX_W1)) & _MASK32
+    return [v.astype(np.uint32) for v in c]
+
+
+def ase_cn_philox(seed: int, block: int, span: int, n: int) -> np.ndarray:
+    """CN(0,1) ASE draws [n] (complex128) of one (block, span), the generator the GPU kernel uses."""
+    i = np.arange(n, dtype=np.uint64)
+    m = i >> np.uint64(1)
+    x0, x1, x2, x3 = philox4x32_10(m, np.full(n, span), np.full(n, block & 0xFFFFFFFF),
+                                   np.full(n, (block >> 32) & 0xFFFFFFFF), seed & 0xFFFFFFFF,
+                                   (seed >> 32) & 0xFFFFFFFF)
+    odd = (i & np.uint64(1)).astype(bool)
+    a = np.where(odd, x2, x0).astype(np.float64)
+    b = np.where(odd, x3, x1).astype(np.float64)
+    u1 = (a + 0.5) * 2.0 ** -32
+    u2 = (b + 0.5) * 2.0 ** -32
+    r = np.sqrt(-2.0 * np.log(u1))
+    return r * np.exp(2j * np.pi * u2) / np.sqrt(2.0)

@@ -106,8 +106,9 @@ def _load():
         "ldbp_essm_loss_grad": (ctypes.c_int, [D, ctypes.c_int32, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
         "ldbp_ssfm_workspace_bytes": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]),
         "ldbp_ssfm_link": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
-                                          ctypes.POINTER(ctypes.c_double), dbl, dbl, dbl, dbl, dbl, dbl, P, P, P,
-                                          ctypes.c_int32, dbl, P, ctypes.c_size_t, P]),
+                                          ctypes.POINTER(ctypes.c_double), dbl, dbl, dbl, dbl, dbl, dbl, P,
+                                          ctypes.c_uint64, ctypes.c_int64, P, P, ctypes.c_int32, dbl, P,
+                                          ctypes.c_size_t, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -353,22 +353,26 @@ def ldbp_essm_loss_grad(x, target, taps, gamma, eta, *, symmetric=True, precise=
 
 @_on_stream
 def ldbp_ssfm_link(u, deltas_km, *, spans, span_km, alpha_np, beta2, gamma, fs_hz, ase_sigma=0.0, noise=None,
-                   decim=0, cutoff=0.5, ws=None, stream=None):
-    """GPU SSFM channel generator (§8(f) NEXT-2): propagates u [B][n] (complex64, in place) over
-    `spans` spans of len(deltas_km) steps each, EDFA + ASE (noise [spans][B][n] CN(0,1) or None);
+                   ase_seed=None, block0=0, decim=0, cutoff=0.5, ws=None, stream=None):
+    """GPU SSFM channel generator (§8(f) NEXT-2): propagates u [B][n] (complex64, n a power of two
+    <= 65536, in place) over `spans` spans of len(deltas_km) steps each, EDFA + ASE.  ASE draws:
+    ``noise`` [spans][B][n] CN(0,1), or (noise None, ase_sigma != 0) Philox draws keyed by
+    (ase_seed, global block block0 + b, span, sample) — ldbp_inputs.ase_cn_philox.
     decim > 0 returns the low-passed (|fftfreq| <= cutoff), decimated output [B][n // decim]."""
     _need(u, "u", torch.complex64)
     B, n = u.shape
     if noise is not None:
         _need(noise, "noise", torch.complex64, (spans, B, n))
+    elif ase_sigma != 0.0 and ase_seed is None:
+        raise ValueError("ase_sigma != 0 needs either noise draws or an ase_seed")
     d = (ctypes.c_double * len(deltas_km))(*[float(v) for v in deltas_km])
     nb = ctypes.c_size_t(0)
     check(lib.ldbp_ssfm_workspace_bytes(n, len(deltas_km), ctypes.byref(nb)), "ldbp_ssfm_workspace_bytes")
     w, nbv = _ws(u.device, int(nb.value), ws)
     r = torch.empty((B, n // decim), dtype=torch.complex64, device=u.device) if decim > 0 else None
     check(lib.ldbp_ssfm_link(B, n, spans, len(deltas_km), d, span_km, alpha_np, beta2, gamma, fs_hz, ase_sigma,
-                             _p(noise), _p(u), _p(r), int(decim), float(cutoff), _p(w), nbv, _stream_handle(stream)),
-          "ldbp_ssfm_link")
+                             _p(noise), int(ase_seed or 0) & 0xFFFFFFFFFFFFFFFF, int(block0), _p(u), _p(r), int(decim),
+                             float(cutoff), _p(w), nbv, _stream_handle(stream)), "ldbp_ssfm_link")
     return r if decim > 0 else u
 
 

@@ -1480,82 +1480,102 @@ int ldbp_essm_loss_grad(const ldbp_dims* d, int32_t kappa, const void* x, const 
 }
 
 // ---- GPU SSFM channel generator (§8(f) NEXT-2), ldbp_ssfm.cuh ----
-static size_t ssfm_ws_bytes(int64_t n, int S) {
-  return align256(sizeof(float2) * (size_t)S * n) + align256(sizeof(double) * S) + align256(sizeof(float) * S);
-}
+static size_t ssfm_ws_bytes(int64_t n, int S) { return align256(sizeof(float2) * (size_t)S * n); }
 
 int ldbp_ssfm_workspace_bytes(int64_t n, int32_t steps_per_span, size_t* bytes) {
   g_err[0] = 0;
   if (!bytes) return fail(LDBP_EINVAL, "bytes is NULL");
   if (n < 2 || (n & (n - 1)) || n > (1 << ldbp::kSsfmMaxLog2))
     return fail(LDBP_ESHAPE, "n %lld must be a power of two in [2, %d]", (long long)n, 1 << ldbp::kSsfmMaxLog2);
-  if (steps_per_span < 1) return fail(LDBP_ESHAPE, "steps_per_span %d < 1", steps_per_span);
+  if (steps_per_span < 1 || steps_per_span > ldbp::kSsfmMaxSteps)
+    return fail(LDBP_ESHAPE, "steps_per_span %d not in [1, %d]", steps_per_span, ldbp::kSsfmMaxSteps);
   *bytes = ssfm_ws_bytes(n, steps_per_span);
   return LDBP_OK;
 }
 
+static cudaError_t ssfm_launch(int C, const ldbp::SsfmArgs& a, int64_t batch, size_t smem, cudaStream_t st) {
+  void (*kern)(const ldbp::SsfmArgs) = C == 1 ? ldbp::ssfm_link_kernel<1>
+                                       : C == 2 ? ldbp::ssfm_link_kernel<2> : ldbp::ssfm_link_kernel<4>;
+  cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(batch * C));
+  cfg.blockDim = dim3(ldbp::kSsfmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = C > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 int ldbp_ssfm_link(int64_t batch, int64_t n, int32_t spans, int32_t steps_per_span, const double* deltas_km_host,
                    double span_km, double alpha_np, double beta2, double gamma, double fs_hz, double ase_sigma,
-                   const void* noise_or_null, void* u, void* r_or_null, int32_t decim, double cutoff, void* ws,
-                   size_t ws_bytes, void* cuda_stream) {
+                   const void* noise_or_null, uint64_t ase_seed, int64_t ase_block0, void* u, void* r_or_null,
+                   int32_t decim, double cutoff, void* ws, size_t ws_bytes, void* cuda_stream) {
   g_err[0] = 0;
   size_t need = 0;
   LDBP_TRY(ldbp_ssfm_workspace_bytes(n, steps_per_span, &need));
   if (batch < 0 || spans < 0) return fail(LDBP_ESHAPE, "batch and spans must be >= 0");
   if (batch == 0) return LDBP_OK;
   if (!deltas_km_host) return fail(LDBP_EINVAL, "deltas_km_host is NULL");
+  if (ase_block0 < 0) return fail(LDBP_EINVAL, "ase_block0 %lld < 0", (long long)ase_block0);
   LDBP_TRY(check_ptr(u, "u", 8));
   if (noise_or_null) LDBP_TRY(check_ptr(noise_or_null, "noise", 8));
+  // one CTA holds up to 2^14 samples; longer blocks are split over a 2- or 4-CTA cluster
+  const int C = n > (1 << ldbp::kSsfmLocalMaxLog2) ? (int)(n >> ldbp::kSsfmLocalMaxLog2) : 1;
+  const int64_t L = n / C;
   if (decim > 0) {
     LDBP_TRY(check_ptr(r_or_null, "r", 8));
-    if (n % decim) return fail(LDBP_ESHAPE, "n %% decim != 0");
+    if (L % decim) return fail(LDBP_ESHAPE, "n / cluster (%lld) %% decim != 0", (long long)L);
   }
   if (!ws || ws_bytes < need) return fail(LDBP_EWORKSPACE, "ssfm needs %zu workspace bytes, got %zu", need, ws_bytes);
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const int S = steps_per_span;
-  unsigned char* wb = (unsigned char*)ws;
-  float2* H = reinterpret_cast<float2*>(wb);
-  double* dd = reinterpret_cast<double*>(wb + align256(sizeof(float2) * (size_t)S * n));
-  float* kp = reinterpret_cast<float*>(wb + align256(sizeof(float2) * (size_t)S * n) + align256(sizeof(double) * S));
-  std::vector<float> kph(S);
+  float2* H = reinterpret_cast<float2*>(ws);
+  // step lengths and Kerr phases travel in the kernel parameters: no copy, no host sync
+  ldbp::SsfmDeltas dd;
+  ldbp::SsfmArgs a;
   for (int s = 0; s < S; ++s) {
     const double d = deltas_km_host[s];
+    dd.d[s] = d;
     const double leff = alpha_np == 0.0 ? d : (1.0 - exp(-alpha_np * d)) / alpha_np;
-    kph[s] = (float)(gamma * leff);
+    a.kerr_phase[s] = (float)(gamma * leff);
   }
-  if (cudaMemcpyAsync(dd, deltas_km_host, sizeof(double) * S, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-      cudaMemcpyAsync(kp, kph.data(), sizeof(float) * S, cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return fail(LDBP_ECUDA, "cudaMemcpyAsync: %s", cudaGetErrorString(cudaGetLastError()));
-  if (cudaStreamSynchronize(st) != cudaSuccess)  // kph lives on this host stack frame
-    return fail(LDBP_ECUDA, "cudaStreamSynchronize: %s", cudaGetErrorString(cudaGetLastError()));
+  int log2L = 0;
+  while ((int64_t(1) << log2L) < L) ++log2L;
   {
     TraceScope ts(LDBP_K_SSFM, S, 0, st);
-    int lg = 0;
-    while ((int64_t(1) << lg) < n) ++lg;
-    ldbp::ssfm_htable_kernel<<<256, 256, 0, st>>>(H, dd, S, n, alpha_np, beta2, fs_hz, lg);
+    ldbp::ssfm_htable_kernel<<<256, 256, 0, st>>>(H, dd, S, n, C, alpha_np, beta2, fs_hz, log2L);
   }
   LDBP_TRY(cuda_check("ssfm_htable_kernel launch"));
-  ldbp::SsfmArgs a;
   a.u = (float2*)u;
   a.r = (float2*)r_or_null;
   a.H = H;
   a.noise = (const float2*)noise_or_null;
-  a.kerr_phase = kp;
   a.n = n;
+  a.log2L = log2L;
   a.log2n = 0;
   while ((int64_t(1) << a.log2n) < n) ++a.log2n;
   a.spans = spans;
   a.S = S;
   a.decim = decim;
+  a.ase_mode = noise_or_null ? 1 : (ase_sigma != 0.0 ? 2 : 0);
+  a.ase_seed = ase_seed;
+  a.block0 = ase_block0;
   a.span_gain = (float)exp(0.5 * alpha_np * span_km);
   a.ase_sigma = (float)ase_sigma;
   a.cutoff = (float)cutoff;
-  const size_t smem = sizeof(float2) * ((size_t)n + n / 16 + 1 + n / 2);
-  cudaFuncSetAttribute((const void*)ldbp::ssfm_link_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = sizeof(float2) * ((size_t)L + L / 16 + 1 + L / 2 + (C > 1 ? (size_t)n / 64 + 64 : 0));
+  cudaError_t e;
   {
     TraceScope ts(LDBP_K_SSFM, spans * S, batch * n, st);
-    ldbp::ssfm_link_kernel<<<(unsigned)batch, ldbp::kSsfmThreads, smem, st>>>(a);
+    e = ssfm_launch(C, a, batch, smem, st);
   }
+  if (e != cudaSuccess) return fail(LDBP_ECUDA, "ssfm_link_kernel launch: %s", cudaGetErrorString(e));
   return cuda_check("ssfm_link_kernel launch");
 }
 

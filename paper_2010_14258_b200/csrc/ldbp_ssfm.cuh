@@ -13,42 +13,83 @@
 // The dispersion factors H_s[k] (one row per distinct step length) are precomputed in fp64 by
 // ssfm_htable_kernel: omega^2 delta reaches hundreds of radians, beyond fp32 sincos accuracy.
 #pragma once
+#include <cooperative_groups.h>
 
 namespace ldbp {
 
 constexpr int kSsfmThreads = 1024;
-constexpr int kSsfmMaxLog2 = 14;
+constexpr int kSsfmLocalMaxLog2 = 14;  // samples per CTA (shared memory)
+constexpr int kSsfmMaxLog2 = 16;       // per block: a cluster of up to 4 CTAs holds 2^16 samples
+constexpr int kSsfmMaxSteps = 64;      // steps per span (kernel parameters)
 
 struct SsfmArgs {
   float2* u;               // [B][n] in: transmitted waveform; out (decim == 0): channel output
   float2* r;               // [B][n / decim] out when decim > 0 (LPF + decimation)
-  const float2* H;         // [S][n] dispersion factors of the S step lengths of one span
-  const float2* noise;     // [spans][B][n] CN(0,1) ASE draws, or nullptr (noiseless)
-  const float* kerr_phase; // [S] gamma * L_eff(delta_s) (1/W)
+  const float2* H;         // [S][n] dispersion factors, per cluster rank in its own bin order
+  const float2* noise;     // [spans][B][n] CN(0,1) ASE draws (ase_mode 1)
+  float kerr_phase[kSsfmMaxSteps];  // gamma * L_eff(delta_s) (1/W)
   int64_t n;
-  int log2n, spans, S, decim;
+  int log2n, log2L, spans, S, decim;
+  int ase_mode;            // 0 noiseless, 1 draws from `noise`, 2 Philox keyed by (seed, block, span, i)
+  uint64_t ase_seed;
+  int64_t block0;          // global index of block 0 (Philox key)
   float span_gain;         // e^{alpha L_sp / 2}
   float ase_sigma;         // sqrt(PSD * f_sim)
   float cutoff;            // pass |fftfreq| <= cutoff (cycles/sample)
 };
 
-// H[s][k] = e^{-alpha delta_s/2} e^{j beta2/2 omega_k^2 delta_s}, omega_k = 2 pi fftfreq(k) fs (fp64)
-// Stored in bit-reversed bin order (slot bitrev(k)): the forward FFT is decimation-in-frequency
-// (natural in, bit-reversed out), so the dispersion multiply needs no permutation.
-__global__ void ssfm_htable_kernel(float2* H, const double* deltas, int S, int64_t n, double alpha, double beta2,
-                                   double fs, int log2n) {
+struct SsfmDeltas {
+  double d[kSsfmMaxSteps];
+};
+
+// Philox4x32-10 (Salmon et al., SC'11), the generator ldbp_inputs.ase_cn_philox implements in
+// numpy: CN(0,1) draw of sample i of span sp of global block b, Box-Muller on the (x0, x1) pair
+// for even i and (x2, x3) for odd i.
+__device__ __forceinline__ float2 ase_philox_cn(uint64_t seed, int64_t b, int sp, int64_t i) {
+  uint32_t c0 = (uint32_t)(i >> 1), c1 = (uint32_t)sp, c2 = (uint32_t)b, c3 = (uint32_t)((uint64_t)b >> 32);
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int rd = 0; rd < 10; ++rd) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const uint32_t a = (i & 1) ? c2 : c0, bb = (i & 1) ? c3 : c1;
+  const float u1 = ((float)a + 0.5f) * 2.3283064365386963e-10f;  // 2^-32
+  const float u2 = ((float)bb + 0.5f) * 2.3283064365386963e-10f;
+  const float rr = sqrtf(-2.f * logf(u1)) * 0.70710678118654752f;
+  float sn, cs;
+  sincospif(2.f * u2, &sn, &cs);
+  return make_float2(rr * cs, rr * sn);
+}
+
+// H[s][rank L + slot] = e^{-alpha delta_s/2} e^{j beta2/2 omega_k^2 delta_s} for the bin k that
+// slot `slot` of cluster rank `rank` holds after the forward transform: k = rank + C bitrev_L(slot)
+// (C = 1: k = bitrev_n(slot), natural in, bit-reversed out; C > 1: the four-step split below).
+// omega_k = 2 pi fftfreq(k) fs, fp64 (omega^2 delta reaches hundreds of radians).
+__global__ void ssfm_htable_kernel(float2* H, SsfmDeltas deltas, int S, int64_t n, int C, double alpha,
+                                   double beta2, double fs, int log2L) {
   const int64_t total = (int64_t)S * n;
+  const int64_t L = n / C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int s = (int)(i / n);
-    const int64_t k = i % n;
+    const int64_t j = i % n;
+    const int64_t rank = j / L, slot = j % L;
+    const int64_t k = rank + C * (int64_t)(log2L > 0 ? (__brev((unsigned)slot) >> (32 - log2L)) : 0);
     const double f = (k < (n + 1) / 2 ? (double)k : (double)(k - n)) / (double)n * fs;  // fftfreq
     const double w = 2.0 * 3.14159265358979323846 * f;
-    const double d = deltas[s];
+    const double d = deltas.d[s];
     const double ph = 0.5 * beta2 * w * w * d;
     double sn, cs;
     sincos(ph, &sn, &cs);
     const double g = exp(-0.5 * alpha * d);
-    H[(int64_t)s * n + (__brev((unsigned)k) >> (32 - log2n))] = make_float2((float)(g * cs), (float)(g * sn));
+    H[i] = make_float2((float)(g * cs), (float)(g * sn));
   }
 }
 
@@ -133,25 +174,105 @@ __device__ __forceinline__ void ssfm_fft(float2* X, const float2* tw, int n, int
   }
 }
 
-__global__ void __launch_bounds__(kSsfmThreads) ssfm_link_kernel(const SsfmArgs a) {
+// Cluster split of a block of n = C L samples (C = 1, 2, 4; CTA `rank` of the cluster holds
+// x[rank L + i], i < L, in its shared memory).  Forward DFT (four-step, P = C):
+//   y_k1[i] = W_n^{i k1} sum_r x[r L + i] W_C^{r k1}          (CTA k1: reads the other ranks' x
+//                                                              through distributed shared memory)
+//   X[k1 + C k2] = sum_i y_k1[i] W_L^{i k2}                   (local L-point DIF, bit-reversed k2)
+// Inverse: the local L-point DIT (natural out) then x[r L + i] = sum_k1 W_C^{-r k1} W_n^{-i k1} y'_k1[i].
+// W_n^m (m < n) = ta[m >> 6] * tb[m & 63] from two small fp64-accurate tables.
+template <int C>
+__device__ __forceinline__ float2 ssfm_wC(int e) {  // W_C^e = e^{-2 pi j e / C}
+  e &= C - 1;
+  if (C == 2) return e ? make_float2(-1.f, 0.f) : make_float2(1.f, 0.f);
+  const float2 t[4] = {make_float2(1.f, 0.f), make_float2(0.f, -1.f), make_float2(-1.f, 0.f), make_float2(0.f, 1.f)};
+  return t[e];
+}
+
+template <int C, bool FORWARD>
+__device__ __forceinline__ void ssfm_cross(float2* X, const float2* ta, const float2* tb, int L, int rank) {
+  if constexpr (C > 1) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    constexpr int PER = (1 << kSsfmLocalMaxLog2) / kSsfmThreads;
+    float2 acc[PER];
+    cl.sync();  // every rank's X is final
+    const float2* Xr[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) Xr[q] = cl.map_shared_rank(X, q);
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int i = threadIdx.x + t * kSsfmThreads;
+      float2 y = make_float2(0.f, 0.f);
+      if (i < L) {
+        const int pi = ssfm_pidx(i);
+        if constexpr (FORWARD) {
+#pragma unroll
+          for (int q = 0; q < C; ++q) {
+            const float2 v = cmulf(Xr[q][pi], ssfm_wC<C>(q * rank));
+            y.x += v.x;
+            y.y += v.y;
+          }
+          const int m = i * rank;
+          y = cmulf(y, cmulf(ta[m >> 6], tb[m & 63]));
+        } else {
+#pragma unroll
+          for (int q = 0; q < C; ++q) {
+            const int m = i * q;
+            float2 w = cmulf(ta[m >> 6], tb[m & 63]);
+            w = cmulf(w, ssfm_wC<C>(q * rank));
+            w.y = -w.y;  // conj(W_n^{i q} W_C^{q rank})
+            const float2 v = cmulf(Xr[q][pi], w);
+            y.x += v.x;
+            y.y += v.y;
+          }
+        }
+      }
+      acc[t] = y;
+    }
+    cl.sync();  // every rank has read
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int i = threadIdx.x + t * kSsfmThreads;
+      if (i < L) X[ssfm_pidx(i)] = acc[t];
+    }
+    __syncthreads();
+  }
+}
+
+template <int C>
+__global__ void __launch_bounds__(kSsfmThreads, 1) ssfm_link_kernel(const SsfmArgs a) {
   extern __shared__ __align__(16) unsigned char ss_smem[];
   const int n = (int)a.n;
-  float2* X = reinterpret_cast<float2*>(ss_smem);  // [n + n/16] padded
-  float2* tw = X + n + n / 16 + 1;                 // [n/2]
-  const int b = blockIdx.x;
-  float2* ub = a.u + (int64_t)b * n;
-  for (int k = threadIdx.x; k < n / 2; k += kSsfmThreads) {
+  const int L = n / C;
+  float2* X = reinterpret_cast<float2*>(ss_smem);  // [L + L/16] padded
+  float2* tw = X + L + L / 16 + 1;                 // [L/2]   W_L^k
+  float2* ta = tw + L / 2;                         // [n/64]  W_n^{64 a}  (C > 1)
+  float2* tb = ta + (C > 1 ? n / 64 : 0);          // [64]    W_n^{b}
+  int rank = 0;
+  if constexpr (C > 1) rank = (int)cooperative_groups::this_cluster().block_rank();
+  const int b = blockIdx.x / C;
+  float2* ub = a.u + (int64_t)b * n + (int64_t)rank * L;
+  for (int k = threadIdx.x; k < L / 2; k += kSsfmThreads) {
     double sn, cs;
-    sincospi(-2.0 * (double)k / (double)n, &sn, &cs);
+    sincospi(-2.0 * (double)k / (double)L, &sn, &cs);
     tw[k] = make_float2((float)cs, (float)sn);
   }
-  for (int i = threadIdx.x; i < n; i += kSsfmThreads) X[ssfm_pidx(i)] = ub[i];
+  if constexpr (C > 1) {
+    for (int k = threadIdx.x; k < n / 64 + 64; k += kSsfmThreads) {
+      const int m = k < n / 64 ? 64 * k : k - n / 64;
+      double sn, cs;
+      sincospi(-2.0 * (double)m / (double)n, &sn, &cs);
+      (k < n / 64 ? ta[k] : tb[k - n / 64]) = make_float2((float)cs, (float)sn);
+    }
+  }
+  for (int i = threadIdx.x; i < L; i += kSsfmThreads) X[ssfm_pidx(i)] = ub[i];
   __syncthreads();
   const float inv_n = 1.f / (float)n;
   for (int sp = 0; sp < a.spans; ++sp) {
     for (int s = 0; s < a.S; ++s) {
       const float kp = a.kerr_phase[s];
-      for (int i = threadIdx.x; i < n; i += kSsfmThreads) {  // Kerr step (L_eff), pointwise
+      for (int i = threadIdx.x; i < L; i += kSsfmThreads) {  // Kerr step (L_eff), pointwise
         const int pi = ssfm_pidx(i);
         const float2 v = X[pi];
         float sn, cs;
@@ -159,24 +280,26 @@ __global__ void __launch_bounds__(kSsfmThreads) ssfm_link_kernel(const SsfmArgs 
         X[pi] = make_float2(v.x * cs - v.y * sn, v.x * sn + v.y * cs);
       }
       __syncthreads();
-      ssfm_fft<true>(X, tw, n, a.log2n);
-      const float2* Hs = a.H + (int64_t)s * n;
-      for (int k = threadIdx.x; k < n; k += kSsfmThreads) {  // lossy dispersion (and 1/n), bit-reversed slots
+      ssfm_cross<C, true>(X, ta, tb, L, rank);
+      ssfm_fft<true>(X, tw, L, a.log2L);
+      const float2* Hs = a.H + (int64_t)s * n + (int64_t)rank * L;
+      for (int k = threadIdx.x; k < L; k += kSsfmThreads) {  // lossy dispersion (and 1/n), bit-reversed slots
         const int pk_ = ssfm_pidx(k);
         const float2 h = Hs[k], v = X[pk_];
         X[pk_] = make_float2((v.x * h.x - v.y * h.y) * inv_n, (v.x * h.y + v.y * h.x) * inv_n);
       }
       __syncthreads();
-      ssfm_fft<false>(X, tw, n, a.log2n);
+      ssfm_fft<false>(X, tw, L, a.log2L);
+      ssfm_cross<C, false>(X, ta, tb, L, rank);
     }
     // EDFA: gain + ASE
-    const float2* nz = a.noise ? a.noise + ((int64_t)sp * gridDim.x + b) * n : nullptr;
-    for (int i = threadIdx.x; i < n; i += kSsfmThreads) {
+    const float2* nz = a.ase_mode == 1 ? a.noise + ((int64_t)sp * (gridDim.x / C) + b) * n + (int64_t)rank * L : nullptr;
+    for (int i = threadIdx.x; i < L; i += kSsfmThreads) {
       float2 v = X[ssfm_pidx(i)];
       v.x *= a.span_gain;
       v.y *= a.span_gain;
-      if (nz) {
-        const float2 z = nz[i];
+      if (a.ase_mode) {
+        const float2 z = a.ase_mode == 1 ? nz[i] : ase_philox_cn(a.ase_seed, a.block0 + b, sp, (int64_t)rank * L + i);
         v.x = fmaf(a.ase_sigma, z.x, v.x);
         v.y = fmaf(a.ase_sigma, z.y, v.y);
       }
@@ -185,22 +308,24 @@ __global__ void __launch_bounds__(kSsfmThreads) ssfm_link_kernel(const SsfmArgs 
     __syncthreads();
   }
   if (a.decim <= 0) {
-    for (int i = threadIdx.x; i < n; i += kSsfmThreads) ub[i] = X[ssfm_pidx(i)];
+    for (int i = threadIdx.x; i < L; i += kSsfmThreads) ub[i] = X[ssfm_pidx(i)];
     return;
   }
   // receiver front end: brick-wall LPF |fftfreq| <= cutoff, then every decim-th sample
-  ssfm_fft<true>(X, tw, n, a.log2n);
-  for (int i = threadIdx.x; i < n; i += kSsfmThreads) {  // slot i holds bin bitrev(i)
-    const int k = (int)ssfm_bitrev((unsigned)i, a.log2n);
+  ssfm_cross<C, true>(X, ta, tb, L, rank);
+  ssfm_fft<true>(X, tw, L, a.log2L);
+  for (int i = threadIdx.x; i < L; i += kSsfmThreads) {  // slot i holds bin rank + C bitrev_L(i)
+    const int k = rank + C * (int)(a.log2L > 0 ? ssfm_bitrev((unsigned)i, a.log2L) : 0);
     const float f = (float)(k < (n + 1) / 2 ? k : k - n) / (float)n;
     const int pi = ssfm_pidx(i);
     const float2 v = X[pi];
     X[pi] = fabsf(f) <= a.cutoff ? make_float2(v.x * inv_n, v.y * inv_n) : make_float2(0.f, 0.f);
   }
   __syncthreads();
-  ssfm_fft<false>(X, tw, n, a.log2n);
-  float2* rb = a.r + (int64_t)b * (n / a.decim);
-  for (int i = threadIdx.x; i < n / a.decim; i += kSsfmThreads) rb[i] = X[ssfm_pidx(i * a.decim)];
+  ssfm_fft<false>(X, tw, L, a.log2L);
+  ssfm_cross<C, false>(X, ta, tb, L, rank);
+  float2* rb = a.r + (int64_t)b * (n / a.decim) + (int64_t)rank * (L / a.decim);
+  for (int i = threadIdx.x; i < L / a.decim; i += kSsfmThreads) rb[i] = X[ssfm_pidx(i * a.decim)];
 }
 
 }  // namespace ldbp

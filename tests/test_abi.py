@@ -30,7 +30,7 @@ def test_header_symbols_exported(L):
     for name in names:
         assert hasattr(L.lib, name), name
     assert sorted(L.EXPORTED) == names
-    assert L.lib.ldbp_abi_version() == 1
+    assert L.lib.ldbp_abi_version() == 2
 
 
 def test_validation_before_launch(L):
@@ -118,7 +118,9 @@ def test_rx_essm_ssfm_validation(L):
     assert lib.ldbp_essm_workspace_bytes(ctypes.byref(d), 4, 2, ctypes.byref(out)) == 0
     assert out.value >= 3 * 2 * 32 * 8
     assert lib.ldbp_essm_workspace_bytes(ctypes.byref(d), 4, 1, ctypes.byref(out)) == -1  # no BACKWARD op
-    # SSFM: power-of-two n <= 2^14
+    # SSFM: power-of-two n <= 2^16 (2- and 4-CTA clusters above 2^14), at most 64 steps per span
     assert lib.ldbp_ssfm_workspace_bytes(1000, 4, ctypes.byref(out)) == -2
-    assert lib.ldbp_ssfm_workspace_bytes(1 << 15, 4, ctypes.byref(out)) == -2
+    assert lib.ldbp_ssfm_workspace_bytes(1 << 17, 4, ctypes.byref(out)) == -2
+    assert lib.ldbp_ssfm_workspace_bytes(1 << 16, 65, ctypes.byref(out)) == -2
+    assert lib.ldbp_ssfm_workspace_bytes(1 << 16, 4, ctypes.byref(out)) == 0 and out.value >= 4 * (1 << 16) * 8
     assert lib.ldbp_ssfm_workspace_bytes(1 << 14, 4, ctypes.byref(out)) == 0 and out.value >= 4 * (1 << 14) * 8
