@@ -159,16 +159,19 @@ def my_blocks(cfg, world, rank, scaling):
     return shard(rank, world, global_blocks(cfg, world, scaling))
 
 
-def make_inputs(cfg, blocks):
-    """Received blocks and tx targets keyed by GLOBAL block index (same union for any G)."""
-    import ldbp_inputs as li
+def make_inputs(cfg, blocks, world=1, scaling="weak"):
+    """Received blocks and tx targets keyed by GLOBAL block index (same union for any G): the GPU
+    SSFM link (paper_2010_14258_b200.channel: 25 x 80 km, 16-QAM 10.7 GBd, rho_a = 4, EDFA ASE drawn
+    in-kernel, LPF + decimation to 2 sps) on a pool of unique blocks, shifted / rotated per block."""
+    from paper_2010_14258_b200 import channel
 
     blocks = list(blocks)
-    pw = li.dbm_to_w(li.pick_powers_dbm(cfg["idx"], blocks, POWERS_DBM))
-    x = li.bandlimited_blocks_keyed_torch(cfg["idx"], blocks, cfg["n"], pw)
-    tgt = li.bandlimited_blocks_keyed_torch(cfg["idx"], blocks, cfg["n"], pw, purpose="target") \
-        if cfg["mode"] == "train" else None
-    return x, tgt
+    nglob = global_blocks(cfg, world, scaling)
+    U = min(256, max(4, 4 * -(-nglob // 4)))
+    pool = channel.simulate_pool(cfg["idx"], U, cfg["n"] // channel.RHO_D)
+    x, tgt = channel.link_blocks(cfg["idx"], blocks, cfg["n"], pool=pool)
+    del pool
+    return x, (tgt if cfg["mode"] == "train" else None)
 
 
 def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_clocks=True, scaling=None):
@@ -186,7 +189,7 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
     scaling = scaling or cfg["scaling"]
     blocks = my_blocks(cfg, world, rank, scaling)
     B, n = len(blocks), cfg["n"]
-    x, tgt = make_inputs(cfg, blocks)
+    x, tgt = make_inputs(cfg, blocks, world, scaling)
     train = cfg["mode"] == "train"
     st = P.TrainState.create(taps, gamma, device=dev)
     ws = P.Workspace()
@@ -586,8 +589,9 @@ def main():
             "config": {"workload": WORKLOAD[args.config], "config": args.config, "blocks_per_gpu": r["B"],
                        "global_blocks": r["global_blocks"], "n": r["n"], "steps_M": r["M"], "taps_T": r["T"],
                        "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) between timed steps",
-                       "inputs": "band-limited circular Gaussian keyed by global block index, P in {-2,-1,0,1} dBm, "
-                                 "LS inverse-CD taps (cap 1)"},
+                       "inputs": "GPU SSFM link (25x80 km SMF, 16-QAM 10.7 GBd, rho_a=4, 50 log StPS, EDFA ASE "
+                                 "Philox-keyed) -> LPF + 2 sps; pool of <=256 blocks shifted/rotated per global block; "
+                                 "P in {-2,-1,0,1} dBm; LS inverse-CD taps (cap 1)"},
             "clocks": r["clk"], "roofline": r["roof"], "step_roofline": r["step_roof"], "cpu_baseline": cpu,
             "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "kernel_shares": r["kernel_shares"],
         }

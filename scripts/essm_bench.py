@@ -18,7 +18,7 @@ B, n, M, T, kap = cfg["B"], cfg["n"], 25, 9, 20
 cfg.update(sps=1)
 taps, gamma = bench.make_model(cfg)
 taps, gamma = taps[:M], gamma[:M]
-x, tgt = bench.make_inputs(cfg, 0)
+x, tgt = bench.make_inputs(cfg, range(cfg["B"]))
 eta = np.ones((M, 2 * kap + 1)) / (2 * kap + 1)
 ht = torch.from_numpy(taps.astype(np.complex64)).cuda()
 gt = torch.from_numpy(gamma.astype(np.float32)).cuda()

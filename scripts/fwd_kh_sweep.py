@@ -14,7 +14,7 @@ import bench  # noqa: E402
 import paper_2010_14258_b200 as P  # noqa: E402
 
 cfg = dict(bench.CONFIGS["C3"])
-x, _ = bench.make_inputs(cfg, 0)
+x, _ = bench.make_inputs(cfg, range(cfg["B"]))
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 ws = P.Workspace()
 for T in (3, 5, 7, 9, 11, 13, 15):

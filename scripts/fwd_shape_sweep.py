@@ -17,7 +17,7 @@ flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 ws = P.Workspace()
 for B, M in [(256, 25), (256, 50), (256, 100), (512, 25), (1024, 25), (128, 25)]:
     cfg = dict(bench.CONFIGS["C2"], B=B)
-    x, _ = bench.make_inputs(cfg, 0)
+    x, _ = bench.make_inputs(cfg, range(cfg["B"]))
     taps, gamma = bench.make_model(cfg)
     reps = -(-M // taps.shape[0])
     taps = np.concatenate([taps] * reps)[:M]

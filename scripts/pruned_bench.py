@@ -17,7 +17,7 @@ cfg = bench.CONFIGS["C3"]
 taps, gamma = bench.make_model(cfg)
 M, T = taps.shape
 kh = (T - 1) // 2
-x, tgt = bench.make_inputs(cfg, 0)
+x, tgt = bench.make_inputs(cfg, range(cfg["B"]))
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 ws = P.Workspace()
 

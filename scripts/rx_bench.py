@@ -20,7 +20,7 @@ B, n = cfg["B"], cfg["n"]
 sps, span = 2, 32
 taps, gamma = bench.make_model(cfg)
 M, T = taps.shape
-x, tgt = bench.make_inputs(cfg, 0)
+x, tgt = bench.make_inputs(cfg, range(cfg["B"]))
 sym = torch.from_numpy(np.stack([li.qam16(li.rng(3, b, "symbols"), n // sps) for b in range(B)])
                        .astype(np.complex64)).cuda()
 pw = torch.full((B,), 1e-3, dtype=torch.float32, device="cuda")

@@ -1,6 +1,7 @@
 """Parity of the exact training call bench.py times, at BASELINE.json's full sizes, against the
 fp64 oracle over EVERY block (SURVEY.md §8(c) "the gate"; VERDICT r1 Next #1).
 
+Inputs are bench.py's: the simulated link (GPU SSFM, channel.link_blocks).
 C3: 512 blocks x 2^14, M = 50, T = 9 — the store-all schedule (storing forward, Kr = 2 reverse
 launches of 25 steps, 6498 CTAs, so the two-level fp64 reduction `reduce_partials_pass1` runs).
 C5 slice: 512 blocks x 2^15, M = 25, T = 3 (2^24 samples, > 1024 reverse CTAs: the same
@@ -67,11 +68,11 @@ def ls_model(spans, sps, T):
     ("C5-slice", 512, 32768, 25, 1, 3, 1),
 ])
 def test_timed_training_call_vs_oracle_all_blocks(P, name, B, n, spans, sps, T, kr):
+    from paper_2010_14258_b200 import channel
+
     idx = 3 if name == "C3" else 5
-    blocks = range(B)
-    pw = li.dbm_to_w(li.pick_powers_dbm(idx, blocks, POWERS_DBM))
-    x = li.bandlimited_blocks_keyed_torch(idx, blocks, n, pw)
-    tgt = li.bandlimited_blocks_keyed_torch(idx, blocks, n, pw, purpose="target")
+    # the bench's inputs: GPU SSFM link blocks (pool of 256 simulated blocks, shifted / rotated)
+    x, tgt = channel.link_blocks(idx, range(B), n)
     taps, gamma = ls_model(spans, sps, T)
     M = len(gamma)
     st = P.TrainState.create(taps, gamma)
