@@ -15,6 +15,7 @@ from .api import (  # noqa: F401
     ldbp_essm_loss_grad,
     ldbp_forward,
     ldbp_loss_grad,
+    ldbp_loss_grad_state,
     ldbp_rx_loss_grad,
     ldbp_rx_train_grad,
     ldbp_ssfm_link,

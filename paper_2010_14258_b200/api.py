@@ -11,6 +11,7 @@ import functools
 import threading
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -181,6 +182,30 @@ def ldbp_loss_grad(x, target, taps, gamma, *, mask=None, symmetric=True, precise
     return out
 
 
+def ldbp_loss_grad_state(state, x, target, *, buf=None, ws=None, stream=None):
+    """ldbp_loss_grad on a TrainState's working copies.  When the mask leaves only the central
+    active_T < T taps (progressive pruning), the call runs on that central window (the
+    T'-tap kernels; masked taps are exactly zero, so the result is the same computation) and the
+    gradient is laid out back into the full [1 + M + 2 M T] buffer with zeros for the pruned taps."""
+    M, T = state.taps.shape
+    Ta = state.active_T
+    if state.mask is None or Ta is None or Ta >= T:
+        return ldbp_loss_grad(x, target, state.taps, state.gamma, mask=state.mask, symmetric=state.symmetric,
+                              precise=state.precise, buf=buf, ws=ws, stream=stream)
+    lo = (T - Ta) // 2
+    ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    with ctx:
+        taps_c = state.taps[:, lo:lo + Ta].contiguous()
+        mask_c = state.mask[:, lo:lo + Ta].contiguous()
+        bc = ldbp_loss_grad(x, target, taps_c, state.gamma, mask=mask_c, symmetric=state.symmetric,
+                            precise=state.precise, ws=ws, stream=stream)
+        out = _check_buf(buf, 1 + M + 2 * M * T, x.device)
+        out.zero_()
+        out[:1 + M] = bc[:1 + M]
+        out[1 + M:].view(M, T, 2)[:, lo:lo + Ta] = bc[1 + M:].view(M, Ta, 2)
+    return out
+
+
 @dataclass
 class AdamConfig:
     lr: float = 1e-3  # Table I (P:1007)
@@ -201,6 +226,7 @@ class TrainState:
     t: int = 0
     mask: torch.Tensor | None = None            # uint8 [M][T]
     gamma_learnable: torch.Tensor | None = None  # uint8 [M]
+    active_T: int | None = None                  # host-known: every tap outside the central active_T is masked
     symmetric: bool = True
     precise: bool = False
     adam: AdamConfig = field(default_factory=AdamConfig)
@@ -217,10 +243,23 @@ class TrainState:
                         gamma=gamma.to(torch.float32).to(device).contiguous(), master=master.contiguous(),
                         m=z.clone(), v=z.clone(), symmetric=symmetric, precise=precise, adam=adam or AdamConfig())
         if mask is not None:
-            st.mask = torch.as_tensor(mask, dtype=torch.uint8).to(device).contiguous()
+            st.set_mask(mask)
         if gamma_learnable is not None:
             st.gamma_learnable = torch.as_tensor(gamma_learnable, dtype=torch.uint8).to(device).contiguous()
         return st
+
+    def set_mask(self, mask):
+        """Install a (host) tap mask; records the narrowest odd window that holds every unmasked tap,
+        so that training runs the shorter-filter kernels (§8(f) NEXT-3: pruned taps cost nothing)."""
+        m = np.asarray(mask.cpu() if isinstance(mask, torch.Tensor) else mask, dtype=np.uint8)
+        if self.mask is None:
+            self.mask = torch.from_numpy(m).to(self.taps.device).contiguous()
+        else:
+            self.mask.copy_(torch.from_numpy(m), non_blocking=False)
+        kh = (m.shape[1] - 1) // 2
+        cols = np.nonzero(m.any(axis=0))[0]
+        k = int(max(abs(cols - kh).max(), 0)) if len(cols) else 0
+        self.active_T = 2 * k + 1
 
     @property
     def M(self):

@@ -42,8 +42,7 @@ class DataParallelLDBP:
 
             st = self.state
             if self.loss_grad_fn is None:
-                self.loss_grad_fn = lambda x, t: api.ldbp_loss_grad(
-                    x, t, st.taps, st.gamma, mask=st.mask, symmetric=st.symmetric, precise=st.precise)
+                self.loss_grad_fn = lambda x, t: api.ldbp_loss_grad_state(st, x, t)
             if self.adam_fn is None:
                 self.adam_fn = lambda buf, n: api.ldbp_adam_update(st, buf, n)
 

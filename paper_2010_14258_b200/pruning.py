@@ -94,9 +94,5 @@ class PruneSchedule:
             return False
         import torch
 
-        new = torch.from_numpy(self.mask_at(iteration))
-        if state.mask is None:
-            state.mask = new.to(state.taps.device)
-        else:
-            state.mask.copy_(new, non_blocking=True)
+        state.set_mask(self.mask_at(iteration))
         return True

@@ -36,7 +36,8 @@ def timed(fn, reps=10):
     return sum(a.elapsed_time(b) for a, b in ev) / reps
 
 
-for name, pattern in (("unpruned", [kh] * M), ("pruned 9/5", [kh if i % 2 == 0 else kh - 2 for i in range(M)])):
+for name, pattern in (("unpruned", [kh] * M), ("pruned 9/5", [kh if i % 2 == 0 else kh - 2 for i in range(M)]),
+                      ("pruned 5/3", [2 if i % 2 == 0 else 1 for i in range(M)])):
     mask = np.ones((M, T), np.uint8)
     for i, k in enumerate(pattern):
         for j in range(k + 1, kh + 1):
@@ -46,7 +47,8 @@ for name, pattern in (("unpruned", [kh] * M), ("pruned 9/5", [kh if i % 2 == 0 e
     mt = torch.from_numpy(mask).cuda()
     active = int(mask.sum())
     t_f = timed(lambda: P.ldbp_forward(x, ht, gt, ws=ws))
-    t_g = timed(lambda: P.ldbp_loss_grad(x, tgt, ht, gt, mask=mt, ws=ws))
+    st = P.TrainState.create(taps * mask, gamma, mask=mask)
+    t_g = timed(lambda: P.ldbp_loss_grad_state(st, x, tgt, ws=ws))  # active-window training (NEXT-3)
     ss = cfg["B"] * cfg["n"] * M
     print(f"{name:12s} active taps {active:4d}: forward {t_f:.3f} ms ({ss / t_f / 1e6:.1f} Gss/s), "
           f"loss+grad {t_g:.3f} ms ({ss / t_g / 1e6:.1f} Gss/s)")

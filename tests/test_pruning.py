@@ -75,3 +75,40 @@ def test_training_with_pruning_keeps_pruned_taps_zero():
     assert torch.all(master[~m] == 0)
     mm = st.m[: 2 * M * T].view(M, T, 2)
     assert torch.all(mm[~m] == 0)
+
+
+@pytest.mark.gpu
+def test_pruned_training_runs_on_active_window():
+    """NEXT-3 in the training path: a 9-tap model pruned to alternating 5/3 taps
+    trains on the central 5-tap window (the Kh = 2 kernels); the gradient buffer keeps the full
+    [1 + M + 2 M T] layout, matches the oracle per step and is exactly zero on pruned taps."""
+    import torch
+
+    import __graft_entry__
+    import ldbp_inputs as li
+    from oracle import ldbp as O
+
+    __graft_entry__.build()
+    import paper_2010_14258_b200 as P
+
+    B, n, M, T = 3, 4096, 6, 9
+    x = li.gaussian_blocks(41, range(B), n, 1e-3)
+    tgt = li.gaussian_blocks(41, range(B), n, 1e-3, purpose="target")
+    taps = li.random_sym_taps(41, M, T)
+    gamma = li.random_gamma(41, M)
+    mask = mask_for_lengths([5 if i % 2 == 0 else 3 for i in range(M)], T)
+    st = P.TrainState.create(taps * mask, gamma, mask=mask)
+    assert st.active_T == 5
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda()
+    td = torch.from_numpy(tgt.astype(np.complex64)).cuda()
+    buf = P.ldbp_loss_grad_state(st, xd, td).cpu().numpy()
+    full = P.ldbp_loss_grad(xd, td, st.taps, st.gamma, mask=st.mask).cpu().numpy()
+    r32 = lambda a: a.astype(np.complex64).astype(np.complex128)  # noqa: E731
+    ref = O.loss_grad(r32(x), r32(tgt), r32(taps * mask), gamma.astype(np.float32).astype(np.float64), mask=mask)
+    assert abs(buf[0] - ref[0]) <= 1e-5 * ref[0]
+    dt, rdt = buf[1 + M:].reshape(M, T, 2), ref[1 + M:].reshape(M, T, 2)
+    for i in range(M):
+        assert np.linalg.norm(dt[i] - rdt[i]) <= 1e-4 * np.linalg.norm(rdt[i]), i
+        assert abs(buf[1 + i] - ref[1 + i]) <= 1e-4 * abs(ref[1 + i]), i
+    assert np.all(dt[mask == 0] == 0)
+    assert np.linalg.norm(buf - full) <= 1e-5 * np.linalg.norm(full)
