@@ -200,6 +200,30 @@ int ldbp_rx_train_grad(const ldbp_dims* d, const void* x, const void* symbols, c
                        void* ws, size_t ws_bytes, void* cuda_stream);
 
 /*
+ * Receiver-chain loss with the EXACT circulant matched filter (Eq. (12),
+ * M is "a circulant matrix that represents the matched filter"; Eq. (13)).
+ * Per block b of n samples (power of two, n <= 65536) at sps in [1, 4] samples/symbol:
+ *   z = F^-1 diag(RRC_rolloff) F y   (root-raised-cosine response of the periodic frame)
+ *   s_tilde_k = z[k sps],  phi_b = arg(s^H s_tilde),  a = e^{-j phi_b} / sqrt(power_w[b])
+ *   errs_b = sum_k |a s_tilde_k - s_k|^2,   L = sum_b w_b errs_b   (w = weights, or all 1)
+ *   gy = dL/dy (full chain rule incl. the genie phase; M^T = F^-1 diag(RRC) F U, U = upsampling)
+ * y, gy [B][n] complex64; symbols [B][n/sps] complex64; power_w, weights [B] float32; errs [B]
+ * float64 out (unweighted); gy may be NULL.  No workspace.  One CTA per block up to 2^14 samples,
+ * a 2-/4-CTA cluster beyond (fp32 shared-memory FFTs, fp64 fixed-order reductions: deterministic).
+ *   ldbp_rx_exact_train_grad: buf = [sum_b w_b errs_b | d/dgamma' [M] | d/dtaps [M][T][2]] through
+ *   LDBP (UNscaled, this device's blocks; tap_mask as in ldbp_loss_grad), y = f_theta(x).
+ */
+int ldbp_rx_exact_loss_grad(int64_t batch, int64_t n, int32_t sps, float rolloff, const void* y,
+                            const void* symbols, const float* power_w, const float* weights_or_null,
+                            double* errs, void* gy_or_null, void* cuda_stream);
+int ldbp_rx_exact_train_workspace_bytes(const ldbp_dims* d, int32_t sps, size_t* bytes);
+int ldbp_rx_exact_train_grad(const ldbp_dims* d, const void* x, const void* symbols,
+                             const float* power_w, const float* weights_or_null, int32_t sps,
+                             float rolloff, const void* taps, const float* gamma,
+                             const uint8_t* tap_mask_or_null, double* buf, void* ws, size_t ws_bytes,
+                             void* cuda_stream);
+
+/*
  * Learned ESSM (paper §III-D, Eq. nl_filtered): the nonlinear
  * step of Eq. (7) becomes  v_t = a_t exp(j gamma'_i sum_{k=-kappa}^{kappa} eta^(i)_k |a_{(t-k) mod n}|^2)
  * with real per-step filters eta [M][2 kappa + 1] (tap k at index k + kappa), 0 <= kappa <= 32,

@@ -113,3 +113,44 @@ def rx_loss_grad(y, s, power_w, h, sps):
     g_st = g_direct + dL_dphi[..., None] * g_phi
     gy = mf_fir_adjoint(g_st, h, sps, y.shape[-1]).reshape(y.shape)
     return errs, gy, dL_dphi
+
+
+# ---------------------------------------------------------------------------------------------
+# Exact circulant matched filter (Eq. (12): "M ... a circulant matrix that represents
+# the matched filter"): M y = (F^-1 diag(RRC) F y)[::sps].  C = F^-1 diag(RRC) F is real and
+# symmetric (RRC real and even in frequency), so M^T g = C U g with U the zero-stuffing upsampler.
+# This is the definition itself; the truncated-FIR form above is its approximation (reading G19).
+# ---------------------------------------------------------------------------------------------
+def mf_exact(y: np.ndarray, sps: int, rolloff: float = 0.1) -> np.ndarray:
+    """s_tilde = M y (unnormalised), exact circulant RRC matched filter then downsampling."""
+    y = np.asarray(y, np.complex128)
+    n = y.shape[-1]
+    return np.fft.ifft(np.fft.fft(y, axis=-1) * rrc_response(n, sps, rolloff), axis=-1)[..., ::sps]
+
+
+def mf_exact_adjoint(g: np.ndarray, sps: int, n: int, rolloff: float = 0.1) -> np.ndarray:
+    """M^T g = C U g (zero-stuff the symbol-rate gradient, then the same circulant)."""
+    g = np.asarray(g, np.complex128)
+    u = np.zeros(g.shape[:-1] + (n,), np.complex128)
+    u[..., ::sps] = g
+    return np.fft.ifft(np.fft.fft(u, axis=-1) * rrc_response(n, sps, rolloff), axis=-1)
+
+
+def rx_loss_grad_exact(y, s, power_w, sps: int, rolloff: float = 0.1, weights=None):
+    """L = sum_b w_b errs_b with the exact M (Eq. (12)-(13)); returns (errs [B] unweighted, dL/dy).
+    Same chain rule as rx_loss_grad (genie phase included), with M and M^T exact."""
+    y = np.atleast_2d(np.asarray(y, np.complex128))
+    s = np.atleast_2d(np.asarray(s, np.complex128))
+    B, n = y.shape
+    w = np.ones(B) if weights is None else np.asarray(weights, np.float64)
+    st = mf_exact(y, sps, rolloff)
+    z = np.sum(np.conj(s) * st, axis=-1)
+    phi = np.angle(z)
+    a = np.exp(-1j * phi) / np.sqrt(np.asarray(power_w, np.float64))
+    sh = a[:, None] * st
+    e = sh - s
+    errs = np.sum(np.abs(e) ** 2, axis=-1)
+    g_direct = 2.0 * np.conj(a)[:, None] * e
+    dL_dphi = 2.0 * np.sum(np.real(np.conj(e) * (-1j) * sh), axis=-1)
+    g_st = w[:, None] * (g_direct + dL_dphi[:, None] * (1j * s / np.conj(z)[:, None]))
+    return errs, mf_exact_adjoint(g_st, sps, n, rolloff)

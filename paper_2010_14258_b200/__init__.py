@@ -16,6 +16,8 @@ from .api import (  # noqa: F401
     ldbp_forward,
     ldbp_loss_grad,
     ldbp_loss_grad_state,
+    ldbp_rx_exact_loss_grad,
+    ldbp_rx_exact_train_grad,
     ldbp_rx_loss_grad,
     ldbp_rx_train_grad,
     ldbp_ssfm_link,

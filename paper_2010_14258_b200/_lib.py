@@ -37,6 +37,9 @@ EXPORTED = (
     "ldbp_essm_workspace_bytes",
     "ldbp_essm_forward",
     "ldbp_essm_loss_grad",
+    "ldbp_rx_exact_loss_grad",
+    "ldbp_rx_exact_train_workspace_bytes",
+    "ldbp_rx_exact_train_grad",
     "ldbp_ssfm_workspace_bytes",
     "ldbp_ssfm_link",
 )
@@ -101,6 +104,11 @@ def _load():
         "ldbp_rx_train_workspace_bytes": (ctypes.c_int, [D, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]),
         "ldbp_rx_train_grad": (ctypes.c_int, [D, P, P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P,
                                               ctypes.c_size_t, P]),
+        "ldbp_rx_exact_loss_grad": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_float,
+                                                   P, P, P, P, P, P, P]),
+        "ldbp_rx_exact_train_workspace_bytes": (ctypes.c_int, [D, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]),
+        "ldbp_rx_exact_train_grad": (ctypes.c_int, [D, P, P, P, P, ctypes.c_int32, ctypes.c_float, P, P, P, P, P,
+                                                    ctypes.c_size_t, P]),
         "ldbp_essm_workspace_bytes": (ctypes.c_int, [D, ctypes.c_int32, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
         "ldbp_essm_forward": (ctypes.c_int, [D, ctypes.c_int32, P, P, P, P, P, P, ctypes.c_size_t, P]),
         "ldbp_essm_loss_grad": (ctypes.c_int, [D, ctypes.c_int32, P, P, P, P, P, P, P, ctypes.c_size_t, P]),

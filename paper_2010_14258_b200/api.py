@@ -349,6 +349,48 @@ def ldbp_rx_train_grad(x, symbols, power_w, h_mf, taps, gamma, *, sps=2, mask=No
     return out
 
 
+@_on_stream
+def ldbp_rx_exact_loss_grad(y, symbols, power_w, *, sps=2, rolloff=0.1, weights=None, need_grad=True, stream=None):
+    """Receiver-chain symbol loss with the exact circulant matched filter (§8(f) NEXT-1, Eq. (12)).
+    Returns (errs float64 [B] unweighted, gy complex64 [B][n] = dL/dy of L = sum_b w_b errs_b, or None)."""
+    _need(y, "y", torch.complex64)
+    B, n = y.shape
+    if n % sps:
+        raise ValueError(f"n = {n} is not a multiple of sps = {sps}")
+    _need(symbols, "symbols", torch.complex64, (B, n // sps))
+    _need(power_w, "power_w", torch.float32, (B,))
+    if weights is not None:
+        _need(weights, "weights", torch.float32, (B,))
+    errs = torch.empty(B, dtype=torch.float64, device=y.device)
+    gy = torch.empty_like(y) if need_grad else None
+    check(lib.ldbp_rx_exact_loss_grad(B, n, sps, float(rolloff), _p(y), _p(symbols), _p(power_w), _p(weights),
+                                      _p(errs), _p(gy), _stream_handle(stream)), "ldbp_rx_exact_loss_grad")
+    return errs, gy
+
+
+@_on_stream
+def ldbp_rx_exact_train_grad(x, symbols, power_w, taps, gamma, *, sps=2, rolloff=0.1, weights=None, mask=None,
+                             symmetric=True, precise=False, buf=None, ws=None, stream=None):
+    """[sum_b w_b errs_b | dgamma[M] | dtaps[M][T][2]] of the exact receiver-chain loss through LDBP."""
+    B, n, M, T = _check_model(x, taps, gamma)
+    _need(symbols, "symbols", torch.complex64, (B, n // sps))
+    _need(power_w, "power_w", torch.float32, (B,))
+    if weights is not None:
+        _need(weights, "weights", torch.float32, (B,))
+    if mask is not None:
+        _need(mask, "mask", torch.uint8, (M, T))
+    d = make_dims(B, n, M, T, symmetric, precise)
+    out = _check_buf(buf, 1 + M + 2 * M * T, x.device)
+    nb = ctypes.c_size_t(0)
+    check(lib.ldbp_rx_exact_train_workspace_bytes(ctypes.byref(d), sps, ctypes.byref(nb)),
+          "ldbp_rx_exact_train_workspace_bytes")
+    w, nbv = _ws(x.device, int(nb.value), ws)
+    check(lib.ldbp_rx_exact_train_grad(ctypes.byref(d), _p(x), _p(symbols), _p(power_w), _p(weights), sps,
+                                       float(rolloff), _p(taps), _p(gamma), _p(mask), _p(out), _p(w), nbv,
+                                       _stream_handle(stream)), "ldbp_rx_exact_train_grad")
+    return out
+
+
 def _check_eta(eta, M):
     _need(eta, "eta", torch.float32)
     if eta.dim() != 2 or eta.shape[0] != M or eta.shape[1] % 2 == 0:

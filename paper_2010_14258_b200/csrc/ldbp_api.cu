@@ -20,6 +20,7 @@
 #include "ldbp_rx.cuh"
 #include "ldbp_essm.cuh"
 #include "ldbp_ssfm.cuh"
+#include "ldbp_rx_exact.cuh"
 
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
@@ -96,6 +97,7 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 int ntaps_used(int kh, bool sym) { return sym ? kh + 1 : 2 * kh + 1; }
+constexpr int kRxMaxSpsExact = 4;
 
 // ----------------------------------------------------------------------------------------
 // Kernel dispatch tables
@@ -1390,6 +1392,162 @@ int ldbp_rx_train_grad(const ldbp_dims* d, const void* x, const void* symbols, c
   ldbp::rx_errs_kernel<<<1, 256, 0, st>>>(reinterpret_cast<double*>(wb + w.rx_off + rw2.epart_off), d->batch,
                                           rw2.chunks, errs, buf);
   return cuda_check("rx_errs_kernel launch");
+}
+
+// ---- exact circulant matched filter (ldbp_rx_exact.cuh) ----
+static int validate_rx_exact(int64_t B, int64_t n, int sps, float rolloff) {
+  if (B < 0) return fail(LDBP_ESHAPE, "batch %lld < 0", (long long)B);
+  if (n < 2 || (n & (n - 1)) || n > (1 << ldbp::kSsfmMaxLog2))
+    return fail(LDBP_ESHAPE, "n %lld must be a power of two in [2, %d]", (long long)n, 1 << ldbp::kSsfmMaxLog2);
+  if (sps < 1 || sps > kRxMaxSpsExact || n % sps) return fail(LDBP_ESHAPE, "sps %d must divide n, 1 <= sps <= 4", sps);
+  if (!(rolloff > 0.f && rolloff <= 1.f)) return fail(LDBP_EINVAL, "rolloff %g not in (0, 1]", (double)rolloff);
+  return LDBP_OK;
+}
+
+static int launch_rx_exact(int64_t B, int64_t n, int sps, float rolloff, const float2* y, const float2* sym,
+                           const float* pw, const float* weights, double* errs, float2* gy, cudaStream_t st) {
+  const int C = n > (1 << ldbp::kSsfmLocalMaxLog2) ? (int)(n >> ldbp::kSsfmLocalMaxLog2) : 1;
+  const int64_t L = n / C;
+  ldbp::RxExactArgs a;
+  a.y = y;
+  a.sym = sym;
+  a.power_w = pw;
+  a.weights = weights;
+  a.gy = gy;
+  a.errs = errs;
+  a.n = n;
+  a.K = (int)(n / sps);
+  a.sps = sps;
+  a.log2L = 0;
+  while ((int64_t(1) << a.log2L) < L) ++a.log2L;
+  a.rolloff = rolloff;
+  const size_t smem = sizeof(float2) * ((size_t)L + L / 16 + 1 + L / 2 + (C > 1 ? (size_t)n / 64 + 64 : 0) + 1) +
+                      sizeof(double) * (32 * 4 + 4);
+  void (*kern)(const ldbp::RxExactArgs) = C == 1 ? ldbp::rx_exact_kernel<1>
+                                          : C == 2 ? ldbp::rx_exact_kernel<2> : ldbp::rx_exact_kernel<4>;
+  cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(B * C));
+  cfg.blockDim = dim3(ldbp::kSsfmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = C > 1 ? 1 : 0;
+  cudaError_t e;
+  {
+    TraceScope ts(LDBP_K_RX, 0, B * n, st);
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+  }
+  if (e != cudaSuccess) return fail(LDBP_ECUDA, "rx_exact_kernel launch: %s", cudaGetErrorString(e));
+  return cuda_check("rx_exact_kernel launch");
+}
+
+int ldbp_rx_exact_loss_grad(int64_t batch, int64_t n, int32_t sps, float rolloff, const void* y, const void* symbols,
+                            const float* power_w, const float* weights_or_null, double* errs, void* gy_or_null,
+                            void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_rx_exact(batch, n, sps, rolloff));
+  if (batch == 0) return LDBP_OK;
+  LDBP_TRY(check_ptr(y, "y", 8));
+  LDBP_TRY(check_ptr(symbols, "symbols", 8));
+  LDBP_TRY(check_ptr(power_w, "power_w", 4));
+  LDBP_TRY(check_ptr(errs, "errs", 8));
+  if (weights_or_null) LDBP_TRY(check_ptr(weights_or_null, "weights", 4));
+  if (gy_or_null) {
+    LDBP_TRY(check_ptr(gy_or_null, "gy", 8));
+    if (gy_or_null == y) return fail(LDBP_EINVAL, "gy aliases y");
+  }
+  return launch_rx_exact(batch, n, sps, rolloff, (const float2*)y, (const float2*)symbols, power_w, weights_or_null,
+                         errs, (float2*)gy_or_null, (cudaStream_t)cuda_stream);
+}
+
+struct RxExTrainWs {
+  bool store_all = false;
+  size_t y_off = 0, gy_off = 0, errs_off = 0, pp_off = 0, total = 0;
+};
+static RxExTrainWs rx_exact_train_ws(const ldbp_dims* d, bool query) {
+  RxExTrainWs w;
+  w.store_all = use_store_all(d);
+  size_t off = 0;
+  if (w.store_all) {
+    off = rev_ws(d, plan_rev(d, query)).total;
+  } else {
+    off = bwd_ws(d, plan_bwd(d, query)).total;
+    w.pp_off = off;
+    off += align256(fwd_ws(d).total);
+  }
+  const size_t blk = align256(sizeof(float2) * (size_t)d->batch * d->n);
+  w.y_off = off;
+  off += blk;
+  w.gy_off = off;
+  off += blk;
+  w.errs_off = off;
+  off += align256(sizeof(double) * (size_t)d->batch);
+  w.total = off;
+  return w;
+}
+
+int ldbp_rx_exact_train_workspace_bytes(const ldbp_dims* d, int32_t sps, size_t* bytes) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  LDBP_TRY(validate_rx_exact(d->batch, d->n, sps, 0.1f));
+  if (!bytes) return fail(LDBP_EINVAL, "bytes is NULL");
+  *bytes = d->batch == 0 ? 0 : rx_exact_train_ws(d, true).total;
+  return LDBP_OK;
+}
+
+int ldbp_rx_exact_train_grad(const ldbp_dims* d, const void* x, const void* symbols, const float* power_w,
+                             const float* weights_or_null, int32_t sps, float rolloff, const void* taps,
+                             const float* gamma, const uint8_t* mask, double* buf, void* ws, size_t ws_bytes,
+                             void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_dims(d));
+  LDBP_TRY(validate_rx_exact(d->batch, d->n, sps, rolloff));
+  LDBP_TRY(check_ptr(buf, "buf", 8));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (d->batch == 0) return zero_outputs(buf, (size_t)1 + d->steps + 2 * (size_t)d->steps * d->taps, st);
+  LDBP_TRY(check_ptr(x, "x", 8));
+  LDBP_TRY(check_ptr(symbols, "symbols", 8));
+  LDBP_TRY(check_ptr(power_w, "power_w", 4));
+  if (weights_or_null) LDBP_TRY(check_ptr(weights_or_null, "weights", 4));
+  LDBP_TRY(check_ptr(taps, "taps", 8));
+  LDBP_TRY(check_ptr(gamma, "gamma", 4));
+  const RxExTrainWs w = rx_exact_train_ws(d, true);
+  if (!ws || ws_bytes < w.total)
+    return fail(LDBP_EWORKSPACE, "rx_exact_train_grad needs %zu workspace bytes, got %zu", w.total, ws_bytes);
+  LDBP_TRY(check_ptr(ws, "ws", 16));
+  unsigned char* wb = (unsigned char*)ws;
+  float2* ybuf = reinterpret_cast<float2*>(wb + w.y_off);
+  float2* gybuf = reinterpret_cast<float2*>(wb + w.gy_off);
+  double* errs = reinterpret_cast<double*>(wb + w.errs_off);
+  if (w.store_all) {
+    const RevPlan rp = plan_rev(d, true);
+    const RevWs rw = rev_ws(d, rp);
+    FiniteCheck fc(d, ws, rw.total, st);
+    LDBP_TRY(fc.finish(run_rev_chain(d, (const float2*)x, nullptr, nullptr, (const float2*)taps, gamma, mask, nullptr,
+                                     wb, rp, rw, st, nullptr, nullptr, nullptr, ybuf, /*forward_only=*/true),
+                       st));
+    LDBP_TRY(launch_rx_exact(d->batch, d->n, sps, rolloff, ybuf, (const float2*)symbols, power_w, weights_or_null,
+                             errs, gybuf, st));
+    LDBP_TRY(run_rev_chain(d, (const float2*)x, gybuf, nullptr, (const float2*)taps, gamma, mask, nullptr, wb, rp, rw,
+                           st, buf, nullptr, nullptr, nullptr, false, /*skip_forward=*/true));
+  } else {
+    const BwdPlan bp = plan_bwd(d, true);
+    const BwdWs bw = bwd_ws(d, bp);
+    LDBP_TRY(run_forward_chain(d, (const float2*)x, ybuf, (const float2*)taps, gamma, mask,
+                               reinterpret_cast<float2*>(wb + w.pp_off), st));
+    LDBP_TRY(launch_rx_exact(d->batch, d->n, sps, rolloff, ybuf, (const float2*)symbols, power_w, weights_or_null,
+                             errs, gybuf, st));
+    LDBP_TRY(run_backward_chain(d, (const float2*)x, gybuf, nullptr, (const float2*)taps, gamma, mask, nullptr, wb, bp,
+                                bw, st, buf, nullptr, nullptr));
+  }
+  ldbp::rx_wsum_kernel<<<1, 32, 0, st>>>(errs, weights_or_null, d->batch, buf);  // buf[0] = sum_b w_b errs_b
+  return cuda_check("rx_wsum_kernel launch");
 }
 
 int ldbp_essm_workspace_bytes(const ldbp_dims* d, int32_t kappa, int op, size_t* bytes) {

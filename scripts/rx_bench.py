@@ -65,3 +65,9 @@ print(f"rx loss+grad alone: {t_rx:.3f} ms  ({lane_ops / (t_rx * 1e-3) / (148 * 1
       f"launches {[(k, round(ms, 3)) for k, _, _, ms in tr.records]})")
 print(f"waveform-MSE train grad: {t_mse:.3f} ms ({ss / t_mse / 1e6:.1f} Gss/s)")
 print(f"receiver-chain train grad: {t_rxt:.3f} ms ({ss / t_rxt / 1e6:.1f} Gss/s)")
+t_rxe = timed(lambda: P.ldbp_rx_exact_loss_grad(x, sym, pw, sps=sps))
+t_rxet = timed(lambda: P.ldbp_rx_exact_train_grad(x, sym, pw, ht, gt, sps=sps, ws=ws))
+# 4 FFTs of n points per block (5 n log2 n flops each): MF forward + inverse, adjoint forward + inverse
+fft_flops = 4 * 5 * n * np.log2(n) * B
+print(f"exact circulant MF loss+grad alone: {t_rxe:.3f} ms ({fft_flops / (t_rxe * 1e-3) / 1e12:.2f} TFLOP/s of FFT work)")
+print(f"receiver-chain train grad, exact MF: {t_rxet:.3f} ms ({ss / t_rxet / 1e6:.1f} Gss/s)")

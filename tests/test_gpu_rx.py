@@ -91,3 +91,58 @@ def test_rx_train_grad_parity(P, monkeypatch, mode):
     dt = dt[..., 0] + 1j * dt[..., 1]
     for i in range(M):
         assert rel(dt[i], rdt[i]) <= 1e-4, i
+
+
+# ---- exact circulant matched filter (Eq. (12) as written: M is the circulant, no truncation) ----
+@pytest.mark.parametrize("B,K,sps,weighted", [
+    (3, 512, 2, False),     # one CTA per block
+    (2, 8192, 2, True),     # n = 2^14 (C3 block), per-block weights
+    (2, 16384, 2, False),   # n = 2^15 (C5 block): 2-CTA cluster
+    (2, 1024, 4, True),     # sps = 4
+    (2, 4096, 1, False),    # sps = 1
+])
+def test_rx_exact_loss_grad_parity(P, B, K, sps, weighted):
+    s, pw, y = link(13, B, K, sps)
+    w = np.linspace(0.5, 2.0, B) if weighted else None
+    errs, gy = P.ldbp_rx_exact_loss_grad(dev(y), dev(s), dev(pw, np.float32), sps=sps,
+                                         weights=None if w is None else dev(w, np.float32))
+    errs, gy = errs.cpu().numpy(), gy.cpu().numpy()
+    re, rgy = receiver.rx_loss_grad_exact(r32(y), r32(s), r32(pw), sps,
+                                          weights=None if w is None else r32(w))
+    for b in range(B):
+        assert abs(errs[b] - re[b]) <= 1e-5 * re[b], (b, errs[b], re[b])
+        assert rel(gy[b], rgy[b]) <= 1e-4, (b, rel(gy[b], rgy[b]))
+    e2, g2 = P.ldbp_rx_exact_loss_grad(dev(y), dev(s), dev(pw, np.float32), sps=sps, need_grad=False)
+    assert g2 is None and np.allclose(e2.cpu().numpy(), errs, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_rx_exact_train_grad_parity(P, monkeypatch, mode):
+    """Exact receiver-chain loss through LDBP vs the oracle chain (forward, exact MF loss and its
+    gradient, adjoint), both activation schedules, with per-block weights."""
+    monkeypatch.setenv("LDBP_BWD_MODE", mode)
+    monkeypatch.setenv("LDBP_STORE_ALL_MIN_SAMPLES", "0")
+    B, K, sps, M, T = 3, 2048, 2, 6, 5
+    s, pw, x = link(14, B, K, sps, snr_noise=0.02)
+    w = np.array([1.0, 0.5, 2.0])
+    taps = li.random_sym_taps(14, M, T, 0.05)
+    gamma = li.random_gamma(14, M, -3.0, -1.0)
+    buf = P.ldbp_rx_exact_train_grad(dev(x), dev(s), dev(pw, np.float32), dev(taps), dev(gamma, np.float32),
+                                     sps=sps, weights=dev(w, np.float32)).cpu().numpy()
+    yo = O.forward(r32(x), r32(taps), r32(gamma))
+    errs, gyo = receiver.rx_loss_grad_exact(yo, r32(s), r32(pw), sps, weights=r32(w))
+    rdt, rdg, _ = O.backward(r32(x), gyo, r32(taps), r32(gamma))
+    rdt = O.sym_fold(rdt)
+    L = float(np.sum(r32(w) * errs))
+    assert abs(buf[0] - L) <= 1e-5 * L
+    # dgamma'_i per step.  The last step's sum_t Im(gy_t conj(y_t)) |y_t|^2 cancels strongly (the
+    # loss is stationary in the global phase at the genie phi, P:772-775), so it is checked against
+    # the magnitude of its terms; every other step against its own value.
+    cancel = np.sum(np.abs(np.imag(gyo * np.conj(yo)) * np.abs(yo) ** 2))
+    for i in range(M):
+        scale = abs(rdg[i]) if i < M - 1 else max(abs(rdg[i]), cancel)
+        assert abs(buf[1 + i] - rdg[i]) <= 1e-4 * scale, (i, buf[1 + i], rdg[i], scale)
+    dt = buf[1 + M:].reshape(M, T, 2)
+    dt = dt[..., 0] + 1j * dt[..., 1]
+    for i in range(M):
+        assert rel(dt[i], rdt[i]) <= 1e-4, i

@@ -176,3 +176,69 @@ def test_rx_loss_gradient_finite_differences():
             fd = (receiver.rx_loss(yp, s, P, h, sps)[0].sum() - receiver.rx_loss(ym, s, P, h, sps)[0].sum()) / (2 * eps)
             an = gy[b, t].real if u == 1.0 else gy[b, t].imag
             assert abs(fd - an) <= 1e-6 * scale
+
+
+# ---- exact circulant matched filter (NEXT-1, Eq. (12)) ----
+def test_exact_mf_recovers_symbols_and_is_zero_loss():
+    """Nyquist pin (P11): modulate -> exact circulant MF -> downsample returns s exactly, so the
+    receiver-chain loss of the transmitted waveform itself is 0 (any power, any phase)."""
+    from oracle import receiver
+
+    s = li.qam16(li.rng(81, 0, "symbols"), 512)
+    for sps in (2, 4):
+        x = channel.modulate(s, sps, 2e-3) * np.exp(0.7j)
+        errs, gy = receiver.rx_loss_grad_exact(x, s, [2e-3], sps)
+        assert errs[0] < 1e-20 * len(s)
+        assert np.max(np.abs(gy)) < 1e-9
+
+
+def test_exact_mf_adjoint_identity():
+    """Re<M y, g> = Re<y, M^T g> for random y, g (the adjoint used by the gradient)."""
+    from oracle import receiver
+
+    g0 = np.random.default_rng(3)
+    for n, sps in ((1024, 2), (512, 4), (96, 1)):
+        y = g0.standard_normal(n) + 1j * g0.standard_normal(n)
+        g = g0.standard_normal(n // sps) + 1j * g0.standard_normal(n // sps)
+        lhs = np.real(np.vdot(g, receiver.mf_exact(y, sps)))
+        rhs = np.real(np.vdot(receiver.mf_exact_adjoint(g, sps, n), y))
+        assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+
+
+def test_exact_rx_loss_finite_differences_and_weights():
+    """Central finite differences of L = sum_b w_b errs_b w.r.t. Re / Im of sampled y entries
+    match dL/dy (gradient convention dL/dRe + j dL/dIm), including the genie-phase path."""
+    from oracle import receiver
+
+    B, nsym, sps = 2, 64, 2
+    s = np.stack([li.qam16(li.rng(82, b, "symbols"), nsym) for b in range(B)])
+    y = np.stack([channel.modulate(s[b], sps, 1e-3) for b in range(B)])
+    y = y + 1e-3 * (li.cn(li.rng(82, 9, "ase"), y.shape))  # noisy: non-zero loss and gradient
+    pw, w = [1e-3, 1e-3], np.array([0.7, 1.9])
+    errs, gy = receiver.rx_loss_grad_exact(y, s, pw, sps, weights=w)
+    L = lambda yy: float(np.sum(w * receiver.rx_loss_grad_exact(yy, s, pw, sps)[0]))  # noqa: E731
+    h = 1e-8
+    for b, t in ((0, 3), (1, 50), (0, 127)):
+        for unit in (1.0, 1j):
+            yp, ym = y.copy(), y.copy()
+            yp[b, t] += h * unit
+            ym[b, t] -= h * unit
+            fd = (L(yp) - L(ym)) / (2 * h)
+            an = gy[b, t].real if unit == 1.0 else gy[b, t].imag
+            assert abs(fd - an) <= 1e-5 * np.max(np.abs(gy)) + 1e-6 * abs(an), (b, t, unit, fd, an)
+    # weights scale each block's gradient, not its (unweighted) error
+    errs1, gy1 = receiver.rx_loss_grad_exact(y, s, pw, sps)
+    np.testing.assert_allclose(errs, errs1, rtol=1e-14)
+    np.testing.assert_allclose(gy[1], w[1] * gy1[1], rtol=1e-12, atol=1e-18)
+
+
+def test_truncated_fir_converges_to_exact_mf():
+    """The round-1 truncated FIR (reading G19) approaches the exact circulant as its span grows."""
+    from oracle import receiver
+
+    s = li.qam16(li.rng(83, 0, "symbols"), 2048)
+    y = channel.modulate(s, 2, 1.0) + 0.1 * li.cn(li.rng(83, 1, "ase"), 4096)
+    ex = receiver.mf_exact(y, 2)
+    errs = [np.max(np.abs(receiver.mf_fir_downsample(y, receiver.rrc_fir_taps(2, span_symbols=sp), 2) - ex))
+            for sp in (8, 32, 256)]
+    assert errs[0] > errs[1] > errs[2]
