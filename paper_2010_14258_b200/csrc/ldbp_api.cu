@@ -110,6 +110,7 @@ constexpr int kRxMaxSpsExact = 4;
   BwdFn ldbp_get_bwd_##K(bool sym, bool fast);      \
   RevFn ldbp_get_rev_##K(bool sym, bool fast);      \
   RevFn ldbp_get_rev2_##K(bool fast);               \
+  RevFn ldbp_get_rev3_##K(bool fast);               \
   ParFn ldbp_get_params_##K(bool sym);
 }  // namespace
 LDBP_DECL_GETTERS(0)
@@ -187,6 +188,15 @@ RevFn get_rev2(int kh, bool fast) {
     case 5: return ldbp_get_rev2_5(fast);
     case 6: return ldbp_get_rev2_6(fast);
     case 7: return ldbp_get_rev2_7(fast);
+  }
+  return nullptr;
+}
+
+RevFn get_rev3(int kh, bool fast) {
+  switch (kh) {
+    case 2: return ldbp_get_rev3_2(fast);
+    case 4: return ldbp_get_rev3_4(fast);
+    case 6: return ldbp_get_rev3_6(fast);
   }
   return nullptr;
 }
@@ -419,8 +429,20 @@ int rev_occupancy(RevFn fn, int nthreads, size_t smem) {
 // stalls), and barrier-free 1-warp tiles pay 19-25 % halo recompute.  LDBP_REV2=1 selects it.
 bool use_rev2(const ldbp_dims* d) { return (d->flags & LDBP_SYMMETRIC) && env_int("LDBP_REV2", 0) != 0; }
 
+// The skewed one-sided reverse (ldbp_reverse3.cuh; symmetric taps, even Kh so the shifted windows
+// stay 16-byte aligned) is OFF by default: parity-green but measured slower (C3 reverse 2.82 ms vs
+// 1.95 ms): the one-way dependencies removed most barrier waiting (barrier + sleep stalls 8 %), but
+// the shifted register windows cost 25 % register moves and the larger loop body 28 % instruction-
+// fetch stalls.  LDBP_REV3=1 selects it.
+bool use_rev3(const ldbp_dims* d) {
+  const int kh = (d->taps - 1) / 2;
+  return (d->flags & LDBP_SYMMETRIC) && (kh == 2 || kh == 4 || kh == 6) && !use_rev2(d) &&
+         env_int("LDBP_REV3", 0) != 0;
+}
+
 size_t rev_smem_any(const ldbp_dims* d, int steps) {
   const int kh = (d->taps - 1) / 2;
+  if (use_rev3(d)) return ldbp::rev3_smem_bytes(kh, steps, d->steps);
   return use_rev2(d) ? ldbp::rev2_smem_bytes(kh, steps, d->steps)
                      : rev_smem(kh, d->flags & LDBP_SYMMETRIC, steps, d->steps);
 }
@@ -428,6 +450,7 @@ size_t rev_smem_any(const ldbp_dims* d, int steps) {
 RevFn get_rev_any(const ldbp_dims* d) {
   const int kh = (d->taps - 1) / 2;
   const bool fast = !(d->flags & LDBP_PRECISE);
+  if (use_rev3(d)) return get_rev3(kh, fast);
   return use_rev2(d) ? get_rev2(kh, fast) : get_rev(kh, d->flags & LDBP_SYMMETRIC, fast);
 }
 
@@ -435,12 +458,13 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
   RevPlan p;
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
-  const bool v2 = use_rev2(d);
+  const bool v2 = use_rev2(d), v3 = use_rev3(d);
   const int M = d->steps;
-  const int R = v2 ? ldbp::rev2_r(kh) : rev_r(kh);
+  const int R = v2 ? ldbp::rev2_r(kh) : v3 ? ldbp::rev3_r(kh) : rev_r(kh);
   // window slots per CTA (rev2: 30 owned lanes per warp + the two duplicate end lanes)
-  const int slots = v2 ? ldbp::rev2_slots(ldbp::rev2_warps(kh)) : ldbp::rev_threads(kh);
-  const int nthr = v2 ? 32 * ldbp::rev2_warps(kh) : ldbp::rev_threads(kh);
+  const int slots = v2 ? ldbp::rev2_slots(ldbp::rev2_warps(kh)) : v3 ? 32 * ldbp::rev3_warps(kh)
+                                                                      : ldbp::rev_threads(kh);
+  const int nthr = v2 ? 32 * ldbp::rev2_warps(kh) : v3 ? 32 * ldbp::rev3_warps(kh) : ldbp::rev_threads(kh);
   p.V = 1 + 2 * ntaps_used(kh, sym);
   // cost model in step units: a launch of S steps costs S * window / (window - 2*H) plus a
   // fixed ~2 steps (prologue: staging, first load, seed), H = S*kh rounded up to whole slots;

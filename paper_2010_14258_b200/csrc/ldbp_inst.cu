@@ -51,3 +51,13 @@ RevFn LDBP_CAT(ldbp_get_rev2_, LDBP_KH)(bool fast) {
   constexpr int K = LDBP_KH;
   return fast ? ldbp::rev2_tile_kernel<K, true> : ldbp::rev2_tile_kernel<K, false>;
 }
+
+RevFn LDBP_CAT(ldbp_get_rev3_, LDBP_KH)(bool fast) {
+#if LDBP_KH == 2 || LDBP_KH == 4 || LDBP_KH == 6
+  constexpr int K = LDBP_KH;
+  return fast ? ldbp::rev3_tile_kernel<K, true> : ldbp::rev3_tile_kernel<K, false>;
+#else
+  (void)fast;
+  return nullptr;
+#endif
+}

@@ -634,3 +634,4 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * re
 
 }  // namespace ldbp
 #include "ldbp_reverse2.cuh"
+#include "ldbp_reverse3.cuh"
