@@ -524,6 +524,9 @@ def main():
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: a functional dry run of the N > 1 path when fewer GPUs than ranks exist "
+                         "(ranks share a device; the timings are then not scaling numbers)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -536,6 +539,7 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (libldbp has no CPU path)")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -543,7 +547,10 @@ def main():
         # communicator lines (ranks, NVLS/P2P transport) on stderr for the driver's rank check
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     import __graft_entry__
 
     if rank == 0:
@@ -585,6 +592,7 @@ def main():
             "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
             "scaling": r["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "dist_backend": args.dist_backend if world > 1 else None,
             "extra": extra,
             "config": {"workload": WORKLOAD[args.config], "config": args.config, "blocks_per_gpu": r["B"],
                        "global_blocks": r["global_blocks"], "n": r["n"], "steps_M": r["M"], "taps_T": r["T"],
