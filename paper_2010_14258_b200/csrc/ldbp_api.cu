@@ -903,6 +903,108 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
 }
 
 // ---------------------------------------------------------------------------------------
+// Overlapped store-all training step (loss_grad): the batch is cut into K chunks of whole blocks;
+// the storing forwards run on a side stream and the reverse of chunk c starts as soon as forward
+// c has finished, so the HBM-bound storing forward of chunk c + 1 runs concurrently with the
+// latency-bound reverse of chunk c (CTAs of both kernels share the SMs).  Each chunk keeps its own
+// workspace region and gradient buffer; a final fixed-order sum gives buf (deterministic).
+// ---------------------------------------------------------------------------------------
+struct OverlapPlan {
+  int K = 1;          // chunks
+  int64_t Bc = 0;     // blocks per chunk (last one may be shorter)
+  size_t chunk_off[16] = {};
+  size_t bufs_off = 0, buf_stride = 0, total = 0;
+};
+
+ldbp_dims chunk_dims(const ldbp_dims* d, const OverlapPlan& o, int c) {
+  ldbp_dims dc = *d;
+  const int64_t b0 = (int64_t)c * o.Bc;
+  dc.batch = std::min(d->batch, b0 + o.Bc) - b0;
+  return dc;
+}
+
+OverlapPlan plan_overlap(const ldbp_dims* d, bool query) {
+  OverlapPlan o;
+  // default 1 (no overlap): measured, the overlapped schedule is not faster (C3 2.73 ms at K = 1,
+  // 3.02 at 2, 3.34 at 4; C5 23.2 / 23.2 / 23.7 ms): the storing forward and the reverse slow each
+  // other down as much as they overlap, and each chunk adds prologues and a partial last wave
+  int K = env_int("LDBP_OVERLAP", 1);
+  if (d->flags & LDBP_CHECK_FINITE) K = 1;
+  K = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)K, d->batch, 16}));
+  o.K = K;
+  o.Bc = cdiv(d->batch, K);
+  o.K = (int)cdiv(d->batch, o.Bc);
+  size_t off = 0;
+  for (int c = 0; c < o.K; ++c) {
+    const ldbp_dims dc = chunk_dims(d, o, c);
+    o.chunk_off[c] = off;
+    off += align256(rev_ws(&dc, plan_rev(&dc, query)).total);
+  }
+  o.buf_stride = 1 + (size_t)d->steps + 2 * (size_t)d->steps * d->taps;
+  o.bufs_off = off;
+  off += align256(sizeof(double) * o.buf_stride * o.K);
+  o.total = off;
+  return o;
+}
+
+// Per-thread, per-device side stream and fork / join events (created on first use).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[17] = {};
+};
+thread_local SideStream g_side[16];
+
+int side_stream(SideStream** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return fail(LDBP_ECUDA, "cudaGetDevice");
+  SideStream& ss = g_side[dev];
+  if (!ss.s) {
+    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(LDBP_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(cudaGetLastError()));
+    for (auto& e : ss.ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+        return fail(LDBP_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  *out = &ss;
+  return LDBP_OK;
+}
+
+int run_overlapped(const ldbp_dims* d, const OverlapPlan& o, const float2* x, const float2* target,
+                   const float2* taps, const float* gamma, const uint8_t* mask, unsigned char* ws, cudaStream_t st,
+                   double* buf) {
+  SideStream* ss = nullptr;
+  LDBP_TRY(side_stream(&ss));
+  double* bufs = reinterpret_cast<double*>(ws + o.bufs_off);
+  if (cudaEventRecord(ss->ev[16], st) != cudaSuccess || cudaStreamWaitEvent(ss->s, ss->ev[16], 0) != cudaSuccess)
+    return fail(LDBP_ECUDA, "fork: %s", cudaGetErrorString(cudaGetLastError()));
+  for (int c = 0; c < o.K; ++c) {  // storing forwards, side stream
+    const ldbp_dims dc = chunk_dims(d, o, c);
+    const int64_t off = (int64_t)c * o.Bc * d->n;
+    const RevPlan rp = plan_rev(&dc, true);
+    const RevWs rw = rev_ws(&dc, rp);
+    LDBP_TRY(run_rev_chain(&dc, x + off, nullptr, target + off, taps, gamma, mask, nullptr, ws + o.chunk_off[c], rp,
+                           rw, ss->s, nullptr, nullptr, nullptr, nullptr, /*forward_only=*/true));
+    if (cudaEventRecord(ss->ev[c], ss->s) != cudaSuccess) return fail(LDBP_ECUDA, "cudaEventRecord");
+  }
+  for (int c = 0; c < o.K; ++c) {  // reverses, caller's stream, each after its forward
+    const ldbp_dims dc = chunk_dims(d, o, c);
+    const int64_t off = (int64_t)c * o.Bc * d->n;
+    const RevPlan rp = plan_rev(&dc, true);
+    const RevWs rw = rev_ws(&dc, rp);
+    if (cudaStreamWaitEvent(st, ss->ev[c], 0) != cudaSuccess) return fail(LDBP_ECUDA, "cudaStreamWaitEvent");
+    LDBP_TRY(run_rev_chain(&dc, x + off, nullptr, target + off, taps, gamma, mask, nullptr, ws + o.chunk_off[c], rp,
+                           rw, st, bufs + (size_t)c * o.buf_stride, nullptr, nullptr, nullptr, false,
+                           /*skip_forward=*/true));
+  }
+  {
+    TraceScope ts(LDBP_K_REDUCE, d->steps, 0, st);
+    ldbp::sum_bufs_kernel<<<(unsigned)cdiv((int64_t)o.buf_stride, 256), 256, 0, st>>>(
+        bufs, (int64_t)o.buf_stride, o.K, (int)o.buf_stride, buf);
+  }
+  return cuda_check("sum_bufs_kernel launch");
+}
+
+// ---------------------------------------------------------------------------------------
 // Receiver-chain symbol loss (§8(f) NEXT-1), ldbp_rx.cuh
 // ---------------------------------------------------------------------------------------
 struct RxWs {
@@ -1114,7 +1216,9 @@ int ldbp_workspace_bytes(const ldbp_dims* d, int op, size_t* bytes) {
     case LDBP_OP_LOSS_GRAD:
     case LDBP_OP_TRAIN_STEP: {
       if (use_store_all(d)) {
-        *bytes = rev_ws(d, plan_rev(d, true)).total;
+        const size_t single = rev_ws(d, plan_rev(d, true)).total;
+        // loss_grad / train_step may run the overlapped chunked schedule (its own layout)
+        *bytes = op == LDBP_OP_BACKWARD ? single : std::max(single, plan_overlap(d, true).total);
         return LDBP_OK;
       }
       BwdPlan p = plan_bwd(d, true);
@@ -1132,9 +1236,22 @@ int ldbp_launch_count(const ldbp_dims* d, int op, int* launches) {
   if (d->batch == 0) { *launches = (op == LDBP_OP_FORWARD) ? 0 : 1; return LDBP_OK; }
   if (op == LDBP_OP_FORWARD) { *launches = plan_fwd_segments(d->steps, (d->taps - 1) / 2).segs; return LDBP_OK; }
   if (use_store_all(d)) {
-    const RevPlan rp = plan_rev(d, true);
-    int n = 1 /* params_kernel */ + plan_fwd_segments(d->steps, (d->taps - 1) / 2, kFwdR).segs + rp.Kr + 1 +
-            (reduce_chunks(rp.tile.grid) > 0 ? 1 : 0);
+    const OverlapPlan o = plan_overlap(d, true);
+    auto chain = [&](const ldbp_dims* dc, bool two_params) {
+      const RevPlan rp = plan_rev(dc, true);
+      return (two_params ? 2 : 1) /* params_kernel */ + plan_fwd_segments(dc->steps, (dc->taps - 1) / 2, kFwdR).segs +
+             rp.Kr + 1 + (reduce_chunks(rp.tile.grid) > 0 ? 1 : 0);
+    };
+    int n = 0;
+    if (op != LDBP_OP_BACKWARD && o.K > 1) {
+      for (int c = 0; c < o.K; ++c) {
+        const ldbp_dims dc = chunk_dims(d, o, c);
+        n += chain(&dc, true);
+      }
+      n += 1;  // sum_bufs_kernel
+    } else {
+      n = chain(d, false);
+    }
     if (op == LDBP_OP_TRAIN_STEP) n += 1;
     *launches = n;
     return LDBP_OK;
@@ -1223,6 +1340,14 @@ int ldbp_loss_grad(const ldbp_dims* d, const void* x, const void* target, const 
   LDBP_TRY(check_ptr(taps, "taps", 8));
   LDBP_TRY(check_ptr(gamma, "gamma", 4));
   if (use_store_all(d)) {
+    const OverlapPlan o = plan_overlap(d, true);
+    if (o.K > 1) {
+      if (!ws || ws_bytes < o.total)
+        return fail(LDBP_EWORKSPACE, "loss_grad needs %zu workspace bytes, got %zu", o.total, ws_bytes);
+      LDBP_TRY(check_ptr(ws, "ws", 16));
+      return run_overlapped(d, o, (const float2*)x, (const float2*)target, (const float2*)taps, gamma, mask,
+                            (unsigned char*)ws, st, buf);
+    }
     const RevPlan rp = plan_rev(d, true);
     const RevWs rw = rev_ws(d, rp);
     if (!ws || ws_bytes < rw.total)

@@ -1878,6 +1878,14 @@ __global__ void adam_kernel(const AdamArgs a) {
   }
 }
 
+// buf[i] = sum_c bufs[c * stride + i], c = 0..K-1 in order (chunked training step, deterministic).
+__global__ void sum_bufs_kernel(const double* __restrict__ bufs, int64_t stride, int K, int len, double* buf) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int c = 0; c < K; ++c) t += bufs[(int64_t)c * stride + i];
+    buf[i] = t;
+  }
+}
 #endif  // LDBP_AUX_KERNELS
 
 }  // namespace ldbp

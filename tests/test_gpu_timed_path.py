@@ -63,12 +63,15 @@ def ls_model(spans, sps, T):
     return taps, g
 
 
-@pytest.mark.parametrize("name,B,n,spans,sps,T,kr", [
-    ("C3", 512, 16384, 25, 2, 9, 2),
-    ("C5-slice", 512, 32768, 25, 1, 3, 1),
+@pytest.mark.parametrize("name,B,n,spans,sps,T,kr,overlap", [
+    ("C3", 512, 16384, 25, 2, 9, 2, 1),        # exactly the call bench.py times
+    ("C3", 512, 16384, 25, 2, 9, 2, 4),        # the optional overlapped chunked schedule (LDBP_OVERLAP)
+    ("C5-slice", 512, 32768, 25, 1, 3, 1, 1),  # > 1024 reverse CTAs: reduce_partials_pass1 runs
 ])
-def test_timed_training_call_vs_oracle_all_blocks(P, name, B, n, spans, sps, T, kr):
+def test_timed_training_call_vs_oracle_all_blocks(P, monkeypatch, name, B, n, spans, sps, T, kr, overlap):
     from paper_2010_14258_b200 import channel
+
+    monkeypatch.setenv("LDBP_OVERLAP", str(overlap))
 
     idx = 3 if name == "C3" else 5
     # the bench's inputs: GPU SSFM link blocks (pool of 256 simulated blocks, shifted / rotated)
@@ -83,11 +86,16 @@ def test_timed_training_call_vs_oracle_all_blocks(P, name, B, n, spans, sps, T, 
         buf = P.ldbp_loss_grad(x, tgt, st.taps, st.gamma, ws=ws)
         torch.cuda.synchronize()
     kinds = [r[0] for r in tr.records]
-    # the store-all schedule: params + storing forward, Kr reverse launches, two-level reduction
-    assert kinds.count(K_REVERSE) == kr, kinds
-    assert kinds.count(K_FORWARD) >= 1, kinds
-    assert kinds.count(K_REDUCE) == 3, kinds  # params_kernel, reduce_partials_pass1, reduce_partials_kernel
-    assert sum(r[1] for r in tr.records if r[0] == K_REVERSE) == M
+    # the store-all schedule, per chunk (one chain unless overlapped): params + storing forward, Kr
+    # reverse launches, params again when chunked, the two-level fp64 reduction (pass1 + final:
+    # > 1024 CTAs per chain); chunks summed last
+    chunks = kinds.count(K_FORWARD)
+    assert chunks == overlap, kinds
+    assert kinds.count(K_REVERSE) == kr * chunks, kinds
+    per_chunk_reduce = (2 if chunks > 1 else 1) + 2  # params kernel(s), reduce_partials_pass1, final
+    assert kinds.count(K_REDUCE) == per_chunk_reduce * chunks + (1 if chunks > 1 else 0), kinds
+    assert sum(r[1] for r in tr.records if r[0] == K_REVERSE) == M * chunks
+    assert len(tr.records) == P.launch_count(P.make_dims(B, n, M, T), P._lib.OP_LOSS_GRAD)
     b = buf.cpu().numpy()
 
     h64 = st.taps.cpu().numpy().astype(np.complex128)
