@@ -316,9 +316,8 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
         bi = x.numel() * 8 * (2 if train else 1)
         bo = 8 if train else y.numel() * 8
         e2e = {"value": samples_global * M / (e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": bi,
-               "d2h_bytes_per_step": bo, "ms_per_step": e_ms,
-               "pipeline": "inputs of step i+1 copied H2D (pinned, copy stream) during step i; every step's result "
-               "copied D2H (pinned) and read by the host while the next step runs"}
+               "d2h_bytes_per_step": bo, "ms_per_step": round(e_ms, 4),
+               "pipeline": "pinned H2D of step i+1 overlaps step i; result D2H + host read every step"}
 
     # roofline of the dominant kernel (largest total time)
     sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
@@ -334,7 +333,7 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
              _lib.K_REDUCE: "reduce_partials_kernel+params_kernel" if store_all else "reduce_partials_kernel",
              _lib.K_ADAM: "adam_kernel", _lib.K_REVERSE: "rev_tile_kernel"}
     for k, v in per_kind.items():
-        kernel_shares[names[k]] = {"share": v["ms"] / tot_ms, "avg_ms": v["ms"] / v["launches"],
+        kernel_shares[names[k]] = {"share": round(v["ms"] / tot_ms, 4), "avg_ms": round(v["ms"] / v["launches"], 4),
                                    "launches": v["launches"]}
     if dom:
         kind, v = dom
@@ -344,8 +343,7 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
         achieved = per_launch_instr / (avg_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "kernel": names[kind], "achieved": achieved, "peak": peak_tinst,
                 "unit": "Tinst/s (FP32 lane-instructions)", "frac": achieved / peak_tinst,
-                "frac_at_max_clock": achieved / peak_max, "peak_source": "derived: 148 SM x 128 FP32 lanes x "
-                f"{sm_mhz:.0f} MHz (median SM clock during the timed region)",
+                "frac_at_max_clock": achieved / peak_max, "peak_source": f"148 SM x 128 FP32 lanes x {sm_mhz:.0f} MHz",
                 "algorithmic_instr_per_sample_step": ipss, "traffic": traffic_from_profiles(name, names[kind])}
     # whole-step roofline: throughput vs the FP32 bound of the step's algorithmic work
     ips = instr_fwd(kh) + (instr_bwd(kh) if train else 0)
@@ -597,9 +595,8 @@ def main():
             "config": {"workload": WORKLOAD[args.config], "config": args.config, "blocks_per_gpu": r["B"],
                        "global_blocks": r["global_blocks"], "n": r["n"], "steps_M": r["M"], "taps_T": r["T"],
                        "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) between timed steps",
-                       "inputs": "GPU SSFM link (25x80 km SMF, 16-QAM 10.7 GBd, rho_a=4, 50 log StPS, EDFA ASE "
-                                 "Philox-keyed) -> LPF + 2 sps; pool of <=256 blocks shifted/rotated per global block; "
-                                 "P in {-2,-1,0,1} dBm; LS inverse-CD taps (cap 1)"},
+                       "inputs": "GPU SSFM link 25x80 km, 16-QAM, ASE; pool<=256 blocks shifted/rotated; "
+                                 "P in {-2..1} dBm; LS taps"},
             "clocks": r["clk"], "roofline": r["roof"], "step_roofline": r["step_roof"], "cpu_baseline": cpu,
             "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "kernel_shares": r["kernel_shares"],
         }
