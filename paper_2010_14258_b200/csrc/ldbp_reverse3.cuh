@@ -46,34 +46,37 @@ __host__ __device__ constexpr int rev3_regs(int kh) { return kh <= 1 ? 96 : 128;
 // index < 0 from gl (2 Kh left-neighbour samples, gl[2Kh + idx]).
 #define LDBP_WIN3(g, gl, i) ((i) < 0 ? gl[2 * KH + (i)] : g[(i)])
 
-template <int KH, int R, bool FAST, bool NORM, bool NL, int S0, int SE>
-__device__ __forceinline__ void rev3_range(const f2x (&g)[R], const f2x (&gl)[2 * KH], const f2x* __restrict__ ub,
+// Outputs s = S1-1 down to S0 (compile-time) of the shifted window, IN PLACE: output s needs the
+// inputs g[s - 2Kh .. s] only (index < 0: the left halo gl[2Kh + idx]), so in decreasing order
+// every input an output needs is still the old value when it is read, and g[s] can take the new
+// value at once — no second register array and no copy at the end of the step.
+template <int KH, int R, bool FAST, bool NORM, bool NL, int S0, int S1>
+__device__ __forceinline__ void rev3_range(f2x (&g)[R], const f2x (&gl)[2 * KH], const f2x* __restrict__ ub,
                                            const TapP (&hs)[KH + 1], f2x (&A)[KH + 1], f2x (&Bq)[KH + 1],
-                                           f2x (&ng)[R], uint32_t own, float gmn, float& dgam_next) {
-  if constexpr (S0 < SE) {
-    constexpr int s = S0;
+                                           uint32_t own, float gmn, float& dgam_next) {
+  if constexpr (S1 > S0) {
+    constexpr int s = S1 - 1;
     constexpr int c = s - KH;  // centre input index of output s
     const f2x us = ub[s];
     const bool mine = (own >> s) & 1u;
-    const f2x ux = bcast(lof(us)), uy = bcast(hif(us));
+    // ownership by zeroing u in the tap-gradient products (2 selects per sample) instead of
+    // predicated packed FMAs: ptxas turns a predicated FFMA2 into a temp + 2 conditional moves
+    // (measured: 25 % of the instructions were such moves)
+    const f2x ux = bcast(mine ? lof(us) : 0.f), uy = bcast(mine ? hif(us) : 0.f);
     const f2x g0 = LDBP_WIN3(g, gl, c);
     f2x acc = NORM ? g0 : tmul(hs[0], g0);
-    if (mine) {
-      A[0] = fma2(ux, g0, A[0]);
-      Bq[0] = fma2(uy, g0, Bq[0]);
-    }
+    A[0] = fma2(ux, g0, A[0]);
+    Bq[0] = fma2(uy, g0, Bq[0]);
 #pragma unroll
     for (int j = 1; j <= KH; ++j) {
       const f2x P = add2(LDBP_WIN3(g, gl, c - j), LDBP_WIN3(g, gl, c + j));
       acc = tmac(acc, hs[j], P);
-      if (mine) {
-        A[j] = fma2(ux, P, A[j]);
-        Bq[j] = fma2(uy, P, Bq[j]);
-      }
+      A[j] = fma2(ux, P, A[j]);
+      Bq[j] = fma2(uy, P, Bq[j]);
     }
     if constexpr (NL) nl_adjoint<FAST, true>(acc, us, gmn, 2.f * gmn, mine, dgam_next);
-    ng[s] = acc;
-    rev3_range<KH, R, FAST, NORM, NL, S0 + 1, SE>(g, gl, ub, hs, A, Bq, ng, own, gmn, dgam_next);
+    g[s] = acc;
+    rev3_range<KH, R, FAST, NORM, NL, S0, S1 - 1>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
   }
 }
 
@@ -219,22 +222,21 @@ __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring
     const TapP* hs_sm = taps_adj + li * NTU;
 #pragma unroll
     for (int j = 0; j <= KH; ++j) hs[j] = hs_sm[j];
-    f2x A[KH + 1], Bq[KH + 1], ng[R], gl[KE2];
-#pragma unroll
-    for (int j = 0; j <= KH; ++j) A[j] = Bq[j] = 0ull;
-#pragma unroll
-    for (int i = 0; i < KE2; ++i) gl[i] = 0ull;
-    float dgam_next = 0.f;
-    const float gmn = l > s0 ? gam[li - 1] : 0.f;
-    // interior outputs [2 Kh, R): own inputs only
-    if (l > s0)
-      rev3_range<KH, R, FAST, NORM, true, KE2, R>(g, gl, ub, hs, A, Bq, ng, own, gmn, dgam_next);
-    else
-      rev3_range<KH, R, FAST, NORM, false, KE2, R>(g, gl, ub, hs, A, Bq, ng, own, gmn, dgam_next);
-    // left halo: the last 2 Kh inputs of slot p - 1 (lane 0: from warp - 1 through the ring)
+    // left halo first (the neighbour overwrites its tail in place during this step): the last 2 Kh
+    // inputs of slot p - 1 by shuffle; lane 0 of warp w > 0 takes them from the ring below
+    f2x A[KH + 1], Bq[KH + 1], gl[KE2];
 #pragma unroll
     for (int i = 0; i < KE2; ++i) gl[i] = __shfl_up_sync(kFull, g[R - KE2 + i], 1);
-    if (warp > 0) {  // warp-uniform
+#pragma unroll
+    for (int j = 0; j <= KH; ++j) A[j] = Bq[j] = 0ull;
+    float dgam_next = 0.f;
+    const float gmn = l > s0 ? gam[li - 1] : 0.f;
+    // outputs [2 Kh, R) (own inputs only), from the top down
+    if (l > s0)
+      rev3_range<KH, R, FAST, NORM, true, KE2, R>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
+    else
+      rev3_range<KH, R, FAST, NORM, false, KE2, R>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
+    if (warp > 0) {  // warp-uniform: warp w - 1 finished step k - 1 (its lane 31 tail is in the ring)
       const int j = k % D;
       mbar_wait_parity(full + warp * D + j, (k / D) & 1);
       const bool l0 = lane == 0;
@@ -246,12 +248,11 @@ __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring
       __syncwarp();
       if (l0) mbar_arrive(empty + warp * D + j);
     }
+    // outputs [0, 2 Kh): need the left halo
     if (l > s0)
-      rev3_range<KH, R, FAST, NORM, true, 0, KE2>(g, gl, ub, hs, A, Bq, ng, own, gmn, dgam_next);
+      rev3_range<KH, R, FAST, NORM, true, 0, KE2>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
     else
-      rev3_range<KH, R, FAST, NORM, false, 0, KE2>(g, gl, ub, hs, A, Bq, ng, own, gmn, dgam_next);
-#pragma unroll
-    for (int i = 0; i < R; ++i) g[i] = ng[i];
+      rev3_range<KH, R, FAST, NORM, false, 0, KE2>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
     if (l > s0) produce(k + 1);
     {
       float vals[VP];
