@@ -128,6 +128,30 @@ __device__ __forceinline__ uint32_t rev3_own(const Pos3& p, int W, const Geo& g)
   return m & r;
 }
 
+// Steps k (within [0, S)) for which `len` samples starting at p0 - k Kh are consecutive real
+// samples of one block (the window moves left by Kh per step; S Kh <= H keeps it in one block).
+struct KRange {
+  int ka, kb;
+};
+template <int KH>
+__device__ __forceinline__ KRange fast_steps(const Pos3& p0, int len, const Geo& g, int S) {
+  if (p0.b < 0 || p0.b >= g.B || p0.q < g.H) return {1, 0};
+  const int kb = min((p0.q - (int)g.H) / KH, S - 1);  // q - k Kh >= H
+  const int over = p0.q + len - (int)g.H - (int)g.n;  // need q - k Kh + len <= H + n
+  const int ka = over > 0 ? (over + KH - 1) / KH : 0;
+  return {ka, kb};
+}
+// Bits of the R samples at rel (relative to the owned range [0, W)) inside the range.
+template <int R>
+__device__ __forceinline__ uint32_t range_mask(int rel, int W) {
+  constexpr uint32_t FULL = (1u << R) - 1u;
+  if (rel + R <= 0 || rel >= W) return 0u;
+  uint32_t m = FULL;
+  if (rel < 0) m &= FULL << (-rel);
+  if (rel + R > W) m &= FULL >> (rel + R - W);
+  return m;
+}
+
 template <int KH, int R, int NW, bool FAST, bool NORM>
 __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring, uint64_t* bars,
                                           const TapP* taps_adj, const StepNorm* norm, float* red, float* lred,
@@ -150,12 +174,33 @@ __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring
   f2x* nxring = ring + (size_t)(warp + 1) * D * KE2;    // produced by this warp (lane 31) for warp + 1
   Pos3 po = pos3_make(ep - KH, lo, a.g);      // first OUTPUT position of step k (k = 0 now)
 
-  // window copy of u^(i) at the output positions of the step whose first output is at `p`
-  auto window = [&](int i, const Pos3& p, int buf) {
-    const int64_t fo = pos3_fast<R>(p, a.g) ? (int64_t)p.b * a.g.n + (p.q - a.g.H) : -1;
-    async_window<true, R, NT>(rev_src(a, i), lo + p.rel, a.g, ubuf + (size_t)buf * NT * RS, fo);
+  const int S = s1 - s0;
+  // loop-invariant copy / ownership bookkeeping (the windows move left by Kh per step):
+  // the warp's 32 R samples are on the contiguous fast path for steps [wf.ka, wf.kb] (uniform),
+  // this slot's R samples are all real samples for steps [sf.ka, sf.kb]
+  const Pos3 pw0 = {__shfl_sync(kFull, po.rel, 0), __shfl_sync(kFull, po.b, 0), __shfl_sync(kFull, po.q, 0)};
+  const KRange wf = fast_steps<KH>(pw0, 32 * R, a.g, S);
+  const KRange sf = fast_steps<KH>(po, R, a.g, S);
+  const int64_t woff0 = (int64_t)pw0.b * a.g.n + (pw0.q - a.g.H);  // lane 0's element offset at k = 0
+  CoalCopy<R, NT> cc = coal_setup<R, NT>(ubuf, 0);
+  // window copy of u^(i) at the output positions of step k (first output of this slot at p)
+  auto window = [&](int i, int k, const Pos3& p, int buf) {
+    const float2* src = rev_src(a, i);
+    if (k >= wf.ka && k <= wf.kb && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      const char* base = reinterpret_cast<const char*>(reinterpret_cast<const f2x*>(src) + woff0 -
+                                                       (int64_t)k * KH) + 16 * lane;
+      const uint32_t boff = (uint32_t)(buf * NT * RS * 8);
+#pragma unroll
+      for (int m = 0; m < R / 2; ++m)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(cc.dst[m] + boff), "l"(base + 512 * m)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    } else {
+      const int64_t fo = pos3_fast<R>(p, a.g) ? (int64_t)p.b * a.g.n + (p.q - a.g.H) : -1;
+      async_window<true, R, NT>(src, lo + p.rel, a.g, ubuf + (size_t)buf * NT * RS, fo);
+    }
   };
-  window(s1 - 1, po, (s1 - 1) & 1);
+  window(s1 - 1, 0, po, (s1 - 1) & 1);
   // state at k = 0: ga^(s1-1) on the input positions [ep, ep + R)
   f2x v[R], g[R];
   load_window<R>(rev_src(a, s1), ep, a.g, v);
@@ -214,9 +259,9 @@ __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring
     const int k = s1 - 1 - l;
     cp_async_wait_all();
     __syncwarp();
-    const uint32_t own = rev3_own<R>(po, W, a.g);
+    const uint32_t own = (k >= sf.ka && k <= sf.kb) ? range_mask<R>(po.rel, W) : rev3_own<R>(po, W, a.g);
     pos3_left(po, KH, a.g);  // -> first output of step k + 1
-    if (l - 1 >= s0) window(l - 1, po, (l - 1) & 1);
+    if (l - 1 >= s0) window(l - 1, k + 1, po, (l - 1) & 1);
     const f2x* ub = ubuf + (size_t)(l & 1) * NT * RS + (size_t)tid * RS;
     TapP hs[KH + 1];
     const TapP* hs_sm = taps_adj + li * NTU;
@@ -231,11 +276,10 @@ __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring
     for (int j = 0; j <= KH; ++j) A[j] = Bq[j] = 0ull;
     float dgam_next = 0.f;
     const float gmn = l > s0 ? gam[li - 1] : 0.f;
-    // outputs [2 Kh, R) (own inputs only), from the top down
-    if (l > s0)
-      rev3_range<KH, R, FAST, NORM, true, KE2, R>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
-    else
-      rev3_range<KH, R, FAST, NORM, false, KE2, R>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
+    // outputs [2 Kh, R) (own inputs only), from the top down.  One code path for every step: on
+    // the launch's last step gmn = 0 and the fused NL adjoint is an exact identity (sin 0 = 0,
+    // cos 0 = 1; its dgamma' contribution is discarded) — half the loop body (instruction fetch)
+    rev3_range<KH, R, FAST, NORM, true, KE2, R>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
     if (warp > 0) {  // warp-uniform: warp w - 1 finished step k - 1 (its lane 31 tail is in the ring)
       const int j = k % D;
       mbar_wait_parity(full + warp * D + j, (k / D) & 1);
@@ -249,10 +293,7 @@ __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring
       if (l0) mbar_arrive(empty + warp * D + j);
     }
     // outputs [0, 2 Kh): need the left halo
-    if (l > s0)
-      rev3_range<KH, R, FAST, NORM, true, 0, KE2>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
-    else
-      rev3_range<KH, R, FAST, NORM, false, 0, KE2>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
+    rev3_range<KH, R, FAST, NORM, true, 0, KE2>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
     if (l > s0) produce(k + 1);
     {
       float vals[VP];
@@ -296,7 +337,6 @@ __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring
     a.loss_partials[blockIdx.x] = tot;
   }
   constexpr int npairs = 1 + NTU;
-  const int S = s1 - s0;
   for (int i = tid; i < S * npairs; i += NT) {
     const int li = i / npairs, q = i % npairs;
     const int l = s0 + li;
