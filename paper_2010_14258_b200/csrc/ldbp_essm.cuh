@@ -19,7 +19,16 @@
 namespace ldbp {
 
 constexpr int kEssmThreads = 256;
-constexpr int kEssmW = 1024;      // owned samples per CTA
+#ifndef LDBP_ESSM_W
+#define LDBP_ESSM_W 1960  // owned samples per CTA: with the largest halo (A: 2 (Kh + 2 kappa) = 88 at
+                          // kappa = 20, Kh = 4) every filter phase is ONE pass of 256 threads x 8
+                          // outputs (round 1's 1024 left ~half the threads idle in every phase:
+                          // measured 24 % barrier stalls)
+#endif
+#ifndef LDBP_ESSM_QN
+#define LDBP_ESSM_QN 8    // owned samples per thread in the gradient sums (QN x threads >= W)
+#endif
+constexpr int kEssmW = LDBP_ESSM_W;
 constexpr int kEssmMaxKappa = 32;
 constexpr int kEssmMaxT = 15;
 
@@ -61,10 +70,16 @@ __device__ __forceinline__ f2x essm_mac_conj(f2x acc, float2 h, f2x s) {
 // with compile-time register indices (the window is reloaded per block).
 constexpr int kEQ = 8;
 constexpr int kESlack = 16;  // logical slack after every array (blocked reads run past the end)
-__device__ __forceinline__ int pcx(int i) { return i + (i >> 4); }  // f2x arrays
-__device__ __forceinline__ int pfl(int i) { return i + (i >> 5); }  // float arrays
-__host__ __device__ __forceinline__ int essm_pc_size(int n) { return n + (n >> 4) + 1; }
-__host__ __device__ __forceinline__ int essm_pf_size(int n) { return n + (n >> 5) + 1; }
+// Row-padded layouts: rows of 8 elements with one pad element (stride 9).  A thread's run starting
+// at an 8-aligned logical index b then sits at pfl(b) + i + (i >> 3) — one address per run with
+// compile-time offsets (the filter windows below all start 8-aligned: b = o0 + j0), and lanes 8
+// outputs apart land 9 words apart: conflict-free (f2x: 18 words, conflict-free per half-warp).
+// (Round 1 padded per 16 / 32 elements, which needs the full index arithmetic at every access.)
+__device__ __forceinline__ int pcx(int i) { return i + (i >> 3); }  // f2x arrays
+__device__ __forceinline__ int pfl(int i) { return i + (i >> 3); }  // float arrays
+__host__ __device__ __forceinline__ int essm_pc_size(int n) { return n + (n >> 3) + 1; }
+__host__ __device__ __forceinline__ int essm_pf_size(int n) { return n + (n >> 3) + 1; }
+__device__ __forceinline__ constexpr int prow(int i) { return i + (i >> 3); }  // offset within an aligned run
 __host__ __device__ __forceinline__ int essm_nj(int kap) { return ((2 * kap + 1 + 7) / 8) * 8; }
 
 // tt[j] = eta_{k}, k = kap - j (dir = +1: X index o - k = o - kap + j) or k = j - kap (dir = -1:
@@ -83,11 +98,11 @@ __device__ __forceinline__ void essm_rfilt(const float* __restrict__ X, int x0, 
   const int NJ = essm_nj(kap);
 #pragma unroll
   for (int q = 0; q < kEQ; ++q) acc[q] = 0.f;
-  for (int j0 = 0; j0 < NJ; j0 += 8) {
-    const int b = x0 - kap + j0;
+  const float* xb = X + pfl(x0 - kap);  // x0 - kap is 8-aligned for every caller (o0 + kappa - kappa)
+  for (int j0 = 0; j0 < NJ; j0 += 8, xb += 9) {
     float w[kEQ + 7];
 #pragma unroll
-    for (int i = 0; i < kEQ + 7; ++i) w[i] = X[pfl(b + i)];
+    for (int i = 0; i < kEQ + 7; ++i) w[i] = xb[prow(i)];
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const float h = tt[j0 + t];
@@ -102,8 +117,9 @@ template <int KH, bool ADJ>
 __device__ __forceinline__ void essm_cfir(const f2x* __restrict__ In, int x0, const float2* __restrict__ sh_h,
                                           f2x (&acc)[kEQ]) {
   f2x w[kEQ + 2 * KH];
+  const f2x* ib = In + pcx(x0 - KH);  // 8-aligned run start (callers pass x0 = o0 + KH)
 #pragma unroll
-  for (int i = 0; i < kEQ + 2 * KH; ++i) w[i] = In[pcx(x0 - KH + i)];
+  for (int i = 0; i < kEQ + 2 * KH; ++i) w[i] = ib[prow(i)];
 #pragma unroll
   for (int q = 0; q < kEQ; ++q) acc[q] = 0ull;
 #pragma unroll
@@ -285,8 +301,8 @@ __global__ void __launch_bounds__(kEssmThreads) essm_bwd_step_kernel(const EssmA
   __shared__ float lred[kEssmThreads / 32];
   __shared__ float red[kEssmThreads / 32][2 + 2 * kEssmMaxT + 2 * kEssmMaxKappa + 1 + 8];
   if (lane == 0) lred[warp] = lsum;
-  static_assert(kEssmW == 4 * kEssmThreads, "4 owned samples per thread");
-  constexpr int QN = 4;
+  constexpr int QN = LDBP_ESSM_QN;
+  static_assert(QN * kEssmThreads >= kEssmW, "QN owned samples per thread cover the tile");
   const int i0 = QN * threadIdx.x;
   float cq[QN];
 #pragma unroll

@@ -31,6 +31,10 @@ namespace ldbp {
 #ifndef LDBP_REV3_NW
 #define LDBP_REV3_NW 4  // warps per CTA
 #endif
+#ifndef LDBP_REV3_TAILSMEM
+#define LDBP_REV3_TAILSMEM 0  // 1: the left halo passes through shared memory (frees 16 registers
+                              // that would hold the shuffled halo across the step)
+#endif
 #ifndef LDBP_REV3_D
 #define LDBP_REV3_D 4  // depth of the cross-warp ring (steps warp w-1 may run ahead of warp w)
 #endif
@@ -153,7 +157,7 @@ __device__ __forceinline__ uint32_t range_mask(int rel, int W) {
 }
 
 template <int KH, int R, int NW, bool FAST, bool NORM>
-__device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring, uint64_t* bars,
+__device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring, f2x* tailb, uint64_t* bars,
                                           const TapP* taps_adj, const StepNorm* norm, float* red, float* lred,
                                           const float* gam) {
   constexpr int NT = NW * 32;
@@ -270,8 +274,14 @@ __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring
     // left halo first (the neighbour overwrites its tail in place during this step): the last 2 Kh
     // inputs of slot p - 1 by shuffle; lane 0 of warp w > 0 takes them from the ring below
     f2x A[KH + 1], Bq[KH + 1], gl[KE2];
+    if (LDBP_REV3_TAILSMEM) {  // publish the old tail now, read the neighbour's when needed
 #pragma unroll
-    for (int i = 0; i < KE2; ++i) gl[i] = __shfl_up_sync(kFull, g[R - KE2 + i], 1);
+      for (int i = 0; i < KE2; ++i) tailb[tid * (KE2 + 2) + i] = g[R - KE2 + i];
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int i = 0; i < KE2; ++i) gl[i] = __shfl_up_sync(kFull, g[R - KE2 + i], 1);
+    }
 #pragma unroll
     for (int j = 0; j <= KH; ++j) A[j] = Bq[j] = 0ull;
     float dgam_next = 0.f;
@@ -280,6 +290,11 @@ __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring
     // the launch's last step gmn = 0 and the fused NL adjoint is an exact identity (sin 0 = 0,
     // cos 0 = 1; its dgamma' contribution is discarded) — half the loop body (instruction fetch)
     rev3_range<KH, R, FAST, NORM, true, KE2, R>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
+    if (LDBP_REV3_TAILSMEM) {
+      const f2x* tp = tailb + (lane > 0 ? tid - 1 : tid) * (KE2 + 2);
+#pragma unroll
+      for (int i = 0; i < KE2; ++i) gl[i] = tp[i];
+    }
     if (warp > 0) {  // warp-uniform: warp w - 1 finished step k - 1 (its lane 31 tail is in the ring)
       const int j = k % D;
       mbar_wait_parity(full + warp * D + j, (k / D) & 1);
@@ -294,6 +309,7 @@ __device__ __forceinline__ void rev3_body(const RevArgs& a, f2x* ubuf, f2x* ring
     }
     // outputs [0, 2 Kh): need the left halo
     rev3_range<KH, R, FAST, NORM, true, 0, KE2>(g, gl, ub, hs, A, Bq, own, gmn, dgam_next);
+    if (LDBP_REV3_TAILSMEM) __syncwarp();  // the neighbour has read this slot's tail (WAR next step)
     if (l > s0) produce(k + 1);
     {
       float vals[VP];
@@ -375,6 +391,7 @@ __host__ __device__ constexpr size_t rev3_smem_bytes(int kh, int steps, int M) {
   return 16 * (size_t)2 * NW * D                                        // full / empty mbarriers
          + sizeof(unsigned long long) * 2 * (size_t)NT * (R + 2)        // window copies
          + sizeof(unsigned long long) * (size_t)NW * D * 2 * (kh > 0 ? kh : 1)  // ring (NW slots)
+         + (LDBP_REV3_TAILSMEM ? sizeof(unsigned long long) * (size_t)NT * (2 * kh + 2) : 0)  // tails
          + 16 * (size_t)steps * NTU                                     // adjoint taps
          + 16 * (size_t)M                                               // StepNorm
          + 4 * (size_t)((steps * NW * V + 3) & ~3)                      // per-warp partials
@@ -394,7 +411,8 @@ __global__ void __launch_bounds__(rev3_warps(KH) * 32, 65536 / (rev3_warps(KH) *
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                          // [2][NW][D] (16 B each)
   f2x* ubuf = reinterpret_cast<f2x*>(smem_raw + 16 * 2 * NW * D);                  // [2][NT][R+2]
   f2x* ring = ubuf + (size_t)2 * NT * (R + 2);                                     // [NW][D][2 Kh]
-  TapP* taps_adj = reinterpret_cast<TapP*>(ring + (size_t)NW * D * 2 * KH);        // [S][NTU]
+  f2x* tailb = ring + (size_t)NW * D * 2 * KH;                                     // [NT][2 Kh + 2]
+  TapP* taps_adj = reinterpret_cast<TapP*>(tailb + (LDBP_REV3_TAILSMEM ? (size_t)NT * (2 * KH + 2) : 0));
   StepNorm* norm = reinterpret_cast<StepNorm*>(taps_adj + S * NTU);                // [M]
   float* red = reinterpret_cast<float*>(norm + a.M);                               // [S][NW][V]
   float* lred = red + ((S * NW * V + 3) & ~3);                                     // [NW]
@@ -406,9 +424,9 @@ __global__ void __launch_bounds__(rev3_warps(KH) * 32, 65536 / (rev3_warps(KH) *
   load_ptab<NTU>(a.ptab, a.M, a.s0, a.s1, norm, nullptr, taps_adj, gam, kj, flag);
   __syncthreads();
   if (*flag)
-    rev3_body<KH, R, NW, FAST, true>(a, ubuf, ring, bars, taps_adj, norm, red, lred, gam);
+    rev3_body<KH, R, NW, FAST, true>(a, ubuf, ring, tailb, bars, taps_adj, norm, red, lred, gam);
   else
-    rev3_body<KH, R, NW, FAST, false>(a, ubuf, ring, bars, taps_adj, norm, red, lred, gam);
+    rev3_body<KH, R, NW, FAST, false>(a, ubuf, ring, tailb, bars, taps_adj, norm, red, lred, gam);
 }
 
 }  // namespace ldbp
