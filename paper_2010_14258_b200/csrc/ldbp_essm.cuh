@@ -82,6 +82,29 @@ __host__ __device__ __forceinline__ int essm_pf_size(int n) { return n + (n >> 3
 __device__ __forceinline__ constexpr int prow(int i) { return i + (i >> 3); }  // offset within an aligned run
 __host__ __device__ __forceinline__ int essm_nj(int kap) { return ((2 * kap + 1 + 7) / 8) * 8; }
 
+// Asynchronous tile load: dst[pcx(i)] = src[(t_start + i) mod n] for i < cnt, zeros for the slack
+// (cp.async 8-byte copies straight into shared memory: every thread's loads are in flight at
+// once instead of load -> store round trips).  t_start may be negative; one conditional wrap per
+// element when the halo is shorter than the block (always for the BJ shapes), a modulo otherwise.
+__device__ __forceinline__ void essm_tile_async(f2x* dst, const f2x* __restrict__ src, int64_t t_start, int cnt,
+                                                int64_t n) {
+  const int64_t s0 = t_start < 0 ? t_start + n : t_start;                  // in [0, n) when t_start > -n
+  const bool simple = t_start > -n && t_start < n && s0 + cnt <= 2 * n;    // at most one wrap
+  for (int i = threadIdx.x; i < cnt + kESlack; i += kEssmThreads) {
+    if (i < cnt) {
+      int64_t t = s0 + i;
+      if (simple) {
+        if (t >= n) t -= n;
+      } else {
+        t = essm_mod(t_start + i, n);
+      }
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst + pcx(i))), "l"(src + t) : "memory");
+    } else {
+      dst[pcx(i)] = 0ull;
+    }
+  }
+}
+
 // tt[j] = eta_{k}, k = kap - j (dir = +1: X index o - k = o - kap + j) or k = j - kap (dir = -1:
 // X index o + k = o - kap + j); zero for j >= 2 kap + 1.
 __device__ __forceinline__ void essm_tap_table(const float* __restrict__ eta, int kap, int dir, float* tt) {
@@ -149,8 +172,9 @@ __global__ void __launch_bounds__(kEssmThreads) essm_fwd_step_kernel(const EssmA
   essm_tap_table(a.eta, kap, +1, tt);
   const f2x* ub = reinterpret_cast<const f2x*>(a.u) + (int64_t)b * a.n;
   const int64_t su = essm_mod(t0 - hu, a.n);
-  for (int i = threadIdx.x; i < nu + kESlack; i += kEssmThreads)
-    U[pcx(i)] = i < nu ? ub[essm_wrap(su, i, a.n)] : 0ull;
+  (void)su;
+  essm_tile_async(U, ub, t0 - hu, nu, a.n);
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
   for (int i = threadIdx.x; i < kESlack; i += kEssmThreads) P[pfl(na + i)] = 0.f;
   __syncthreads();
   // a_t = sum_j h_j u_{t-j}, A index i <-> t = t0 - kappa + i <-> U index i + KH
@@ -210,8 +234,12 @@ __global__ void __launch_bounds__(kEssmThreads) essm_bwd_step_kernel(const EssmA
   essm_tap_table(a.eta, kap, +1, tt_f);
   essm_tap_table(a.eta, kap, -1, tt_b);
   const f2x* ub = reinterpret_cast<const f2x*>(a.u) + (int64_t)b * a.n;
-  for (int i = threadIdx.x; i < nU + kESlack; i += kEssmThreads)  // (essm_wrap here: measured +8 %)
-    U[pcx(i)] = i < nU ? ub[essm_mod(t0 - hU + i, a.n)] : 0ull;
+  essm_tile_async(U, ub, t0 - hU, nU, a.n);
+  {  // the incoming adjoint (or the target, seed mode) on the G region, straight into G
+    const f2x* gsrc = reinterpret_cast<const f2x*>(a.gin ? a.gin : a.target) + (int64_t)b * a.n;
+    essm_tile_async(G, gsrc, t0 - hG, nG, a.n);
+  }
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
   for (int i = threadIdx.x; i < kESlack; i += kEssmThreads) {  // finite slack (zero taps x slack)
     P[pfl(nA + i)] = 0.f;
     C[pfl(nG + i)] = 0.f;
@@ -246,12 +274,11 @@ __global__ void __launch_bounds__(kEssmThreads) essm_bwd_step_kernel(const EssmA
       sincos_phase<FAST>(gam * psi[q], &s, &c);
       const float2 av = upk(A[pcx(i + kap)]);
       const float vx = fmaf(av.x, c, -av.y * s), vy = fmaf(av.x, s, av.y * c);
-      const int64_t t = essm_mod(t0 - hG + i, a.n);
       float2 g;
       if (gb) {
-        g = upk(gb[t]);
+        g = upk(G[pcx(i)]);  // prefetched adjoint
       } else {
-        const float2 tv = upk(tb[t]);
+        const float2 tv = upk(G[pcx(i)]);  // prefetched target
         const float ex = vx - tv.x, ey = vy - tv.y;
         g = make_float2(2.f * ex, 2.f * ey);
         if (i >= hG && i < hG + own) lsum = fmaf(ex, ex, fmaf(ey, ey, lsum));
