@@ -527,3 +527,34 @@ def test_check_finite_reports_first_step(P, monkeypatch):
     with pytest.raises(LdbpError) as e:
         P.ldbp_loss_grad(x, tgt, hb, gt, check_finite=True)
     assert e.value.status == -6 and "step 3" in str(e.value)
+
+
+@pytest.mark.parametrize("env", [{"LDBP_BWD_MODE": "1"}, {"LDBP_BWD_MODE": "0"}, {"LDBP_BWD_MODE": "1", "LDBP_REV3": "1"},
+                                 {"LDBP_BWD_MODE": "1", "LDBP_OVERLAP": "3"}, {"LDBP_BWD_MODE": "1", "LDBP_REV2": "1"}])
+def test_repeated_runs_bitwise_identical(P, monkeypatch, env):
+    """Race detector by repetition (compute-sanitizer is closed on this GPU pool): 12 repeated
+    loss_grad calls of a store-all-sized problem, on two streams, must agree bit for bit — the
+    mbarrier split barriers, ring buffers, cp.async windows and the fixed-order reductions leave
+    no room for nondeterminism; a race would show as differing low bits.  Every schedule option."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    monkeypatch.setenv("LDBP_STORE_ALL_MIN_SAMPLES", "0")
+    B, n, M, T = 24, 16384, 10, 9
+    x = dev(li.gaussian_blocks(61, range(B), n, 1e-3))
+    tgt = dev(li.gaussian_blocks(61, range(B), n, 1e-3, purpose="target"))
+    taps, gamma = model(61, M, T, True)
+    ht, gt = dev(taps), dev(gamma, np.float32)
+    ref = P.ldbp_loss_grad(x, tgt, ht, gt).cpu()
+    s2 = torch.cuda.Stream()
+    outs = []
+    for i in range(12):
+        st = s2 if i % 2 else torch.cuda.current_stream()
+        s2.wait_stream(torch.cuda.current_stream())
+        outs.append(P.ldbp_loss_grad(x, tgt, ht, gt, stream=st))
+        torch.cuda.current_stream().wait_stream(s2)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o.cpu(), ref)
+    r = O.loss_grad(r32(x.cpu().numpy()), r32(tgt.cpu().numpy()), r32(taps), r32(gamma), symmetric=True)
+    assert abs(ref[0].item() - r[0]) <= OUT_TOL * r[0]
+    assert rel(ref[1:].numpy(), r[1:]) <= GRAD_TOL
