@@ -1110,11 +1110,13 @@ size_t essm_smem(int T, int kappa, bool bwd) {
   const int kh = (T - 1) / 2;
   const int W = kEssmW, S = kESlack;
   size_t s = sizeof(float2) * kEssmMaxT + sizeof(float) * (2 * essm_nj(kEssmMaxKappa) + 2);
+  (void)kh;
+  const int k8 = (kappa + 7) & ~7;  // halos padded to multiples of 8 (ldbp_essm.cuh, essm_k8)
   if (!bwd) {
-    const int nu = W + 2 * (kh + kappa), na = W + 2 * kappa;
+    const int nu = W + 2 * (8 + k8), na = W + 2 * k8;
     return s + sizeof(float2) * (essm_pc_size(nu + S) + essm_pc_size(na + S)) + sizeof(float) * essm_pf_size(na + S);
   }
-  const int nU = W + 2 * (2 * kh + 2 * kappa), nA = W + 2 * (kh + 2 * kappa), nG = W + 2 * (kh + kappa), nQ = W + 2 * kh;
+  const int nU = W + 2 * (16 + 2 * k8), nA = W + 2 * (8 + 2 * k8), nG = W + 2 * (8 + k8), nQ = W + 2 * 8;
   s += sizeof(float2) * (essm_pc_size(nU + S) + essm_pc_size(nA + S) + essm_pc_size(nG + S) + essm_pc_size(nQ + S));
   s += sizeof(float) * (essm_pf_size(nA + S) + 2 * essm_pf_size(nG + S));
   return s;

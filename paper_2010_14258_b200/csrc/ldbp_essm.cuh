@@ -20,10 +20,10 @@ namespace ldbp {
 
 constexpr int kEssmThreads = 256;
 #ifndef LDBP_ESSM_W
-#define LDBP_ESSM_W 1960  // owned samples per CTA: with the largest halo (A: 2 (Kh + 2 kappa) = 88 at
-                          // kappa = 20, Kh = 4) every filter phase is ONE pass of 256 threads x 8
-                          // outputs (round 1's 1024 left ~half the threads idle in every phase:
-                          // measured 24 % barrier stalls)
+#define LDBP_ESSM_W 1936  // owned samples per CTA: with the largest computed region (A: W + 2 (8 + 2
+                          // kappa_8) = 2048 at kappa <= 24) every filter phase is ONE pass of 256
+                          // threads x 8 outputs (round 1's 1024 left ~half the threads idle in every
+                          // phase: measured 24 % barrier stalls)
 #endif
 #ifndef LDBP_ESSM_QN
 #define LDBP_ESSM_QN 8    // owned samples per thread in the gradient sums (QN x threads >= W)
@@ -105,23 +105,30 @@ __device__ __forceinline__ void essm_tile_async(f2x* dst, const f2x* __restrict_
   }
 }
 
-// tt[j] = eta_{k}, k = kap - j (dir = +1: X index o - k = o - kap + j) or k = j - kap (dir = -1:
-// X index o + k = o - kap + j); zero for j >= 2 kap + 1.
+// Halos are padded to multiples of 8 (kappa_8 = roundup8(kappa), 8 for the FIR halo) so that the
+// offset between any two arrays is a multiple of 8 and every register window below starts at an
+// 8-aligned index (one address per run, compile-time offsets, conflict-free rows).
+__device__ __forceinline__ int essm_k8(int kap) { return (kap + 7) & ~7; }
+__host__ __device__ __forceinline__ int essm_nj2(int kap) { return (((kap + 7) & ~7) + kap + 1 + 7) & ~7; }
+
+// Shifted tap table: tt[j] = eta_k with k = k8 - j (dir = +1) or k = j - k8 (dir = -1), zero where
+// |k| > kappa; then acc[q] = sum_j tt[j] X[x0 + q - k8 + j] is sum_k eta_k X[x0 + q -+ k] with an
+// 8-aligned window start x0 - k8.
 __device__ __forceinline__ void essm_tap_table(const float* __restrict__ eta, int kap, int dir, float* tt) {
-  const int NJ = essm_nj(kap);
+  const int k8 = essm_k8(kap), NJ = essm_nj2(kap);
   for (int j = threadIdx.x; j < NJ; j += kEssmThreads) {
-    const int k = dir > 0 ? kap - j : j - kap;
-    tt[j] = j < 2 * kap + 1 ? eta[k + kap] : 0.f;
+    const int k = dir > 0 ? k8 - j : j - k8;
+    tt[j] = (k >= -kap && k <= kap) ? eta[k + kap] : 0.f;
   }
 }
 
-// acc[q] = sum_j tt[j] X[x0 + q - kap + j]  (X float, padded)
+// acc[q] = sum_j tt[j] X[x0 + q - k8 + j]  (X float, row-padded; x0 - k8 8-aligned)
 __device__ __forceinline__ void essm_rfilt(const float* __restrict__ X, int x0, int kap, const float* __restrict__ tt,
                                            float (&acc)[kEQ]) {
-  const int NJ = essm_nj(kap);
+  const int NJ = essm_nj2(kap);
 #pragma unroll
   for (int q = 0; q < kEQ; ++q) acc[q] = 0.f;
-  const float* xb = X + pfl(x0 - kap);  // x0 - kap is 8-aligned for every caller (o0 + kappa - kappa)
+  const float* xb = X + pfl(x0 - essm_k8(kap));
   for (int j0 = 0; j0 < NJ; j0 += 8, xb += 9) {
     float w[kEQ + 7];
 #pragma unroll
@@ -135,14 +142,16 @@ __device__ __forceinline__ void essm_rfilt(const float* __restrict__ X, int x0, 
   }
 }
 
-// complex FIR, acc[q] = sum_j h_j In[x0 + q - j] (ADJ: sum_j conj(h_j) In[x0 + q + j]), j in [-KH, KH]
+// complex FIR with output q centred at In index xa + 8 + q (xa 8-aligned):
+// acc[q] = sum_j h_j In[xa + 8 + q - j] (ADJ: sum_j conj(h_j) In[xa + 8 + q + j]), j in [-KH, KH]
 template <int KH, bool ADJ>
-__device__ __forceinline__ void essm_cfir(const f2x* __restrict__ In, int x0, const float2* __restrict__ sh_h,
+__device__ __forceinline__ void essm_cfir(const f2x* __restrict__ In, int xa, const float2* __restrict__ sh_h,
                                           f2x (&acc)[kEQ]) {
+  constexpr int SH = 8 - KH;  // window start xa + SH
   f2x w[kEQ + 2 * KH];
-  const f2x* ib = In + pcx(x0 - KH);  // 8-aligned run start (callers pass x0 = o0 + KH)
+  const f2x* ib = In + pcx(xa);
 #pragma unroll
-  for (int i = 0; i < kEQ + 2 * KH; ++i) w[i] = ib[prow(i)];
+  for (int i = 0; i < kEQ + 2 * KH; ++i) w[i] = ib[prow(SH + i)];
 #pragma unroll
   for (int q = 0; q < kEQ; ++q) acc[q] = 0ull;
 #pragma unroll
@@ -154,15 +163,16 @@ __device__ __forceinline__ void essm_cfir(const f2x* __restrict__ In, int x0, co
   }
 }
 
-// Forward step: U on [-(Kh+kappa), W+Kh+kappa), A/P on [-kappa, W+kappa), v on [0, W).
+// Forward step (halos padded, see essm_k8): U on [-(8 + k8), W + 8 + k8), A/P on [-k8, W + k8),
+// v on [0, W).  A index i <-> U index i + 8; owned i <-> A/P index i + k8.
 template <int KH, bool FAST>
 __global__ void __launch_bounds__(kEssmThreads) essm_fwd_step_kernel(const EssmArgs a) {
   extern __shared__ __align__(16) unsigned char es_smem[];
-  const int kap = a.kappa;
+  const int kap = a.kappa, k8 = essm_k8(kap);
   const float gam = a.gamma[a.step];
   const int b = blockIdx.y, tile = blockIdx.x;
   const int64_t t0 = (int64_t)tile * kEssmW;
-  const int hu = KH + kap, nu = kEssmW + 2 * hu, na = kEssmW + 2 * kap;
+  const int hu = 8 + k8, nu = kEssmW + 2 * hu, na = kEssmW + 2 * k8;
   float2* sh_h = reinterpret_cast<float2*>(es_smem);                // [kEssmMaxT]
   float* tt = reinterpret_cast<float*>(sh_h + kEssmMaxT);           // [essm_nj(kEssmMaxKappa)]
   f2x* U = reinterpret_cast<f2x*>(tt + essm_nj(kEssmMaxKappa) + 2); // [pc(nu + slack)]
@@ -171,52 +181,55 @@ __global__ void __launch_bounds__(kEssmThreads) essm_fwd_step_kernel(const EssmA
   for (int i = threadIdx.x; i < 2 * KH + 1; i += kEssmThreads) sh_h[i] = a.taps[i];
   essm_tap_table(a.eta, kap, +1, tt);
   const f2x* ub = reinterpret_cast<const f2x*>(a.u) + (int64_t)b * a.n;
-  const int64_t su = essm_mod(t0 - hu, a.n);
-  (void)su;
   essm_tile_async(U, ub, t0 - hu, nu, a.n);
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
   for (int i = threadIdx.x; i < kESlack; i += kEssmThreads) P[pfl(na + i)] = 0.f;
   __syncthreads();
-  // a_t = sum_j h_j u_{t-j}, A index i <-> t = t0 - kappa + i <-> U index i + KH
+  // a_t = sum_j h_j u_{t-j}
   for (int o0 = threadIdx.x * kEQ; o0 < na; o0 += kEssmThreads * kEQ) {
     f2x acc[kEQ];
-    essm_cfir<KH, false>(U, o0 + KH, sh_h, acc);
+    essm_cfir<KH, false>(U, o0, sh_h, acc);
+    f2x* ar = A + pcx(o0);
+    float* pr = P + pfl(o0);
 #pragma unroll
     for (int q = 0; q < kEQ; ++q) {
-      A[pcx(o0 + q)] = acc[q];
+      ar[prow(q)] = acc[q];
       const float2 av = upk(acc[q]);
-      P[pfl(o0 + q)] = fmaf(av.x, av.x, av.y * av.y);
+      pr[prow(q)] = fmaf(av.x, av.x, av.y * av.y);
     }
   }
   __syncthreads();
-  // psi_t = sum_k eta_k p_{t-k}; owned output i <-> P index i + kappa
+  // psi_t = sum_k eta_k p_{t-k}
   f2x* vb = reinterpret_cast<f2x*>(a.out) + (int64_t)b * a.n;
   const int own = (int)(a.n - t0 < (int64_t)kEssmW ? a.n - t0 : (int64_t)kEssmW);
   for (int o0 = threadIdx.x * kEQ; o0 < own; o0 += kEssmThreads * kEQ) {
     float psi[kEQ];
-    essm_rfilt(P, o0 + kap, kap, tt, psi);
+    essm_rfilt(P, o0 + k8, kap, tt, psi);
+    const f2x* ar = A + pcx(o0 + k8);
 #pragma unroll
     for (int q = 0; q < kEQ; ++q) {
       if (o0 + q >= own) break;
       float s, c;
       sincos_phase<FAST>(gam * psi[q], &s, &c);
-      const float2 av = upk(A[pcx(o0 + q + kap)]);
+      const float2 av = upk(ar[prow(q)]);
       vb[t0 + o0 + q] = pk(fmaf(av.x, c, -av.y * s), fmaf(av.x, s, av.y * c));
     }
   }
 }
 
-// Backward step.  Regions relative to t0 (halo widths): U: 2Kh+2kappa, A/P: Kh+2kappa,
-// G/PSI/C (and phi): Kh+kappa, GA/Q: Kh; outputs and gradient sums on owned [0, W).
+// Backward step.  Regions relative to t0, halos padded to multiples of 8 (k8 = roundup8(kappa)):
+// U: 16 + 2 k8, A/P: 8 + 2 k8, G/PSI/C (and phi): 8 + k8, GA/Q: 8; outputs and gradient sums on
+// owned [0, W).  Index relations: A i <-> U i + 8; G i <-> A/P i + k8; Q i <-> G/C i + k8, A i + 2 k8;
+// owned s <-> Q s + 8, G s + 8 + k8, A s + 8 + 2 k8, U s + 16 + 2 k8.
 template <int KH, bool FAST>
 __global__ void __launch_bounds__(kEssmThreads) essm_bwd_step_kernel(const EssmArgs a) {
   extern __shared__ __align__(16) unsigned char es_smem[];
-  const int kap = a.kappa;
+  const int kap = a.kappa, k8 = essm_k8(kap);
   const float gam = a.gamma[a.step];
   const int b = blockIdx.y, tile = blockIdx.x;
   const int64_t t0 = (int64_t)tile * kEssmW;
   const int own = (int)(a.n - t0 < (int64_t)kEssmW ? a.n - t0 : (int64_t)kEssmW);
-  const int hU = 2 * KH + 2 * kap, hA = KH + 2 * kap, hG = KH + kap, hQ = KH;
+  const int hU = 16 + 2 * k8, hA = 8 + 2 * k8, hG = 8 + k8, hQ = 8;
   const int nU = kEssmW + 2 * hU, nA = kEssmW + 2 * hA, nG = kEssmW + 2 * hG, nQ = kEssmW + 2 * hQ;
   const int T = 2 * KH + 1, NE = 2 * kap + 1;
   const int V = 2 + 2 * T + NE;  // [dgamma | loss | dh re/im (T) | deta (NE)]
@@ -247,80 +260,86 @@ __global__ void __launch_bounds__(kEssmThreads) essm_bwd_step_kernel(const EssmA
     GA[pcx(nQ + i)] = 0ull;
   }
   __syncthreads();
-  // a, p on hA: A index i <-> U index i + (hU - hA) = i + KH
+  // a, p on the A region
   for (int o0 = threadIdx.x * kEQ; o0 < nA; o0 += kEssmThreads * kEQ) {
     f2x acc[kEQ];
-    essm_cfir<KH, false>(U, o0 + KH, sh_h, acc);
+    essm_cfir<KH, false>(U, o0, sh_h, acc);
+    f2x* ar = A + pcx(o0);
+    float* pr = P + pfl(o0);
 #pragma unroll
     for (int q = 0; q < kEQ; ++q) {
-      A[pcx(o0 + q)] = acc[q];
+      ar[prow(q)] = acc[q];
       const float2 av = upk(acc[q]);
-      P[pfl(o0 + q)] = fmaf(av.x, av.x, av.y * av.y);
+      pr[prow(q)] = fmaf(av.x, av.x, av.y * av.y);
     }
   }
   __syncthreads();
-  // psi, v, g (loaded or seeded), c on hG: G index i <-> A/P index i + kappa
-  const f2x* gb = a.gin ? reinterpret_cast<const f2x*>(a.gin) + (int64_t)b * a.n : nullptr;
-  const f2x* tb = a.gin ? nullptr : reinterpret_cast<const f2x*>(a.target) + (int64_t)b * a.n;
+  // psi, v, g (loaded or seeded), c on the G region
+  const bool have_g = a.gin != nullptr;
   float lsum = 0.f;
   for (int o0 = threadIdx.x * kEQ; o0 < nG; o0 += kEssmThreads * kEQ) {
     float psi[kEQ];
-    essm_rfilt(P, o0 + kap, kap, tt_f, psi);
+    essm_rfilt(P, o0 + k8, kap, tt_f, psi);
+    const f2x* ar = A + pcx(o0 + k8);
+    f2x* gr = G + pcx(o0);
+    float* psr = PSI + pfl(o0);
+    float* cr = C + pfl(o0);
 #pragma unroll
     for (int q = 0; q < kEQ; ++q) {
       const int i = o0 + q;
       if (i >= nG) break;
       float s, c;
       sincos_phase<FAST>(gam * psi[q], &s, &c);
-      const float2 av = upk(A[pcx(i + kap)]);
+      const float2 av = upk(ar[prow(q)]);
       const float vx = fmaf(av.x, c, -av.y * s), vy = fmaf(av.x, s, av.y * c);
-      float2 g;
-      if (gb) {
-        g = upk(G[pcx(i)]);  // prefetched adjoint
-      } else {
-        const float2 tv = upk(G[pcx(i)]);  // prefetched target
-        const float ex = vx - tv.x, ey = vy - tv.y;
+      float2 g = upk(gr[prow(q)]);  // prefetched adjoint, or the target in seed mode
+      if (!have_g) {
+        const float ex = vx - g.x, ey = vy - g.y;
         g = make_float2(2.f * ex, 2.f * ey);
         if (i >= hG && i < hG + own) lsum = fmaf(ex, ex, fmaf(ey, ey, lsum));
       }
-      G[pcx(i)] = pk(g.x, g.y);
-      PSI[pfl(i)] = psi[q];
-      C[pfl(i)] = fmaf(g.y, vx, -g.x * vy);  // Im(g conj v)
+      gr[prow(q)] = pk(g.x, g.y);
+      psr[prow(q)] = psi[q];
+      cr[prow(q)] = fmaf(g.y, vx, -g.x * vy);  // Im(g conj v)
     }
   }
   __syncthreads();
-  // q and ga on hQ: Q index i <-> G/C index i + kappa, A index i + 2 kappa
+  // q and ga on the Q region
   for (int o0 = threadIdx.x * kEQ; o0 < nQ; o0 += kEssmThreads * kEQ) {
     float qv[kEQ];
-    essm_rfilt(C, o0 + kap, kap, tt_b, qv);  // sum_k eta_k c_{m+k}
+    essm_rfilt(C, o0 + k8, kap, tt_b, qv);  // sum_k eta_k c_{m+k}
+    const float* psr = PSI + pfl(o0 + k8);
+    const f2x* gr = G + pcx(o0 + k8);
+    const f2x* ar = A + pcx(o0 + 2 * k8);
+    f2x* gar = GA + pcx(o0);
 #pragma unroll
     for (int q = 0; q < kEQ; ++q) {
       const int i = o0 + q;
       if (i >= nQ) break;
       const float qq = gam * qv[q];
       float s, c;
-      sincos_phase<FAST>(gam * PSI[pfl(i + kap)], &s, &c);
-      const float2 gv = upk(G[pcx(i + kap)]), av = upk(A[pcx(i + 2 * kap)]);
-      GA[pcx(i)] = pk(fmaf(gv.x, c, fmaf(gv.y, s, 2.f * qq * av.x)), fmaf(gv.y, c, fmaf(-gv.x, s, 2.f * qq * av.y)));
+      sincos_phase<FAST>(gam * psr[prow(q)], &s, &c);
+      const float2 gv = upk(gr[prow(q)]), av = upk(ar[prow(q)]);
+      gar[prow(q)] = pk(fmaf(gv.x, c, fmaf(gv.y, s, 2.f * qq * av.x)), fmaf(gv.y, c, fmaf(-gv.x, s, 2.f * qq * av.y)));
     }
   }
   __syncthreads();
-  // gu on owned: sum_j conj(h_j) ga_{s+j}, GA index of s is i + KH
+  // gu on owned: sum_j conj(h_j) ga_{s+j}, owned s <-> Q index s + 8
   if (a.out) {
     f2x* ob = reinterpret_cast<f2x*>(a.out) + (int64_t)b * a.n;
     for (int o0 = threadIdx.x * kEQ; o0 < own; o0 += kEssmThreads * kEQ) {
       f2x acc[kEQ];
-      essm_cfir<KH, true>(GA, o0 + KH, sh_h, acc);
+      essm_cfir<KH, true>(GA, o0, sh_h, acc);
 #pragma unroll
       for (int q = 0; q < kEQ; ++q)
         if (o0 + q < own) ob[t0 + o0 + q] = acc[q];
     }
   }
-  // gradient sums over owned t, register-blocked: thread tid owns samples i = 4 tid + q (q < 4,
-  // W = 4 * threads) and forms its partial of every component from register windows (dh: the
-  // T-tap correlation of ga with conj(u); deta: the (2 kappa + 1)-tap correlation of c with p, in
-  // chunks of 8 taps); each chunk of 8 partials is reduced across the warp with the transposing
-  // butterfly into red[warp][v]; the CTA then sums the 8 warps in fixed order.
+  // gradient sums over owned t, register-blocked: thread tid owns samples i = QN tid + q and forms
+  // its partial of every component from register windows (dh: the T-tap correlation of ga with
+  // conj(u); deta: the (2 kappa + 1)-tap correlation of c with p, in blocks of 8 lags placed so
+  // that every p window starts 8-aligned); each block of 8 partials is reduced across the warp with
+  // the transposing butterfly into red[warp][v]; the CTA then sums the 8 warps in fixed order.
   lsum = warp_sum(lsum);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cta = blockIdx.y * gridDim.x + blockIdx.x;
@@ -329,29 +348,45 @@ __global__ void __launch_bounds__(kEssmThreads) essm_bwd_step_kernel(const EssmA
   __shared__ float red[kEssmThreads / 32][2 + 2 * kEssmMaxT + 2 * kEssmMaxKappa + 1 + 8];
   if (lane == 0) lred[warp] = lsum;
   constexpr int QN = LDBP_ESSM_QN;
+  static_assert(QN == 8, "aligned runs of 8 owned samples per thread");
   static_assert(QN * kEssmThreads >= kEssmW, "QN owned samples per thread cover the tile");
   const int i0 = QN * threadIdx.x;
+  // threads past the tile (QN x threads > W) read their windows at 0 (finite data; all their
+  // products are multiplied by zeroed c / ga values)
+  const int iw = i0 < own ? i0 : 0;
   float cq[QN];
+  {
+    const float* cr = C + pfl(i0 + hG);
 #pragma unroll
-  for (int q = 0; q < QN; ++q) cq[q] = i0 + q < own ? C[pfl(i0 + q + hG)] : 0.f;
-  auto flush8 = [&](float (&v)[8], int comp0, int lim) {  // warp-reduce 8 partials -> red[warp][comp0 + .]
+    for (int q = 0; q < QN; ++q) cq[q] = i0 + q < own ? cr[prow(q)] : 0.f;
+  }
+  auto flush8 = [&](float (&v)[8], int comp0, int lo, int lim) {  // warp-reduce 8 partials -> red[warp][.]
     const float r = warp_reduce_scatter<8>(v, lane);
     const int idx = lane >> 2;
-    if ((lane & 3) == 0 && comp0 + idx < lim) red[warp][comp0 + idx] = r;
+    if ((lane & 3) == 0 && comp0 + idx >= lo && comp0 + idx < lim) red[warp][comp0 + idx] = r;
   };
   {  // comp 0 (dgamma') and the T complex tap correlations, comps 2 .. 2 + 2T
     float vals[2 + 2 * kEssmMaxT + 6];  // padded to a multiple of 8
 #pragma unroll
     for (int v = 0; v < 2 + 2 * kEssmMaxT + 6; ++v) vals[v] = 0.f;
+    {
+      const float* psr = PSI + pfl(i0 + hG);
 #pragma unroll
-    for (int q = 0; q < QN; ++q) vals[0] = fmaf(cq[q], i0 + q < own ? PSI[pfl(i0 + q + hG)] : 0.f, vals[0]);
+      for (int q = 0; q < QN; ++q) vals[0] = fmaf(cq[q], i0 + q < own ? psr[prow(q)] : 0.f, vals[0]);
+    }
     float2 gq[QN];
+    {
+      const f2x* gar = GA + pcx(i0 + hQ);
 #pragma unroll
-    for (int q = 0; q < QN; ++q) gq[q] = i0 + q < own ? upk(GA[pcx(i0 + q + hQ)]) : make_float2(0.f, 0.f);
-    // u window: U index i + du, du = hU - (jj - KH) for jj in [0, T): i0 + q + hU + KH - jj
+      for (int q = 0; q < QN; ++q) gq[q] = i0 + q < own ? upk(gar[prow(q)]) : make_float2(0.f, 0.f);
+    }
+    // u window: U index i + hU - j, j = jj - KH: from U index i0 + hU - KH = (i0 + hU - 8) + SH
     float2 uw[QN + 2 * KH];
+    {
+      const f2x* ur = U + pcx(iw + hU - 8);
 #pragma unroll
-    for (int w = 0; w < QN + 2 * KH; ++w) uw[w] = upk(U[pcx(i0 + hU - KH + w)]);
+      for (int w = 0; w < QN + 2 * KH; ++w) uw[w] = upk(ur[prow(8 - KH + w)]);
+    }
 #pragma unroll
     for (int jj = 0; jj < 2 * KH + 1; ++jj) {
       float re = 0.f, im = 0.f;
@@ -370,25 +405,29 @@ __global__ void __launch_bounds__(kEssmThreads) essm_bwd_step_kernel(const EssmA
       float v8[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) v8[t] = vals[8 * c8 + t];
-      flush8(v8, 8 * c8, 2 + 2 * T);  // comps below the deta block only
+      flush8(v8, 8 * c8, 0, 2 + 2 * T);  // comps below the deta block only
     }
   }
-  {  // deta_k = sum_t c_t p_{t-k}, k = kk - kappa, P index i + dp, dp = hA - k; comps 2 + 2T + kk
-    const int NE = 2 * kap + 1, base = 2 + 2 * T;
-    for (int k0 = 0; k0 < NE; k0 += 8) {
-      // P[i0 + q + hA - (k0 + t - kap)] for t < 8, q < 4: window index w = q - t + 7
+  {  // deta_kk = sum_t c_t p_{t-k}, k = kk - kappa: P index t + hA + kappa - kk; comps 2 + 2T + kk.
+     // Lag blocks [k0, k0 + 8) with k0 = kappa + 1 (mod 8): the window start i0 + hA + kappa - k0 - 7
+     // is then 8-aligned (hA is a multiple of 8); lags outside [0, NE) are dropped.
+    const int base = 2 + 2 * T;
+    const int k0s = ((kap + 1) & 7) - 8;
+    for (int k0 = k0s; k0 < NE; k0 += 8) {
+      // P[i0 + q + hA + kappa - (k0 + t)] for t < 8, q < 8: window index w = q - t + 7
       float pw[QN + 7];
+      const float* pr = P + pfl(iw + hA + kap - k0 - 7);
 #pragma unroll
-      for (int w = 0; w < QN + 7; ++w) pw[w] = P[pfl(i0 + hA + kap - k0 - 7 + w)];
+      for (int w = 0; w < QN + 7; ++w) pw[w] = pr[prow(w)];
       float v8[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         float acc = 0.f;
 #pragma unroll
         for (int q = 0; q < QN; ++q) acc = fmaf(cq[q], pw[q - t + 7], acc);
-        v8[t] = k0 + t < NE ? acc : 0.f;
+        v8[t] = (k0 + t >= 0 && k0 + t < NE) ? acc : 0.f;
       }
-      flush8(v8, base + k0, V);  // comps base + k0 .. base + k0 + 7
+      flush8(v8, base + k0, base, V);  // comps base + k0 .. base + k0 + 7 (inside [base, V))
     }
   }
   __syncthreads();
