@@ -246,7 +246,7 @@ size_t fwd_smem(int kh, bool sym, int steps, int nthreads = 1024, int nnorm = 0,
 size_t rev_smem(int kh, bool sym, int steps, int M) {
   const int NT = ldbp::rev_threads(kh), nw = NT / 32;
   const int V = 1 + 2 * ntaps_used(kh, sym);
-  size_t s = 16 * (size_t)nw;                                         // split-barrier mbarriers
+  size_t s = 32 * (size_t)nw;                                         // split-barrier + bulk-copy mbarriers
   s += sizeof(float2) * LDBP_REV_PIPE * (size_t)(rev_r(kh) + (ldbp::rev_coal(kh) ? 2 : 0)) * NT;                       // u window copies
   s += sizeof(float2) * 4 * (size_t)std::max(kh, 1) * NT;             // ga edges
   s += sizeof(ldbp::TapP) * (size_t)steps * ntaps_used(kh, sym);      // adjoint taps

@@ -94,13 +94,17 @@ __host__ __device__ constexpr int rev_threads(int) { return LDBP_REV_NTHR; }
 __host__ __device__ constexpr int rev_threads(int) { return 128; }
 #endif
 
+#ifndef LDBP_REV_BULK
+#define LDBP_REV_BULK 1  // window copies of whole warps by one bulk-async (TMA engine) copy each:
+                         // linear layout, sample k of thread t at t*R + k (see rev_body)
+#endif
 #ifndef LDBP_REV_COALESCED
 #define LDBP_REV_COALESCED 1  // warp-cooperative coalesced window copies into a padded thread-major
                               // layout: 1 = for Kh <= 1 (C5 reverse -6 %; C3 (Kh = 4) +1 %, measured),
                               // 2 = always, 0 = never
 #endif
 __host__ __device__ constexpr bool rev_coal(int kh) {
-  return LDBP_REV_COALESCED == 2 || (LDBP_REV_COALESCED == 1 && kh <= 1);
+  return !LDBP_REV_BULK && (LDBP_REV_COALESCED == 2 || (LDBP_REV_COALESCED == 1 && kh <= 1));
 }
 // Shared-memory window copy of u^(l).  LDBP_REV_COALESCED: sample k of thread t at f2x index
 // t*(R+2) + k (one pad pair per thread: a thread's own 16-byte LDS.128 reads, 8 lanes apart by
@@ -113,11 +117,11 @@ template <bool COAL, int R>
 __host__ __device__ constexpr int rev_rs() { return COAL ? R + 2 : R; }
 template <bool COAL, int R, int NT>
 __device__ __forceinline__ constexpr int ubuf_idx(int k, int t) {
-  return COAL ? t * (R + 2) + k : ((k >> 1) * NT + t) * 2 + (k & 1);
+  return COAL ? t * (R + 2) + k : (LDBP_REV_BULK ? t * R + k : ((k >> 1) * NT + t) * 2 + (k & 1));
 }
 template <bool COAL, int R, int NT>
 __device__ __forceinline__ constexpr int ubuf_off(int k) {  // offset of sample k from the thread's slot 0
-  return COAL ? k : (k >> 1) * 2 * NT + (k & 1);
+  return COAL ? k : (LDBP_REV_BULK ? k : (k >> 1) * 2 * NT + (k & 1));
 }
 
 // Issue the asynchronous copy of this thread's R window samples of `src` (zeros outside [0, E)).
@@ -372,11 +376,49 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   constexpr int UB = rev_rs<COAL, R>() * NT;  // f2x per window buffer
   CoalCopy<R, NT> cc{};
   if constexpr (COAL) cc = coal_setup<R, NT>(sm.ubuf, fast_off);
+  // LDBP_REV_BULK: a warp whose 32 R samples are one contiguous run of real samples (fixed for the
+  // launch: the window does not move) copies each step's window with ONE cp.async.bulk (the TMA
+  // engine; SASS UBLKCP) issued by lane 0, completion tracked by the transaction count of the
+  // warp's mbarrier for that buffer; other warps keep the per-thread copies.
+  const int64_t woff = __shfl_sync(kFull, fast_off, 0);
+  const bool wbulk = LDBP_REV_BULK && PIPE == 2 &&
+                     __all_sync(kFull, fast_off >= 0 && fast_off == woff + (int64_t)lane * R);
+  uint64_t* bbar = sm.bar + 2 * NW + 2 * warp;  // [warp][buffer]
+  bool bused[2] = {false, false};               // buffer b was filled by a bulk copy
+  unsigned bph[2] = {0u, 0u};                   // next phase parity of bbar[b]
   auto window = [&](int i, int b) {  // async copy of u^(i) into window buffer b
+    const float2* src = rev_src(a, i);
+    if (wbulk && ((reinterpret_cast<uintptr_t>(src + woff)) & 15) == 0) {
+      bused[b] = true;
+      if (lane == 0) {
+        f2x* dst = sm.ubuf + (size_t)b * UB + ubuf_idx<COAL, R, NT>(0, warp * 32);
+        constexpr unsigned bytes = 32u * R * 8u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of dst
+        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bbar + b)),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(dst)),
+            "l"(src + woff), "r"(bytes), "r"(smem_u32(bbar + b))
+            : "memory");
+      }
+      return;
+    }
+    bused[b] = false;
     if constexpr (COAL)
-      async_window_cc<R, NT>(cc, rev_src(a, i), e0, a.g, sm.ubuf + (size_t)b * UB, (uint32_t)(b * UB * 8), fast_off);
+      async_window_cc<R, NT>(cc, src, e0, a.g, sm.ubuf + (size_t)b * UB, (uint32_t)(b * UB * 8), fast_off);
     else
-      async_window<COAL, R, NT>(rev_src(a, i), e0, a.g, sm.ubuf + (size_t)b * UB, fast_off);
+      async_window<COAL, R, NT>(src, e0, a.g, sm.ubuf + (size_t)b * UB, fast_off);
+  };
+  auto window_wait = [&](int b) {  // buffer b's copy has landed (and the warp may reuse the other)
+    if (bused[b]) {
+      mbar_wait_parity(bbar + b, bph[b]);
+      bph[b] ^= 1u;
+    } else {
+      cp_async_wait_all();
+    }
+    __syncwarp();
   };
   window(s1 - 1, (s1 - 1) % PIPE);
   if (PIPE == 3 && s1 - 2 >= s0)
@@ -464,11 +506,12 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   for (int l = s1 - 1; l >= s0; --l) {
     const int li = l - s0;
     const int ph = s1 - 1 - l;  // barrier phase of this step
-    if (PIPE == 3 && l > s0)
+    if (PIPE == 3 && l > s0) {
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // u^(l) landed, u^(l-1) may be in flight
-    else
-      cp_async_wait_all();  // own u^(l) slots landed
-    if (COAL) __syncwarp();  // ... and the warp's cooperative copies (and WAR on reuse)
+      if (COAL) __syncwarp();
+    } else {
+      window_wait(l % PIPE);  // u^(l) landed (bulk: mbarrier transaction count; else cp.async)
+    }
     // prefetch u^(l-PIPE+1) into a free buffer (this thread's own slots, consumed later)
     if (l - (PIPE - 1) >= s0)
       window(l - (PIPE - 1), (l - (PIPE - 1)) % PIPE);
@@ -585,8 +628,8 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * re
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // carve-up (16-byte aligned regions; mirrored by rev_smem() on the host)
   RevSmem sm;
-  sm.bar = reinterpret_cast<uint64_t*>(smem_raw);                                    // 2*NW words
-  sm.ubuf = reinterpret_cast<f2x*>(smem_raw) + 2 * NW;                               // PIPE*RS*NT
+  sm.bar = reinterpret_cast<uint64_t*>(smem_raw);                                    // 4*NW words
+  sm.ubuf = reinterpret_cast<f2x*>(smem_raw) + 4 * NW;                               // PIPE*RS*NT
   sm.edge = sm.ubuf + (size_t)LDBP_REV_PIPE * rev_rs<rev_coal(KH), R>() * NT;                                           // 4*KH*NT
   sm.taps_adj = reinterpret_cast<TapP*>(sm.edge + (size_t)4 * (KH > 0 ? KH : 1) * NT);  // S*NTU
   sm.norm = reinterpret_cast<StepNorm*>(sm.taps_adj + S * NTU);                      // M
@@ -604,6 +647,10 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * re
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(sm.bar + threadIdx.x)),
                  "r"(LDBP_NB_WAIT ? 1 : NT / 32)
                  : "memory");
+  }
+  if (LDBP_REV_BULK && threadIdx.x < 2 * NW) {  // bulk-copy barriers [warp][buffer]: one arrival + tx bytes
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(sm.bar + 2 * NW + threadIdx.x)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (a.ptab) {
     load_ptab<NTU>(a.ptab, a.M, a.s0, a.s1, sm.norm, nullptr, sm.taps_adj, sm.gamma, sm.kj, sm.flag);
