@@ -197,7 +197,8 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
     y = torch.empty_like(x)
     trainer = None
     if train:
-        trainer = DataParallelLDBP(state=st, loss_grad_fn=lambda a, b: P.ldbp_loss_grad(a, b, st.taps, st.gamma, ws=ws))
+        trainer = DataParallelLDBP(state=st, loss_grad_fn=lambda a, b: P.ldbp_loss_grad(a, b, st.taps, st.gamma, ws=ws),
+                                   train_step_fn=lambda a, b: P.ldbp_train_step(st, a, b, ws=ws))
         trainer.set_local_samples(B * n)
 
     def step(xx, tt):
@@ -247,7 +248,13 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
         d["ms"] += kms
         d["launches"] += 1
         d["sample_steps"] += samples * nsteps
-    launches_per_step = P.launch_count(P.make_dims(B, n, M, T), _lib.OP_TRAIN_STEP if train else _lib.OP_FORWARD)
+    dims = P.make_dims(B, n, M, T)
+    if not train:
+        launches_per_step = P.launch_count(dims, _lib.OP_FORWARD)
+    elif world == 1:  # DataParallelLDBP.step -> ldbp_train_step
+        launches_per_step = P.launch_count(dims, _lib.OP_TRAIN_STEP)
+    else:  # loss_grad -> all_reduce (NCCL's kernel, not counted) -> adam_kernel
+        launches_per_step = P.launch_count(dims, _lib.OP_LOSS_GRAD) + 1
     gpu_launches = launches_per_step * steps
 
     # e2e: pinned host inputs -> device, step, device -> host read of the result, every step.
@@ -331,13 +338,13 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
     names = {_lib.K_FORWARD: "fwd_store_kernel" if store_all else "fwd_tile_kernel",
              _lib.K_BACKWARD: "bwd_segment_kernel",
              _lib.K_REDUCE: "reduce_partials_kernel+params_kernel" if store_all else "reduce_partials_kernel",
-             _lib.K_ADAM: "adam_kernel", _lib.K_REVERSE: "rev_tile_kernel"}
+             _lib.K_ADAM: "adam_kernel", _lib.K_REVERSE: "rev_tile_kernel", _lib.K_TINY: "tiny_train_kernel"}
     for k, v in per_kind.items():
         kernel_shares[names[k]] = {"share": round(v["ms"] / tot_ms, 4), "avg_ms": round(v["ms"] / v["launches"], 4),
                                    "launches": v["launches"]}
     if dom:
         kind, v = dom
-        ipss = instr_fwd(kh) if kind == _lib.K_FORWARD else instr_bwd(kh)
+        ipss = {_lib.K_FORWARD: instr_fwd(kh), _lib.K_TINY: instr_fwd(kh) + instr_bwd(kh)}.get(kind, instr_bwd(kh))
         avg_ms = v["ms"] / v["launches"]
         per_launch_instr = ipss * v["sample_steps"] / v["launches"]
         achieved = per_launch_instr / (avg_ms * 1e-3) / 1e12
@@ -354,9 +361,11 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
                 B=B, n=n, wall_s=t_wall1 - t_wall0, scaling=scaling, global_blocks=global_blocks(cfg, world, scaling))
 
 
-def graph_latency(cfg, reps=50):
-    """Per-step device time with the whole step (forward, or loss_grad + Adam) captured in one CUDA
-    graph and replayed back to back (graphs hide the launch cost of C1/C2)."""
+def graph_latency(cfg, reps=10, inner=20):
+    """Per-step device time with `inner` whole steps (forward, or ldbp_train_step) captured in one
+    CUDA graph, replayed back to back (graphs hide the launch cost of C1/C2).  Several
+    steps per graph, so that the host's per-replay submission cost (~10 us from Python) is not
+    what is measured."""
     import torch
 
     import paper_2010_14258_b200 as P
@@ -371,9 +380,8 @@ def graph_latency(cfg, reps=50):
     y = torch.empty_like(x)
 
     def step():
-        if train:
-            P.ldbp_loss_grad(x, tgt, st.taps, st.gamma, buf=buf, ws=ws)
-            P.ldbp_adam_update(st, buf, cfg["B"] * cfg["n"])
+        if train:  # the single-process training call (one fused launch when the problem is tiny)
+            P.ldbp_train_step(st, x, tgt, buf=buf, ws=ws)
         else:
             P.ldbp_forward(x, st.taps, st.gamma, out=y, ws=ws)
 
@@ -386,7 +394,8 @@ def graph_latency(cfg, reps=50):
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        step()
+        for _ in range(inner):
+            step()
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
@@ -396,7 +405,7 @@ def graph_latency(cfg, reps=50):
         g.replay()
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps * 1e3  # us
+    return e0.elapsed_time(e1) / (reps * inner) * 1e3  # us
 
 
 def traffic_from_profiles(cfg_name, kernel):

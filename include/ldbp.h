@@ -288,7 +288,8 @@ typedef enum ldbp_kernel_kind {
   LDBP_K_REVERSE = 5,   /* store-all reverse tile kernel (rows a5, a6, a8)         */
   LDBP_K_RX = 6,        /* receiver-chain loss kernels (NEXT-1)                    */
   LDBP_K_ESSM = 7,      /* ESSM step kernels (NEXT-4)                              */
-  LDBP_K_SSFM = 8       /* SSFM channel generator kernels (NEXT-2)                 */
+  LDBP_K_SSFM = 8,      /* SSFM channel generator kernels (NEXT-2)                 */
+  LDBP_K_TINY = 9       /* one-CTA fused training step of tiny problems (C1)      */
 } ldbp_kernel_kind;
 
 typedef struct ldbp_trace_record {

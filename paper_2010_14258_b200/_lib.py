@@ -44,7 +44,7 @@ EXPORTED = (
     "ldbp_ssfm_link",
 )
 
-K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM, K_REVERSE, K_RX, K_ESSM, K_SSFM = 1, 2, 3, 4, 5, 6, 7, 8
+K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM, K_REVERSE, K_RX, K_ESSM, K_SSFM, K_TINY = 1, 2, 3, 4, 5, 6, 7, 8, 9
 
 
 class LdbpDims(ctypes.Structure):

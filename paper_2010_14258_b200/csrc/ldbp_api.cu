@@ -21,6 +21,7 @@
 #include "ldbp_essm.cuh"
 #include "ldbp_ssfm.cuh"
 #include "ldbp_rx_exact.cuh"
+#include "ldbp_tiny.cuh"
 
 using FwdFn = void (*)(const ldbp::FwdArgs);
 using BwdFn = void (*)(const ldbp::BwdArgs);
@@ -500,6 +501,99 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
   p.tile.nthreads = nthr;  // the kernel's layout is compiled for exactly this many threads
   return p;
 }
+
+// Tiny problems (BASELINE C1): the whole training step in one cluster (ldbp_tiny.cuh).  B >= 8:
+// 8 CTAs own whole blocks; B < 8: each block split into S segments of >= 256 samples (C = B S
+// <= 16 CTAs, DSMEM halos).  At most kTinyPer samples per thread, <= 200 KB shared memory.
+// Measured (profiles/r02_tiny_sweep.txt, 20 steps per CUDA graph, T = 3): one step of the fused
+// kernel costs ~5.5 us + ~1.35 us per model step (a latency chain: two barriers and two
+// shared-memory round trips per model step), the segment schedule ~10.3 us + ~0.5 us per step;
+// the fused kernel wins up to M ~ 5 (C1, M = 4: 11.0 vs 12.5 us).
+constexpr int kTinyAutoMaxSteps = 5;
+
+struct TinyPlan {
+  bool ok = false;
+  int C = 1, S = 1, nrows = 1, lenmax = 0, nthr = 32;
+  size_t smem = 0;
+};
+
+TinyPlan plan_tiny(const ldbp_dims* d, int max_cluster) {
+  TinyPlan p;
+  // LDBP_TINY: 0 off, 1 (default) when M <= kTinyAutoMaxSteps, 2 whenever it fits
+  const int mode = env_int("LDBP_TINY", 1);
+  if (mode == 0 || (d->flags & LDBP_CHECK_FINITE)) return p;
+  if (mode == 1 && d->steps > kTinyAutoMaxSteps) return p;
+  if (d->batch <= 0 || d->n <= 0 || d->batch * d->n > (int64_t)1 << 24) return p;
+  const int kh = (d->taps - 1) / 2;
+  if (d->batch >= 8 || max_cluster < d->batch) {
+    p.C = (int)std::min<int64_t>(max_cluster, d->batch);
+    p.nrows = (int)cdiv(d->batch, p.C);
+    p.lenmax = (int)d->n;
+  } else {
+    int S = (int)std::min<int64_t>(max_cluster / d->batch, d->n / 256);
+    while (S > 1 && d->n / S < std::max(kh, 1)) --S;
+    p.S = std::max(S, 1);
+    p.C = (int)d->batch * p.S;
+    p.lenmax = (int)cdiv(d->n, p.S);
+  }
+  const int64_t per_cta = (int64_t)p.nrows * p.lenmax;
+  if (per_cta > (int64_t)ldbp::kTinyPer * ldbp::kTinyMaxThreads) return p;
+  p.nthr = (int)std::min<int64_t>(ldbp::kTinyMaxThreads, cdiv(per_cta, 32) * 32);
+  p.smem = ldbp::tiny_smem_bytes(p.nrows, p.lenmax, d->steps, d->taps);
+  p.ok = p.smem <= (size_t)200 * 1024;
+  return p;
+}
+
+void (*tiny_kernel(int kh, bool precise))(const ldbp::TinyArgs) {
+  using ldbp::tiny_train_kernel;
+  static void (*const kerns[2][8])(const ldbp::TinyArgs) = {
+      {tiny_train_kernel<0, false>, tiny_train_kernel<1, false>, tiny_train_kernel<2, false>,
+       tiny_train_kernel<3, false>, tiny_train_kernel<4, false>, tiny_train_kernel<5, false>,
+       tiny_train_kernel<6, false>, tiny_train_kernel<7, false>},
+      {tiny_train_kernel<0, true>, tiny_train_kernel<1, true>, tiny_train_kernel<2, true>, tiny_train_kernel<3, true>,
+       tiny_train_kernel<4, true>, tiny_train_kernel<5, true>, tiny_train_kernel<6, true>, tiny_train_kernel<7, true>}};
+  return kerns[precise ? 1 : 0][kh];
+}
+
+// Largest cluster the tiny kernels may use on this device: 16 (non-portable) when a 16-CTA
+// cluster of the largest tiny CTAs is schedulable, else 8.  Cached per device.
+int tiny_max_cluster() {
+  static std::atomic<int> cached[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 8;
+  int v = cached[dev].load();
+  if (v) return v;
+  v = 8;
+  void (*k)(const ldbp::TinyArgs) = tiny_kernel(1, false);
+  if (cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(ldbp::kTinyMaxThreads);
+    cfg.dynamicSmemBytes = 200 * 1024;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 16;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)k, &cfg) == cudaSuccess && nclusters > 0) v = 16;
+  }
+  cudaGetLastError();
+  cached[dev].store(v);
+  return v;
+}
+
+// LDBP_TINY_MAX_CLUSTER caps the cluster (and so the segments per block) for experiments.
+int tiny_cluster_cap(const ldbp_dims* d) {
+  const int cap = d->batch < 8 ? tiny_max_cluster() : 8;
+  return std::max(1, std::min(cap, env_int("LDBP_TINY_MAX_CLUSTER", cap)));
+}
+
+bool use_tiny(const ldbp_dims* d) { return plan_tiny(d, tiny_cluster_cap(d)).ok; }
 
 // Which training path: 1 = store-all activations + fused reverse (default when the activations
 // fit the budget), 0 = checkpoint + recompute segments (memory-lean fallback).
@@ -1237,6 +1331,7 @@ int ldbp_launch_count(const ldbp_dims* d, int op, int* launches) {
   if (!launches) return fail(LDBP_EINVAL, "launches is NULL");
   if (d->batch == 0) { *launches = (op == LDBP_OP_FORWARD) ? 0 : 1; return LDBP_OK; }
   if (op == LDBP_OP_FORWARD) { *launches = plan_fwd_segments(d->steps, (d->taps - 1) / 2).segs; return LDBP_OK; }
+  if (op != LDBP_OP_BACKWARD && use_tiny(d)) { *launches = 1; return LDBP_OK; }  // fused (Adam included)
   if (use_store_all(d)) {
     const OverlapPlan o = plan_overlap(d, true);
     auto chain = [&](const ldbp_dims* dc, bool two_params) {
@@ -1330,6 +1425,86 @@ int ldbp_backward(const ldbp_dims* d, const void* x, const void* gy, const void*
                             (float2*)gx_or_null, (unsigned char*)ws, p, w, st, nullptr, dtaps, dgamma);
 }
 
+// Adam arguments (validated) shared by ldbp_adam_update and the fused tiny training step.
+int fill_adam(const ldbp_dims* d, const double* buf, double n_global, double* master, double* m, double* v, int64_t t,
+              double lr, double b1, double b2, double eps, const uint8_t* mask, const uint8_t* glearn,
+              void* taps_out, float* gamma_out, ldbp::AdamArgs* a) {
+  LDBP_TRY(check_ptr(buf, "buf", 8));
+  LDBP_TRY(check_ptr(master, "master", 8));
+  LDBP_TRY(check_ptr(m, "m", 8));
+  LDBP_TRY(check_ptr(v, "v", 8));
+  LDBP_TRY(check_ptr(taps_out, "taps_out", 8));
+  LDBP_TRY(check_ptr(gamma_out, "gamma_out", 4));
+  if (!(n_global > 0)) return fail(LDBP_EINVAL, "n_global must be > 0");
+  if (t < 1) return fail(LDBP_EINVAL, "t must be >= 1");
+  if (!(lr > 0) || !(b1 >= 0 && b1 < 1) || !(b2 >= 0 && b2 < 1) || !(eps > 0))
+    return fail(LDBP_EINVAL, "bad Adam hyper-parameters");
+  a->buf = buf;
+  a->inv_n = 1.0 / n_global;
+  a->master = master;
+  a->m = m;
+  a->v = v;
+  a->lr = lr;
+  a->b1 = b1;
+  a->b2 = b2;
+  a->eps = eps;
+  a->bc1 = 1.0 - pow(b1, (double)t);
+  a->bc2 = 1.0 - pow(b2, (double)t);
+  a->mask = mask;
+  a->glearn = glearn;
+  a->taps_out = (float2*)taps_out;
+  a->gamma_out = gamma_out;
+  a->M = d->steps;
+  a->T = d->taps;
+  return LDBP_OK;
+}
+
+int launch_tiny(const ldbp_dims* d, const float2* x, const float2* target, const float2* taps, const float* gamma,
+                const uint8_t* mask, double* buf, const ldbp::AdamArgs* adam, cudaStream_t st) {
+  const TinyPlan p = plan_tiny(d, tiny_cluster_cap(d));
+  if (!p.ok) return fail(LDBP_EINVAL, "tiny_train_kernel: problem too large");
+  ldbp::TinyArgs a;
+  a.x = x;
+  a.target = target;
+  a.taps = taps;
+  a.gamma = gamma;
+  a.mask = mask;
+  a.buf = buf;
+  a.B = (int)d->batch;
+  a.n = (int)d->n;
+  a.M = d->steps;
+  a.S = p.S;
+  a.lenmax = p.lenmax;
+  a.nrows = p.nrows;
+  a.sym = (d->flags & LDBP_SYMMETRIC) ? 1 : 0;
+  a.precise = (d->flags & LDBP_PRECISE) ? 1 : 0;
+  a.seed_scale = 2.0f;
+  a.do_adam = adam != nullptr;
+  if (adam) a.adam = *adam;
+  void (*kern)(const ldbp::TinyArgs) = tiny_kernel((d->taps - 1) / 2, a.precise != 0);
+  cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  if (p.C > 8) cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.C);
+  cfg.blockDim = dim3((unsigned)p.nthr);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  {
+    TraceScope ts(LDBP_K_TINY, d->steps, d->batch * d->n, st);
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+  }
+  if (e != cudaSuccess) return fail(LDBP_ECUDA, "tiny_train_kernel launch: %s", cudaGetErrorString(e));
+  return cuda_check("tiny_train_kernel launch");
+}
+
 int ldbp_loss_grad(const ldbp_dims* d, const void* x, const void* target, const void* taps, const float* gamma,
                    const uint8_t* mask, double* buf, void* ws, size_t ws_bytes, void* cuda_stream) {
   g_err[0] = 0;
@@ -1341,6 +1516,8 @@ int ldbp_loss_grad(const ldbp_dims* d, const void* x, const void* target, const 
   LDBP_TRY(check_ptr(target, "target", 8));
   LDBP_TRY(check_ptr(taps, "taps", 8));
   LDBP_TRY(check_ptr(gamma, "gamma", 4));
+  if (use_tiny(d))
+    return launch_tiny(d, (const float2*)x, (const float2*)target, (const float2*)taps, gamma, mask, buf, nullptr, st);
   if (use_store_all(d)) {
     const OverlapPlan o = plan_overlap(d, true);
     if (o.K > 1) {
@@ -1373,34 +1550,8 @@ int ldbp_adam_update(const ldbp_dims* d, const double* buf, double n_global, dou
                      const uint8_t* glearn, void* taps_out, float* gamma_out, void* cuda_stream) {
   g_err[0] = 0;
   LDBP_TRY(validate_dims(d));
-  LDBP_TRY(check_ptr(buf, "buf", 8));
-  LDBP_TRY(check_ptr(master, "master", 8));
-  LDBP_TRY(check_ptr(m, "m", 8));
-  LDBP_TRY(check_ptr(v, "v", 8));
-  LDBP_TRY(check_ptr(taps_out, "taps_out", 8));
-  LDBP_TRY(check_ptr(gamma_out, "gamma_out", 4));
-  if (!(n_global > 0)) return fail(LDBP_EINVAL, "n_global must be > 0");
-  if (t < 1) return fail(LDBP_EINVAL, "t must be >= 1");
-  if (!(lr > 0) || !(b1 >= 0 && b1 < 1) || !(b2 >= 0 && b2 < 1) || !(eps > 0))
-    return fail(LDBP_EINVAL, "bad Adam hyper-parameters");
   ldbp::AdamArgs a;
-  a.buf = buf;
-  a.inv_n = 1.0 / n_global;
-  a.master = master;
-  a.m = m;
-  a.v = v;
-  a.lr = lr;
-  a.b1 = b1;
-  a.b2 = b2;
-  a.eps = eps;
-  a.bc1 = 1.0 - pow(b1, (double)t);
-  a.bc2 = 1.0 - pow(b2, (double)t);
-  a.mask = mask;
-  a.glearn = glearn;
-  a.taps_out = (float2*)taps_out;
-  a.gamma_out = gamma_out;
-  a.M = d->steps;
-  a.T = d->taps;
+  LDBP_TRY(fill_adam(d, buf, n_global, master, m, v, t, lr, b1, b2, eps, mask, glearn, taps_out, gamma_out, &a));
   const int total = 2 * d->steps * d->taps + d->steps;
   {
     TraceScope ts(LDBP_K_ADAM, d->steps, 0, (cudaStream_t)cuda_stream);
@@ -1413,6 +1564,18 @@ int ldbp_train_step(const ldbp_dims* d, const void* x, const void* target, void*
                     double* master, double* m, double* v, int64_t t, double lr, double b1, double b2, double eps,
                     const uint8_t* mask, const uint8_t* glearn, double* buf, void* ws, size_t ws_bytes,
                     void* cuda_stream) {
+  if (d && validate_dims(d) == LDBP_OK && d->batch > 0 && use_tiny(d)) {  // one launch: loss, gradient, Adam
+    g_err[0] = 0;
+    LDBP_TRY(check_ptr(x, "x", 8));
+    LDBP_TRY(check_ptr(target, "target", 8));
+    LDBP_TRY(check_ptr(taps_work, "taps", 8));
+    LDBP_TRY(check_ptr(gamma_work, "gamma", 4));
+    ldbp::AdamArgs a;
+    LDBP_TRY(fill_adam(d, buf, (double)d->batch * (double)d->n, master, m, v, t, lr, b1, b2, eps, mask, glearn,
+                       taps_work, gamma_work, &a));
+    return launch_tiny(d, (const float2*)x, (const float2*)target, (const float2*)taps_work, gamma_work, mask, buf,
+                       &a, (cudaStream_t)cuda_stream);
+  }
   LDBP_TRY(ldbp_loss_grad(d, x, target, taps_work, gamma_work, mask, buf, ws, ws_bytes, cuda_stream));
   const double n_global = (double)d->batch * (double)d->n;
   if (d->batch == 0) return LDBP_OK;

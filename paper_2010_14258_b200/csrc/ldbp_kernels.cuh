@@ -1840,41 +1840,52 @@ struct AdamArgs {
   int M, T;
 };
 
+// One parameter's update (shared by adam_kernel and the fused tiny step: identical arithmetic).
+// g is the raw (unscaled) gradient; th/m/v the current master, first and second moments.
+// frozen / zero: the mask (zero: masked tap, forced to 0) and the non-learnable gamma' flags.
+__device__ __forceinline__ void adam_elem_flags(const AdamArgs& a, int i, double g, double th, double m0, double v0,
+                                                bool frozen, bool zero) {
+  const int ntap = 2 * a.M * a.T;
+  if (zero) {
+    th = 0.0;
+    a.m[i] = 0.0;
+    a.v[i] = 0.0;
+  } else if (!frozen) {
+    g *= a.inv_n;
+    const double m = a.b1 * m0 + (1.0 - a.b1) * g;
+    const double v = a.b2 * v0 + (1.0 - a.b2) * g * g;
+    a.m[i] = m;
+    a.v[i] = v;
+    const double mh = m / a.bc1, vh = v / a.bc2;
+    th -= a.lr * mh / (sqrt(vh) + a.eps);
+  }
+  a.master[i] = th;
+  if (i < ntap) {
+    float* to = reinterpret_cast<float*>(a.taps_out);
+    to[i] = (float)th;
+  } else {
+    a.gamma_out[i - ntap] = (float)th;
+  }
+}
+
+__device__ __forceinline__ void adam_elem(const AdamArgs& a, int i, double g, double th, double m0, double v0) {
+  const int ntap = 2 * a.M * a.T;
+  bool frozen, zero = false;
+  if (i < ntap) {
+    frozen = a.mask && !a.mask[i >> 1];
+    zero = frozen;
+  } else {
+    frozen = a.glearn && !a.glearn[i - ntap];
+  }
+  adam_elem_flags(a, i, g, th, m0, v0, frozen, zero);
+}
+
 __global__ void adam_kernel(const AdamArgs a) {
   const int ntap = 2 * a.M * a.T;
   const int total = ntap + a.M;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    bool frozen, zero = false;
-    double g;
-    if (i < ntap) {
-      g = a.buf[1 + a.M + i];
-      frozen = a.mask && !a.mask[i >> 1];
-      zero = frozen;
-    } else {
-      g = a.buf[1 + (i - ntap)];
-      frozen = a.glearn && !a.glearn[i - ntap];
-    }
-    double th = a.master[i];
-    if (zero) {
-      th = 0.0;
-      a.m[i] = 0.0;
-      a.v[i] = 0.0;
-    } else if (!frozen) {
-      g *= a.inv_n;
-      const double m = a.b1 * a.m[i] + (1.0 - a.b1) * g;
-      const double v = a.b2 * a.v[i] + (1.0 - a.b2) * g * g;
-      a.m[i] = m;
-      a.v[i] = v;
-      const double mh = m / a.bc1, vh = v / a.bc2;
-      th -= a.lr * mh / (sqrt(vh) + a.eps);
-    }
-    a.master[i] = th;
-    if (i < ntap) {
-      float* to = reinterpret_cast<float*>(a.taps_out);
-      to[i] = (float)th;
-    } else {
-      a.gamma_out[i - ntap] = (float)th;
-    }
+    const double g = i < ntap ? a.buf[1 + a.M + i] : a.buf[1 + (i - ntap)];
+    adam_elem(a, i, g, a.master[i], a.m[i], a.v[i]);
   }
 }
 

@@ -35,6 +35,10 @@ class DataParallelLDBP:
     loss_grad_fn: Optional[Callable] = None
     adam_fn: Optional[Callable] = None
     n_global: float = 0.0
+    # optional fused single-process step ``train_step_fn(x, target) -> buf`` (ldbp_train_step: one
+    # launch for tiny problems); used when world == 1, where there is no exchange between the
+    # gradient and Adam
+    train_step_fn: Optional[Callable] = None
 
     def __post_init__(self):
         if self.loss_grad_fn is None or self.adam_fn is None:
@@ -66,6 +70,8 @@ class DataParallelLDBP:
         """loss_grad (local) -> all_reduce(SUM) -> Adam.  Returns the reduced buffer."""
         if self.n_global <= 0:
             raise RuntimeError("call set_local_samples() first")
+        if self.train_step_fn is not None and self.world == 1:
+            return self.train_step_fn(x_local, target_local)
         buf = self.loss_grad_fn(x_local, target_local)
         if dist.is_initialized() and self.world > 1:
             dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)

@@ -96,6 +96,25 @@ def test_store_all_schedule_workspace(L):
         del os.environ["LDBP_BWD_MODE"]
 
 
+def test_tiny_fused_step_plan(L):
+    """C1-sized problems (M <= 5, the per-CTA activations fit shared memory) train in ONE launch
+    (ldbp_tiny.cuh); LDBP_TINY=0 restores the segment schedule; over-size or long models never
+    take the fused kernel by default."""
+    lib = L.lib
+    nl = ctypes.c_int(0)
+    d1 = L.dims(4, 1024, 4, 3, 1)  # C1
+    for op in (2, 3):
+        assert lib.ldbp_launch_count(ctypes.byref(d1), op, ctypes.byref(nl)) == 0 and nl.value == 1
+    assert lib.ldbp_launch_count(ctypes.byref(d1), 1, ctypes.byref(nl)) == 0 and nl.value > 1  # backward: no
+    os.environ["LDBP_TINY"] = "0"
+    try:
+        assert lib.ldbp_launch_count(ctypes.byref(d1), 3, ctypes.byref(nl)) == 0 and nl.value > 2
+    finally:
+        del os.environ["LDBP_TINY"]
+    for d in (L.dims(4, 1024, 8, 3, 1), L.dims(64, 4096, 4, 3, 1), L.dims(2, 1 << 16, 2, 3, 1)):
+        assert lib.ldbp_launch_count(ctypes.byref(d), 3, ctypes.byref(nl)) == 0 and nl.value > 1
+
+
 def test_rx_essm_ssfm_validation(L):
     """The NEXT-row entry points validate shapes and pointers before any launch."""
     lib = L.lib

@@ -149,6 +149,7 @@ MODES = ["0", "1"]
 
 def set_mode(monkeypatch, mode, cmax):
     monkeypatch.setenv("LDBP_BWD_MODE", mode)
+    monkeypatch.setenv("LDBP_TINY", "0")  # the schedule under test, not the fused C1 kernel
     if cmax:
         monkeypatch.setenv("LDBP_BWD_MAX_STEPS", cmax)
         monkeypatch.setenv("LDBP_REV_MAX_STEPS", cmax)
@@ -203,6 +204,7 @@ def test_loss_grad_parity(P, monkeypatch, sym, masked, cmax, mode):
 def test_gradient_gauge_identities_gpu(P, monkeypatch, mode):
     """P6/P7 on the GPU gradients (Remark 4): exact in exact arithmetic, <= 1e-4 relative here."""
     monkeypatch.setenv("LDBP_BWD_MODE", mode)
+    monkeypatch.setenv("LDBP_TINY", "0")
     B, n, M, T = 8, 4096, 10, 5
     x = li.gaussian_blocks(41, range(B), n, 2e-3)
     tgt = li.gaussian_blocks(41, range(B), n, 2e-3, purpose="target")
@@ -256,7 +258,10 @@ def test_train_step_is_loss_grad_plus_adam(P):
         b2 = P.ldbp_loss_grad(x, tgt, s2.taps, s2.gamma)
         P.ldbp_adam_update(s2, b2, B * n)
         assert torch.equal(b1, b2)
-    assert torch.equal(s1.master, s2.master) and torch.equal(s1.taps, s2.taps)
+    # same gradient; Adam in the fused tiny kernel (C1-sized problems) or adam_kernel: the same
+    # adam_elem arithmetic, compiled into two kernels (fp64 contraction may differ by an ulp)
+    assert rel(s1.master.cpu().numpy(), s2.master.cpu().numpy()) <= 1e-14
+    assert rel(s1.taps.cpu().numpy(), s2.taps.cpu().numpy()) <= 1e-7
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -264,6 +269,7 @@ def test_determinism_and_shard_sum(P, monkeypatch, mode):
     """Fixed-order reductions: bitwise repeatable; the data-parallel sum of per-shard buffers
     equals the full-batch buffer (gradient is linear in the blocks; §8(e))."""
     monkeypatch.setenv("LDBP_BWD_MODE", mode)
+    monkeypatch.setenv("LDBP_TINY", "0")
     B, n, M, T = 8, 3000, 6, 5
     x = li.gaussian_blocks(71, range(B), n, 1e-3)
     tgt = li.gaussian_blocks(71, range(B), n, 1e-3, purpose="target")
@@ -329,6 +335,7 @@ def test_backward_unnormalised_path(P, monkeypatch, mode):
     """Taps whose centre tap is ~0 make the h0-normalised kernels fall back to the plain folded
     FIR (launch-wide, decided on the device); gradients must still match the oracle."""
     monkeypatch.setenv("LDBP_BWD_MODE", mode)
+    monkeypatch.setenv("LDBP_TINY", "0")
     B, n, M, T = 2, 900, 4, 5
     x = li.gaussian_blocks(81, range(B), n, 1e-3)
     gy = li.gaussian_blocks(81, range(B), n, 1.0, purpose="grad")
@@ -349,6 +356,7 @@ def test_backward_unnormalised_path(P, monkeypatch, mode):
 @pytest.mark.parametrize("mode", MODES)
 def test_precise_backward(P, monkeypatch, mode):
     monkeypatch.setenv("LDBP_BWD_MODE", mode)
+    monkeypatch.setenv("LDBP_TINY", "0")
     B, n, M, T = 2, 1200, 5, 7
     x = li.gaussian_blocks(82, range(B), n, 1e-3)
     tgt = li.gaussian_blocks(82, range(B), n, 1e-3, purpose="target")
@@ -457,6 +465,7 @@ def pruned_model(seed, M, T, kh_steps):
 ])
 def test_variable_tap_lengths(P, monkeypatch, mode, B, n, M, T, kh_steps):
     monkeypatch.setenv("LDBP_BWD_MODE", mode)
+    monkeypatch.setenv("LDBP_TINY", "0")
     monkeypatch.setenv("LDBP_STORE_ALL_MIN_SAMPLES", "0")
     taps, gamma, mask = pruned_model(91, M, T, kh_steps)
     x = li.gaussian_blocks(91, range(B), n, 1e-3)
@@ -485,6 +494,7 @@ def test_sharding_bit_identity(P, monkeypatch, mode):
     of the shards sum to the full buffer up to the grouping of the per-CTA fp32 partial sums (the
     tiles differ between shardings; every grouping is a valid fp32 sum, ~1e-9 apart)."""
     monkeypatch.setenv("LDBP_BWD_MODE", mode)
+    monkeypatch.setenv("LDBP_TINY", "0")
     monkeypatch.setenv("LDBP_STORE_ALL_MIN_SAMPLES", "0")
     B, n, M, T = 8, 6000, 10, 9
     x = dev(li.gaussian_blocks(95, range(B), n, 1e-3))
@@ -517,6 +527,7 @@ def test_check_finite_reports_first_step(P, monkeypatch):
     ht, gt = dev(taps), dev(gamma, np.float32)
     assert torch.equal(P.ldbp_forward(x, ht, gt, check_finite=True), P.ldbp_forward(x, ht, gt))
     monkeypatch.setenv("LDBP_BWD_MODE", "1")  # checked training calls run the store-all schedule
+    monkeypatch.setenv("LDBP_TINY", "0")  # (the unchecked call too, so that both are the same schedule)
     assert torch.equal(P.ldbp_loss_grad(x, tgt, ht, gt, check_finite=True), P.ldbp_loss_grad(x, tgt, ht, gt))
     bad = taps.copy()
     bad[2] *= 1e25  # |a| ~ 1e22 after step 3: |a|^2 overflows -> NaN phase
@@ -558,3 +569,125 @@ def test_repeated_runs_bitwise_identical(P, monkeypatch, env):
     r = O.loss_grad(r32(x.cpu().numpy()), r32(tgt.cpu().numpy()), r32(taps), r32(gamma), symmetric=True)
     assert abs(ref[0].item() - r[0]) <= OUT_TOL * r[0]
     assert rel(ref[1:].numpy(), r[1:]) <= GRAD_TOL
+
+
+# ---- C1: the one-CTA fused training step (ldbp_tiny.cuh) ----
+K_TINY = 9
+TINY_CASES = [
+    # (B, n, M, T, sym, masked)
+    (4, 1024, 4, 3, True, False),    # BASELINE C1 exactly (4 segments per block, 16-CTA cluster)
+    (2, 777, 3, 5, False, False),    # general taps, odd n: 3 uneven segments per block
+    (3, 500, 5, 9, True, True),      # pruning mask
+    (1, 5, 2, 5, True, False),       # n == T
+    (2, 16, 6, 7, False, True),      # blocks shorter than the filter span (several wraps)
+    (2, 64, 1, 1, True, False),      # T = 1, M = 1
+    (1, 1000, 8, 15, True, False),   # Kh = 7 (the largest T)
+    (11, 300, 3, 5, True, False),    # B > 8: 8-CTA cluster, CTAs 0-2 own two blocks
+    (9, 64, 4, 3, False, True),      # ragged ownership, general taps, mask
+    (8, 2048, 2, 9, True, False),    # whole blocks, 2 samples per thread
+    (1, 4000, 3, 15, True, True),    # one block in 15 uneven segments (266/267), Kh = 7 halos over DSMEM
+    (3, 300, 4, 7, False, False),    # blocks too short to split: whole blocks, C = 3
+]
+
+
+@pytest.mark.parametrize("B,n,M,T,sym,masked", TINY_CASES)
+def test_tiny_fused_loss_grad_vs_oracle(P, monkeypatch, B, n, M, T, sym, masked):
+    monkeypatch.setenv("LDBP_TINY", "2")  # whenever it fits (the default picks it for M <= 5)
+    """Problems whose per-CTA activations fit shared memory run as ONE cluster launch (trace kind 9);
+    parity with the oracle at the §8(c) tolerances, masked taps exactly 0, and agreement with the
+    multi-launch segment schedule (LDBP_TINY=0) to the same tolerances."""
+    x = li.gaussian_blocks(131, range(B), n, 1e-3)
+    tgt = li.gaussian_blocks(131, range(B), n, 1e-3, purpose="target")
+    taps, gamma = model(131, M, T, sym)
+    mask = None
+    if masked:
+        kh = (T - 1) // 2
+        mask = np.ones((M, T), np.uint8)
+        mask[0, [0, T - 1]] = 0
+        if M > 2 and kh > 1:
+            mask[2, [0, 1, T - 2, T - 1]] = 0
+        taps = taps * mask
+    mk = None if mask is None else torch.from_numpy(mask).cuda()
+    with P.api.trace() as tr:
+        buf = P.ldbp_loss_grad(dev(x), dev(tgt), dev(taps), dev(gamma, np.float32), symmetric=sym, mask=mk)
+        torch.cuda.synchronize()
+    assert [r[0] for r in tr.records] == [K_TINY]
+    assert P.launch_count(P.make_dims(B, n, M, T, sym), P._lib.OP_LOSS_GRAD) == 1
+    buf = buf.cpu().numpy()
+    ref = O.loss_grad(r32(x), r32(tgt), r32(taps), r32(gamma), mask=mask, symmetric=sym)
+    assert abs(buf[0] - ref[0]) <= OUT_TOL * ref[0]
+    for i in range(M):
+        assert abs(buf[1 + i] - ref[1 + i]) <= GRAD_TOL * abs(ref[1 + i]) + 1e-12 * np.abs(ref[1:1 + M]).max(), i
+    dt, rdt = buf[1 + M:].reshape(M, T, 2), ref[1 + M:].reshape(M, T, 2)
+    for i in range(M):
+        assert rel(dt[i], rdt[i]) <= GRAD_TOL, (i, rel(dt[i], rdt[i]))
+    if masked:
+        assert np.all(dt[mask == 0] == 0)
+    monkeypatch.setenv("LDBP_TINY", "0")
+    seg = P.ldbp_loss_grad(dev(x), dev(tgt), dev(taps), dev(gamma, np.float32), symmetric=sym, mask=mk).cpu().numpy()
+    assert abs(seg[0] - buf[0]) <= OUT_TOL * ref[0]
+    assert rel(seg[1 + M:], buf[1 + M:]) <= GRAD_TOL
+
+
+def test_tiny_fused_train_step(P):
+    """ldbp_train_step at C1 is ONE launch (loss, gradient, fold, Adam); equal to the tiny
+    loss_grad followed by ldbp_adam_update (same buffer bit for bit, fp64 master <= 1e-13), and its
+    first Adam step equals the oracle's Adam on the oracle gradient to the gradient tolerance."""
+    B, n, M, T = 4, 1024, 4, 3
+    x = dev(li.gaussian_blocks(137, range(B), n, 1e-3))
+    tgt = dev(li.gaussian_blocks(137, range(B), n, 1e-3, purpose="target"))
+    taps, gamma = model(137, M, T, True)
+    mask = np.ones((M, T), np.uint8)
+    mask[1, [0, 2]] = 0
+    gl = np.array([1, 0, 1, 1], np.uint8)
+    taps = taps * mask
+    s1 = P.TrainState.create(taps, gamma, mask=mask, gamma_learnable=gl)
+    s2 = P.TrainState.create(taps, gamma, mask=mask, gamma_learnable=gl)
+    for it in range(3):
+        with P.api.trace() as tr:
+            b1 = P.ldbp_train_step(s1, x, tgt)
+            torch.cuda.synchronize()
+        assert [r[0] for r in tr.records] == [K_TINY]
+        b2 = P.ldbp_loss_grad(x, tgt, s2.taps, s2.gamma, mask=s2.mask)
+        P.ldbp_adam_update(s2, b2, B * n)
+        assert torch.equal(b1, b2), it
+        assert rel(s1.master.cpu().numpy(), s2.master.cpu().numpy()) <= 1e-13
+        assert torch.equal(s1.taps, s2.taps) or rel(s1.taps.cpu().numpy(), s2.taps.cpu().numpy()) <= 1e-7
+    assert P.launch_count(P.make_dims(B, n, M, T), P._lib.OP_TRAIN_STEP) == 1
+    # first step against the oracle
+    s3 = P.TrainState.create(taps, gamma, mask=mask, gamma_learnable=gl)
+    P.ldbp_train_step(s3, x, tgt)
+    ref = O.loss_grad(r32(x.cpu().numpy()), r32(tgt.cpu().numpy()), r32(taps), r32(gamma), mask=mask, symmetric=True)
+    th0 = O.pack_params(r32(taps), r32(gamma))
+    th, _, _ = O.adam_update(ref, B * n, th0, np.zeros_like(th0), np.zeros_like(th0), 1, M, T, tap_mask=mask,
+                             gamma_learnable=gl)
+    # Adam's first step moves each parameter by ~lr sign(g): compare the step, not the value
+    step, rstep = s3.master.cpu().numpy() - th0, th - th0
+    assert rel(step, rstep) <= 1e-3
+
+
+def test_tiny_fused_train_step_cuda_graph(P):
+    """The fused C1 step captured in a CUDA graph (one kernel node) replays like eager calls."""
+    B, n, M, T = 4, 1024, 4, 3
+    x = dev(li.gaussian_blocks(139, range(B), n, 1e-3))
+    tgt = dev(li.gaussian_blocks(139, range(B), n, 1e-3, purpose="target"))
+    taps, gamma = model(139, M, T, True)
+    eager = P.TrainState.create(taps, gamma)
+    graphed = P.TrainState.create(taps, gamma)
+    buf = torch.empty(1 + M + 2 * M * T, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        P.ldbp_loss_grad(x, tgt, graphed.taps, graphed.gamma, buf=buf)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    graphed.t = 0
+    with torch.cuda.graph(g):
+        P.ldbp_train_step(graphed, x, tgt, buf=buf)
+    graphed.t = 0
+    b_e = P.ldbp_train_step(eager, x, tgt)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(b_e, buf)
+    assert torch.equal(eager.master, graphed.master)
