@@ -508,7 +508,8 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
 // Measured (profiles/r02_tiny_sweep.txt, 20 steps per CUDA graph, T = 3): one step of the fused
 // kernel costs ~5.5 us + ~1.35 us per model step (a latency chain: two barriers and two
 // shared-memory round trips per model step), the segment schedule ~10.3 us + ~0.5 us per step;
-// the fused kernel wins up to M ~ 5 (C1, M = 4: 11.0 vs 12.5 us).
+// the fused kernel wins up to M ~ 5 (C1, M = 4: 11.0 vs 12.5 us), and whenever the segment
+// schedule needs more than one recompute segment (M = 16: ~27 vs ~37 us).
 constexpr int kTinyAutoMaxSteps = 5;
 
 struct TinyPlan {
@@ -522,7 +523,7 @@ TinyPlan plan_tiny(const ldbp_dims* d, int max_cluster) {
   // LDBP_TINY: 0 off, 1 (default) when M <= kTinyAutoMaxSteps, 2 whenever it fits
   const int mode = env_int("LDBP_TINY", 1);
   if (mode == 0 || (d->flags & LDBP_CHECK_FINITE)) return p;
-  if (mode == 1 && d->steps > kTinyAutoMaxSteps) return p;
+  if (mode == 1 && d->steps > kTinyAutoMaxSteps && plan_bwd(d, false).K == 1) return p;
   if (d->batch <= 0 || d->n <= 0 || d->batch * d->n > (int64_t)1 << 24) return p;
   const int kh = (d->taps - 1) / 2;
   if (d->batch >= 8 || max_cluster < d->batch) {

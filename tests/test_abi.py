@@ -97,7 +97,8 @@ def test_store_all_schedule_workspace(L):
 
 
 def test_tiny_fused_step_plan(L):
-    """C1-sized problems (M <= 5, the per-CTA activations fit shared memory) train in ONE launch
+    """C1-sized problems (M <= 5 or more than one recompute segment, the per-CTA activations fit
+    shared memory) train in ONE launch
     (ldbp_tiny.cuh); LDBP_TINY=0 restores the segment schedule; over-size or long models never
     take the fused kernel by default."""
     lib = L.lib
@@ -111,6 +112,8 @@ def test_tiny_fused_step_plan(L):
         assert lib.ldbp_launch_count(ctypes.byref(d1), 3, ctypes.byref(nl)) == 0 and nl.value > 2
     finally:
         del os.environ["LDBP_TINY"]
+    d16 = L.dims(4, 1024, 16, 3, 1)  # two recompute segments in the segment schedule: fused instead
+    assert lib.ldbp_launch_count(ctypes.byref(d16), 3, ctypes.byref(nl)) == 0 and nl.value == 1
     for d in (L.dims(4, 1024, 8, 3, 1), L.dims(64, 4096, 4, 3, 1), L.dims(2, 1 << 16, 2, 3, 1)):
         assert lib.ldbp_launch_count(ctypes.byref(d), 3, ctypes.byref(nl)) == 0 and nl.value > 1
 
