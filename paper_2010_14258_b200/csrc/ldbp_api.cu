@@ -112,6 +112,7 @@ constexpr int kRxMaxSpsExact = 4;
   RevFn ldbp_get_rev_##K(bool sym, bool fast);      \
   RevFn ldbp_get_rev2_##K(bool fast);               \
   RevFn ldbp_get_rev3_##K(bool fast);               \
+  RevFn ldbp_get_rev4_##K(bool fast);               \
   ParFn ldbp_get_params_##K(bool sym);
 }  // namespace
 LDBP_DECL_GETTERS(0)
@@ -198,6 +199,19 @@ RevFn get_rev3(int kh, bool fast) {
     case 2: return ldbp_get_rev3_2(fast);
     case 4: return ldbp_get_rev3_4(fast);
     case 6: return ldbp_get_rev3_6(fast);
+  }
+  return nullptr;
+}
+
+RevFn get_rev4(int kh, bool fast) {
+  switch (kh) {
+    case 1: return ldbp_get_rev4_1(fast);
+    case 2: return ldbp_get_rev4_2(fast);
+    case 3: return ldbp_get_rev4_3(fast);
+    case 4: return ldbp_get_rev4_4(fast);
+    case 5: return ldbp_get_rev4_5(fast);
+    case 6: return ldbp_get_rev4_6(fast);
+    case 7: return ldbp_get_rev4_7(fast);
   }
   return nullptr;
 }
@@ -441,8 +455,15 @@ bool use_rev3(const ldbp_dims* d) {
          env_int("LDBP_REV3", 0) != 0;
 }
 
+// Shared-memory-adjoint reverse (ldbp_reverse4.cuh, symmetric taps, 1 <= Kh): LDBP_REV4=1/0 forces.
+bool use_rev4(const ldbp_dims* d) {
+  const int kh = (d->taps - 1) / 2;
+  return (d->flags & LDBP_SYMMETRIC) && kh >= 1 && !use_rev2(d) && !use_rev3(d) && env_int("LDBP_REV4", 0) != 0;
+}
+
 size_t rev_smem_any(const ldbp_dims* d, int steps) {
   const int kh = (d->taps - 1) / 2;
+  if (use_rev4(d)) return ldbp::rev4_smem_bytes(kh, steps, d->steps);
   if (use_rev3(d)) return ldbp::rev3_smem_bytes(kh, steps, d->steps);
   return use_rev2(d) ? ldbp::rev2_smem_bytes(kh, steps, d->steps)
                      : rev_smem(kh, d->flags & LDBP_SYMMETRIC, steps, d->steps);
@@ -452,6 +473,7 @@ RevFn get_rev_any(const ldbp_dims* d) {
   const int kh = (d->taps - 1) / 2;
   const bool fast = !(d->flags & LDBP_PRECISE);
   if (use_rev3(d)) return get_rev3(kh, fast);
+  if (use_rev4(d)) return get_rev4(kh, fast);
   return use_rev2(d) ? get_rev2(kh, fast) : get_rev(kh, d->flags & LDBP_SYMMETRIC, fast);
 }
 
@@ -459,13 +481,14 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
   RevPlan p;
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
-  const bool v2 = use_rev2(d), v3 = use_rev3(d);
+  const bool v2 = use_rev2(d), v3 = use_rev3(d), v4 = use_rev4(d);
   const int M = d->steps;
-  const int R = v2 ? ldbp::rev2_r(kh) : v3 ? ldbp::rev3_r(kh) : rev_r(kh);
+  const int R = v2 ? ldbp::rev2_r(kh) : v3 ? ldbp::rev3_r(kh) : v4 ? ldbp::rev4_r(kh) : rev_r(kh);
   // window slots per CTA (rev2: 30 owned lanes per warp + the two duplicate end lanes)
   const int slots = v2 ? ldbp::rev2_slots(ldbp::rev2_warps(kh)) : v3 ? 32 * ldbp::rev3_warps(kh)
-                                                                      : ldbp::rev_threads(kh);
-  const int nthr = v2 ? 32 * ldbp::rev2_warps(kh) : v3 ? 32 * ldbp::rev3_warps(kh) : ldbp::rev_threads(kh);
+                                                            : v4 ? ldbp::rev4_threads(kh) : ldbp::rev_threads(kh);
+  const int nthr = v2 ? 32 * ldbp::rev2_warps(kh) : v3 ? 32 * ldbp::rev3_warps(kh)
+                                                   : v4 ? ldbp::rev4_threads(kh) : ldbp::rev_threads(kh);
   p.V = 1 + 2 * ntaps_used(kh, sym);
   // cost model in step units: a launch of S steps costs S * window / (window - 2*H) plus a
   // fixed ~2 steps (prologue: staging, first load, seed), H = S*kh rounded up to whole slots;

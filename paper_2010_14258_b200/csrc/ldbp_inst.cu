@@ -61,3 +61,13 @@ RevFn LDBP_CAT(ldbp_get_rev3_, LDBP_KH)(bool fast) {
   return nullptr;
 #endif
 }
+
+RevFn LDBP_CAT(ldbp_get_rev4_, LDBP_KH)(bool fast) {
+#if LDBP_KH >= 1
+  constexpr int K = LDBP_KH;
+  return fast ? ldbp::rev4_tile_kernel<K, true> : ldbp::rev4_tile_kernel<K, false>;
+#else
+  (void)fast;
+  return nullptr;
+#endif
+}

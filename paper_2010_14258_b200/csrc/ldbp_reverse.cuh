@@ -81,6 +81,9 @@ __device__ __forceinline__ constexpr bool rev_vark() { return LDBP_REV_VARK && S
 #ifndef LDBP_REV_PIPE
 #define LDBP_REV_PIPE 2  // window-copy buffers of the reverse: 2 = prefetch one step ahead, 3 = two
 #endif
+#ifndef LDBP_REV_UNROLL2
+#define LDBP_REV_UNROLL2 0  // 1: two reverse steps per loop iteration (register renaming instead of moves)
+#endif
 #ifndef LDBP_NB_WAIT
 #define LDBP_NB_WAIT 0  // split step barrier: 1 = wait only for the neighbouring warps, 0 = CTA-wide phase
 #endif
@@ -384,12 +387,14 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   const bool wbulk = LDBP_REV_BULK && PIPE == 2 &&
                      __all_sync(kFull, fast_off >= 0 && fast_off == woff + (int64_t)lane * R);
   uint64_t* bbar = sm.bar + 2 * NW + 2 * warp;  // [warp][buffer]
-  bool bused[2] = {false, false};               // buffer b was filled by a bulk copy
-  unsigned bph[2] = {0u, 0u};                   // next phase parity of bbar[b]
+  // per-buffer state as register bit masks (bit b = buffer b; indexing small arrays with the
+  // runtime buffer number put them in local memory: STL/LDL in the step loop)
+  unsigned bused = 0u;  // buffer b was filled by a bulk copy
+  unsigned bph = 0u;    // next phase parity of bbar[b]
   auto window = [&](int i, int b) {  // async copy of u^(i) into window buffer b
     const float2* src = rev_src(a, i);
     if (wbulk && ((reinterpret_cast<uintptr_t>(src + woff)) & 15) == 0) {
-      bused[b] = true;
+      bused |= 1u << b;
       if (lane == 0) {
         f2x* dst = sm.ubuf + (size_t)b * UB + ubuf_idx<COAL, R, NT>(0, warp * 32);
         constexpr unsigned bytes = 32u * R * 8u;
@@ -405,16 +410,16 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
       }
       return;
     }
-    bused[b] = false;
+    bused &= ~(1u << b);
     if constexpr (COAL)
       async_window_cc<R, NT>(cc, src, e0, a.g, sm.ubuf + (size_t)b * UB, (uint32_t)(b * UB * 8), fast_off);
     else
       async_window<COAL, R, NT>(src, e0, a.g, sm.ubuf + (size_t)b * UB, fast_off);
   };
   auto window_wait = [&](int b) {  // buffer b's copy has landed (and the warp may reuse the other)
-    if (bused[b]) {
-      mbar_wait_parity(bbar + b, bph[b]);
-      bph[b] ^= 1u;
+    if ((bused >> b) & 1u) {
+      mbar_wait_parity(bbar + b, (bph >> b) & 1u);
+      bph ^= 1u << b;
     } else {
       cp_async_wait_all();
     }
@@ -503,6 +508,9 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
     if (LDBP_REV_DEFER_RED && pend_li >= 0) reduce_step(pend, pend_li);
   };
 
+#if LDBP_REV_UNROLL2
+#pragma unroll 2
+#endif
   for (int l = s1 - 1; l >= s0; --l) {
     const int li = l - s0;
     const int ph = s1 - 1 - l;  // barrier phase of this step
@@ -682,3 +690,4 @@ __global__ void __launch_bounds__(rev_threads(KH), 65536 / (rev_threads(KH) * re
 }  // namespace ldbp
 #include "ldbp_reverse2.cuh"
 #include "ldbp_reverse3.cuh"
+#include "ldbp_reverse4.cuh"

@@ -143,11 +143,17 @@ BWD_CASES = [
 ]
 
 
-# the two row-a7 schedules: 0 = checkpoint + recompute segments, 1 = store-all + fused reverse
-MODES = ["0", "1"]
+# the two row-a7 schedules: 0 = checkpoint + recompute segments, 1 = store-all + fused reverse;
+# "1r4" = store-all with the shared-memory-adjoint reverse kernel (ldbp_reverse4.cuh), "1rt" = with
+# the register-resident one (rev_tile_kernel)
+MODES = ["0", "1", "1r4", "1rt"]
 
 
 def set_mode(monkeypatch, mode, cmax):
+    if mode.startswith("1r"):
+        monkeypatch.setenv("LDBP_REV4", "1" if mode == "1r4" else "0")
+        monkeypatch.setenv("LDBP_STORE_ALL_MIN_SAMPLES", "0")
+        mode = "1"
     monkeypatch.setenv("LDBP_BWD_MODE", mode)
     monkeypatch.setenv("LDBP_TINY", "0")  # the schedule under test, not the fused C1 kernel
     if cmax:
@@ -541,6 +547,7 @@ def test_check_finite_reports_first_step(P, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{"LDBP_BWD_MODE": "1"}, {"LDBP_BWD_MODE": "0"}, {"LDBP_BWD_MODE": "1", "LDBP_REV3": "1"},
+                                 {"LDBP_BWD_MODE": "1", "LDBP_REV4": "1"}, {"LDBP_BWD_MODE": "1", "LDBP_REV4": "0"},
                                  {"LDBP_BWD_MODE": "1", "LDBP_OVERLAP": "3"}, {"LDBP_BWD_MODE": "1", "LDBP_REV2": "1"}])
 def test_repeated_runs_bitwise_identical(P, monkeypatch, env):
     """Race detector by repetition (compute-sanitizer is closed on this GPU pool): 12 repeated

@@ -63,15 +63,17 @@ def ls_model(spans, sps, T):
     return taps, g
 
 
+@pytest.mark.parametrize("rev4", ["0", "1"])  # reverse kernel: register-resident / shared-memory adjoint
 @pytest.mark.parametrize("name,B,n,spans,sps,T,kr,overlap", [
     ("C3", 512, 16384, 25, 2, 9, 2, 1),        # exactly the call bench.py times
     ("C3", 512, 16384, 25, 2, 9, 2, 4),        # the optional overlapped chunked schedule (LDBP_OVERLAP)
     ("C5-slice", 512, 32768, 25, 1, 3, 1, 1),  # > 1024 reverse CTAs: reduce_partials_pass1 runs
 ])
-def test_timed_training_call_vs_oracle_all_blocks(P, monkeypatch, name, B, n, spans, sps, T, kr, overlap):
+def test_timed_training_call_vs_oracle_all_blocks(P, monkeypatch, name, B, n, spans, sps, T, kr, overlap, rev4):
     from paper_2010_14258_b200 import channel
 
     monkeypatch.setenv("LDBP_OVERLAP", str(overlap))
+    monkeypatch.setenv("LDBP_REV4", rev4)
 
     idx = 3 if name == "C3" else 5
     # the bench's inputs: GPU SSFM link blocks (pool of 256 simulated blocks, shifted / rotated)
