@@ -37,6 +37,11 @@ namespace ldbp {
 #ifndef LDBP_REV4_NT
 #define LDBP_REV4_NT 128
 #endif
+#ifndef LDBP_REV4_ABL
+#define LDBP_REV4_ABL 0  // timing ablations (WRONG results; tuning only): 1 no warp reduction, 2 no NL
+                         // adjoint, 4 no step barrier, 8 no u window wait, 16 no tap-gradient sums,
+                         // 32 no FIR adjoint (g = ga)
+#endif
 #ifndef LDBP_REV4_PIPE
 #define LDBP_REV4_PIPE 1
 #endif
@@ -90,7 +95,7 @@ struct Rev4Smem {
   f2x* ubuf;        // [PIPE][NT*R] u^(l) windows (linear rows)
   TapP* taps_adj;   // [S][NTU]
   StepNorm* norm;   // [M]
-  float* red;       // [2][NW][V] (step parity)
+  float* red;       // [S][NW][V]
   float* lred;      // [NW]
   float* gamma;     // [S]
   int* flag;
@@ -135,44 +140,61 @@ __device__ __forceinline__ void rev4_load_pair(f2x (&w)[R + 2 * KH], const Rev4R
   }
 }
 
+#ifndef LDBP_REV4_G
+#define LDBP_REV4_G 3  // output pairs per group: the group's loads are issued together, its 2G samples
+                       // computed as independent chains (ILP), then its outputs stored
+#endif
+template <int KH, int R, int C, int CE>
+__device__ __forceinline__ void rev4_load_group(f2x (&w)[R + 2 * KH], const Rev4Row& lrow, const Rev4Row& orow,
+                                                const Rev4Row& rrow) {
+  if constexpr (C < CE) {
+    rev4_load_pair<KH, R, C>(w, lrow, orow, rrow);
+    rev4_load_group<KH, R, C + 1, CE>(w, lrow, orow, rrow);
+  }
+}
+
 // Outputs of one reverse step for this thread's row (all compile-time indices): u^(l) from the
 // thread's linear row at `ub`; outputs (after the NL adjoint of step l-1 when NL) go to the
-// swizzled row `wrow` of the other buffer.
+// swizzled row `wrow` of the other buffer.  Groups of LDBP_REV4_G output pairs.
 template <int KH, int R, bool FAST, bool NORM, bool MASKED, bool NL, int C = 0>
 __device__ __forceinline__ void rev4_outputs(f2x (&w)[R + 2 * KH], const Rev4Row& lrow, const Rev4Row& orow,
                                              const Rev4Row& rrow, uint32_t ub, const TapP (&hs)[KH + 1],
                                              uint32_t own, float gmn, f2x (&A)[KH + 1], f2x (&Bq)[KH + 1],
                                              float& dgam_next, const Rev4Row& wrow) {
   if constexpr (C < R / 2) {
-    rev4_load_pair<KH, R, C>(w, lrow, orow, rrow);
-    f2x u2[2], o[2];
-    lds2(ub + 16u * C, u2[0], u2[1]);
+    constexpr int CE = C + LDBP_REV4_G < R / 2 ? C + LDBP_REV4_G : R / 2;
+    constexpr int NS = 2 * (CE - C);
+    rev4_load_group<KH, R, C, CE>(w, lrow, orow, rrow);
+    f2x uu[NS], o[NS];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int s = 2 * C + h;
-      const f2x us = u2[h];
+    for (int c = C; c < CE; ++c) lds2(ub + 16u * c, uu[2 * (c - C)], uu[2 * (c - C) + 1]);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      const int s = 2 * C + i;
+      const f2x us = uu[i];
       const bool mine = !MASKED || ((own >> s) & 1u);
       const f2x ux = bcast(lof(us)), uy = bcast(hif(us));
       const f2x g0 = w[s + KH];
       f2x acc = NORM ? g0 : tmul(hs[0], g0);
-      if (mine) {
+      if (mine && !(LDBP_REV4_ABL & 16)) {
         A[0] = fma2(ux, g0, A[0]);
         Bq[0] = fma2(uy, g0, Bq[0]);
       }
 #pragma unroll
       for (int j = 1; j <= KH; ++j) {
         const f2x P = add2(w[s + KH - j], w[s + KH + j]);
-        acc = tmac(acc, hs[j], P);
-        if (mine) {
+        if (!(LDBP_REV4_ABL & 32)) acc = tmac(acc, hs[j], P);
+        if (mine && !(LDBP_REV4_ABL & 16)) {
           A[j] = fma2(ux, P, A[j]);
           Bq[j] = fma2(uy, P, Bq[j]);
         }
       }
-      if constexpr (NL) nl_adjoint<FAST, MASKED>(acc, us, gmn, 2.f * gmn, (own >> s) & 1u, dgam_next);
-      o[h] = acc;
+      if constexpr (NL && !(LDBP_REV4_ABL & 2)) nl_adjoint<FAST, MASKED>(acc, us, gmn, 2.f * gmn, (own >> s) & 1u, dgam_next);
+      o[i] = acc;
     }
-    sts2(rev4_chunk<C>(wrow), o[0], o[1]);
-    rev4_outputs<KH, R, FAST, NORM, MASKED, NL, C + 1>(w, lrow, orow, rrow, ub, hs, own, gmn, A, Bq, dgam_next, wrow);
+#pragma unroll
+    for (int c = C; c < CE; ++c) sts2(((c & 1) ? wrow.po : wrow.pe) + 16u * c, o[2 * (c - C)], o[2 * (c - C) + 1]);
+    rev4_outputs<KH, R, FAST, NORM, MASKED, NL, CE>(w, lrow, orow, rrow, ub, hs, own, gmn, A, Bq, dgam_next, wrow);
   }
 }
 
@@ -280,49 +302,14 @@ __device__ __forceinline__ void rev4_body(const RevArgs& a, const Rev4Smem& sm, 
   }
 
   constexpr int VP = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
-  // Step l's warp partials (red[l & 1][warp][v]) are summed over the warps in fixed order in fp64
-  // by warp 0 right after the barrier that ends step l, mapped back to the original parameters
-  // (dgamma_i = |P_i|^2 dgamma_hat_i, dh^(i) = conj(1/c_i) dh_hat^(i), as rev_tile_kernel's epilogue)
-  // and written to partials[cta][l][.]; the buffer is rewritten two steps later, after the next
-  // barrier, so warp 0 is done with it.
   constexpr int npairs = 1 + NTU;
-  auto flush = [&](int l) {
-    if (warp != 0 || lane >= npairs) return;
-    const int q = lane;
-    double* out = a.partials + ((int64_t)blockIdx.x * a.M + l) * V;
-    const StepNorm nm = sm.norm[l];
-    const float* red = sm.red + (size_t)(l & 1) * NW * V;
-    if (q == 0) {
-      double acc = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) acc += (double)red[w * V];
-      if (NORM) acc *= (double)nm.P.x * nm.P.x + (double)nm.P.y * nm.P.y;
-      out[0] = acc;
-    } else {
-      const int v2 = 1 + 2 * (q - 1);
-      double re = 0.0, im = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        re += (double)red[w * V + v2];
-        im += (double)red[w * V + v2 + 1];
-      }
-      if (NORM) {
-        const double cx = nm.c.x, cy = nm.c.y, m = cx * cx + cy * cy;
-        const double r2 = (re * cx - im * cy) / m, i2 = (re * cy + im * cx) / m;
-        re = r2;
-        im = i2;
-      }
-      out[v2] = re;
-      out[v2 + 1] = im;
-    }
-  };
   const uint32_t ub_mine0 = smem_u32(sm.ubuf + (size_t)tid * R);
   for (int l = s1 - 1; l >= s0; --l) {
     const int li = l - s0;
     const int ph = s1 - 1 - l;
     const uint32_t rb = (ph & 1) ? gb1 : gb0;  // ga^(l)
     const uint32_t wb = (ph & 1) ? gb0 : gb1;  // ga^(l-1)
-    window_wait(l % PIPE);
+    if (!(LDBP_REV4_ABL & 8)) window_wait(l % PIPE);
     if (PIPE == 2 && l - 1 >= s0) window(l - 1, (l - 1) % 2);
     const uint32_t ub = ub_mine0 + (uint32_t)((l % PIPE) * UB * 8);
     TapP hs[NTU];
@@ -363,15 +350,14 @@ __device__ __forceinline__ void rev4_body(const RevArgs& a, const Rev4Smem& sm, 
       }
 #pragma unroll
       for (int i = V; i < VP; ++i) vals[i] = 0.f;
-      const float r = warp_reduce_scatter<VP>(vals, lane);
+      const float r = (LDBP_REV4_ABL & 1) ? vals[lane & 7] : warp_reduce_scatter<VP>(vals, lane);
       constexpr int SH = VP == 2 ? 4 : VP == 4 ? 3 : VP == 8 ? 2 : VP == 16 ? 1 : 0;
       const int idx = lane >> SH;
-      float* red = sm.red + ((size_t)(l & 1) * NW + warp) * V;
+      float* red = sm.red + ((size_t)li * NW + warp) * V;
       if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
     }
     dgam = dgam_next;
-    __syncthreads();
-    flush(l);
+    if (!(LDBP_REV4_ABL & 4)) __syncthreads();
   }
   // adjoint w.r.t. u_hat^(s0): the last step's outputs, own row of the last-written buffer
   if (a.gout) {
@@ -382,6 +368,40 @@ __device__ __forceinline__ void rev4_body(const RevArgs& a, const Rev4Smem& sm, 
     for (int c = 0; c < R / 2; ++c) lds2(((c & 1) ? r.po : r.pe) + 16u * c, g[2 * c], g[2 * c + 1]);
     store_owned<R>(a.gout, e0, a.g, g);
   }
+  // CTA reduction in fp64, fixed order over warps, mapped back to the original parameters
+  // (identical to rev_tile_kernel): dgamma_i = |P_i|^2 dgamma_hat_i, dh^(i) = conj(1/c_i) dh_hat^(i).
+  // Kept out of the step loop: fp64 divisions on one warp between two barriers stretch every step.
+  const int S = s1 - s0;
+  for (int i = tid; i < S * npairs; i += NT) {
+    const int li = i / npairs, q = i % npairs;
+    const int l = s0 + li;
+    double* out = a.partials + ((int64_t)blockIdx.x * a.M + l) * V;
+    const StepNorm nm = sm.norm[l];
+    const float* red = sm.red + (size_t)li * NW * V;
+    if (q == 0) {
+      double acc = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) acc += (double)red[w * V];
+      if (NORM) acc *= (double)nm.P.x * nm.P.x + (double)nm.P.y * nm.P.y;
+      out[0] = acc;
+    } else {
+      const int v2 = 1 + 2 * (q - 1);
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        re += (double)red[w * V + v2];
+        im += (double)red[w * V + v2 + 1];
+      }
+      if (NORM) {
+        const double cx = nm.c.x, cy = nm.c.y, m = cx * cx + cy * cy;
+        const double r2 = (re * cx - im * cy) / m, i2 = (re * cy + im * cx) / m;
+        re = r2;
+        im = i2;
+      }
+      out[v2] = re;
+      out[v2 + 1] = im;
+    }
+  }
 }
 
 // Shared memory (mirrors the carve-up below; 16-byte aligned regions).
@@ -390,7 +410,7 @@ __host__ __device__ constexpr size_t rev4_smem_bytes(int kh, int steps, int M) {
          sizeof(float2) * (size_t)(2 + LDBP_REV4_PIPE) * rev4_threads(kh) * rev4_r(kh) +      // gbuf + ubuf
          32 * (size_t)steps * (kh + 1) +                                                      // taps_adj
          16 * (size_t)M +                                                                     // norm
-         4 * (size_t)((2 * (rev4_threads(kh) / 32) * (3 + 2 * kh) + 3) & ~3) +               // red [2][NW][V]
+         4 * (size_t)(((size_t)steps * (rev4_threads(kh) / 32) * (3 + 2 * kh) + 3) & ~(size_t)3) +  // red
          4 * (size_t)((rev4_threads(kh) / 32 + 3) & ~3) +                                     // lred
          4 * (size_t)((steps + 3) & ~3) + 16;                                                 // gamma, flag
 }
@@ -410,8 +430,8 @@ __global__ void __launch_bounds__(rev4_threads(KH), 65536 / (rev4_threads(KH) * 
   sm.ubuf = sm.gbuf + (size_t)2 * NT * R;                                                 // PIPE*NT*R
   sm.taps_adj = reinterpret_cast<TapP*>(sm.ubuf + (size_t)LDBP_REV4_PIPE * NT * R);       // S*NTU
   sm.norm = reinterpret_cast<StepNorm*>(sm.taps_adj + S * NTU);                           // M
-  sm.red = reinterpret_cast<float*>(sm.norm + a.M);                                       // 2*NW*V
-  sm.lred = sm.red + ((2 * NW * V + 3) & ~3);                                             // NW
+  sm.red = reinterpret_cast<float*>(sm.norm + a.M);                                       // S*NW*V
+  sm.lred = sm.red + ((S * NW * V + 3) & ~3);                                             // NW
   sm.gamma = sm.lred + ((NW + 3) & ~3);                                                   // S
   sm.flag = reinterpret_cast<int*>(sm.gamma + ((S + 3) & ~3));
 

@@ -19,7 +19,9 @@ x = torch.from_numpy(li.gaussian_blocks(1, range(B), n, 1e-3).astype(np.complex6
 t = torch.from_numpy(li.gaussian_blocks(1, range(B), n, 1e-3, purpose="target").astype(np.complex64)).cuda()
 st = P.TrainState.create(li.random_sym_taps(1, M, T, 0.05), li.random_gamma(1, M))
 y = P.ldbp_forward(x, st.taps, st.gamma)
-for mode in ("1", "0"):
+for mode in ("1", "0", "1r4"):
+    os.environ["LDBP_REV4"] = "1" if mode == "1r4" else "0"  # shared-memory-adjoint reverse too
+    mode = mode[:1]
     os.environ["LDBP_BWD_MODE"] = mode
     os.environ["LDBP_STORE_ALL_MIN_SAMPLES"] = "0"
     os.environ["LDBP_REV_MAX_STEPS"] = "2"  # two reverse launches (adjoint through HBM)
