@@ -427,6 +427,7 @@ struct RevPlan {
   int Cr = 1, Kr = 1;  // steps per reverse launch, number of reverse launches
   int V = 1;
   Tile tile;           // uniform geometry for all reverse launches (H = Cr*kh)
+  int launch_grid = 0; // persistent kernels (rev4): resident CTAs, each walking tiles; 0 = tile.grid
 };
 
 int rev_occupancy(RevFn fn, int nthreads, size_t smem) {
@@ -522,6 +523,8 @@ RevPlan plan_rev(const ldbp_dims* d, bool query_device) {
   const int H = v2 ? std::max(p.Cr * kh, 1) : p.Cr * kh;
   p.tile = plan_tiles(d->batch, d->n, H, R, slots, occ, sms, /*align_r=*/true);
   p.tile.nthreads = nthr;  // the kernel's layout is compiled for exactly this many threads
+  if (v4 && env_int("LDBP_REV4_PERSIST", 0))
+    p.launch_grid = (int)std::min<int64_t>(p.tile.grid, (int64_t)occ * sms);
   return p;
 }
 
@@ -989,7 +992,7 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
   double* lossp = reinterpret_cast<double*>(ws + w.loss_off);
   for (int k = p.Kr - 1; k >= 0; --k) {
     const int s0 = k * p.Cr, s1 = std::min(M, (k + 1) * p.Cr);
-    ldbp::RevArgs a;
+    ldbp::RevArgs a{};
     a.x = x;
     a.act = act(1);
     a.act_stride = stride;
@@ -1008,11 +1011,12 @@ int run_rev_chain(const ldbp_dims* d, const float2* x, const float2* gy, const f
     a.s0 = s0;
     a.s1 = s1;
     a.g = p.tile.g;
+    a.ntiles = p.tile.grid;  // persistent kernels (rev4) walk the tiles with a grid stride
     const size_t smem = rev_smem_any(d, s1 - s0);
     cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     {
       TraceScope ts(LDBP_K_REVERSE, s1 - s0, d->batch * d->n, st);
-      fn<<<p.tile.grid, p.tile.nthreads, smem, st>>>(a);
+      fn<<<p.launch_grid > 0 ? p.launch_grid : p.tile.grid, p.tile.nthreads, smem, st>>>(a);
     }
     LDBP_TRY(cuda_check("rev_tile_kernel launch"));
   }
@@ -1204,6 +1208,8 @@ int launch_rx(int64_t B, int64_t n, int sps, int L, const float2* y, const float
 struct EssmWs {
   size_t act_off = 0, act_each = 0, g_off = 0, part_off = 0, total = 0;
   int tiles = 0, V = 0;
+  int nch = 1;           // first-level reduction chunks per step
+  size_t part1_off = 0;  // [M][nch][V] chunk totals
 };
 
 EssmWs essm_ws(const ldbp_dims* d, int kappa, bool train) {
@@ -1219,6 +1225,9 @@ EssmWs essm_ws(const ldbp_dims* d, int kappa, bool train) {
   if (train) off += 2 * blk;
   w.part_off = off;
   if (train) off += align256(sizeof(double) * (size_t)d->steps * w.tiles * d->batch * w.V);
+  w.nch = (int)cdiv((int64_t)w.tiles * d->batch, ldbp::kEssmRedChunk);
+  w.part1_off = off;
+  if (train) off += align256(sizeof(double) * (size_t)d->steps * w.nch * w.V);
   w.total = off;
   return w;
 }
@@ -1960,10 +1969,17 @@ int ldbp_essm_loss_grad(const ldbp_dims* d, int32_t kappa, const void* x, const 
     LDBP_TRY(launch_essm_step(d, kappa, true, i, u, gin, (const float2*)target, gout, (const float2*)taps, gamma,
                               eta, part + (size_t)i * part_step, st));
   }
+  const int nblk = w.tiles * (int)d->batch;
+  double* part1 = reinterpret_cast<double*>(wb + w.part1_off);
+  {
+    TraceScope ts(LDBP_K_REDUCE, M, 0, st);
+    ldbp::essm_reduce_chunks_kernel<<<dim3((unsigned)w.nch, (unsigned)M), 128, 0, st>>>(part, nblk, w.V, part1);
+  }
+  LDBP_TRY(cuda_check("essm_reduce_chunks_kernel launch"));
   ldbp::EssmReduceArgs r;
-  r.partials = part;
+  r.partials = part1;
   r.M = M;
-  r.nblk = w.tiles * (int)d->batch;
+  r.nblk = w.nch;
   r.T = d->taps;
   r.kappa = kappa;
   r.sym = (d->flags & LDBP_SYMMETRIC) ? 1 : 0;

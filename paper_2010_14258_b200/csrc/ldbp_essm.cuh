@@ -452,6 +452,25 @@ struct EssmReduceArgs {
   double* buf;
 };
 
+// First level of the fixed-order reduction: CTA (chunk ch, step st) sums partials of CTAs
+// [ch*CH, ch*CH + CH) in order, one thread per component v (coalesced over v), into
+// out[st][ch][v]; essm_reduce_kernel then sums the chunk totals in order.  (A single thread per
+// component walking all CTAs was a chain of dependent L2 round trips: ~1.2 ms at the C3-like
+// shape, 4608 CTAs per step.)
+constexpr int kEssmRedChunk = 64;
+__global__ void __launch_bounds__(128) essm_reduce_chunks_kernel(const double* __restrict__ partials, int nblk, int V,
+                                                                 double* __restrict__ out) {
+  const int ch = blockIdx.x, st = blockIdx.y, nch = gridDim.x;
+  const int c0 = ch * kEssmRedChunk, c1 = min(nblk, c0 + kEssmRedChunk);
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const double* p = partials + ((int64_t)st * nblk + c0) * V + v;
+    double s = 0.0;
+#pragma unroll 8
+    for (int c = c0; c < c1; ++c, p += V) s += *p;
+    out[((int64_t)st * nch + ch) * V + v] = s;
+  }
+}
+
 __global__ void __launch_bounds__(256) essm_reduce_kernel(const EssmReduceArgs a) {
   const int V = 2 + 2 * a.T + 2 * a.kappa + 1;
   const int NE = 2 * a.kappa + 1;

@@ -171,9 +171,10 @@ __device__ __forceinline__ void load_window(const float2* __restrict__ src, int6
 
 // Bitmask of which of this thread's R samples are owned real samples of this CTA.
 template <int R>
-__device__ __forceinline__ uint32_t owned_mask(int64_t e0, const Geo& g) {
-  const int64_t lo = tile_lo(g, blockIdx.x);
-  const int64_t hi = min(lo + ((int64_t)blockIdx.x < g.NS ? g.Wh : g.W), g.E);
+__device__ __forceinline__ uint32_t owned_mask(int64_t e0, const Geo& g, int64_t tile = -1) {
+  if (tile < 0) tile = blockIdx.x;  // persistent kernels pass the tile they are working on
+  const int64_t lo = tile_lo(g, tile);
+  const int64_t hi = min(lo + (tile < g.NS ? g.Wh : g.W), g.E);
   const Span sp = make_span(e0, g);
   constexpr uint32_t FULL = R >= 32 ? 0xffffffffu : ((1u << R) - 1u);
   if (e0 + R <= lo || e0 >= hi) return 0u;

@@ -40,6 +40,7 @@ struct RevArgs {
   float seed_scale;        // seed g = seed_scale * (y - target)
   int T, M, s0, s1;
   Geo g;
+  int ntiles;              // persistent kernels (rev4): tiles to cover (grid-stride); 0 = gridDim.x
 };
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {

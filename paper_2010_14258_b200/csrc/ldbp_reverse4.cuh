@@ -40,7 +40,7 @@ namespace ldbp {
 #ifndef LDBP_REV4_ABL
 #define LDBP_REV4_ABL 0  // timing ablations (WRONG results; tuning only): 1 no warp reduction, 2 no NL
                          // adjoint, 4 no step barrier, 8 no u window wait, 16 no tap-gradient sums,
-                         // 32 no FIR adjoint (g = ga)
+                         // 32 no FIR adjoint (g = ga), 64 no step loop (prologue + epilogue only)
 #endif
 #ifndef LDBP_REV4_PIPE
 #define LDBP_REV4_PIPE 1
@@ -200,7 +200,7 @@ __device__ __forceinline__ void rev4_outputs(f2x (&w)[R + 2 * KH], const Rev4Row
 
 template <int KH, int R, bool FAST, bool NORM>
 __device__ __forceinline__ void rev4_body(const RevArgs& a, const Rev4Smem& sm, int64_t e0, int64_t fast_off,
-                                          uint32_t own, int lane, int warp) {
+                                          uint32_t own, int lane, int warp, int tile, unsigned& bph) {
   constexpr int NT = rev4_threads(KH), NW = NT / 32;
   constexpr int NTU = KH + 1;
   constexpr int V = 1 + 2 * NTU;
@@ -217,7 +217,7 @@ __device__ __forceinline__ void rev4_body(const RevArgs& a, const Rev4Smem& sm, 
   const int64_t woff = __shfl_sync(kFull, fast_off, 0);
   const bool wbulk = __all_sync(kFull, fast_off >= 0 && fast_off == woff + (int64_t)lane * R);
   uint64_t* bbar = sm.bbar + 2 * warp;
-  unsigned bused = 0u, bph = 0u;
+  unsigned bused = 0u;  // bph: phase parities of the bulk-copy barriers, carried over tiles
   auto window = [&](int i, int b) {
     const float2* src = rev_src(a, i);
     if (wbulk && ((reinterpret_cast<uintptr_t>(src + woff)) & 15) == 0) {
@@ -298,13 +298,13 @@ __device__ __forceinline__ void rev4_body(const RevArgs& a, const Rev4Smem& sm, 
   if (a.gin == nullptr && threadIdx.x == 0) {
     double tot = 0.0;
     for (int w = 0; w < NW; ++w) tot += (double)sm.lred[w];
-    a.loss_partials[blockIdx.x] = tot;
+    a.loss_partials[tile] = tot;
   }
 
   constexpr int VP = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
   constexpr int npairs = 1 + NTU;
   const uint32_t ub_mine0 = smem_u32(sm.ubuf + (size_t)tid * R);
-  for (int l = s1 - 1; l >= s0; --l) {
+  for (int l = s1 - 1; l >= ((LDBP_REV4_ABL & 64) ? s1 : s0); --l) {
     const int li = l - s0;
     const int ph = s1 - 1 - l;
     const uint32_t rb = (ph & 1) ? gb1 : gb0;  // ga^(l)
@@ -375,7 +375,7 @@ __device__ __forceinline__ void rev4_body(const RevArgs& a, const Rev4Smem& sm, 
   for (int i = tid; i < S * npairs; i += NT) {
     const int li = i / npairs, q = i % npairs;
     const int l = s0 + li;
-    double* out = a.partials + ((int64_t)blockIdx.x * a.M + l) * V;
+    double* out = a.partials + ((int64_t)tile * a.M + l) * V;
     const StepNorm nm = sm.norm[l];
     const float* red = sm.red + (size_t)li * NW * V;
     if (q == 0) {
@@ -393,8 +393,13 @@ __device__ __forceinline__ void rev4_body(const RevArgs& a, const Rev4Smem& sm, 
         im += (double)red[w * V + v2 + 1];
       }
       if (NORM) {
+        // conj(1/c) dh_hat = dh_hat c / |c|^2; 1/|c|^2 by two Newton steps from the fp32 reciprocal
+        // (full fp64 accuracy without the long DDIV sequence at the end of every tile)
         const double cx = nm.c.x, cy = nm.c.y, m = cx * cx + cy * cy;
-        const double r2 = (re * cx - im * cy) / m, i2 = (re * cy + im * cx) / m;
+        double r = (double)__frcp_rn((float)m);
+        r = r * (2.0 - m * r);
+        r = r * (2.0 - m * r);
+        const double r2 = (re * cx - im * cy) * r, i2 = (re * cy + im * cx) * r;
         re = r2;
         im = i2;
       }
@@ -435,10 +440,6 @@ __global__ void __launch_bounds__(rev4_threads(KH), 65536 / (rev4_threads(KH) * 
   sm.gamma = sm.lred + ((NW + 3) & ~3);                                                   // S
   sm.flag = reinterpret_cast<int*>(sm.gamma + ((S + 3) & ~3));
 
-  const int64_t e0 = thread_e0(a.g, R);
-  const Span sp = make_span(e0, a.g);
-  const int64_t fast_off = span_fast<R>(sp, a.g, e0) ? sp.b0 * a.g.n + (sp.q0 - a.g.H) : -1;
-  const uint32_t own = owned_mask<R>(e0, a.g);
   if (threadIdx.x < 2 * NW) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(sm.bbar + threadIdx.x)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -452,10 +453,21 @@ __global__ void __launch_bounds__(rev4_threads(KH), 65536 / (rev4_threads(KH) * 
                                        sm.norm, norm0);
   }
   __syncthreads();
-  if (*sm.flag)
-    rev4_body<KH, R, FAST, true>(a, sm, e0, fast_off, own, lane, warp);
-  else
-    rev4_body<KH, R, FAST, false>(a, sm, e0, fast_off, own, lane, warp);
+  const bool norm = *sm.flag;
+  // persistent: the CTA walks tiles blockIdx.x, + gridDim.x, ... (parameter table staged once)
+  const int ntiles = a.ntiles > 0 ? a.ntiles : (int)gridDim.x;
+  unsigned bph = 0u;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t e0 = tile_lo(a.g, tile) - a.g.H + (int64_t)threadIdx.x * R;
+    const Span sp = make_span(e0, a.g);
+    const int64_t fast_off = span_fast<R>(sp, a.g, e0) ? sp.b0 * a.g.n + (sp.q0 - a.g.H) : -1;
+    const uint32_t own = owned_mask<R>(e0, a.g, tile);
+    if (norm)
+      rev4_body<KH, R, FAST, true>(a, sm, e0, fast_off, own, lane, warp, tile, bph);
+    else
+      rev4_body<KH, R, FAST, false>(a, sm, e0, fast_off, own, lane, warp, tile, bph);
+    __syncthreads();  // shared buffers are reused by the next tile
+  }
 }
 
 }  // namespace ldbp
