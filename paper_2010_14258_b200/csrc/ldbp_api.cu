@@ -4,6 +4,8 @@
 // (see ldbp_kernels.cuh).  The planner picks, per launch, the threads per CTA, the halo H =
 // (#steps in the launch) * Kh (x2 for backward segments), and the owned width W such that the
 // grid is a whole number of waves of resident CTAs on this device.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -776,6 +778,35 @@ struct FiniteCheck {
 // ----------------------------------------------------------------------------------------
 // Launch helpers
 // ----------------------------------------------------------------------------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda
+// dependency); nullptr when the driver does not provide it (the lane-store path is used).
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encode_fn() {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// Tensor map of the storing forward's activation slots (LDBP_FWD_TMA, ldbp_kernels.cuh): rows of
+// 16 complex64 samples (128 bytes) over ckpt[0, rows * 16), box 32 rows, 128-byte swizzle.
+bool make_act_tmap(CUtensorMap* m, float2* ckpt, int64_t rows) {
+  const PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encode_fn();
+  if (!enc || rows <= 0 || rows > (int64_t)0x7fffffff || (reinterpret_cast<uintptr_t>(ckpt) & 15)) return false;
+  const cuuint64_t dims[2] = {16, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {16, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, ckpt, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2* taps, const float* gamma,
                const uint8_t* mask, int s0, int s1, cudaStream_t st, float2* ckpt = nullptr, int ckpt_every = 0,
                int64_t ckpt_stride = 0, bool global_norm = false, bool scale_dst = false, float2* y_out = nullptr,
@@ -809,6 +840,13 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   a.scale_dst = scale_dst ? 1 : 0;
   a.staged = staged ? 1 : 0;
   a.g = t.g;
+  a.use_tmap = 0;
+  // TMA activation stores where the storing forward is FP32-bound (Kh >= 2; measured C3, Kh = 4: 0.767 ->
+  // 0.731 ms); at Kh = 1 it is bound by the HBM writes and the TMA path measured slower (C5: 9.4 ->
+  // 13.1 ms).  LDBP_FWD_TMA = 0 never, 2 always.
+  const int tma_mode = env_int("LDBP_FWD_TMA", 1);
+  if (staged && kFwdR == 16 && ckpt && ckpt_stride % 16 == 0 && s1 >= 2 && (tma_mode == 2 || (tma_mode == 1 && kh >= 2)))
+    a.use_tmap = make_act_tmap(&a.tmap, ckpt, (int64_t)(s1 - 1) * ckpt_stride / 16) ? 1 : 0;
   cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
   {
     TraceScope ts(LDBP_K_FORWARD, s1 - s0, d->batch * d->n, st);

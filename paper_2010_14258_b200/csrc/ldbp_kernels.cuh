@@ -17,6 +17,7 @@
 // double-buffered shared-memory edge array (one __syncthreads per step).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -939,6 +940,10 @@ struct FwdArgs {
   const void* ptab;  // store-all training: parameter table (params_kernel), or nullptr
   int* nonfinite; // LDBP_CHECK_FINITE: atomicMin of the first (1-based) step with a NaN/Inf output
   Geo g;
+  // storing forward (LDBP_FWD_TMA): activation rows of 16 samples as a 2-D tensor [rows][16] x 8 B
+  // over ckpt, 128-byte swizzle, box 32 rows; use_tmap = 0: lane stores
+  int use_tmap;
+  CUtensorMap tmap;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -981,8 +986,18 @@ __host__ __device__ constexpr int fwd_max_threads(int kh) {
 #define LDBP_FWD_WSTAGE 1  // store-all forward: 1 = halos through the edge arrays + per-warp store stage,
                            // 0 = one CTA-wide double-buffered stage for halos and stores
 #endif
+#ifndef LDBP_FWD_TMA
+#define LDBP_FWD_TMA 1  // storing forward: activation stores by TMA tensor stores (see fwd_steps_split)
+#endif
+#ifndef LDBP_FWD_TMA_BUF
+#define LDBP_FWD_TMA_BUF 2  // TMA stage buffers per warp (2: the next step's stage is written while the
+                            // previous box is still being read by the TMA engine)
+#endif
 __host__ __device__ constexpr int fwd_stage_elems(int kh, int r) {
-  return LDBP_FWD_WSTAGE ? fwd_max_threads(kh) * (4 * (kh > 0 ? kh : 1) + (r + 2) + 1)
+  // LDBP_FWD_TMA with two stage buffers per warp: 2 x 4 KB per warp plus 1 KB of alignment slack
+  // (2r + 2 f2x per thread covers it for r = 16 and >= 32 threads)
+  return LDBP_FWD_WSTAGE ? fwd_max_threads(kh) * (4 * (kh > 0 ? kh : 1) +
+                                                  (LDBP_FWD_TMA && LDBP_FWD_TMA_BUF == 2 && r == 16 ? 2 * r + 2 : r + 2) + 1)
                          : fwd_max_threads(kh) * (2 * (r + 2) + 1);
 }
 #ifdef LDBP_FWD_NTHR
@@ -1142,9 +1157,26 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
   f2x* const wstage = sh_edge + 4 * KE * ST + (tid >> 5) * 32 * RS;
   const int64_t* const wrun_off = run_off + (tid & ~31);
   int t_lo = 0, t_hi = 0;
+  // LDBP_FWD_TMA (R = 16: one run = one 128-byte row): a warp whose 32 runs are one contiguous,
+  // 16-sample-aligned range of owned real samples writes them into a 1024-byte-aligned 4 KB stage
+  // in the 128-byte-swizzled layout (chunk c of row L at c ^ (L & 7): conflict-free 16-byte
+  // stores) and lane 0 hands the box to the TMA engine (cp.async.bulk.tensor store, SASS
+  // UTMASTG), which un-swizzles it into the activation slot; other warps store from registers.
+  constexpr bool TMA = WST && LDBP_FWD_TMA && R == 16;
+  bool wtma = false;
+  uint32_t tstage = 0;
+  int64_t trow0 = 0;
   if constexpr (WST) {
     static_assert(R % 2 == 0 && 32 % (R / 2) == 0, "warp store stage: R/2 must divide 32");
     run_off[tid] = smap.off >= 0 ? smap.off : -1;  // warp-local: ordered by the __syncwarp of the first store
+    if constexpr (TMA) {
+      const int64_t off0 = __shfl_sync(kFull, smap.off, 0);
+      wtma = a.use_tmap && __all_sync(kFull, smap.off >= 0 && smap.off == off0 + (int64_t)lane * R) &&
+             (off0 % R) == 0;
+      trow0 = off0 / R;  // + (gs - 1) * ckpt_stride / R per step
+      const uint32_t sbase = (smem_u32(sh_edge + 4 * KE * ST) + 1023u) & ~1023u;
+      tstage = sbase + (uint32_t)(tid >> 5) * (4096u * LDBP_FWD_TMA_BUF);
+    }
   } else if constexpr (STG) {
     const bool fullrun = smap.off >= 0;
     run_off[tid] = fullrun ? smap.off : (smap.mask ? -2 : -1);
@@ -1247,7 +1279,49 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
       if (__any_sync(kFull, bad) && lane == 0 && a.nonfinite) atomicMin(a.nonfinite, gs);
     }
     if (gs < a.s1) publish((s + 1) & 1);
-    if constexpr (WST) {
+    if (TMA && a.use_tmap) {
+      if (gs < a.s1 && wtma) {
+        // stage buffer of this step free again: the box stored from it LDBP_FWD_TMA_BUF steps ago has
+        // been read by the TMA engine
+        if (lane == 0) {
+          if constexpr (LDBP_FWD_TMA_BUF == 2)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncwarp();
+        const uint32_t tst = tstage + (LDBP_FWD_TMA_BUF == 2 ? (uint32_t)(gs & 1) * 4096u : 0u);
+        const uint32_t row = tst + (uint32_t)lane * 128u;
+        const uint32_t sw = (uint32_t)(lane & 7);
+#pragma unroll
+        for (int m = 0; m < R / 2; ++m)
+          asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(row + ((((uint32_t)m) ^ sw) << 4)), "l"(u[2 * m]),
+                       "l"(u[2 * m + 1])
+                       : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          const int r = (int)(trow0 + (int64_t)(gs - 1) * (a.ckpt_stride / R));
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  reinterpret_cast<uint64_t>(&a.tmap)),
+              "r"(0), "r"(r), "r"(tst)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      } else if (gs < a.s1 && smap.off >= 0) {  // warps off the TMA path: own run from registers
+        f2x* const d2 = reinterpret_cast<f2x*>(a.ckpt + (int64_t)(gs - 1) * a.ckpt_stride + smap.off);
+        if ((reinterpret_cast<uintptr_t>(d2) & 15) == 0) {
+#pragma unroll
+          for (int m = 0; m < R / 2; ++m)
+            reinterpret_cast<ulonglong2*>(d2)[m] = make_ulonglong2(u[2 * m], u[2 * m + 1]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < R; ++k) d2[k] = u[k];
+        }
+      }
+    } else if constexpr (WST) {
+      // (use_tmap == 0 for the whole launch, so no warp uses the TMA stage region)
       // u^(gs) -> activation slot gs-1: the warp's 32 runs through its stage, 16-byte lane-consecutive
       // stores (R/2 lanes per run); irregular runs are stored by their owners below
       if (gs < a.s1) {
@@ -1280,6 +1354,10 @@ __device__ __forceinline__ void fwd_steps_split(const FwdArgs& a, f2x (&u)[R], c
       next_ck += a.ckpt_every;
       ck_ptr += a.ckpt_stride;
     }
+  }
+  if constexpr (TMA) {  // the stage must outlive the copies; activations complete before exit
+    if (wtma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   if (NORM && (!global || a.scale_dst))
     store_mapped_scaled<R>(a.dst, smap, e0, a.g, u, sh_norm[a.s1 - a.s0 - 1].P);
@@ -1388,7 +1466,7 @@ __global__ void __launch_bounds__(fwd_max_threads(KH), fwd_min_blocks(KH)) fwd_t
 #endif
 template <int KH, int R, bool SYM, bool CHK = false>
 __global__ void __launch_bounds__(fwd_max_threads(KH), 65536 / (fwd_max_threads(KH) * LDBP_FWD_STORE_REGS))
-    fwd_store_kernel(const FwdArgs a) {
+    fwd_store_kernel(const __grid_constant__ FwdArgs a) {
   fwd_tile_body<KH, R, SYM, true, true, CHK>(a);
 }
 
