@@ -224,6 +224,22 @@ int ldbp_rx_exact_train_grad(const ldbp_dims* d, const void* x, const void* symb
                              void* cuda_stream);
 
 /*
+ * Transmitted waveform (the target of the waveform-MSE loss; BASELINE C3 "MSE loss vs
+ * transmitted waveform") from transmitted symbols, on the device: Eq. (11) on the periodic frame
+ * (P:737-743), RRC roll-off `rolloff` applied as its exact frequency response:
+ *   w_b = sqrt(power_w[b]) * sps * e^{j phase[b]} * F^-1 diag(RRC) F U s_b,
+ *   out[b][t] = w_b[(t - shift[b]) mod n]          (U: upsampling by sps with zeros)
+ * codes: uint8 [batch][n / sps] indices into constellation (complex64 [q], 1 <= q <= 256; codes >= q
+ * read entry 0); shift (int32 [batch]) and phase (float32 [batch], rad) may be NULL (0); out:
+ * complex64 [batch][n].  n a power of two <= 2^16, sps in [1, 4] dividing n.  Device pointers, the
+ * caller's stream, no workspace, no host sync.  Lets a training step's targets cross PCIe as 1 byte
+ * per symbol (bench.py e2e).
+ */
+int ldbp_tx_waveform(int64_t batch, int64_t n, int32_t sps, float rolloff, const uint8_t* codes,
+                     const void* constellation, int32_t q, const float* power_w, const int32_t* shift_or_null,
+                     const float* phase_or_null, void* out, void* cuda_stream);
+
+/*
  * Learned ESSM (paper §III-D, Eq. nl_filtered): the nonlinear
  * step of Eq. (7) becomes  v_t = a_t exp(j gamma'_i sum_{k=-kappa}^{kappa} eta^(i)_k |a_{(t-k) mod n}|^2)
  * with real per-step filters eta [M][2 kappa + 1] (tap k at index k + kappa), 0 <= kappa <= 32,

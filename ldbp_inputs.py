@@ -53,6 +53,17 @@ def qam16(g: np.random.Generator, count: int) -> np.ndarray:
     return QAM16_LEVELS[i] + 1j * QAM16_LEVELS[q]
 
 
+# code 4 i + q  <->  QAM16_LEVELS[i] + j QAM16_LEVELS[q]
+QAM16_TABLE = (QAM16_LEVELS[:, None] + 1j * QAM16_LEVELS[None, :]).reshape(-1)
+
+
+def qam16_codes(g: np.random.Generator, count: int) -> np.ndarray:
+    """The same draws as qam16(g, count) as uint8 codes into QAM16_TABLE."""
+    i = g.integers(0, 4, size=count)
+    q = g.integers(0, 4, size=count)
+    return (4 * i + q).astype(np.uint8)
+
+
 def dbm_to_w(p_dbm):
     return 10.0 ** ((np.asarray(p_dbm, dtype=np.float64) - 30.0) / 10.0)
 

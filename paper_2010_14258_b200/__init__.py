@@ -22,6 +22,7 @@ from .api import (  # noqa: F401
     ldbp_rx_train_grad,
     ldbp_ssfm_link,
     ldbp_train_step,
+    ldbp_tx_waveform,
     make_dims,
     workspace_bytes,
 )

@@ -42,6 +42,7 @@ EXPORTED = (
     "ldbp_rx_exact_train_grad",
     "ldbp_ssfm_workspace_bytes",
     "ldbp_ssfm_link",
+    "ldbp_tx_waveform",
 )
 
 K_FORWARD, K_BACKWARD, K_REDUCE, K_ADAM, K_REVERSE, K_RX, K_ESSM, K_SSFM, K_TINY = 1, 2, 3, 4, 5, 6, 7, 8, 9
@@ -112,6 +113,8 @@ def _load():
         "ldbp_essm_workspace_bytes": (ctypes.c_int, [D, ctypes.c_int32, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
         "ldbp_essm_forward": (ctypes.c_int, [D, ctypes.c_int32, P, P, P, P, P, P, ctypes.c_size_t, P]),
         "ldbp_essm_loss_grad": (ctypes.c_int, [D, ctypes.c_int32, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
+        "ldbp_tx_waveform": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_float, P, P,
+                                            ctypes.c_int32, P, P, P, P, P]),
         "ldbp_ssfm_workspace_bytes": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]),
         "ldbp_ssfm_link": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.POINTER(ctypes.c_double), dbl, dbl, dbl, dbl, dbl, dbl, P,

@@ -369,6 +369,31 @@ def ldbp_rx_exact_loss_grad(y, symbols, power_w, *, sps=2, rolloff=0.1, weights=
 
 
 @_on_stream
+def ldbp_tx_waveform(codes, constellation, power_w, *, sps=2, rolloff=0.1, shift=None, phase=None, out=None,
+                     stream=None):
+    """Transmitted waveform [B][K sps] complex64 from symbol codes (uint8 [B][K] into `constellation`,
+    complex64 [Q]) on the device: sqrt(P_b) sps e^{j phase_b} (RRC-shaped periodic frame, Eq. (11)),
+    circularly shifted by shift_b samples (int32) — the waveform-MSE training target."""
+    _need(codes, "codes", torch.uint8)
+    B, K = codes.shape
+    n = K * sps
+    _need(constellation, "constellation", torch.complex64)
+    q = constellation.numel()
+    _need(power_w, "power_w", torch.float32, (B,))
+    if shift is not None:
+        _need(shift, "shift", torch.int32, (B,))
+    if phase is not None:
+        _need(phase, "phase", torch.float32, (B,))
+    if out is None:
+        out = torch.empty((B, n), dtype=torch.complex64, device=codes.device)
+    else:
+        _need(out, "out", torch.complex64, (B, n))
+    check(lib.ldbp_tx_waveform(B, n, sps, float(rolloff), _p(codes), _p(constellation), q, _p(power_w), _p(shift),
+                               _p(phase), _p(out), _stream_handle(stream)), "ldbp_tx_waveform")
+    return out
+
+
+@_on_stream
 def ldbp_rx_exact_train_grad(x, symbols, power_w, taps, gamma, *, sps=2, rolloff=0.1, weights=None, mask=None,
                              symmetric=True, precise=False, buf=None, ws=None, stream=None):
     """[sum_b w_b errs_b | dgamma[M] | dtaps[M][T][2]] of the exact receiver-chain loss through LDBP."""

@@ -108,3 +108,26 @@ def link_blocks(cfg_index: int, blocks, n: int, pool=None, U: int = 256, device=
         x[a:e] = torch.gather(r[idx[a:e]], 1, cols[a:e]) * ph[a:e, None]
         t[a:e] = torch.gather(tgt[idx[a:e]], 1, cols[a:e]) * ph[a:e, None]
     return x, t
+
+
+def qam16_table(device="cuda") -> torch.Tensor:
+    """complex64 [16] constellation of ldbp_inputs.qam16_codes (code 4 i + q)."""
+    return torch.from_numpy(li.QAM16_TABLE.astype(np.complex64)).to(device)
+
+
+def link_codes(cfg_index: int, blocks, n: int, U: int = 256, device="cuda"):
+    """What a training step needs to rebuild link_blocks' targets on the device
+    (api.ldbp_tx_waveform): uint8 symbol codes [len(blocks)][n / RHO_D] of each block's pool entry,
+    its launch power (W, float32), circular shift (int32) and rotation (rad, float32)."""
+    blocks = list(blocks)
+    nsym = n // RHO_D
+    per = U // 4
+    pset = (-2.0, -1.0, 0.0, 1.0)
+    q = np.searchsorted(np.array(pset), li.pick_powers_dbm(cfg_index, blocks, pset))
+    pool = q * per + np.array(blocks) % per
+    codes = np.stack([li.qam16_codes(li.rng(cfg_index, 1_000_000 + int(p), "symbols"), nsym) for p in pool])
+    pw = np.array([float(li.dbm_to_w(pset[int(qq)])) for qq in q], dtype=np.float32)
+    ks, phis = li.augment_params(cfg_index, blocks, n)
+    return (torch.from_numpy(codes).to(device), torch.from_numpy(pw).to(device),
+            torch.from_numpy(np.asarray(ks, dtype=np.int32)).to(device),
+            torch.from_numpy(np.asarray(phis, dtype=np.float32)).to(device))

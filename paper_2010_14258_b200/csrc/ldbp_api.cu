@@ -1851,6 +1851,60 @@ int ldbp_rx_exact_loss_grad(int64_t batch, int64_t n, int32_t sps, float rolloff
                          errs, (float2*)gy_or_null, (cudaStream_t)cuda_stream);
 }
 
+int ldbp_tx_waveform(int64_t batch, int64_t n, int32_t sps, float rolloff, const uint8_t* codes,
+                     const void* constellation, int32_t q, const float* power_w, const int32_t* shift_or_null,
+                     const float* phase_or_null, void* out, void* cuda_stream) {
+  g_err[0] = 0;
+  LDBP_TRY(validate_rx_exact(batch, n, sps, rolloff));
+  if (q < 1 || q > 256) return fail(LDBP_EINVAL, "constellation size %d not in [1, 256]", q);
+  if (batch == 0) return LDBP_OK;
+  LDBP_TRY(check_ptr(codes, "codes", 1));
+  LDBP_TRY(check_ptr(constellation, "constellation", 8));
+  LDBP_TRY(check_ptr(power_w, "power_w", 4));
+  LDBP_TRY(check_ptr(out, "out", 8));
+  if (shift_or_null) LDBP_TRY(check_ptr(shift_or_null, "shift", 4));
+  if (phase_or_null) LDBP_TRY(check_ptr(phase_or_null, "phase", 4));
+  const int C = n > (1 << ldbp::kSsfmLocalMaxLog2) ? (int)(n >> ldbp::kSsfmLocalMaxLog2) : 1;
+  const int64_t L = n / C;
+  ldbp::TxArgs a;
+  a.codes = codes;
+  a.constel = (const float2*)constellation;
+  a.power_w = power_w;
+  a.shift = shift_or_null;
+  a.phase = phase_or_null;
+  a.out = (float2*)out;
+  a.n = n;
+  a.K = (int)(n / sps);
+  a.sps = sps;
+  a.Q = q;
+  a.log2L = 0;
+  while ((int64_t(1) << a.log2L) < L) ++a.log2L;
+  a.rolloff = rolloff;
+  const size_t smem = sizeof(float2) * ((size_t)L + L / 16 + 1 + L / 2 + (C > 1 ? (size_t)n / 64 + 64 : 0) + 1);
+  void (*kern)(const ldbp::TxArgs) = C == 1 ? ldbp::tx_waveform_kernel<1>
+                                     : C == 2 ? ldbp::tx_waveform_kernel<2> : ldbp::tx_waveform_kernel<4>;
+  cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(batch * C));
+  cfg.blockDim = dim3(ldbp::kSsfmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)cuda_stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = C > 1 ? 1 : 0;
+  cudaError_t e;
+  {
+    TraceScope ts(LDBP_K_RX, 0, batch * n, (cudaStream_t)cuda_stream);
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+  }
+  if (e != cudaSuccess) return fail(LDBP_ECUDA, "tx_waveform_kernel launch: %s", cudaGetErrorString(e));
+  return cuda_check("tx_waveform_kernel launch");
+}
+
 struct RxExTrainWs {
   bool store_all = false;
   size_t y_off = 0, gy_off = 0, errs_off = 0, pp_off = 0, total = 0;

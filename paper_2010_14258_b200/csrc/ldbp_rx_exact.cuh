@@ -194,6 +194,77 @@ __global__ void __launch_bounds__(kSsfmThreads, 1) rx_exact_kernel(const RxExact
   for (int i = threadIdx.x; i < L; i += kSsfmThreads) gb[i] = X[ssfm_pidx(i)];
 }
 
+// Transmitted waveform on the device (the training target of the waveform-MSE loss, P:280-290,
+// from the transmitted symbols; Eq. (11) on the periodic frame):
+//   w = sqrt(P_b) sps e^{j phi_b} F^-1 diag(RRC) F U s_b,  out_b[t] = w[(t - k_b) mod n]
+// (U: upsampling by sps with zeros; phi_b, k_b the optional per-block rotation / circular shift
+// of the training-set augmentation, exact by equivariance).  Symbols are codes into a small
+// constellation table, so a step's targets cross PCIe as 1 byte per symbol instead of 16 bytes
+// per symbol of complex64 waveform.  Same shared-memory / cluster FFTs as rx_exact_kernel.
+struct TxArgs {
+  const uint8_t* codes;     // [B][K] constellation indices
+  const float2* constel;    // [Q]
+  const float* power_w;     // [B]
+  const int32_t* shift;     // [B] or nullptr
+  const float* phase;       // [B] or nullptr
+  float2* out;              // [B][n]
+  int64_t n;
+  int K, sps, log2L, Q;
+  float rolloff;
+};
+
+template <int C>
+__global__ void __launch_bounds__(kSsfmThreads, 1) tx_waveform_kernel(const TxArgs a) {
+  extern __shared__ __align__(16) unsigned char tx_smem[];
+  const int n = (int)a.n;
+  const int L = n / C;
+  float2* X = reinterpret_cast<float2*>(tx_smem);
+  float2* tw = X + L + L / 16 + 1;
+  float2* ta = tw + L / 2;
+  float2* tb = ta + (C > 1 ? n / 64 : 0);
+  int rank = 0;
+  if constexpr (C > 1) rank = (int)cooperative_groups::this_cluster().block_rank();
+  const int b = blockIdx.x / C;
+  const int sps = a.sps;
+  const int Kl = L / sps;
+  for (int k = threadIdx.x; k < L / 2; k += kSsfmThreads) {
+    double sn, cs;
+    sincospi(-2.0 * (double)k / (double)L, &sn, &cs);
+    tw[k] = make_float2((float)cs, (float)sn);
+  }
+  if constexpr (C > 1) {
+    for (int k = threadIdx.x; k < n / 64 + 64; k += kSsfmThreads) {
+      const int m = k < n / 64 ? 64 * k : k - n / 64;
+      double sn, cs;
+      sincospi(-2.0 * (double)m / (double)n, &sn, &cs);
+      (k < n / 64 ? ta[k] : tb[k - n / 64]) = make_float2((float)cs, (float)sn);
+    }
+  }
+  // amplitude sqrt(P) sps e^{j phi}, applied to the symbols before the (linear) filter
+  double ps = 0.0, pc = 1.0;
+  if (a.phase) sincos((double)a.phase[b], &ps, &pc);
+  const double amp = sqrt((double)a.power_w[b]) * (double)sps;
+  const float2 ap = make_float2((float)(amp * pc), (float)(amp * ps));
+  for (int i = threadIdx.x; i < L; i += kSsfmThreads) X[ssfm_pidx(i)] = make_float2(0.f, 0.f);
+  __syncthreads();
+  const uint8_t* cb = a.codes + (int64_t)b * a.K + (int64_t)rank * Kl;
+  for (int k = threadIdx.x; k < Kl; k += kSsfmThreads) {
+    const int q = cb[k];
+    const float2 s = a.constel[q < a.Q ? q : 0];
+    X[ssfm_pidx(k * sps)] = make_float2(ap.x * s.x - ap.y * s.y, ap.x * s.y + ap.y * s.x);
+  }
+  __syncthreads();
+  rx_circulant<C>(X, tw, ta, tb, L, rank, a.n, a.log2L, sps, a.rolloff);
+  const int64_t kb = a.shift ? (int64_t)a.shift[b] : 0;
+  const int64_t k0 = ((kb % n) + n) % n;
+  float2* ob = a.out + (int64_t)b * n;
+  for (int i = threadIdx.x; i < L; i += kSsfmThreads) {
+    int64_t t = (int64_t)rank * L + i + k0;
+    if (t >= n) t -= n;
+    ob[t] = X[ssfm_pidx(i)];
+  }
+}
+
 // buf[0] = sum_b w_b errs_b (fixed order)
 __global__ void rx_wsum_kernel(const double* errs, const float* weights, int64_t B, double* buf) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
