@@ -50,7 +50,10 @@ typedef struct ldbp_dims {
   int32_t reserved;/* must be 0                                                             */
 } ldbp_dims;
 
-#define LDBP_MAX_TAPS 15
+/* Compiled specialisations per Kh = 0..15 (T <= 31).  T <= 15 covers every
+   BASELINE config and model of the paper; 17..31 are correct but register-heavy (the per-thread
+   tap and halo windows spill), and the ESSM entry points keep T <= 15. */
+#define LDBP_MAX_TAPS 31
 
 enum ldbp_flags {
   /* Symmetric filters h_{-j} = h_j.  The kernels read only taps[Kh..T-1] of each

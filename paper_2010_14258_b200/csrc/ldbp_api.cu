@@ -125,6 +125,14 @@ LDBP_DECL_GETTERS(4)
 LDBP_DECL_GETTERS(5)
 LDBP_DECL_GETTERS(6)
 LDBP_DECL_GETTERS(7)
+LDBP_DECL_GETTERS(8)
+LDBP_DECL_GETTERS(9)
+LDBP_DECL_GETTERS(10)
+LDBP_DECL_GETTERS(11)
+LDBP_DECL_GETTERS(12)
+LDBP_DECL_GETTERS(13)
+LDBP_DECL_GETTERS(14)
+LDBP_DECL_GETTERS(15)
 namespace {
 
 FwdFn get_fwd(int kh, bool sym, bool fast, bool chk = false) {
@@ -137,6 +145,14 @@ FwdFn get_fwd(int kh, bool sym, bool fast, bool chk = false) {
     case 5: return ldbp_get_fwd_5(sym, fast, chk);
     case 6: return ldbp_get_fwd_6(sym, fast, chk);
     case 7: return ldbp_get_fwd_7(sym, fast, chk);
+    case 8: return ldbp_get_fwd_8(sym, fast, chk);
+    case 9: return ldbp_get_fwd_9(sym, fast, chk);
+    case 10: return ldbp_get_fwd_10(sym, fast, chk);
+    case 11: return ldbp_get_fwd_11(sym, fast, chk);
+    case 12: return ldbp_get_fwd_12(sym, fast, chk);
+    case 13: return ldbp_get_fwd_13(sym, fast, chk);
+    case 14: return ldbp_get_fwd_14(sym, fast, chk);
+    case 15: return ldbp_get_fwd_15(sym, fast, chk);
   }
   return nullptr;
 }
@@ -150,6 +166,14 @@ BwdFn get_bwd(int kh, bool sym, bool fast) {
     case 5: return ldbp_get_bwd_5(sym, fast);
     case 6: return ldbp_get_bwd_6(sym, fast);
     case 7: return ldbp_get_bwd_7(sym, fast);
+    case 8: return ldbp_get_bwd_8(sym, fast);
+    case 9: return ldbp_get_bwd_9(sym, fast);
+    case 10: return ldbp_get_bwd_10(sym, fast);
+    case 11: return ldbp_get_bwd_11(sym, fast);
+    case 12: return ldbp_get_bwd_12(sym, fast);
+    case 13: return ldbp_get_bwd_13(sym, fast);
+    case 14: return ldbp_get_bwd_14(sym, fast);
+    case 15: return ldbp_get_bwd_15(sym, fast);
   }
   return nullptr;
 }
@@ -164,6 +188,14 @@ FwdFn get_fwd_store(int kh, bool sym, bool chk = false) {
     case 5: return ldbp_get_fwd_store_5(sym, chk);
     case 6: return ldbp_get_fwd_store_6(sym, chk);
     case 7: return ldbp_get_fwd_store_7(sym, chk);
+    case 8: return ldbp_get_fwd_store_8(sym, chk);
+    case 9: return ldbp_get_fwd_store_9(sym, chk);
+    case 10: return ldbp_get_fwd_store_10(sym, chk);
+    case 11: return ldbp_get_fwd_store_11(sym, chk);
+    case 12: return ldbp_get_fwd_store_12(sym, chk);
+    case 13: return ldbp_get_fwd_store_13(sym, chk);
+    case 14: return ldbp_get_fwd_store_14(sym, chk);
+    case 15: return ldbp_get_fwd_store_15(sym, chk);
   }
   return nullptr;
 }
@@ -178,6 +210,14 @@ RevFn get_rev(int kh, bool sym, bool fast) {
     case 5: return ldbp_get_rev_5(sym, fast);
     case 6: return ldbp_get_rev_6(sym, fast);
     case 7: return ldbp_get_rev_7(sym, fast);
+    case 8: return ldbp_get_rev_8(sym, fast);
+    case 9: return ldbp_get_rev_9(sym, fast);
+    case 10: return ldbp_get_rev_10(sym, fast);
+    case 11: return ldbp_get_rev_11(sym, fast);
+    case 12: return ldbp_get_rev_12(sym, fast);
+    case 13: return ldbp_get_rev_13(sym, fast);
+    case 14: return ldbp_get_rev_14(sym, fast);
+    case 15: return ldbp_get_rev_15(sym, fast);
   }
   return nullptr;
 }
@@ -192,6 +232,14 @@ RevFn get_rev2(int kh, bool fast) {
     case 5: return ldbp_get_rev2_5(fast);
     case 6: return ldbp_get_rev2_6(fast);
     case 7: return ldbp_get_rev2_7(fast);
+    case 8: return ldbp_get_rev2_8(fast);
+    case 9: return ldbp_get_rev2_9(fast);
+    case 10: return ldbp_get_rev2_10(fast);
+    case 11: return ldbp_get_rev2_11(fast);
+    case 12: return ldbp_get_rev2_12(fast);
+    case 13: return ldbp_get_rev2_13(fast);
+    case 14: return ldbp_get_rev2_14(fast);
+    case 15: return ldbp_get_rev2_15(fast);
   }
   return nullptr;
 }
@@ -214,6 +262,14 @@ RevFn get_rev4(int kh, bool fast) {
     case 5: return ldbp_get_rev4_5(fast);
     case 6: return ldbp_get_rev4_6(fast);
     case 7: return ldbp_get_rev4_7(fast);
+    case 8: return ldbp_get_rev4_8(fast);
+    case 9: return ldbp_get_rev4_9(fast);
+    case 10: return ldbp_get_rev4_10(fast);
+    case 11: return ldbp_get_rev4_11(fast);
+    case 12: return ldbp_get_rev4_12(fast);
+    case 13: return ldbp_get_rev4_13(fast);
+    case 14: return ldbp_get_rev4_14(fast);
+    case 15: return ldbp_get_rev4_15(fast);
   }
   return nullptr;
 }
@@ -228,6 +284,14 @@ ParFn get_params(int kh, bool sym) {
     case 5: return ldbp_get_params_5(sym);
     case 6: return ldbp_get_params_6(sym);
     case 7: return ldbp_get_params_7(sym);
+    case 8: return ldbp_get_params_8(sym);
+    case 9: return ldbp_get_params_9(sym);
+    case 10: return ldbp_get_params_10(sym);
+    case 11: return ldbp_get_params_11(sym);
+    case 12: return ldbp_get_params_12(sym);
+    case 13: return ldbp_get_params_13(sym);
+    case 14: return ldbp_get_params_14(sym);
+    case 15: return ldbp_get_params_15(sym);
   }
   return nullptr;
 }
@@ -445,7 +509,9 @@ int rev_occupancy(RevFn fn, int nthreads, size_t smem) {
 // 3.24 at 2, 3.86 at 1 warp vs 1.95; C5 15.6-20.5 vs 14.9 ms): the refresh barrier every R/Kh
 // steps across 8 warps costs more than the per-step split barrier it replaces (28 % barrier
 // stalls), and barrier-free 1-warp tiles pay 19-25 % halo recompute.  LDBP_REV2=1 selects it.
-bool use_rev2(const ldbp_dims* d) { return (d->flags & LDBP_SYMMETRIC) && env_int("LDBP_REV2", 0) != 0; }
+bool use_rev2(const ldbp_dims* d) {
+  return (d->flags & LDBP_SYMMETRIC) && (d->taps - 1) / 2 <= 12 && env_int("LDBP_REV2", 0) != 0;
+}
 
 // The skewed one-sided reverse (ldbp_reverse3.cuh; symmetric taps, even Kh so the shifted windows
 // stay 16-byte aligned) is OFF by default: parity-green but measured slower (C3 reverse 2.82 ms vs
@@ -461,7 +527,8 @@ bool use_rev3(const ldbp_dims* d) {
 // Shared-memory-adjoint reverse (ldbp_reverse4.cuh, symmetric taps, 1 <= Kh): LDBP_REV4=1/0 forces.
 bool use_rev4(const ldbp_dims* d) {
   const int kh = (d->taps - 1) / 2;
-  return (d->flags & LDBP_SYMMETRIC) && kh >= 1 && !use_rev2(d) && !use_rev3(d) && env_int("LDBP_REV4", 0) != 0;
+  return (d->flags & LDBP_SYMMETRIC) && kh >= 1 && kh <= 12 && !use_rev2(d) && !use_rev3(d) &&
+         env_int("LDBP_REV4", 0) != 0;
 }
 
 size_t rev_smem_any(const ldbp_dims* d, int steps) {
@@ -554,6 +621,7 @@ TinyPlan plan_tiny(const ldbp_dims* d, int max_cluster) {
   if (mode == 1 && d->steps > kTinyAutoMaxSteps && plan_bwd(d, false).K == 1) return p;
   if (d->batch <= 0 || d->n <= 0 || d->batch * d->n > (int64_t)1 << 24) return p;
   const int kh = (d->taps - 1) / 2;
+  if (kh > 7) return p;  // the fused tiny kernel is compiled for T <= 15
   if (d->batch >= 8 || max_cluster < d->batch) {
     p.C = (int)std::min<int64_t>(max_cluster, d->batch);
     p.nrows = (int)cdiv(d->batch, p.C);
@@ -1288,6 +1356,7 @@ size_t essm_smem(int T, int kappa, bool bwd) {
 }
 
 int validate_essm(const ldbp_dims* d, int kappa) {
+  if (d->taps > ldbp::kEssmMaxT) return fail(LDBP_ESHAPE, "ESSM: taps %d > %d", d->taps, ldbp::kEssmMaxT);
   if (kappa < 0 || kappa > ldbp::kEssmMaxKappa) return fail(LDBP_ESHAPE, "kappa %d not in [0, %d]", kappa, ldbp::kEssmMaxKappa);
   if (2 * (int64_t)kappa + 1 > d->n) return fail(LDBP_ESHAPE, "eta longer than the block: 2kappa+1 > n");
   return LDBP_OK;

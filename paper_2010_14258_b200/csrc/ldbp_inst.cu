@@ -48,8 +48,13 @@ ParFn LDBP_CAT(ldbp_get_params_, LDBP_KH)(bool sym) {
 }
 
 RevFn LDBP_CAT(ldbp_get_rev2_, LDBP_KH)(bool fast) {
+#if LDBP_KH <= 12  // warp-overlapped slots of 12 samples: Kh <= 12
   constexpr int K = LDBP_KH;
   return fast ? ldbp::rev2_tile_kernel<K, true> : ldbp::rev2_tile_kernel<K, false>;
+#else
+  (void)fast;
+  return nullptr;
+#endif
 }
 
 RevFn LDBP_CAT(ldbp_get_rev3_, LDBP_KH)(bool fast) {
@@ -63,7 +68,7 @@ RevFn LDBP_CAT(ldbp_get_rev3_, LDBP_KH)(bool fast) {
 }
 
 RevFn LDBP_CAT(ldbp_get_rev4_, LDBP_KH)(bool fast) {
-#if LDBP_KH >= 1
+#if LDBP_KH >= 1 && LDBP_KH <= 12  // rows of 12 samples: Kh <= 12
   constexpr int K = LDBP_KH;
   return fast ? ldbp::rev4_tile_kernel<K, true> : ldbp::rev4_tile_kernel<K, false>;
 #else

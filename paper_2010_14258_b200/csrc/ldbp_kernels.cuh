@@ -35,14 +35,15 @@
 #define LDBP_BWD_R_SMALL 4  // segment backward for Kh <= 2 (C1 CUDA-graph step 18.5 -> 14.4 us: half the
                             // serial per-thread chain of the latency-bound tiny problems)
 #endif
-__host__ __device__ constexpr int bwd_r(int kh) { return kh <= 2 ? LDBP_BWD_R_SMALL : LDBP_BWD_R; }
+// (wide filters, Kh > 8 / Kh > 12: the neighbour halos need R >= Kh samples per thread)
+__host__ __device__ constexpr int bwd_r(int kh) { return kh <= 2 ? LDBP_BWD_R_SMALL : kh <= 8 ? LDBP_BWD_R : 16; }
 #ifndef LDBP_REV_R
 #define LDBP_REV_R 12  // samples per thread, store-all reverse kernel (measured: 12 >= 16 > 8)
 #endif
 #ifndef LDBP_REV_R_SMALL
 #define LDBP_REV_R_SMALL LDBP_REV_R  // samples per thread of the reverse kernel for Kh <= 1
 #endif
-__host__ __device__ constexpr int rev_r(int kh) { return kh <= 1 ? LDBP_REV_R_SMALL : LDBP_REV_R; }
+__host__ __device__ constexpr int rev_r(int kh) { return kh <= 1 ? LDBP_REV_R_SMALL : kh <= 12 ? LDBP_REV_R : 16; }
 
 #ifndef LDBP_NORM
 #define LDBP_NORM 1  // h0-normalised FIR when well conditioned (saves one complex multiply per FIR)
@@ -487,6 +488,35 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&v)[N], int lane) {
 #pragma unroll
   for (int o = 16 / N; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
   return r;
+}
+
+// Padded value count for a warp reduction of V per-lane partials (V <= 64).
+__host__ __device__ constexpr int red_vp(int v) {
+  return v <= 2 ? 2 : v <= 4 ? 4 : v <= 8 ? 8 : v <= 16 ? 16 : v <= 32 ? 32 : 64;
+}
+// Warp totals of the first nvalid of N per-lane partials (N from red_vp) -> red[0, nvalid): the
+// transposing butterfly on chunks of at most 32 values (wide filters, T > 15, have up to 63),
+// one writer lane per value, fixed order (deterministic).  N <= 32 is exactly the single butterfly.
+template <int N>
+__device__ __forceinline__ void warp_reduce_write(float (&v)[N], int lane, float* red, int nvalid) {
+  if constexpr (N <= 32) {
+    const float r = warp_reduce_scatter<N>(v, lane);
+    constexpr int SH = N == 2 ? 4 : N == 4 ? 3 : N == 8 ? 2 : N == 16 ? 1 : 0;
+    const int idx = lane >> SH;
+    if ((lane & ((1 << SH) - 1)) == 0 && idx < nvalid) red[idx] = r;
+  } else {
+    static_assert(N == 64, "at most 64 partials");
+    float lo[32], hi[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      lo[i] = v[i];
+      hi[i] = v[32 + i];
+    }
+    const float r0 = warp_reduce_scatter<32>(lo, lane);
+    if (lane < nvalid) red[lane] = r0;
+    const float r1 = warp_reduce_scatter<32>(hi, lane);
+    if (32 + lane < nvalid) red[32 + lane] = r1;
+  }
 }
 
 // Window accessor: index i in [-KH, R+KH).
@@ -1677,18 +1707,14 @@ __device__ __forceinline__ void bwd_body(const BwdArgs& a, const BwdSmem& sm, f2
     }
     // per-warp reduction of this step's partials (transposing butterfly, see above)
     {
-      constexpr int VP = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
+      constexpr int VP = red_vp(V);
       float vals[VP];
       vals[0] = dgam;
 #pragma unroll
       for (int j = 0; j < NTU; ++j) { vals[1 + 2 * j] = lof(dh[j]); vals[2 + 2 * j] = hif(dh[j]); }
 #pragma unroll
       for (int i = V; i < VP; ++i) vals[i] = 0.f;
-      const float r = warp_reduce_scatter<VP>(vals, lane);
-      constexpr int SH = VP == 2 ? 4 : VP == 4 ? 3 : VP == 8 ? 2 : VP == 16 ? 1 : 0;  // lanes per index = 32/VP
-      const int idx = lane >> SH;
-      float* red = sm.sh_red + (l * nwarps + warp) * V;
-      if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
+      warp_reduce_write<VP>(vals, lane, sm.sh_red + (l * nwarps + warp) * V, V);
     }
   }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -493,13 +493,9 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   publish(0);
 
   // per-warp reduction of one step's partials -> red[li][warp][.]
-  constexpr int VP = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
+  constexpr int VP = red_vp(V);
   auto reduce_step = [&](float (&vals)[VP], int rli) {
-    const float r = warp_reduce_scatter<VP>(vals, lane);
-    constexpr int SH = VP == 2 ? 4 : VP == 4 ? 3 : VP == 8 ? 2 : VP == 16 ? 1 : 0;
-    const int idx = lane >> SH;
-    float* red = sm.red + ((size_t)rli * NW + warp) * V;
-    if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
+    warp_reduce_write<VP>(vals, lane, sm.red + ((size_t)rli * NW + warp) * V, V);
   };
   // LDBP_REV_DEFER_RED: step l's reduction runs inside step l-1's barrier window (after its
   // interior outputs, before the wait), off the path between publish and the next wait

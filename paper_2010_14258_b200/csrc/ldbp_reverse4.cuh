@@ -301,7 +301,7 @@ __device__ __forceinline__ void rev4_body(const RevArgs& a, const Rev4Smem& sm, 
     a.loss_partials[tile] = tot;
   }
 
-  constexpr int VP = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
+  constexpr int VP = red_vp(V);
   constexpr int npairs = 1 + NTU;
   const uint32_t ub_mine0 = smem_u32(sm.ubuf + (size_t)tid * R);
   for (int l = s1 - 1; l >= ((LDBP_REV4_ABL & 64) ? s1 : s0); --l) {
@@ -350,11 +350,7 @@ __device__ __forceinline__ void rev4_body(const RevArgs& a, const Rev4Smem& sm, 
       }
 #pragma unroll
       for (int i = V; i < VP; ++i) vals[i] = 0.f;
-      const float r = (LDBP_REV4_ABL & 1) ? vals[lane & 7] : warp_reduce_scatter<VP>(vals, lane);
-      constexpr int SH = VP == 2 ? 4 : VP == 4 ? 3 : VP == 8 ? 2 : VP == 16 ? 1 : 0;
-      const int idx = lane >> SH;
-      float* red = sm.red + ((size_t)li * NW + warp) * V;
-      if ((lane & ((1 << SH) - 1)) == 0 && idx < V) red[idx] = r;
+      if (!(LDBP_REV4_ABL & 1)) warp_reduce_write<VP>(vals, lane, sm.red + ((size_t)li * NW + warp) * V, V);
     }
     dgam = dgam_next;
     if (!(LDBP_REV4_ABL & 4)) __syncthreads();

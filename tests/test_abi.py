@@ -42,7 +42,7 @@ def test_validation_before_launch(L):
         return lib.ldbp_forward(ctypes.byref(d), x, y, taps, gamma, None, 0, None)
 
     assert fwd(L.dims(1, 16, 2, 4)) == -2           # even T
-    assert fwd(L.dims(1, 16, 2, 17)) == -2          # T > LDBP_MAX_TAPS
+    assert fwd(L.dims(1, 64, 2, 33)) == -2          # T > LDBP_MAX_TAPS (31)
     assert fwd(L.dims(1, 4, 2, 5)) == -2            # T > n
     assert fwd(L.dims(1, 16, 0, 3)) == -2           # M < 1
     assert fwd(L.dims(-1, 16, 2, 3)) == -2          # B < 0

@@ -698,3 +698,27 @@ def test_tiny_fused_train_step_cuda_graph(P):
     torch.cuda.synchronize()
     assert torch.equal(b_e, buf)
     assert torch.equal(eager.master, graphed.master)
+
+
+# ---- wide filters: T = 17 .. 31 (1 <= T <= 31 compiled specialisations) ----
+@pytest.mark.parametrize("T,sym", [(17, True), (17, False), (23, True), (31, True), (31, False)])
+def test_wide_filters_forward_and_gradients(P, monkeypatch, T, sym):
+    B, n, M = 3, 1500, 5
+    x = li.gaussian_blocks(71, range(B), n, 1e-3)
+    tgt = li.gaussian_blocks(71, range(B), n, 1e-3, purpose="target")
+    taps, gamma = model(71, M, T, sym, scale=0.05)
+    y = P.ldbp_forward(dev(x), dev(taps), dev(gamma, np.float32), symmetric=sym).cpu().numpy()
+    ry = O.forward(r32(x), r32(taps), r32(gamma))
+    for b in range(B):
+        assert rel(y[b], ry[b]) <= OUT_TOL, (b, rel(y[b], ry[b]))
+    ref = O.loss_grad(r32(x), r32(tgt), r32(taps), r32(gamma), symmetric=sym)
+    for mode in ("0", "1"):  # checkpoint + segment backward, store-all + reverse
+        set_mode(monkeypatch, mode, None)
+        monkeypatch.setenv("LDBP_STORE_ALL_MIN_SAMPLES", "0")
+        buf = P.ldbp_loss_grad(dev(x), dev(tgt), dev(taps), dev(gamma, np.float32), symmetric=sym).cpu().numpy()
+        assert abs(buf[0] - ref[0]) <= OUT_TOL * ref[0], (mode, buf[0], ref[0])
+        for i in range(M):
+            assert abs(buf[1 + i] - ref[1 + i]) <= GRAD_TOL * abs(ref[1 + i]), (mode, i)
+        dt, rdt = buf[1 + M:].reshape(M, T, 2), ref[1 + M:].reshape(M, T, 2)
+        for i in range(M):
+            assert rel(dt[i], rdt[i]) <= GRAD_TOL, (mode, i, rel(dt[i], rdt[i]))
