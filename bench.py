@@ -434,6 +434,57 @@ def graph_latency(cfg, reps=10, inner=20):
     return e0.elapsed_time(e1) / (reps * inner) * 1e3  # us
 
 
+def pipelined_forward(cfg, sets=4, steps=40, warmup=5, graph=True):
+    """Serving throughput of the forward (BJ config 2: one forward per batch of received blocks):
+    consecutive batches stream through `sets` distinct input/output buffer pairs (4 x 67 MB > the
+    126 MB L2, so every batch is read from HBM, no flush needed) with LDBP_STREAM_PIPELINE, so each
+    forward's CTAs start while the previous one's last wave drains.  Device time per batch (µs),
+    optionally with the `steps` forwards captured in one CUDA graph (PDL edges)."""
+    import torch
+
+    import paper_2010_14258_b200 as P
+
+    taps, gamma = make_model(cfg)
+    x0, _ = make_inputs(cfg, range(cfg["B"]))
+    st = P.TrainState.create(taps, gamma)
+    xs = [x0.clone() for _ in range(sets)]
+    ys = [torch.empty_like(x0) for _ in range(sets)]
+
+    def run():
+        for i in range(steps):
+            P.ldbp_forward(xs[i % sets], st.taps, st.gamma, out=ys[i % sets], pipeline=True)
+
+    for _ in range(warmup):
+        P.ldbp_forward(xs[0], st.taps, st.gamma, out=ys[0], pipeline=True)
+    torch.cuda.synchronize()
+    g = None
+    if graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            run()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            run()
+        g.replay()
+        torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    if g is not None:
+        g.replay()
+    else:
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / steps * 1e3
+    # the pipelined outputs are the plain forward's, bit for bit
+    ref = P.ldbp_forward(xs[(steps - 1) % sets], st.taps, st.gamma)
+    assert torch.equal(ref, ys[(steps - 1) % sets]), "pipelined forward differs from the plain forward"
+    return us
+
+
 def traffic_from_profiles(cfg_name, kernel):
     """dram bytes per launch from a committed `ncu --set full` summary, if one exists."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
@@ -611,6 +662,15 @@ def main():
                 M = len(make_model(c)[1])
                 extra[nm]["graph_us"] = round(us, 2)
                 extra[nm]["graph_value"] = round(c["B"] * c["n"] * M / (us * 1e-6) / 1e9, 2)
+                if c["mode"] == "fwd":  # serving pipeline of independent batches (LDBP_STREAM_PIPELINE)
+                    try:
+                        pus = pipelined_forward(c)
+                        pv = c["B"] * c["n"] * M / (pus * 1e-6) / 1e9
+                        extra[nm]["pipe_us"] = round(pus, 2)
+                        extra[nm]["pipe_value"] = round(pv, 2)
+                        extra[nm]["pipe_frac"] = round(pv / rr["step_roof"]["bound_gsample_steps"], 3)
+                    except Exception as exc:  # an extra: never lose the headline line over it
+                        extra[nm]["pipe_error"] = str(exc)[:200]
             torch.cuda.empty_cache()
     cpu = None
     if rank == 0 and not args.no_cpu:

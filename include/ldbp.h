@@ -68,7 +68,15 @@ enum ldbp_flags {
      in ldbp_last_error().  Applies to ldbp_forward/backward/loss_grad/train_step/rx_train_grad
      (the training calls then use the store-all schedule, so every step is checked); it adds
      256 workspace bytes. */
-  LDBP_CHECK_FINITE = 4u
+  LDBP_CHECK_FINITE = 4u,
+  /* ldbp_forward only (ignored by the other calls; the forward ignores it when it needs more than
+     one launch or LDBP_CHECK_FINITE is set): a serving pipeline of independent batches (BJ config 2,
+     one forward per batch of received blocks).  The caller guarantees that no kernel enqueued earlier
+     on the stream that may still be running writes x / taps / gamma or reads or writes y — e.g.
+     consecutive forwards over a rotation of at least 3 distinct input/output buffers.  The forward is
+     then launched as a programmatic dependent launch (no griddepcontrol.wait): its CTAs start loading
+     their windows while the previous forward's last wave drains, instead of after it completes. */
+  LDBP_STREAM_PIPELINE = 8u
 };
 
 typedef enum ldbp_status {

@@ -14,6 +14,7 @@ LIB_PATH = os.environ.get("LDBP_LIB", os.path.join(_HERE, "libldbp.so"))
 LDBP_SYMMETRIC = 1
 LDBP_PRECISE = 2
 LDBP_CHECK_FINITE = 4
+LDBP_STREAM_PIPELINE = 8
 OP_FORWARD, OP_BACKWARD, OP_LOSS_GRAD, OP_TRAIN_STEP = 0, 1, 2, 3
 
 # Every symbol include/ldbp.h declares (checked by tests/test_abi.py).

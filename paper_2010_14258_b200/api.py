@@ -15,8 +15,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (LDBP_CHECK_FINITE, LDBP_PRECISE, LDBP_SYMMETRIC, OP_BACKWARD, OP_FORWARD, OP_LOSS_GRAD,
-                   OP_TRAIN_STEP, check, lib)
+from ._lib import (LDBP_CHECK_FINITE, LDBP_PRECISE, LDBP_STREAM_PIPELINE, LDBP_SYMMETRIC, OP_BACKWARD, OP_FORWARD,
+                   OP_LOSS_GRAD, OP_TRAIN_STEP, check, lib)
 
 _VP = ctypes.c_void_p
 
@@ -134,12 +134,16 @@ def _check_model(x, taps, gamma):
 
 
 @_on_stream
-def ldbp_forward(x, taps, gamma, *, symmetric=True, precise=False, check_finite=False, out=None, ws=None,
-                 stream=None):
+def ldbp_forward(x, taps, gamma, *, symmetric=True, precise=False, check_finite=False, pipeline=False, out=None,
+                 ws=None, stream=None):
     """y = f_theta(x) (Eq. 7) for complex64 x [B][n], taps [M][T], gamma [M].  check_finite:
-    raise LdbpError (LDBP_ENONFINITE, with the first failing step) on NaN/Inf activations."""
+    raise LdbpError (LDBP_ENONFINITE, with the first failing step) on NaN/Inf activations.
+    pipeline: LDBP_STREAM_PIPELINE (ldbp.h) — the caller guarantees that no earlier, possibly still
+    running kernel on the stream writes x/taps/gamma or touches out (a rotation of >= 3 buffers)."""
     B, n, M, T = _check_model(x, taps, gamma)
     d = make_dims(B, n, M, T, symmetric, precise, check_finite)
+    if pipeline:
+        d.flags |= LDBP_STREAM_PIPELINE
     y = torch.empty_like(x) if out is None else out
     _need(y, "out", torch.complex64, x.shape)
     nb = workspace_bytes(d, OP_FORWARD)

@@ -711,7 +711,7 @@ bool use_store_all(const ldbp_dims* d) {
 int validate_dims(const ldbp_dims* d) {
   if (!d) return fail(LDBP_EINVAL, "dims is NULL");
   if (d->reserved != 0) return fail(LDBP_EINVAL, "dims.reserved must be 0");
-  if (d->flags & ~(uint32_t)(LDBP_SYMMETRIC | LDBP_PRECISE | LDBP_CHECK_FINITE))
+  if (d->flags & ~(uint32_t)(LDBP_SYMMETRIC | LDBP_PRECISE | LDBP_CHECK_FINITE | LDBP_STREAM_PIPELINE))
     return fail(LDBP_EINVAL, "unknown flag bits 0x%x", d->flags);
   if (d->batch < 0) return fail(LDBP_ESHAPE, "batch %lld < 0", (long long)d->batch);
   if (d->n < 1) return fail(LDBP_ESHAPE, "n %lld < 1", (long long)d->n);
@@ -878,7 +878,7 @@ bool make_act_tmap(CUtensorMap* m, float2* ckpt, int64_t rows) {
 int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2* taps, const float* gamma,
                const uint8_t* mask, int s0, int s1, cudaStream_t st, float2* ckpt = nullptr, int ckpt_every = 0,
                int64_t ckpt_stride = 0, bool global_norm = false, bool scale_dst = false, float2* y_out = nullptr,
-               const void* ptab = nullptr) {
+               const void* ptab = nullptr, bool pdl = false) {
   const int kh = (d->taps - 1) / 2;
   const bool sym = d->flags & LDBP_SYMMETRIC;
   const bool fast = !(d->flags & LDBP_PRECISE);
@@ -918,7 +918,23 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
   cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem);
   {
     TraceScope ts(LDBP_K_FORWARD, s1 - s0, d->batch * d->n, st);
-    fn<<<t.grid, t.nthreads, t.smem, st>>>(a);
+    if (pdl && !g_trace_on && !chk) {
+      // LDBP_STREAM_PIPELINE: programmatic dependent launch; the kernel never waits on the previous
+      // grid (the caller guarantees independence), it only lets the next one start early
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(t.grid);
+      cfg.blockDim = dim3(t.nthreads);
+      cfg.dynamicSmemBytes = t.smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, fn, a);
+    } else {
+      fn<<<t.grid, t.nthreads, t.smem, st>>>(a);
+    }
   }
   return cuda_check("fwd_tile_kernel launch");
 }
@@ -927,13 +943,17 @@ int launch_fwd(const ldbp_dims* d, const float2* src, float2* dst, const float2*
 int run_forward_chain(const ldbp_dims* d, const float2* x, float2* y, const float2* taps, const float* gamma,
                       const uint8_t* mask, float2* pp, cudaStream_t st) {
   const FwdPlan p = plan_fwd_segments(d->steps, (d->taps - 1) / 2);
+  // LDBP_STREAM_PIPELINE applies to one-launch forwards only (a multi-launch chain shares its ping-pong
+  // buffer with the previous call's chain)
+  const bool pdl = (d->flags & LDBP_STREAM_PIPELINE) && p.segs == 1 && env_int("LDBP_PDL", 1);
   const float2* src = x;
   for (int k = 0; k < p.segs; ++k) {
     const int s0 = k * p.steps_per, s1 = std::min(d->steps, s0 + p.steps_per);
     // the last launch writes y; earlier ones alternate so that happens
     const int remaining = p.segs - 1 - k;
     float2* dst = (remaining % 2 == 0) ? y : pp;
-    LDBP_TRY(launch_fwd(d, src, dst, taps, gamma, mask, s0, s1, st));
+    LDBP_TRY(launch_fwd(d, src, dst, taps, gamma, mask, s0, s1, st, nullptr, 0, 0, false, false, nullptr, nullptr,
+                        pdl));
     src = dst;
   }
   return LDBP_OK;

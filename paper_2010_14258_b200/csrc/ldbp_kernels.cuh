@@ -1421,6 +1421,11 @@ __device__ __forceinline__ void fwd_tile_body(const FwdArgs& a) {
   int* sh_flag = reinterpret_cast<int*>(sh_gamma + S);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // LDBP_STREAM_PIPELINE: a programmatic-dependent next launch (the next batch's forward) may start
+  // as soon as every CTA of this grid is running, i.e. while the last wave drains.  A next launch
+  // without the PDL attribute still waits for this grid to complete; one with it that reads this
+  // grid's output waits in griddepcontrol.wait (bwd_segment_kernel).
+  if constexpr (!STG) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (LDBP_NB_SYNC && !LDBP_FWD_SPLIT) nb_init(bars);
   if (LDBP_FWD_SPLIT && threadIdx.x == 0) {  // split step barrier: bars[0], count = warps
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars)), "r"(nwarps) : "memory");

@@ -50,7 +50,7 @@ def test_validation_before_launch(L):
     d = L.dims(1, 16, 2, 3)
     d.reserved = 1
     assert fwd(d) == -1
-    assert fwd(L.dims(1, 16, 2, 3, flags=8)) == -1  # unknown flag
+    assert fwd(L.dims(1, 16, 2, 3, flags=16)) == -1  # unknown flag
     assert lib.ldbp_status_string(-6).startswith(b"LDBP_ENONFINITE")
     assert fwd(L.dims(1, 16, 2, 3), x=None) == -1
     assert fwd(L.dims(1, 16, 2, 3), x=P(0x10004)) == -3  # misaligned complex64

@@ -88,6 +88,31 @@ def test_forward_precise_flag(P):
     assert rel(yp, ref) <= 2e-6 and rel(yf, ref) <= OUT_TOL
 
 
+@pytest.mark.parametrize("cmax", [None, "3"])
+def test_forward_stream_pipeline(P, monkeypatch, cmax):
+    """LDBP_STREAM_PIPELINE: back-to-back forwards of independent batches over a rotation of 3
+    buffer pairs (programmatic dependent launches, no wait on the previous grid) give the oracle's
+    outputs and the plain forward's bits; a multi-launch forward (cmax = 3) ignores the flag."""
+    if cmax:
+        monkeypatch.setenv("LDBP_FWD_MAX_STEPS", cmax)
+    B, n, M, T = 5, 3000, 7, 5
+    taps, gamma = model(14, M, T, True)
+    xs = [li.gaussian_blocks(14, range(k * B, (k + 1) * B), n, 2e-3) for k in range(3)]
+    dx = [dev(x) for x in xs]
+    ys = [torch.empty_like(d) for d in dx]
+    tt, gg = dev(taps), dev(gamma, np.float32)
+    for it in range(4):
+        for k in range(3):
+            P.ldbp_forward(dx[k], tt, gg, out=ys[k], pipeline=True)
+    for k in range(3):
+        plain = P.ldbp_forward(dx[k], tt, gg)
+        assert torch.equal(plain, ys[k]), k
+        ref = O.forward(r32(xs[k]), r32(taps), r32(gamma))
+        y = ys[k].cpu().numpy()
+        for b in range(B):
+            assert rel(y[b], ref[b]) <= OUT_TOL, (k, b)
+
+
 def test_forward_chained_launches(P, monkeypatch):
     """Force several launches per forward (checkpoint-style chaining through the workspace)."""
     B, n, M, T = 3, 1500, 10, 5
