@@ -4,12 +4,17 @@
 // each log-distributed step delta: Kerr step u <- u e^{j gamma L_eff(delta) |u|^2}
 // at the segment start (reading G5), then the lossy linear step U_k <- U_k e^{-alpha delta/2}
 // e^{j beta2/2 omega_k^2 delta} (Eqs. (4)-(6)); after the span the EDFA: gain
-// e^{alpha L_sp/2} plus ASE sigma * CN(0,1) (the draws are inputs); at the end an
+// e^{alpha L_sp/2} plus ASE sigma * CN(0,1) (draws from an input array, or in-kernel Philox
+// keyed by (seed, global block, span, sample): ase_philox_cn); at the end an
 // ideal low-pass |f| <= cutoff and decimation (reading G8).
 //
-// One persistent CTA per block: the block (n <= 2^14 complex fp32) stays in shared memory for the
-// whole link; FFTs are in-place radix-2 decimation-in-time (bit-reversal permutation, log2 n
-// butterfly stages, twiddles e^{-2 pi j k / n} from an fp64-accurate table in shared memory).
+// One persistent CTA per block (n <= 2^14 complex fp32), or a 2-/4-CTA thread-block cluster for
+// n = 2^15 / 2^16, keeps the block in shared memory for the whole link.  FFTs: register passes of
+// several radix-2 stages on groups of up to 16 elements (ssfm_pass), decimation-in-frequency
+// forward and decimation-in-time inverse, so the spectrum stays in bit-reversed slot order and
+// no bit-reversal permutation pass exists (the dispersion table is written in that order); across a cluster the four-step split's radix-C stage reads the other
+// ranks through distributed shared memory.  Twiddles W_n^m = ta[m >> 6] * tb[m & 63] from two small
+// fp64-accurate tables.
 // The dispersion factors H_s[k] (one row per distinct step length) are precomputed in fp64 by
 // ssfm_htable_kernel: omega^2 delta reaches hundreds of radians, beyond fp32 sincos accuracy.
 #pragma once
