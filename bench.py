@@ -174,7 +174,8 @@ def make_inputs(cfg, blocks, world=1, scaling="weak"):
     return x, (tgt if cfg["mode"] == "train" else None)
 
 
-def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_clocks=True, scaling=None):
+def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_clocks=True, scaling=None,
+               force_collective=False):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -198,7 +199,8 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
     trainer = None
     if train:
         trainer = DataParallelLDBP(state=st, loss_grad_fn=lambda a, b: P.ldbp_loss_grad(a, b, st.taps, st.gamma, ws=ws),
-                                   train_step_fn=lambda a, b: P.ldbp_train_step(st, a, b, ws=ws))
+                                   train_step_fn=lambda a, b: P.ldbp_train_step(st, a, b, ws=ws),
+                                   force_collective=force_collective)
         trainer.set_local_samples(B * n)
 
     def step(xx, tt):
@@ -251,7 +253,7 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
     dims = P.make_dims(B, n, M, T)
     if not train:
         launches_per_step = P.launch_count(dims, _lib.OP_FORWARD)
-    elif world == 1:  # DataParallelLDBP.step -> ldbp_train_step
+    elif world == 1 and not force_collective:  # DataParallelLDBP.step -> ldbp_train_step
         launches_per_step = P.launch_count(dims, _lib.OP_TRAIN_STEP)
     else:  # loss_grad -> all_reduce (NCCL's kernel, not counted) -> adam_kernel
         launches_per_step = P.launch_count(dims, _lib.OP_LOSS_GRAD) + 1
@@ -611,6 +613,9 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: a functional dry run of the N > 1 path when fewer GPUs than ranks exist "
                          "(ranks share a device; the timings are then not scaling numbers)")
+    ap.add_argument("--force-collective", action="store_true",
+                    help="N = 1 only: create a one-rank NCCL group and run the data-parallel exchange "
+                         "(fp64 all-reduce of the gradient buffer between loss_grad and Adam) every step")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -628,13 +633,23 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        # communicator lines (ranks, NVLS/P2P transport) on stderr for the driver's rank check
+        # communicator lines (ranks, NVLS/P2P transport) for the driver's rank check (NCCL logs to stdout
+        # unless NCCL_DEBUG_FILE says otherwise; the JSON line is printed last, after the group is destroyed)
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
+    elif args.force_collective:
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=dev)
     import __graft_entry__
 
     if rank == 0:
@@ -645,7 +660,7 @@ def main():
 
     main_cfg = CONFIGS[args.config]
     r = run_config(args.config, main_cfg, args.steps, args.warmup, world, rank, dev, want_e2e=not args.no_e2e,
-                   scaling=args.scaling)
+                   scaling=args.scaling, force_collective=args.force_collective and world == 1)
     extra, detail = {}, {}
     if not args.no_extra:
         for nm in ("C2", "C4", "C5", "C1"):
@@ -685,7 +700,8 @@ def main():
             "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
             "scaling": r["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "dist_backend": args.dist_backend if world > 1 else None,
+            "dist_backend": args.dist_backend if world > 1 else ("nccl (1 rank, forced exchange)"
+                                                                 if args.force_collective else None),
             "extra": extra,
             "config": {"workload": WORKLOAD[args.config], "config": args.config, "blocks_per_gpu": r["B"],
                        "global_blocks": r["global_blocks"], "n": r["n"], "steps_M": r["M"], "taps_T": r["T"],
@@ -702,7 +718,7 @@ def main():
         except OSError:
             pass
         print(json.dumps({"extra_detail": detail}), file=sys.stderr, flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
     if line is not None:

@@ -39,6 +39,9 @@ class DataParallelLDBP:
     # launch for tiny problems); used when world == 1, where there is no exchange between the
     # gradient and Adam
     train_step_fn: Optional[Callable] = None
+    # run the collectives even at world == 1 (a one-rank NCCL group on a single GPU exercises the
+    # communicator and the fp64 all-reduce of the gradient buffer: tests/test_gpu_dp_nccl.py)
+    force_collective: bool = False
 
     def __post_init__(self):
         if self.loss_grad_fn is None or self.adam_fn is None:
@@ -58,7 +61,7 @@ class DataParallelLDBP:
         """n_global = sum over ranks of B_local * n (one small all-reduce at setup)."""
         t = torch.tensor([float(local_samples)], dtype=torch.float64,
                          device="cuda" if self._nccl() else "cpu")
-        if dist.is_initialized() and self.world > 1:
+        if self._exchange():
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         self.n_global = float(t.item())
         return self.n_global
@@ -66,14 +69,17 @@ class DataParallelLDBP:
     def _nccl(self) -> bool:
         return dist.is_initialized() and dist.get_backend(self.group) == "nccl"
 
+    def _exchange(self) -> bool:
+        return dist.is_initialized() and (self.world > 1 or self.force_collective)
+
     def step(self, x_local, target_local):
         """loss_grad (local) -> all_reduce(SUM) -> Adam.  Returns the reduced buffer."""
         if self.n_global <= 0:
             raise RuntimeError("call set_local_samples() first")
-        if self.train_step_fn is not None and self.world == 1:
+        if self.train_step_fn is not None and not self._exchange():
             return self.train_step_fn(x_local, target_local)
         buf = self.loss_grad_fn(x_local, target_local)
-        if dist.is_initialized() and self.world > 1:
+        if self._exchange():
             dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
         self.adam_fn(buf, self.n_global)
         return buf
