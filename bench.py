@@ -315,30 +315,33 @@ def run_config(name, cfg, steps, warmup, world, rank, dev, want_e2e=True, want_c
                                        phase=dsym[b][3], out=dt[b], stream=cstream)
                 copied[b].record(cstream)
 
+        # the step's kernels on a high-priority stream: the target rebuild on the copy stream then only
+        # takes the SM slots the step leaves free (wave tails) instead of sharing them equally
+        es = torch.cuda.Stream(device=dev, priority=-1) if os.environ.get("LDBP_BENCH_E2E_PRIO", "1") != "0" else stream
         for b in range(2):
             freed[b].record(stream)
         torch.cuda.synchronize()
         if dist.is_initialized():
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        issue_copy(0)
-        for i in range(e2e_steps):
-            b = i % 2
-            stream.wait_event(copied[b])
-            out = step(dx[b], dt[b])
-            freed[b].record(stream)
-            if i + 1 < e2e_steps:
-                issue_copy(i + 1)  # overlaps this step's compute
-            with torch.cuda.stream(stream):
+        with torch.cuda.stream(es):
+            e0.record(es)
+            issue_copy(0)
+            for i in range(e2e_steps):
+                b = i % 2
+                es.wait_event(copied[b])
+                out = step(dx[b], dt[b])
+                freed[b].record(es)
+                if i + 1 < e2e_steps:
+                    issue_copy(i + 1)  # overlaps this step's compute
                 res[b].copy_(out[:1] if train else out.view(-1), non_blocking=True)
-            read_ev[b].record(stream)
-            if i >= 1:  # the host reads step i-1's result while step i runs (no launch bubble)
-                read_ev[1 - b].synchronize()
-                seen.append(float(res[1 - b][0].real))
-        read_ev[(e2e_steps - 1) % 2].synchronize()
-        seen.append(float(res[(e2e_steps - 1) % 2][0].real))
-        e1.record(stream)
+                read_ev[b].record(es)
+                if i >= 1:  # the host reads step i-1's result while step i runs (no launch bubble)
+                    read_ev[1 - b].synchronize()
+                    seen.append(float(res[1 - b][0].real))
+            read_ev[(e2e_steps - 1) % 2].synchronize()
+            seen.append(float(res[(e2e_steps - 1) % 2][0].real))
+            e1.record(es)
         torch.cuda.synchronize()
         assert len(seen) == e2e_steps
         e_ms = e0.elapsed_time(e1) / e2e_steps
