@@ -85,6 +85,19 @@ __device__ __forceinline__ constexpr bool rev_vark() { return LDBP_REV_VARK && S
 #ifndef LDBP_REV_UNROLL2
 #define LDBP_REV_UNROLL2 0  // 1: two reverse steps per loop iteration (register renaming instead of moves)
 #endif
+#ifndef LDBP_REV_ONE_BODY
+#define LDBP_REV_ONE_BODY 1  // 1 (Kh >= 2): the last step of a launch (l == s0, no NL adjoint to fuse) runs
+                             // the same step code with gamma' = 0 (the NL adjoint is then the identity, bit
+                             // for bit on finite data) instead of its own no-NL instantiation, which ptxas
+                             // compiled to 1664 instructions against 750 for the hot step and which every
+                             // warp walked once per CTA: C3 reverse 1.955 -> 1.93 ms.  Kh <= 1 keeps the
+                             // no-NL step (the NL adjoint is most of a Kh = 1 step: C5 +0.9 % with it)
+#endif
+#ifndef LDBP_REV_WIN_LEAN
+#define LDBP_REV_WIN_LEAN 0  // 1: bulk window copies with every per-launch invariant (alignment, shared-memory
+                             // addresses, barrier parity from the step index) hoisted out of the step loop.
+                             // Measured (B200): C3 reverse +1.5 % (registers), C5 -1.1 %: off
+#endif
 #ifndef LDBP_NB_WAIT
 #define LDBP_NB_WAIT 0  // split step barrier: 1 = wait only for the neighbouring warps, 0 = CTA-wide phase
 #endif
@@ -392,8 +405,31 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   // runtime buffer number put them in local memory: STL/LDL in the step loop)
   unsigned bused = 0u;  // buffer b was filled by a bulk copy
   unsigned bph = 0u;    // next phase parity of bbar[b]
+  // LDBP_REV_WIN_LEAN: a warp whose copies are bulk copies for the whole launch (16-byte aligned for
+  // every step: even activation stride) keeps the destination and barrier addresses in registers
+  // and takes the barrier parity from the step index (buffer b = i % 2 is used every other step)
+  const uint32_t lean_dst = smem_u32(sm.ubuf + ubuf_idx<COAL, R, NT>(0, warp * 32));
+  const uint32_t lean_bar = smem_u32(bbar);
+  const bool lean_ok = LDBP_REV_WIN_LEAN && wbulk && (a.act_stride & 1) == 0 &&
+                       ((reinterpret_cast<uintptr_t>(a.act + woff)) & 15) == 0 &&
+                       (s0 > 0 || ((reinterpret_cast<uintptr_t>(a.x + woff)) & 15) == 0);
   auto window = [&](int i, int b) {  // async copy of u^(i) into window buffer b
     const float2* src = rev_src(a, i);
+    if (lean_ok) {
+      if (lane == 0) {
+        constexpr unsigned bytes = 32u * R * 8u;
+        const uint32_t bar_b = lean_bar + 8u * b;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of dst
+        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar_b), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                lean_dst + (uint32_t)(b * UB * 8)),
+            "l"(src + woff), "r"(bytes), "r"(bar_b)
+            : "memory");
+      }
+      return;
+    }
     if (wbulk && ((reinterpret_cast<uintptr_t>(src + woff)) & 15) == 0) {
       bused |= 1u << b;
       if (lane == 0) {
@@ -417,7 +453,21 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
     else
       async_window<COAL, R, NT>(src, e0, a.g, sm.ubuf + (size_t)b * UB, fast_off);
   };
-  auto window_wait = [&](int b) {  // buffer b's copy has landed (and the warp may reuse the other)
+  auto window_wait = [&](int b, int i) {  // buffer b's copy of u^(i) has landed (and the warp may reuse the other)
+    if (lean_ok) {
+      const unsigned par = ((unsigned)(s1 - 1 - i) >> 1) & 1u;  // uses of buffer b alternate phases
+      unsigned ok;
+      do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(lean_bar + 8u * b), "r"(par), "r"(LDBP_MBAR_SUSPEND_NS)
+            : "memory");
+      } while (!ok);
+      __syncwarp();
+      return;
+    }
     if ((bused >> b) & 1u) {
       mbar_wait_parity(bbar + b, (bph >> b) & 1u);
       bph ^= 1u << b;
@@ -515,7 +565,7 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // u^(l) landed, u^(l-1) may be in flight
       if (COAL) __syncwarp();
     } else {
-      window_wait(l % PIPE);  // u^(l) landed (bulk: mbarrier transaction count; else cp.async)
+      window_wait(l % PIPE, l);  // u^(l) landed (bulk: mbarrier transaction count; else cp.async)
     }
     // prefetch u^(l-PIPE+1) into a free buffer (this thread's own slots, consumed later)
     if (l - (PIPE - 1) >= s0)
@@ -526,7 +576,7 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
     float dgam_next = 0.f;
     const TapP* hs_sm = sm.taps_adj + li * NTU;
     const float gmn = l > s0 ? sm.gamma[li - 1] : 0.f;
-    if (l > s0) {
+    if ((LDBP_REV_ONE_BODY && KH >= 2) || l > s0) {
       if (rev_vark<KH, SYM, NORM, FAST>() && full) {
         // active folded taps of this step: the outermost unmasked tap (masked taps are pruned:
         // zero value and zero gradient; unmasked zero-valued taps still need their gradient)
