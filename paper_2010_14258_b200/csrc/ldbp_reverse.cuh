@@ -94,9 +94,10 @@ __device__ __forceinline__ constexpr bool rev_vark() { return LDBP_REV_VARK && S
                              // no-NL step (the NL adjoint is most of a Kh = 1 step: C5 +0.9 % with it)
 #endif
 #ifndef LDBP_REV_WIN_LEAN
-#define LDBP_REV_WIN_LEAN 0  // 1: bulk window copies with every per-launch invariant (alignment, shared-memory
-                             // addresses, barrier parity from the step index) hoisted out of the step loop.
-                             // Measured (B200): C3 reverse +1.5 % (registers), C5 -1.1 %: off
+#define LDBP_REV_WIN_LEAN 1  // bulk window copies with every per-launch invariant (alignment, shared-memory
+                             // addresses, barrier parity from the step index) hoisted out of the step loop:
+                             // 1 = for Kh <= 1, 2 = always, 0 = never.  Measured (B200): C5 reverse (Kh = 1)
+                             // 14.68 -> 14.39 ms (-2.0 %, three A/B pairs); C3 (Kh = 4) +1.5 % (registers)
 #endif
 #ifndef LDBP_NB_WAIT
 #define LDBP_NB_WAIT 0  // split step barrier: 1 = wait only for the neighbouring warps, 0 = CTA-wide phase
@@ -410,7 +411,7 @@ __device__ __forceinline__ void rev_body(const RevArgs& a, const RevSmem& sm, in
   // and takes the barrier parity from the step index (buffer b = i % 2 is used every other step)
   const uint32_t lean_dst = smem_u32(sm.ubuf + ubuf_idx<COAL, R, NT>(0, warp * 32));
   const uint32_t lean_bar = smem_u32(bbar);
-  const bool lean_ok = LDBP_REV_WIN_LEAN && wbulk && (a.act_stride & 1) == 0 &&
+  const bool lean_ok = (LDBP_REV_WIN_LEAN == 2 || (LDBP_REV_WIN_LEAN == 1 && KH <= 1)) && wbulk && (a.act_stride & 1) == 0 &&
                        ((reinterpret_cast<uintptr_t>(a.act + woff)) & 15) == 0 &&
                        (s0 > 0 || ((reinterpret_cast<uintptr_t>(a.x + woff)) & 15) == 0);
   auto window = [&](int i, int b) {  // async copy of u^(i) into window buffer b
